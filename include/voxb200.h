@@ -1,0 +1,180 @@
+/*
+ * voxb200.h — C-ABI of the B200-native streaming-TTS serving hot path.
+ *
+ * This is the drop-in boundary behind the reference's Python model-execution
+ * interface (/root/reference/pkg/src/speechserve/model_api.py).  Every entry
+ * point takes plain pointers and sizes; no torch or C++ types cross it.  The
+ * reference is pure Python, so the "reference-side binding" is a ctypes stub
+ * (see INTEGRATION.md); the Python mirror of the reference Executor Protocol
+ * lives in paper_2602_00269_b200/executor.py.
+ *
+ * Which reference interface each entry point replaces (file:line in
+ * /root/reference/pkg/src/speechserve/):
+ *   vox_admit         preprocess()                      model_api.py:238-275
+ *   vox_forward       Executor.forward / lm_forward     model_api.py:209-211, 278-294
+ *                     + sample()/sample_batch() fused   model_api.py:355-395
+ *                     + next_input()                    model_api.py:297-308
+ *   vox_sample_logits sample_batch() on given logits    model_api.py:384-395
+ *   vox_detok         Executor.detokenize_windows       model_api.py:213-220, 398-435
+ *                                                       profiles.py:333-356
+ *   vox_release       (no reference hook; called on the final window,
+ *                      profiles.py:279-290 / engine.py:346-353)
+ *
+ * Status codes map 1:1 onto the reference exception tree (errors.py:4-77);
+ * see paper_2602_00269_b200/_lib.py:_STATUS_TO_EXC.
+ *
+ * Ownership: a VoxCtx owns ALL device memory (weights, paged KV pool, token
+ * store, detokenizer state pool, workspaces, CUDA graphs).  One ctx per GPU
+ * per process; calls on one ctx must be serialised by the caller (one engine
+ * loop per ctx, as the reference requires: model_api.py:199-205).
+ */
+#ifndef VOXB200_H_
+#define VOXB200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VOX_ABI_VERSION 1
+
+typedef enum VoxStatus {
+  VOX_OK = 0,
+  VOX_ERR_INVALID = 1,             /* ValueError                                  */
+  VOX_ERR_BATCH_TOO_LARGE = 2,     /* errors.BatchTooLarge       errors.py:28     */
+  VOX_ERR_DEGENERATE = 3,          /* errors.DegenerateDistribution errors.py:36  */
+  VOX_ERR_CODEBOOK_MISMATCH = 4,   /* errors.CodebookMismatch    errors.py:40     */
+  VOX_ERR_WINDOW_RULE = 5,         /* errors.WindowRuleViolation errors.py:44     */
+  VOX_ERR_CACHE_MISSING = 6,       /* errors.CacheMissing        errors.py:48     */
+  VOX_ERR_PROMPT_TOO_LONG = 7,     /* errors.PromptTooLong       errors.py:24     */
+  VOX_ERR_INVALID_TOKEN_COUNT = 8, /* errors.InvalidTokenCount   errors.py:16     */
+  VOX_ERR_NONFINITE = 9,           /* ValueError: NaN/+inf logits model_api.py:370 */
+  VOX_ERR_OUT_OF_MEMORY = 10,      /* KV page pool / slot pool exhausted          */
+  VOX_ERR_CUDA = 11,               /* CUDA runtime error (message in last_error)  */
+  VOX_ERR_NO_DEVICE = 12,          /* no sm_100 device                            */
+  VOX_ERR_EMPTY_BATCH = 13         /* errors.EmptyBatch          errors.py:32     */
+} VoxStatus;
+
+/* Model + capacity configuration.  Shapes follow a Llama-style backbone
+ * (Orpheus-3B = Llama-3.2-3B dims) and a causal SNAC-24kHz-style decoder. */
+typedef struct VoxModelCfg {
+  /* backbone */
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, d_ff, vocab;
+  float rope_theta, rms_eps;
+  float embed_scale;        /* uniform init half-width of the (tied) embedding */
+  int32_t text_vocab;       /* synthetic prompt ids are drawn from [0, text_vocab) */
+  /* Orpheus audio-token layout: frame slot k of 7 may only emit ids in
+   * [audio_base + k*codebook_size, audio_base + (k+1)*codebook_size).
+   * audio_base < 0 disables the mask (generic LM). */
+  int32_t audio_base, codebook_size, frame_tokens;
+  /* capacity */
+  int32_t page_size, n_pages, max_slots, max_ctx, max_rows;
+  /* detokenizer (SNAC-24k-style, causal); detok_enabled = 0 skips it */
+  int32_t detok_enabled;
+  int32_t latent_dim, decoder_dim, n_rates;
+  int32_t rates[4];
+  int32_t max_detok_frames; /* max latent frames per detok call (all requests) */
+} VoxModelCfg;
+
+/* Per-request sampling parameters (SamplingParams, model_api.py:105-121). */
+typedef struct VoxSampling {
+  double temperature;        /* 0 = greedy (Python float, fp64 like the reference) */
+  double top_p;              /* (0, 1]                                             */
+  double repetition_penalty; /* >= 1                                               */
+  int32_t top_k;             /* 0 = disabled                                       */
+  int32_t penalty_window;    /* ring-window length (<= 256)                        */
+} VoxSampling;
+
+/* One row of a mixed prefill/decode batch.  A row feeds token_store[slot][pos]
+ * (or `token` when >= 0, which is also written to the store) at position pos.
+ * Rows with sample != 0 produce the next token into token_store[slot][pos+1]. */
+typedef struct VoxRow {
+  int32_t slot;
+  int32_t pos;
+  int32_t token;
+  int32_t sample;
+} VoxRow;
+
+/* One detokenizer window (WindowSpec, profiles.py:115-124) bound to a slot. */
+typedef struct VoxWindow {
+  int32_t slot;
+  int32_t index;      /* 1-based chunk ordinal */
+  int32_t start;      /* first token (generated-token index) of the window */
+  int32_t length;
+  int32_t new_tokens; /* the last new_tokens of the window are new audio */
+  int32_t final;
+} VoxWindow;
+
+typedef struct VoxCtx VoxCtx;
+
+/* forward flags */
+#define VOX_FWD_SAMPLE 1u       /* run the fused sampler on rows with sample != 0   */
+#define VOX_FWD_FULL_LOGITS 2u  /* LM head over the full vocab (parity path)        */
+#define VOX_FWD_SYNC 4u         /* block until done (implied by host outputs)       */
+#define VOX_FWD_NO_GRAPH 8u     /* eager launches (timing / debugging)              */
+
+int vox_abi_version(void);
+const char* vox_last_error(const VoxCtx* ctx); /* ctx may be NULL (global error) */
+
+int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx** out);
+void vox_destroy(VoxCtx* ctx);
+
+/* preprocess(): allocate a slot, reserve KV pages for prompt_len+target_len
+ * tokens, write the synthetic prompt ids, reset detok state. */
+int vox_admit(VoxCtx* ctx, uint64_t req_seed, int32_t prompt_len, int32_t target_len,
+              const VoxSampling* params, int32_t* slot_out);
+int vox_release(VoxCtx* ctx, int32_t slot);
+int vox_page_table(VoxCtx* ctx, int32_t slot, int32_t* out, int32_t cap, int32_t* n_out);
+int vox_read_tokens(VoxCtx* ctx, int32_t slot, int32_t pos, int32_t n, int32_t* out);
+/* write host-chosen token ids into the device token store (drop-in path,
+ * where the reference engine samples on the host: engine.py:294-303) */
+int vox_write_tokens(VoxCtx* ctx, int32_t slot, int32_t pos, int32_t n, const int32_t* ids);
+int vox_slot_info(VoxCtx* ctx, int32_t slot, int32_t* prompt_len, int32_t* target_len);
+
+/* Mixed prefill/decode forward over n rows.  logits_out (host, may be NULL):
+ * [n_sample, vocab] fp32 masked logits of the sampling rows, in row order
+ * (requires VOX_FWD_FULL_LOGITS).  tokens_out (host, may be NULL): the sampled
+ * ids of the sampling rows.  With both NULL and without VOX_FWD_SYNC the call
+ * is asynchronous on the LM stream. */
+int vox_forward(VoxCtx* ctx, const VoxRow* rows, int32_t n, uint32_t flags,
+                float* logits_out, int32_t* tokens_out);
+
+/* K1 alone over caller logits (host, [n, vocab] fp32): window_ids [n, wcap]
+ * (window_len[i] valid entries, oldest first), seeds/steps drive the
+ * counter-based RNG, lo/hi restrict the candidate range ([0,vocab) = none). */
+int vox_sample_logits(VoxCtx* ctx, const float* logits, int32_t n, int32_t vocab,
+                      const VoxSampling* params, const int32_t* window_ids, int32_t wcap,
+                      const int32_t* window_len, const uint64_t* seeds, const uint64_t* steps,
+                      const int32_t* lo, const int32_t* hi, int32_t* tokens_out);
+
+/* Detokenize n windows on the detok stream (after the LM stream's last
+ * forward).  pcm_out (host, may be NULL): concatenated float PCM, request i
+ * at offset sum(n_samples[:i]).  Returns a ticket usable with
+ * vox_ticket_* when async (pcm_out == NULL). */
+int vox_detok(VoxCtx* ctx, const VoxWindow* w, int32_t n, float* pcm_out,
+              int32_t* n_samples, int64_t* ticket);
+int vox_ticket_query(VoxCtx* ctx, int64_t ticket, int32_t* done, double* t_ms);
+int vox_ticket_pcm(VoxCtx* ctx, int64_t ticket, const float** pcm, int32_t* total);
+int vox_clock_reset(VoxCtx* ctx); /* epoch event for vox_ticket_query t_ms */
+int vox_synchronize(VoxCtx* ctx);
+
+/* streams (cudaStream_t as void*) for external event timing */
+int vox_streams(VoxCtx* ctx, void** lm_stream, void** detok_stream);
+
+/* kernel-class timing with CUDA events on the launching stream (eager mode only) */
+int vox_timing_enable(VoxCtx* ctx, int32_t on);
+int vox_timing_read(VoxCtx* ctx, const char* name, double* total_ms, int64_t* launches,
+                    double* bytes);
+int vox_launch_count(VoxCtx* ctx, int64_t* launches); /* our kernels launched so far */
+
+/* weights / state introspection for parity tests (host copies) */
+int vox_read_weight(VoxCtx* ctx, const char* name, int32_t layer, void* out, size_t bytes);
+int vox_read_kv(VoxCtx* ctx, int32_t layer, int32_t slot, int32_t pos, float* k_out,
+                float* v_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VOXB200_H_ */

@@ -1,0 +1,120 @@
+"""CPU restatement of the decode step (TEST INFRASTRUCTURE ONLY).
+
+The reference's LM forward is a hash stub (profiles.py:318-331), so this
+backbone follows the public Llama architecture ([3P] transformers 5.5.0
+models/llama/modeling_llama.py: LlamaRMSNorm :53, rotate_half RoPE :73,
+LlamaMLP :171, LlamaAttention :225 with GQA) and mirrors the GPU rounding
+points exactly: bf16 weights, fp32 residual stream, bf16 GEMM inputs
+(normalised x, attention output, SiLU*up), fp32 accumulation, fp32 logits.
+Parity status: UNPINNED by the reference (no LM arithmetic there); pinned
+by tests/golden/tiny_greedy.npz generated from this module.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .weights import BackboneWeights, bf16_round
+
+f32 = np.float32
+
+
+def rmsnorm_bf16(h: np.ndarray, w: np.ndarray, eps: float) -> np.ndarray:
+    """lm_kernels.cu:embed_norm_kernel / resid_norm_kernel."""
+    h = h.astype(np.float32)
+    ss = np.sum(h * h, axis=-1, dtype=np.float32, keepdims=True)
+    inv = f32(1.0) / np.sqrt(ss / f32(h.shape[-1]) + f32(eps))
+    return bf16_round((h * inv) * w)
+
+
+def rope(x: np.ndarray, pos: np.ndarray, inv_freq: np.ndarray) -> np.ndarray:
+    """rotate_half RoPE; x [n, heads, hd]; angle=float32(pos)*inv_freq, sin/cos in fp64."""
+    half = x.shape[-1] // 2
+    ang = pos.astype(np.float32)[:, None] * inv_freq[None, :]
+    c = np.cos(ang.astype(np.float64)).astype(np.float32)[:, None, :]
+    s = np.sin(ang.astype(np.float64)).astype(np.float32)[:, None, :]
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+class LlamaOracle:
+    """Per-request contiguous KV (the paged layout is checked via oracle/paging.py)."""
+
+    def __init__(self, cfg, seed: int, weights: BackboneWeights | None = None):
+        self.cfg = cfg
+        self.w = weights or BackboneWeights(cfg, seed)
+        self.k = {}  # rid -> [L, T, KV, hd]
+        self.v = {}
+
+    def _layer_kv(self, rid):
+        if rid not in self.k:
+            c = self.cfg
+            self.k[rid] = np.zeros((c.n_layers, c.max_ctx, c.n_kv_heads, c.head_dim), np.float32)
+            self.v[rid] = np.zeros_like(self.k[rid])
+        return self.k[rid], self.v[rid]
+
+    def forward(self, rid, tokens: np.ndarray, positions: np.ndarray, want_logits: bool = True):
+        """Run tokens [n] at positions [n] (contiguous, ascending) of request rid.
+
+        Returns logits [n, vocab] fp32 of every row (or None) and the final
+        normalised hidden rows xf [n, d] (bf16 values).
+        """
+        c, w = self.cfg, self.w
+        d, H, KV, hd = c.d_model, c.n_heads, c.n_kv_heads, c.head_dim
+        G = H // KV
+        n = len(tokens)
+        K, V = self._layer_kv(rid)
+        h = w.emb[tokens].astype(np.float32)  # fp32 residual
+        x = rmsnorm_bf16(h, w.layers[0]["norm_attn"], c.rms_eps)
+        scale = f32(1.0) / np.sqrt(f32(hd))
+        for l, L in enumerate(w.layers):
+            qkv = x @ L["qkv"].T
+            q = qkv[:, : H * hd].reshape(n, H, hd)
+            k = qkv[:, H * hd: (H + KV) * hd].reshape(n, KV, hd)
+            v = qkv[:, (H + KV) * hd:].reshape(n, KV, hd)
+            q = bf16_round(rope(q, positions, w.inv_freq))
+            k = bf16_round(rope(k, positions, w.inv_freq))
+            v = bf16_round(v)
+            K[l, positions] = k
+            V[l, positions] = v
+            out = np.empty((n, H, hd), np.float32)
+            for i in range(n):
+                T = positions[i] + 1
+                kk = K[l, :T]  # [T, KV, hd]
+                vv = V[l, :T]
+                for hh in range(H):
+                    g = hh // G
+                    s = (kk[:, g, :] @ q[i, hh]) * scale
+                    m = s.max()
+                    p = np.exp(s - m)
+                    out[i, hh] = (p @ vv[:, g, :]) / p.sum(dtype=np.float32)
+            a = bf16_round(out.reshape(n, H * hd))
+            h = h + a @ L["o"].T
+            x = rmsnorm_bf16(h, L["norm_mlp"], c.rms_eps)
+            gu = x @ L["gu"].T
+            g_, u_ = gu[:, : c.d_ff], gu[:, c.d_ff:]
+            act = bf16_round((g_ / (f32(1.0) + np.exp(-g_))) * u_)
+            h = h + act @ L["down"].T
+            nw = w.layers[l + 1]["norm_attn"] if l + 1 < len(w.layers) else w.norm_final
+            x = rmsnorm_bf16(h, nw, c.rms_eps)
+        logits = (x @ w.emb.T).astype(np.float32) if want_logits else None
+        return logits, x
+
+    def release(self, rid):
+        self.k.pop(rid, None)
+        self.v.pop(rid, None)
+
+
+def audio_range(cfg, step: int):
+    """Orpheus frame-slot codebook-offset mask for generated token `step`."""
+    if cfg.audio_base < 0:
+        return 0, cfg.vocab
+    k = step % cfg.frame_tokens
+    lo = cfg.audio_base + k * cfg.codebook_size
+    return lo, lo + cfg.codebook_size
+
+
+def masked(logits_row: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    out = np.full(logits_row.shape, -np.inf, dtype=np.float64)
+    out[lo:hi] = logits_row[lo:hi]
+    return out

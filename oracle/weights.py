@@ -1,0 +1,146 @@
+"""Bit-exact CPU mirror of the device random-init (TEST INFRASTRUCTURE ONLY).
+
+Mirrors paper_2602_00269_b200/csrc/init.cu (w = bf16_rn(unit_pm1(mix64(key+i)) * scale))
+and the tensor-key / scale choices of csrc/vox_api.cu (create_backbone,
+create_detok).  splitmix64 is the reference's mixer (model_api.py:39-51).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+
+# tensor ids (csrc/vox_api.cu: TensorId)
+T_EMB, T_NORM_ATTN, T_NORM_MLP, T_NORM_FINAL = 1, 2, 3, 4
+T_QKV, T_O, T_GU, T_DOWN = 5, 6, 7, 8
+T_VQ_TAB, T_IN_DW_W, T_IN_DW_B, T_IN_PW_W, T_IN_PW_B = 20, 21, 22, 23, 24
+T_UP_ALPHA, T_UP_W, T_UP_B = 30, 34, 38
+T_RU_A1, T_RU_DW_W, T_RU_DW_B, T_RU_A2, T_RU_PW_W, T_RU_PW_B = 50, 70, 90, 110, 130, 150
+T_OUT_ALPHA, T_OUT_W, T_OUT_B = 170, 171, 172
+
+
+def mix64(x: int) -> int:
+    """splitmix64 finalizer (model_api.py:39-44)."""
+    x = (x + GOLDEN) & MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & MASK64
+    return x ^ (x >> 31)
+
+
+def mix64_arr(x: np.ndarray) -> np.ndarray:
+    """Vectorised splitmix64 (model_api.py:47-51)."""
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(GOLDEN)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return x ^ (x >> np.uint64(31))
+
+
+def tensor_key(seed: int, tid: int, layer: int) -> int:
+    a = mix64((seed ^ ((tid * 0xD1B54A32D192ED03) & MASK64)) & MASK64)
+    return mix64(a ^ ((layer * 0x8CB92BA72F3D8DD7) & MASK64))
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> nearest-even bfloat16, returned as float32 (no NaN inputs)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    return b.astype(np.uint32).view(np.float32)
+
+
+def unit_pm1(n: int, key: int, start: int = 0) -> np.ndarray:
+    i = np.arange(start, start + n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = mix64_arr(np.uint64(key) + i)
+    return (h >> np.uint64(40)).astype(np.int32).astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
+
+
+def init_bf16(n: int, key: int, scale, chunk: int = 1 << 24) -> np.ndarray:
+    """csrc/init.cu:init_bf16_kernel, as float32 values."""
+    out = np.empty(n, dtype=np.float32)
+    s = np.float32(scale)
+    for a in range(0, n, chunk):
+        m = min(chunk, n - a)
+        out[a: a + m] = bf16_round(unit_pm1(m, key, a) * s)
+    return out
+
+
+def init_f32(n: int, key: int, scale, offset) -> np.ndarray:
+    """csrc/init.cu:init_f32_kernel."""
+    u = unit_pm1(n, key)
+    return bf16_round(u * np.float32(scale) + np.float32(offset))
+
+
+def f32(x) -> np.float32:
+    return np.float32(x)
+
+
+class BackboneWeights:
+    """All backbone tensors as float32 arrays holding bf16 values."""
+
+    def __init__(self, cfg, seed: int, layers=None):
+        d, hd, H, KV, dff, V = cfg.d_model, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.d_ff, cfg.vocab
+        self.cfg = cfg
+        k = lambda tid, l=0: tensor_key(seed, tid, l)  # noqa: E731
+        self.emb = init_bf16(V * d, k(T_EMB), f32(cfg.embed_half_width)).reshape(V, d)
+        nqkv = (H + 2 * KV) * hd
+        self.layers = []
+        for l in range(cfg.n_layers if layers is None else layers):
+            L = {}
+            L["norm_attn"] = init_f32(d, k(T_NORM_ATTN, l), 0.25, 1.0)
+            L["norm_mlp"] = init_f32(d, k(T_NORM_MLP, l), 0.25, 1.0)
+            L["qkv"] = init_bf16(nqkv * d, k(T_QKV, l), np.sqrt(f32(3.0) / f32(d))).reshape(nqkv, d)
+            L["o"] = init_bf16(d * H * hd, k(T_O, l), np.sqrt(f32(3.0) / f32(H * hd))).reshape(d, H * hd)
+            L["gu"] = init_bf16(2 * dff * d, k(T_GU, l), np.sqrt(f32(3.0) / f32(d))).reshape(2 * dff, d)
+            L["down"] = init_bf16(d * dff, k(T_DOWN, l), np.sqrt(f32(3.0) / f32(dff))).reshape(d, dff)
+            self.layers.append(L)
+        self.norm_final = init_f32(d, k(T_NORM_FINAL), 0.25, 1.0)
+        self.inv_freq = np.array(
+            [np.float32(1.0 / (float(cfg.rope_theta) ** ((2.0 * i) / hd))) for i in range(hd // 2)],
+            dtype=np.float32,
+        )
+
+
+class DetokWeights:
+    """Causal SNAC-style decoder tensors (csrc/vox_api.cu:create_detok)."""
+
+    def __init__(self, cfg, seed: int):
+        k = lambda tid, l=0: tensor_key(seed, tid, l)  # noqa: E731
+        L, D0, cb = cfg.latent_dim, cfg.decoder_dim, cfg.codebook_size
+        self.tabs = init_bf16(3 * cb * L, k(T_VQ_TAB), 0.866).reshape(3, cb, L)
+        self.in_dw_w = init_f32(7 * L, k(T_IN_DW_W), np.sqrt(f32(3.0) / f32(7.0)), 0.0).reshape(L, 7)
+        self.in_dw_b = init_f32(L, k(T_IN_DW_B), 0.05, 0.0)
+        self.in_pw_w = init_bf16(D0 * L, k(T_IN_PW_W), np.sqrt(f32(3.0) / f32(L))).reshape(D0, L)
+        self.in_pw_b = init_f32(D0, k(T_IN_PW_B), 0.05, 0.0)
+        ch = [D0]
+        for _ in range(4):
+            ch.append(ch[-1] // 2)
+        self.ch = ch
+        self.rates = list(cfg.rates)
+        self.up_alpha, self.up_w, self.up_b = [], [], []
+        self.ru = []
+        for b in range(4):
+            Ci, Co, s = ch[b], ch[b + 1], self.rates[b]
+            self.up_alpha.append(init_f32(Ci, k(T_UP_ALPHA + b), 0.5, 1.0))
+            self.up_w.append(init_bf16(s * Co * 2 * Ci, k(T_UP_W + b),
+                                       np.sqrt(f32(3.0) / (f32(2.0) * f32(Ci)))).reshape(s * Co, 2 * Ci))
+            small = init_f32(Co, k(T_UP_B + b), 0.05, 0.0)
+            self.up_b.append(np.tile(small, s))
+            units = []
+            for u in range(3):
+                li = b * 3 + u
+                units.append(dict(
+                    a1=init_f32(Co, k(T_RU_A1, li), 0.5, 1.0),
+                    a2=init_f32(Co, k(T_RU_A2, li), 0.5, 1.0),
+                    dw_w=init_f32(7 * Co, k(T_RU_DW_W, li), np.sqrt(f32(3.0) / f32(7.0)), 0.0).reshape(Co, 7),
+                    dw_b=init_f32(Co, k(T_RU_DW_B, li), 0.05, 0.0),
+                    pw_w=init_bf16(Co * Co, k(T_RU_PW_W, li), f32(0.5) * np.sqrt(f32(3.0) / f32(Co))).reshape(Co, Co),
+                    pw_b=init_f32(Co, k(T_RU_PW_B, li), 0.05, 0.0),
+                ))
+            self.ru.append(units)
+        C4 = ch[4]
+        self.out_alpha = init_f32(C4, k(T_OUT_ALPHA), 0.5, 1.0)
+        self.out_w = init_f32(7 * C4, k(T_OUT_W), np.sqrt(f32(3.0) / (f32(7.0) * f32(C4))), 0.0).reshape(C4, 7)
+        self.out_b = init_f32(1, k(T_OUT_B), 0.05, 0.0)[0]

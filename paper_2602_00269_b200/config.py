@@ -1,0 +1,115 @@
+"""Model + capacity configurations (BASELINE.json configs 1 and 2).
+
+Backbone dims follow public Llama-3.2 shapes (Orpheus-3B is a Llama-3.2-3B
+fine-tune; [3P] transformers LlamaConfig); the detokenizer follows the public
+SNAC-24kHz decoder dims (decoder_dim 1024, rates [8,8,4,2], 3 codebooks of 4096,
+vq strides [4,2,1]), made causal.  Weights are random-init
+from a counter RNG (oracle/weights.py reproduces them bit-for-bit).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import asdict, dataclass, field, replace
+
+# Orpheus token layout: 128256 Llama-3 text ids + 10 special ids, then
+# 7 x 4096 audio ids (frame slot k uses [base + k*4096, base + (k+1)*4096)).
+ORPHEUS_AUDIO_BASE = 128266
+ORPHEUS_VOCAB = 156940
+ORPHEUS_TEXT_VOCAB = 128000
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    name: str
+    n_layers: int
+    d_model: int
+    n_heads: int
+    n_kv_heads: int
+    head_dim: int
+    d_ff: int
+    vocab: int = ORPHEUS_VOCAB
+    rope_theta: float = 500000.0
+    rms_eps: float = 1e-5
+    text_vocab: int = ORPHEUS_TEXT_VOCAB
+    audio_base: int = ORPHEUS_AUDIO_BASE
+    codebook_size: int = 4096
+    frame_tokens: int = 7
+    # capacity
+    page_size: int = 16
+    max_slots: int = 64
+    max_ctx: int = 1024
+    n_pages: int = 0          # 0 -> max_slots * ceil(max_ctx / page_size)
+    max_rows: int = 512
+    # detokenizer
+    detok_enabled: bool = True
+    latent_dim: int = 768
+    decoder_dim: int = 1024
+    rates: tuple = (8, 8, 4, 2)
+    max_detok_frames: int = 256
+    embed_scale: float = 0.0  # 0 -> logit std ~2.5 (see embed_half_width)
+
+    @property
+    def embed_half_width(self) -> float:
+        if self.embed_scale > 0:
+            return self.embed_scale
+        return 2.5 * math.sqrt(3.0) / math.sqrt(self.d_model)
+
+    @property
+    def pages(self) -> int:
+        if self.n_pages > 0:
+            return self.n_pages
+        return self.max_slots * ((self.max_ctx + self.page_size - 1) // self.page_size)
+
+    @property
+    def hop(self) -> int:
+        h = 1
+        for r in self.rates:
+            h *= r
+        return h
+
+    @property
+    def frame_samples(self) -> int:
+        """PCM samples per 7-token frame (4 latent frames x hop)."""
+        return 4 * self.hop
+
+    @property
+    def weight_bytes(self) -> int:
+        """bf16 backbone bytes streamed per decode step (tied embedding/head counted once)."""
+        d, hd = self.d_model, self.head_dim
+        per_layer = (self.n_heads + 2 * self.n_kv_heads) * hd * d + d * self.n_heads * hd
+        per_layer += 3 * d * self.d_ff
+        return 2 * (self.n_layers * per_layer + self.vocab * d)
+
+    @property
+    def kv_bytes_per_token(self) -> int:
+        return 2 * 2 * self.n_layers * self.n_kv_heads * self.head_dim
+
+    def with_capacity(self, **kw) -> "ModelConfig":
+        return replace(self, **kw)
+
+    def to_dict(self) -> dict:
+        d = asdict(self)
+        d["rates"] = list(self.rates)
+        return d
+
+
+def tiny(**kw) -> ModelConfig:
+    """Config 1: 2-layer Llama backbone, d=256 (runs on the CPU oracle)."""
+    base = ModelConfig(
+        name="tiny-orpheus", n_layers=2, d_model=256, n_heads=4, n_kv_heads=2, head_dim=64,
+        d_ff=1024, max_slots=32, max_ctx=1024, max_rows=512, max_detok_frames=256,
+    )
+    return replace(base, **kw)
+
+
+def orpheus3b(**kw) -> ModelConfig:
+    """Config 2: Orpheus-3B-style (Llama-3.2-3B backbone + SNAC-24k-style decoder)."""
+    base = ModelConfig(
+        name="orpheus-3b", n_layers=28, d_model=3072, n_heads=24, n_kv_heads=8, head_dim=128,
+        d_ff=8192, max_slots=320, max_ctx=768, max_rows=1024, max_detok_frames=1024,
+    )
+    return replace(base, **kw)
+
+
+CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b}

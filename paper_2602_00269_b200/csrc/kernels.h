@@ -1,0 +1,136 @@
+// kernels.h — internal launcher declarations shared by the .cu translation units.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/voxb200.h"
+
+namespace vox {
+
+using bf16 = __nv_bfloat16;
+
+// ---------------------------------------------------------------- GEMM
+struct GemmArgs {
+  int M, N, K;            // out features, rows, reduction
+  int n_kb, kb_per_split; // filled by gemm_launch
+  float* out;             // fp32 output / split-K partials
+  int64_t ldo;            // row stride of out (elements)
+  int64_t split_stride;   // elements between split partial planes
+  const float* bias;      // [M] or null (only with 1 split)
+  const float* resid;     // [N, ldr] or null (only with 1 split)
+  int64_t ldr;
+  int m_valid;            // columns m >= m_valid are not stored
+};
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
+                    uint64_t row_stride_bytes, uint32_t box_outer);
+int gemm_bn_for_rows(int rows);
+int gemm_pick_splits(int M, int N, int K, int max_splits);
+cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
+                        int bn, cudaStream_t st);
+
+// ---------------------------------------------------------------- init
+// w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).
+void launch_init_bf16(bf16* w, int64_t n, uint64_t key, float scale, cudaStream_t st);
+// fp32 variant: w[i] = offset + unit_pm1(mix64(key+i)) * scale rounded through bf16.
+void launch_init_f32(float* w, int64_t n, uint64_t key, float scale, float offset,
+                     cudaStream_t st);
+
+// ---------------------------------------------------------------- LM step
+struct RowDev {
+  int32_t slot, pos, token, sample;
+};
+
+struct LmDims {
+  int d, n_heads, n_kv, hd, dff, vocab;
+  float eps;
+  int page_size, max_pages_per_slot, n_pages, max_ctx;
+};
+
+void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
+                       const float* norm_w, const LmDims& dm, float* h, bf16* x, cudaStream_t st);
+void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int splits,
+                            int64_t split_stride, const LmDims& dm, const float* inv_freq,
+                            const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
+                            cudaStream_t st);
+void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
+                        const int* page_table, const LmDims& dm, bf16* out, cudaStream_t st);
+void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
+                       int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
+                       bf16* x_out, const int* out_index, cudaStream_t st);
+void launch_silu_mul(const RowDev* rows, int n, const float* ws, int splits, int64_t split_stride,
+                     const LmDims& dm, bf16* a_out, cudaStream_t st);
+
+// ---------------------------------------------------------------- sampler (K1)
+struct SampRowDesc {
+  int64_t logit_off;  // element offset of this row's column 0
+  int32_t col_base;   // vocab id of column 0
+  int32_t lo, hi;     // candidate vocab-id range [lo, hi)
+  int32_t wlen, woff; // window ids at window_ids[woff .. woff+wlen)
+  int32_t out_index;
+  uint64_t seed, step;
+  VoxSampling params;
+};
+
+struct SampFusedArgs {
+  const RowDev* rows;
+  const int* sample_rows;  // [n_sample] indices into rows
+  int n_sample;
+  const float* logits;     // [n_sample, ld]
+  int64_t ld;
+  int col_base;            // vocab id of logits column 0
+  int* token_store;
+  int max_ctx;
+  const int* slot_prompt_len;
+  const uint64_t* slot_seed;
+  const VoxSampling* slot_params;
+  int audio_base, codebook_size, frame_tokens, vocab;
+  int* tokens_out;         // [n_sample]
+  int* err_flag;
+};
+
+void launch_sample_fused(const SampFusedArgs& a, cudaStream_t st);
+void launch_sample_desc(const float* logits, const SampRowDesc* rows, int n,
+                        const int* window_ids, int* tokens_out, int* err_flag, int max_span,
+                        cudaStream_t st);
+
+// ---------------------------------------------------------------- detokenizer (K4)
+struct DetokReq {      // one request of a detok batch (device copy)
+  int32_t slot;
+  int32_t f0;          // first token frame to decode (generated-token frame index)
+  int32_t nf;          // token frames to decode
+  int32_t lat_off;     // latent-frame row offset of this request in the batch
+  int32_t parity;      // state buffer to read (write 1-parity)
+  int32_t prompt_len;
+  int32_t n_tokens;    // generated tokens available for the last (maybe partial) frame
+  int32_t pcm_off;     // sample offset in the pcm output
+  int32_t n_samples;   // samples to emit
+};
+
+struct DetokDims {
+  int latent, dec, n_rates, rates[4], ch[5];
+  int cb_size, frame_tokens, audio_base, max_ctx;
+  int64_t state_floats;  // per slot per parity
+  int64_t off_in;        // state offsets (floats) within a slot's state
+  int64_t off_up[4];
+  int64_t off_ru[4][3];
+  int64_t off_out;
+};
+
+void launch_vq_dwconv(const DetokReq* reqs, int n_req, int n_lat, const int* token_store,
+                      const bf16* tabs, const float* dw_w, const float* dw_b, float* state,
+                      const DetokDims& dd, bf16* out_bf16, cudaStream_t st);
+void launch_snake_upcat(const DetokReq* reqs, int n_req, int rows, int up_before,
+                        const float* x, int C, const float* alpha, float* state, int64_t st_off,
+                        const DetokDims& dd, bf16* out_cat, cudaStream_t st);
+void launch_ru_prep(const DetokReq* reqs, int n_req, int rows, int up, const float* x, int C,
+                    int dil, const float* alpha1, const float* dw_w, const float* dw_b,
+                    const float* alpha2, float* state, int64_t st_off, const DetokDims& dd,
+                    bf16* out, cudaStream_t st);
+void launch_detok_out(const DetokReq* reqs, int n_req, int rows, int up, const float* x, int C,
+                      const float* alpha, const float* w, float b, float* state, int64_t st_off,
+                      const DetokDims& dd, float* pcm, cudaStream_t st);
+
+}  // namespace vox

@@ -1,0 +1,1368 @@
+// vox_api.cu — the C-ABI runtime: one context per GPU owning weights, the
+// paged KV pool, the device token store, detokenizer state, workspaces and
+// per-bucket CUDA graphs of the decode step.  See include/voxb200.h.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace vox;
+
+namespace {
+
+std::mutex g_err_mu;
+std::string g_err;
+
+// Tensor ids for the counter-based init (oracle/weights.py mirrors these).
+enum TensorId : uint64_t {
+  T_EMB = 1,
+  T_NORM_ATTN = 2,
+  T_NORM_MLP = 3,
+  T_NORM_FINAL = 4,
+  T_QKV = 5,
+  T_O = 6,
+  T_GU = 7,
+  T_DOWN = 8,
+  // detokenizer
+  T_VQ_TAB = 20,
+  T_IN_DW_W = 21,
+  T_IN_DW_B = 22,
+  T_IN_PW_W = 23,
+  T_IN_PW_B = 24,
+  T_UP_ALPHA = 30,  // + block
+  T_UP_W = 34,
+  T_UP_B = 38,
+  T_RU_A1 = 50,  // + block*3 + unit
+  T_RU_DW_W = 70,
+  T_RU_DW_B = 90,
+  T_RU_A2 = 110,
+  T_RU_PW_W = 130,
+  T_RU_PW_B = 150,
+  T_OUT_ALPHA = 170,
+  T_OUT_W = 171,
+  T_OUT_B = 172,
+};
+
+inline uint64_t tensor_key(uint64_t seed, uint64_t tid, uint64_t layer) {
+  return mix64(mix64(seed ^ (tid * 0xD1B54A32D192ED03ull)) ^ (layer * 0x8CB92BA72F3D8DD7ull));
+}
+
+constexpr int kBuckets[] = {16, 32, 64, 128, 256, 512, 1024, 2048};
+
+struct TimingRec {
+  std::string cls;
+  cudaEvent_t a, b;
+  double bytes;
+};
+
+struct Ticket {
+  int64_t id = -1;
+  cudaEvent_t ev = nullptr;
+  float* pcm_host = nullptr;
+  uint8_t* stage_host = nullptr;  // ReqHdr + DetokReq[] (pinned), reused after ev
+  int32_t total = 0;
+};
+
+struct FwdStage {  // pinned per-call staging; reused only after `ev` completed
+  RowDev* rows = nullptr;
+  int* sample_rows = nullptr;
+  int* out_index = nullptr;
+  int* tokens = nullptr;
+  int* err = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool in_flight = false;
+};
+
+struct DetokW {  // detokenizer weights
+  bf16* tabs = nullptr;          // [3][cb][latent]
+  float *in_dw_w = nullptr, *in_dw_b = nullptr;
+  bf16* in_pw_w = nullptr;       // [dec][latent]
+  float* in_pw_b = nullptr;
+  float* up_alpha[4] = {};
+  bf16* up_w[4] = {};            // [s*Cout][2*Cin]
+  float* up_b[4] = {};           // expanded [s*Cout]
+  float* ru_a1[4][3] = {};
+  float* ru_dw_w[4][3] = {};
+  float* ru_dw_b[4][3] = {};
+  float* ru_a2[4][3] = {};
+  bf16* ru_pw_w[4][3] = {};      // [C][C]
+  float* ru_pw_b[4][3] = {};
+  float* out_alpha = nullptr;
+  float* out_w = nullptr;        // [64][7]
+  float out_b = 0.f;
+  CUtensorMap tm_in_pw, tm_up[4], tm_ru[4][3];
+};
+
+}  // namespace
+
+struct VoxCtx {
+  int device = 0;
+  VoxModelCfg cfg{};
+  uint64_t seed = 0;
+  std::string err;
+  cudaStream_t s_lm = nullptr, s_dt = nullptr;
+  cudaEvent_t epoch = nullptr;
+  LmDims dm{};
+  int nqkv = 0, max_pages_per_slot = 0;
+
+  // ---- backbone weights
+  bf16* emb = nullptr;
+  float *norm_attn = nullptr, *norm_mlp = nullptr, *norm_final = nullptr;
+  bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
+  float* inv_freq = nullptr;
+  std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
+  CUtensorMap tm_head_full{}, tm_head_audio{};
+  int head_audio_rows = 0;
+
+  // ---- activations [max_rows, ...]
+  float* h = nullptr;
+  bf16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *xf = nullptr;
+  float* ws = nullptr;
+  size_t ws_elems = 0;
+  float* logits = nullptr;
+  size_t logits_elems = 0;
+  std::map<int, CUtensorMap> tm_x, tm_attn, tm_act, tm_xf;  // by BN
+
+  // ---- KV / tokens / slots
+  bf16 *kc = nullptr, *vc = nullptr;
+  int* token_store = nullptr;
+  int* page_table = nullptr;
+  int* slot_prompt = nullptr;
+  uint64_t* slot_seed = nullptr;
+  VoxSampling* slot_params = nullptr;
+  std::vector<int> free_pages;  // LIFO stack
+  std::vector<std::vector<int>> slot_pages;
+  std::vector<int> slot_used, h_prompt, h_target, slot_chunks, slot_covered;
+  std::vector<int64_t> slot_last_fwd;
+  std::vector<uint64_t> h_seed;
+
+  // ---- per-step staging
+  RowDev* d_rows = nullptr;
+  int* d_sample_rows = nullptr;
+  int* d_out_index = nullptr;
+  int* d_tokens = nullptr;
+  int* d_err = nullptr;
+  std::vector<FwdStage> stages;  // ring
+  int64_t stage_seq = 0;
+  FwdStage* cur = nullptr;       // staging of the call being enqueued
+  double step_attn_bytes = 0;    // per layer, for timing/roofline
+
+  // ---- graphs keyed by (row bucket, sample bucket)
+  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
+  std::map<std::pair<int, int>, int64_t> graph_launches;
+  int64_t fwd_seq = 0;
+  std::vector<cudaEvent_t> fwd_events;  // ring
+  std::vector<int64_t> fwd_event_seq;
+
+  // ---- detokenizer
+  DetokW dw;
+  DetokDims dd{};
+  float* dstate = nullptr;
+  float *dx = nullptr, *dy = nullptr;
+  bf16* dbf = nullptr;
+  size_t dx_elems = 0, dbf_elems = 0;
+  uint8_t* d_dstage = nullptr;  // ReqHdr + DetokReq[]
+  float* d_pcm = nullptr;
+  size_t pcm_cap = 0;
+  std::vector<Ticket> tickets;
+  int64_t next_ticket = 0;
+  std::map<int, CUtensorMap> tm_dbf;  // placeholder (per call maps built on the fly)
+
+  // ---- timing / counting
+  bool timing = false;
+  bool capturing = false;
+  std::vector<TimingRec> trecs;
+  int64_t launches = 0;
+};
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+static int fail(VoxCtx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  std::lock_guard<std::mutex> g(g_err_mu);
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(c, VOX_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));   \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t n) {
+  return cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(n, 1) * sizeof(T));
+}
+
+static int bucket_of(int n) {
+  for (int b : kBuckets)
+    if (n <= b) return b;
+  return -1;
+}
+
+struct TimedLaunch {  // RAII event pair around a launch (eager + timing only)
+  VoxCtx* c;
+  cudaStream_t st;
+  const char* cls;
+  double bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  TimedLaunch(VoxCtx* c_, cudaStream_t s, const char* k, double by, int n_kernels = 1)
+      : c(c_), st(s), cls(k), bytes(by) {
+    c->launches += n_kernels;
+    if (c->timing && !c->capturing) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~TimedLaunch() {
+    if (a) {
+      cudaEventRecord(b, st);
+      c->trecs.push_back({cls, a, b, bytes});
+    }
+  }
+};
+
+static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* base, int K,
+                          int rows) {
+  for (int bn : {16, 32, 64, 128, 256}) {
+    CUtensorMap t;
+    if (!make_tmap_bf16(&t, base, K, rows, static_cast<uint64_t>(K) * 2, bn)) return false;
+    m[bn] = t;
+  }
+  return true;
+}
+
+// GEMM over `rows` activation rows of buffer map set `xm`.
+static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>& xm, int M,
+                    int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
+                    const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
+                    const char* cls = "gemm") {
+  const int bn = gemm_bn_for_rows(rows);
+  GemmArgs a{};
+  a.M = M;
+  a.N = rows;
+  a.K = K;
+  a.out = out;
+  a.ldo = ldo;
+  a.split_stride = static_cast<int64_t>(rows) * ldo;
+  a.bias = bias;
+  a.resid = resid;
+  a.ldr = ldr;
+  a.m_valid = m_valid;
+  const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
+                       static_cast<double>(rows) * m_valid * 4 * splits;
+  TimedLaunch tl(c, st, cls, bytes);
+  cudaError_t e = gemm_launch(tw, xm.at(bn), a, splits, bn, st);
+  if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
+  return VOX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// weights
+// ---------------------------------------------------------------------------
+static int init_bf16(VoxCtx* c, bf16* w, int64_t n, uint64_t tid, uint64_t layer, float scale) {
+  launch_init_bf16(w, n, tensor_key(c->seed, tid, layer), scale, c->s_lm);
+  CK(cudaGetLastError());
+  return VOX_OK;
+}
+static int init_f32(VoxCtx* c, float* w, int64_t n, uint64_t tid, uint64_t layer, float scale,
+                    float offset) {
+  launch_init_f32(w, n, tensor_key(c->seed, tid, layer), scale, offset, c->s_lm);
+  CK(cudaGetLastError());
+  return VOX_OK;
+}
+
+#define RET(x)                  \
+  do {                          \
+    int r_ = (x);               \
+    if (r_ != VOX_OK) return r_; \
+  } while (0)
+
+static int create_backbone(VoxCtx* c) {
+  const VoxModelCfg& g = c->cfg;
+  const int L = g.n_layers, d = g.d_model, hd = g.head_dim, H = g.n_heads, KV = g.n_kv_heads;
+  const int dff = g.d_ff, V = g.vocab;
+  c->nqkv = (H + 2 * KV) * hd;
+  const int64_t n_qkv = static_cast<int64_t>(c->nqkv) * d, n_o = static_cast<int64_t>(d) * H * hd;
+  const int64_t n_gu = static_cast<int64_t>(2) * dff * d, n_dn = static_cast<int64_t>(d) * dff;
+  CK(dalloc(&c->emb, static_cast<size_t>(V) * d));
+  CK(dalloc(&c->norm_attn, static_cast<size_t>(L) * d));
+  CK(dalloc(&c->norm_mlp, static_cast<size_t>(L) * d));
+  CK(dalloc(&c->norm_final, static_cast<size_t>(d)));
+  CK(dalloc(&c->w_qkv, static_cast<size_t>(L * n_qkv)));
+  CK(dalloc(&c->w_o, static_cast<size_t>(L * n_o)));
+  CK(dalloc(&c->w_gu, static_cast<size_t>(L * n_gu)));
+  CK(dalloc(&c->w_down, static_cast<size_t>(L * n_dn)));
+  RET(init_bf16(c, c->emb, static_cast<int64_t>(V) * d, T_EMB, 0, g.embed_scale));
+  for (int l = 0; l < L; ++l) {
+    RET(init_f32(c, c->norm_attn + static_cast<int64_t>(l) * d, d, T_NORM_ATTN, l, 0.25f, 1.0f));
+    RET(init_f32(c, c->norm_mlp + static_cast<int64_t>(l) * d, d, T_NORM_MLP, l, 0.25f, 1.0f));
+    RET(init_bf16(c, c->w_qkv + l * n_qkv, n_qkv, T_QKV, l, std::sqrt(3.0f / d)));
+    RET(init_bf16(c, c->w_o + l * n_o, n_o, T_O, l, std::sqrt(3.0f / (H * hd))));
+    RET(init_bf16(c, c->w_gu + l * n_gu, n_gu, T_GU, l, std::sqrt(3.0f / d)));
+    RET(init_bf16(c, c->w_down + l * n_dn, n_dn, T_DOWN, l, std::sqrt(3.0f / dff)));
+  }
+  RET(init_f32(c, c->norm_final, d, T_NORM_FINAL, 0, 0.25f, 1.0f));
+  // RoPE inverse frequencies, fp64 -> fp32 (oracle: identical table)
+  std::vector<float> inv(hd / 2);
+  for (int i = 0; i < hd / 2; ++i)
+    inv[i] = static_cast<float>(1.0 / std::pow(static_cast<double>(g.rope_theta),
+                                               (2.0 * i) / static_cast<double>(hd)));
+  CK(dalloc(&c->inv_freq, inv.size()));
+  CK(cudaMemcpy(c->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+
+  c->tm_qkv.resize(L);
+  c->tm_o.resize(L);
+  c->tm_gu.resize(L);
+  c->tm_down.resize(L);
+  for (int l = 0; l < L; ++l) {
+    bool ok = make_tmap_bf16(&c->tm_qkv[l], c->w_qkv + l * n_qkv, d, c->nqkv, d * 2ull, 128) &&
+              make_tmap_bf16(&c->tm_o[l], c->w_o + l * n_o, H * hd, d, H * hd * 2ull, 128) &&
+              make_tmap_bf16(&c->tm_gu[l], c->w_gu + l * n_gu, d, 2 * dff, d * 2ull, 128) &&
+              make_tmap_bf16(&c->tm_down[l], c->w_down + l * n_dn, dff, d, dff * 2ull, 128);
+    if (!ok) return fail(c, VOX_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
+  }
+  if (!make_tmap_bf16(&c->tm_head_full, c->emb, d, V, d * 2ull, 128))
+    return fail(c, VOX_ERR_CUDA, "tensor map (lm head)");
+  if (g.audio_base >= 0) {
+    c->head_audio_rows = g.frame_tokens * g.codebook_size;
+    if (!make_tmap_bf16(&c->tm_head_audio, c->emb + static_cast<int64_t>(g.audio_base) * d, d,
+                        c->head_audio_rows, d * 2ull, 128))
+      return fail(c, VOX_ERR_CUDA, "tensor map (audio head)");
+  }
+  return VOX_OK;
+}
+
+static int create_buffers(VoxCtx* c) {
+  const VoxModelCfg& g = c->cfg;
+  const int R = g.max_rows, d = g.d_model, dff = g.d_ff;
+  CK(dalloc(&c->h, static_cast<size_t>(R) * d));
+  CK(dalloc(&c->x, static_cast<size_t>(R) * d));
+  CK(dalloc(&c->xf, static_cast<size_t>(R) * d));
+  CK(dalloc(&c->q, static_cast<size_t>(R) * g.n_heads * g.head_dim));
+  CK(dalloc(&c->attn, static_cast<size_t>(R) * g.n_heads * g.head_dim));
+  CK(dalloc(&c->act, static_cast<size_t>(R) * dff));
+  CK(cudaMemset(c->x, 0, static_cast<size_t>(R) * d * 2));
+  CK(cudaMemset(c->xf, 0, static_cast<size_t>(R) * d * 2));
+  CK(cudaMemset(c->attn, 0, static_cast<size_t>(R) * g.n_heads * g.head_dim * 2));
+  CK(cudaMemset(c->act, 0, static_cast<size_t>(R) * dff * 2));
+  // split-K workspace: worst case splits * rows * max(N)
+  const int maxN = std::max({c->nqkv, d, 2 * dff});
+  c->ws_elems = static_cast<size_t>(16) * R * maxN;
+  CK(dalloc(&c->ws, c->ws_elems));
+  const int head_cols = g.audio_base >= 0 ? c->head_audio_rows : g.vocab;
+  const int full_rows = std::min(R, 256);
+  c->logits_elems = std::max(static_cast<size_t>(R) * head_cols,
+                             static_cast<size_t>(full_rows) * g.vocab);
+  CK(dalloc(&c->logits, c->logits_elems));
+  if (!make_act_maps(c, c->tm_x, c->x, d, R) || !make_act_maps(c, c->tm_xf, c->xf, d, R) ||
+      !make_act_maps(c, c->tm_attn, c->attn, g.n_heads * g.head_dim, R) ||
+      !make_act_maps(c, c->tm_act, c->act, dff, R))
+    return fail(c, VOX_ERR_CUDA, "tensor map (activations)");
+
+  // KV pool
+  c->max_pages_per_slot = (g.max_ctx + g.page_size - 1) / g.page_size;
+  const size_t kv_elems = static_cast<size_t>(g.n_layers) * g.n_pages * g.n_kv_heads *
+                          g.page_size * g.head_dim;
+  CK(dalloc(&c->kc, kv_elems));
+  CK(dalloc(&c->vc, kv_elems));
+  CK(cudaMemset(c->kc, 0, kv_elems * 2));
+  CK(cudaMemset(c->vc, 0, kv_elems * 2));
+  CK(dalloc(&c->token_store, static_cast<size_t>(g.max_slots) * g.max_ctx));
+  CK(cudaMemset(c->token_store, 0, static_cast<size_t>(g.max_slots) * g.max_ctx * 4));
+  CK(dalloc(&c->page_table, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot));
+  CK(cudaMemset(c->page_table, 0, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot * 4));
+  CK(dalloc(&c->slot_prompt, static_cast<size_t>(g.max_slots)));
+  CK(dalloc(&c->slot_seed, static_cast<size_t>(g.max_slots)));
+  CK(dalloc(&c->slot_params, static_cast<size_t>(g.max_slots)));
+  c->free_pages.clear();
+  for (int p = g.n_pages - 1; p >= 0; --p) c->free_pages.push_back(p);  // pop -> 0,1,2..
+  c->slot_pages.assign(g.max_slots, {});
+  c->slot_used.assign(g.max_slots, 0);
+  c->h_prompt.assign(g.max_slots, 0);
+  c->h_target.assign(g.max_slots, 0);
+  c->slot_chunks.assign(g.max_slots, 0);
+  c->slot_covered.assign(g.max_slots, 0);
+  c->slot_last_fwd.assign(g.max_slots, -1);
+  c->h_seed.assign(g.max_slots, 0);
+
+  CK(dalloc(&c->d_rows, static_cast<size_t>(R)));
+  CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
+  CK(dalloc(&c->d_out_index, static_cast<size_t>(R)));
+  CK(dalloc(&c->d_tokens, static_cast<size_t>(R)));
+  CK(dalloc(&c->d_err, 1));
+  CK(cudaMemset(c->d_err, 0, 4));
+  c->stages.resize(8);
+  for (auto& s : c->stages) {
+    CK(cudaHostAlloc(&s.rows, sizeof(RowDev) * R, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&s.sample_rows, sizeof(int) * R, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&s.out_index, sizeof(int) * R, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&s.tokens, sizeof(int) * R, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&s.err, sizeof(int), cudaHostAllocDefault));
+    *s.err = 0;
+    CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+  }
+  c->fwd_events.resize(64);
+  c->fwd_event_seq.assign(64, -1);
+  for (auto& e : c->fwd_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return VOX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// detokenizer weights + state layout
+// ---------------------------------------------------------------------------
+static int create_detok(VoxCtx* c) {
+  const VoxModelCfg& g = c->cfg;
+  DetokDims& dd = c->dd;
+  DetokW& w = c->dw;
+  dd.latent = g.latent_dim;
+  dd.dec = g.decoder_dim;
+  dd.n_rates = g.n_rates;
+  for (int b = 0; b < 4; ++b) dd.rates[b] = g.rates[b];
+  dd.ch[0] = g.decoder_dim;
+  for (int b = 0; b < 4; ++b) dd.ch[b + 1] = dd.ch[b] / 2;
+  dd.cb_size = g.codebook_size;
+  dd.frame_tokens = g.frame_tokens;
+  dd.audio_base = g.audio_base;
+  dd.max_ctx = g.max_ctx;
+  // state layout (floats): in-dwconv history 6*latent; per block: 1 frame of
+  // Cin (transposed conv), RU histories 6*d*Cout for d in {1,3,9}; out 6*C4
+  int64_t off = 0;
+  dd.off_in = off;
+  off += 6LL * dd.latent;
+  const int dils[3] = {1, 3, 9};
+  for (int b = 0; b < 4; ++b) {
+    dd.off_up[b] = off;
+    off += dd.ch[b];
+    for (int u = 0; u < 3; ++u) {
+      dd.off_ru[b][u] = off;
+      off += 6LL * dils[u] * dd.ch[b + 1];
+    }
+  }
+  dd.off_out = off;
+  off += 6LL * dd.ch[4];
+  dd.state_floats = (off + 63) / 64 * 64;
+  CK(dalloc(&c->dstate, static_cast<size_t>(g.max_slots) * 2 * dd.state_floats));
+  CK(cudaMemset(c->dstate, 0, static_cast<size_t>(g.max_slots) * 2 * dd.state_floats * 4));
+
+  const int L = dd.latent, D0 = dd.dec, cb = dd.cb_size;
+  CK(dalloc(&w.tabs, static_cast<size_t>(3) * cb * L));
+  RET(init_bf16(c, w.tabs, 3LL * cb * L, T_VQ_TAB, 0, 0.866f));
+  CK(dalloc(&w.in_dw_w, static_cast<size_t>(L) * 7));
+  CK(dalloc(&w.in_dw_b, static_cast<size_t>(L)));
+  RET(init_f32(c, w.in_dw_w, 7LL * L, T_IN_DW_W, 0, std::sqrt(3.0f / 7.0f), 0.f));
+  RET(init_f32(c, w.in_dw_b, L, T_IN_DW_B, 0, 0.05f, 0.f));
+  CK(dalloc(&w.in_pw_w, static_cast<size_t>(D0) * L));
+  CK(dalloc(&w.in_pw_b, static_cast<size_t>(D0)));
+  RET(init_bf16(c, w.in_pw_w, static_cast<int64_t>(D0) * L, T_IN_PW_W, 0, std::sqrt(3.0f / L)));
+  RET(init_f32(c, w.in_pw_b, D0, T_IN_PW_B, 0, 0.05f, 0.f));
+  if (!make_tmap_bf16(&w.tm_in_pw, w.in_pw_w, L, D0, L * 2ull, 128))
+    return fail(c, VOX_ERR_CUDA, "tmap detok in");
+  for (int b = 0; b < 4; ++b) {
+    const int Ci = dd.ch[b], Co = dd.ch[b + 1], s = dd.rates[b];
+    CK(dalloc(&w.up_alpha[b], static_cast<size_t>(Ci)));
+    RET(init_f32(c, w.up_alpha[b], Ci, T_UP_ALPHA + b, 0, 0.5f, 1.0f));
+    CK(dalloc(&w.up_w[b], static_cast<size_t>(s) * Co * 2 * Ci));
+    RET(init_bf16(c, w.up_w[b], static_cast<int64_t>(s) * Co * 2 * Ci, T_UP_W + b, 0,
+                  std::sqrt(3.0f / (2.0f * Ci))));
+    std::vector<float> bias_small(Co), bias_ext(static_cast<size_t>(s) * Co);
+    float* tmp;
+    CK(dalloc(&tmp, static_cast<size_t>(Co)));
+    RET(init_f32(c, tmp, Co, T_UP_B + b, 0, 0.05f, 0.f));
+    CK(cudaMemcpy(bias_small.data(), tmp, Co * 4, cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+    for (int j = 0; j < s; ++j)
+      for (int o = 0; o < Co; ++o) bias_ext[static_cast<size_t>(j) * Co + o] = bias_small[o];
+    CK(dalloc(&w.up_b[b], bias_ext.size()));
+    CK(cudaMemcpy(w.up_b[b], bias_ext.data(), bias_ext.size() * 4, cudaMemcpyHostToDevice));
+    if (!make_tmap_bf16(&w.tm_up[b], w.up_w[b], 2 * Ci, static_cast<uint64_t>(s) * Co,
+                        2ull * Ci * 2, 128))
+      return fail(c, VOX_ERR_CUDA, "tmap detok up");
+    for (int u = 0; u < 3; ++u) {
+      const uint64_t li = static_cast<uint64_t>(b * 3 + u);
+      CK(dalloc(&w.ru_a1[b][u], static_cast<size_t>(Co)));
+      CK(dalloc(&w.ru_a2[b][u], static_cast<size_t>(Co)));
+      CK(dalloc(&w.ru_dw_w[b][u], static_cast<size_t>(Co) * 7));
+      CK(dalloc(&w.ru_dw_b[b][u], static_cast<size_t>(Co)));
+      CK(dalloc(&w.ru_pw_w[b][u], static_cast<size_t>(Co) * Co));
+      CK(dalloc(&w.ru_pw_b[b][u], static_cast<size_t>(Co)));
+      RET(init_f32(c, w.ru_a1[b][u], Co, T_RU_A1, li, 0.5f, 1.0f));
+      RET(init_f32(c, w.ru_a2[b][u], Co, T_RU_A2, li, 0.5f, 1.0f));
+      RET(init_f32(c, w.ru_dw_w[b][u], 7LL * Co, T_RU_DW_W, li, std::sqrt(3.0f / 7.0f), 0.f));
+      RET(init_f32(c, w.ru_dw_b[b][u], Co, T_RU_DW_B, li, 0.05f, 0.f));
+      RET(init_bf16(c, w.ru_pw_w[b][u], static_cast<int64_t>(Co) * Co, T_RU_PW_W, li,
+                    0.5f * std::sqrt(3.0f / Co)));
+      RET(init_f32(c, w.ru_pw_b[b][u], Co, T_RU_PW_B, li, 0.05f, 0.f));
+      if (!make_tmap_bf16(&w.tm_ru[b][u], w.ru_pw_w[b][u], Co, Co, Co * 2ull, 128))
+        return fail(c, VOX_ERR_CUDA, "tmap detok ru");
+    }
+  }
+  const int C4 = dd.ch[4];
+  CK(dalloc(&w.out_alpha, static_cast<size_t>(C4)));
+  CK(dalloc(&w.out_w, static_cast<size_t>(C4) * 7));
+  RET(init_f32(c, w.out_alpha, C4, T_OUT_ALPHA, 0, 0.5f, 1.0f));
+  RET(init_f32(c, w.out_w, 7LL * C4, T_OUT_W, 0, std::sqrt(3.0f / (7.0f * C4)), 0.f));
+  {
+    float* tmp;
+    CK(dalloc(&tmp, 1));
+    RET(init_f32(c, tmp, 1, T_OUT_B, 0, 0.05f, 0.f));
+    CK(cudaMemcpy(&w.out_b, tmp, 4, cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+  }
+  // activation buffers sized by the largest level: rows*channels
+  const int64_t F = g.max_detok_frames;
+  int64_t mx = F * D0;
+  int64_t mbf = F * L;
+  int up = 1;
+  for (int b = 0; b < 4; ++b) {
+    mbf = std::max<int64_t>(mbf, F * up * 2 * dd.ch[b]);  // upcat operand
+    up *= dd.rates[b];
+    mx = std::max<int64_t>(mx, F * up * dd.ch[b + 1]);
+    mbf = std::max<int64_t>(mbf, F * up * dd.ch[b + 1]);
+  }
+  c->dx_elems = static_cast<size_t>(mx);
+  c->dbf_elems = static_cast<size_t>(mbf);
+  CK(dalloc(&c->dx, c->dx_elems));
+  CK(dalloc(&c->dy, c->dx_elems));
+  CK(dalloc(&c->dbf, c->dbf_elems));
+  CK(cudaMemset(c->dbf, 0, c->dbf_elems * 2));
+  const size_t stage_bytes = 8 + sizeof(DetokReq) * (F / 4 + 8);
+  CK(dalloc(&c->d_dstage, stage_bytes));
+  c->pcm_cap = static_cast<size_t>(F) * up;
+  CK(dalloc(&c->d_pcm, c->pcm_cap));
+  c->tickets.resize(8);
+  for (auto& t : c->tickets) {
+    CK(cudaEventCreate(&t.ev));
+    CK(cudaHostAlloc(&t.pcm_host, c->pcm_cap * 4, cudaHostAllocDefault));
+    CK(cudaHostAlloc(&t.stage_host, stage_bytes, cudaHostAllocDefault));
+  }
+  return VOX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the decode step (eager or captured)
+// ---------------------------------------------------------------------------
+static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
+  const VoxModelCfg& g = c->cfg;
+  const LmDims& dm = c->dm;
+  cudaStream_t st = c->s_lm;
+  const int L = g.n_layers, d = g.d_model, dff = g.d_ff, Hhd = g.n_heads * g.head_dim;
+  {
+    TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * 8);
+    launch_embed_norm(c->d_rows, nrows, c->token_store, g.max_ctx, c->emb, c->norm_attn, dm, c->h,
+                      c->x, st);
+  }
+  const int sp_qkv = gemm_pick_splits(c->nqkv, nrows, d, 16);
+  const int sp_o = gemm_pick_splits(d, nrows, Hhd, 16);
+  const int sp_gu = gemm_pick_splits(2 * dff, nrows, d, 16);
+  const int sp_dn = gemm_pick_splits(d, nrows, dff, 16);
+  const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
+  for (int l = 0; l < L; ++l) {
+    RET(run_gemm(c, c->tm_qkv[l], c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
+                 nullptr, 0, c->nqkv, st));
+    {
+      TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * sp_qkv);
+      launch_qkv_rope_append(c->d_rows, nrows, c->ws, sp_qkv,
+                             static_cast<int64_t>(nrows) * c->nqkv, dm, c->inv_freq,
+                             c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
+    }
+    {
+      TimedLaunch tl(c, st, "attn", c->step_attn_bytes);
+      launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
+                         c->page_table, dm, c->attn, st);
+    }
+    RET(run_gemm(c, c->tm_o[l], c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
+                 st));
+    {
+      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_o + 10));
+      launch_resid_norm(c->d_rows, nrows, c->ws, sp_o, static_cast<int64_t>(nrows) * d, dm, c->h,
+                        c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
+    }
+    RET(run_gemm(c, c->tm_gu[l], c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
+                 nullptr, 0, 2 * dff, st));
+    {
+      TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
+      launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
+                      c->act, st);
+    }
+    RET(run_gemm(c, c->tm_down[l], c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
+                 d, st));
+    {
+      const bool last = (l == L - 1);
+      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_dn + 10));
+      launch_resid_norm(c->d_rows, nrows, c->ws, sp_dn, static_cast<int64_t>(nrows) * d, dm, c->h,
+                        last ? c->norm_final : c->norm_attn + static_cast<int64_t>(l + 1) * d,
+                        last ? c->xf : c->x, last ? c->d_out_index : nullptr, st);
+    }
+  }
+  if (nsamp > 0) {
+    const bool audio = (g.audio_base >= 0) && !full_logits;
+    const int M = audio ? c->head_audio_rows : g.vocab;
+    RET(run_gemm(c, audio ? c->tm_head_audio : c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits,
+                 M, 1, nullptr, nullptr, 0, M, st, "lm_head"));
+    SampFusedArgs a{};
+    a.rows = c->d_rows;
+    a.sample_rows = c->d_sample_rows;
+    a.n_sample = nsamp;
+    a.logits = c->logits;
+    a.ld = M;
+    a.col_base = audio ? g.audio_base : 0;
+    a.token_store = c->token_store;
+    a.max_ctx = g.max_ctx;
+    a.slot_prompt_len = c->slot_prompt;
+    a.slot_seed = c->slot_seed;
+    a.slot_params = c->slot_params;
+    a.audio_base = g.audio_base;
+    a.codebook_size = g.codebook_size;
+    a.frame_tokens = g.frame_tokens;
+    a.vocab = g.vocab;
+    a.tokens_out = c->d_tokens;
+    a.err_flag = c->d_err;
+    {
+      const int span = g.audio_base >= 0 ? g.codebook_size : g.vocab;
+      TimedLaunch tl(c, st, "sampler", static_cast<double>(nsamp) * span * 4);
+      launch_sample_fused(a, st);
+    }
+  }
+  CK(cudaGetLastError());
+  return VOX_OK;
+}
+
+static int check_err_value(VoxCtx* c, int e) {
+  if (e == 0) return VOX_OK;
+  cudaMemsetAsync(c->d_err, 0, 4, c->s_lm);
+  if (e == VOX_ERR_NONFINITE) return fail(c, e, "logits must not contain NaN or +inf");
+  if (e == VOX_ERR_DEGENERATE) return fail(c, e, "all logits are -inf after truncation");
+  return fail(c, e, "device error flag " + std::to_string(e));
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int vox_abi_version(void) { return VOX_ABI_VERSION; }
+
+const char* vox_last_error(const VoxCtx* ctx) {
+  if (ctx) return ctx->err.c_str();
+  return g_err.c_str();
+}
+
+static int validate_cfg(const VoxModelCfg* g) {
+  if (g->n_layers < 1 || g->d_model % 64 || g->d_ff % 64 || g->head_dim % 2) return 0;
+  if (!(g->head_dim == 64 || g->head_dim == 128)) return 0;
+  if (g->n_heads % g->n_kv_heads) return 0;
+  const int grp = g->n_heads / g->n_kv_heads;
+  if (grp < 1 || grp > 4) return 0;
+  if ((g->n_heads * g->head_dim) % 64) return 0;
+  if (g->page_size % 4 || g->max_rows < 1 || g->max_rows > 2048) return 0;
+  if (g->max_slots < 1 || g->n_pages < 1 || g->max_ctx < 2) return 0;
+  if (g->detok_enabled) {
+    if (g->audio_base < 0 || g->n_rates != 4 || g->latent_dim % 64 || g->decoder_dim % 1024)
+      return 0;
+    if (g->max_detok_frames < 4) return 0;
+  }
+  return 1;
+}
+
+int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx** out) {
+  VoxCtx* c = nullptr;
+  if (!cfg || !out) return fail(nullptr, VOX_ERR_INVALID, "null argument");
+  if (!validate_cfg(cfg)) return fail(nullptr, VOX_ERR_INVALID, "invalid VoxModelCfg");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device >= ndev)
+    return fail(nullptr, VOX_ERR_NO_DEVICE, "no CUDA device");
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10) return fail(nullptr, VOX_ERR_NO_DEVICE, "needs an sm_100 (B200) device");
+  c = new VoxCtx();
+  c->device = device;
+  c->cfg = *cfg;
+  c->seed = weight_seed;
+  CK(cudaSetDevice(device));
+  CK(cudaStreamCreateWithFlags(&c->s_lm, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->s_dt, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->epoch));
+  c->dm.d = cfg->d_model;
+  c->dm.n_heads = cfg->n_heads;
+  c->dm.n_kv = cfg->n_kv_heads;
+  c->dm.hd = cfg->head_dim;
+  c->dm.dff = cfg->d_ff;
+  c->dm.vocab = cfg->vocab;
+  c->dm.eps = cfg->rms_eps;
+  c->dm.page_size = cfg->page_size;
+  c->dm.max_ctx = cfg->max_ctx;
+  c->dm.n_pages = cfg->n_pages;
+  int r = create_backbone(c);
+  if (r == VOX_OK) r = create_buffers(c);
+  c->dm.max_pages_per_slot = c->max_pages_per_slot;
+  if (r == VOX_OK && cfg->detok_enabled) r = create_detok(c);
+  if (r == VOX_OK) {
+    cudaError_t e = cudaStreamSynchronize(c->s_lm);
+    if (e != cudaSuccess) r = fail(c, VOX_ERR_CUDA, cudaGetErrorString(e));
+  }
+  if (r != VOX_OK) {
+    std::string m = c->err;
+    vox_destroy(c);
+    return fail(nullptr, r, m);
+  }
+  CK(cudaEventRecord(c->epoch, c->s_lm));
+  *out = c;
+  return VOX_OK;
+}
+
+void vox_destroy(VoxCtx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& t : c->tickets) {
+    if (t.ev) cudaEventDestroy(t.ev);
+    if (t.pcm_host) cudaFreeHost(t.pcm_host);
+    if (t.stage_host) cudaFreeHost(t.stage_host);
+  }
+  for (auto& e : c->fwd_events) cudaEventDestroy(e);
+  for (auto& t : c->trecs) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  void* dev_ptrs[] = {c->emb, c->norm_attn, c->norm_mlp, c->norm_final, c->w_qkv, c->w_o,
+                      c->w_gu, c->w_down, c->inv_freq, c->h, c->x, c->xf, c->q, c->attn, c->act,
+                      c->ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
+                      c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->d_sample_rows,
+                      c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
+                      c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
+                      c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w};
+  for (void* p : dev_ptrs)
+    if (p) cudaFree(p);
+  if (c->cfg.detok_enabled && c->dw.tabs) {
+    for (int b = 0; b < 4; ++b) {
+      cudaFree(c->dw.up_alpha[b]);
+      cudaFree(c->dw.up_w[b]);
+      cudaFree(c->dw.up_b[b]);
+      for (int u = 0; u < 3; ++u) {
+        cudaFree(c->dw.ru_a1[b][u]);
+        cudaFree(c->dw.ru_a2[b][u]);
+        cudaFree(c->dw.ru_dw_w[b][u]);
+        cudaFree(c->dw.ru_dw_b[b][u]);
+        cudaFree(c->dw.ru_pw_w[b][u]);
+        cudaFree(c->dw.ru_pw_b[b][u]);
+      }
+    }
+  }
+  for (auto& s : c->stages) {
+    void* host_ptrs[] = {s.rows, s.sample_rows, s.out_index, s.tokens, s.err};
+    for (void* p : host_ptrs)
+      if (p) cudaFreeHost(p);
+    if (s.ev) cudaEventDestroy(s.ev);
+  }
+  if (c->s_lm) cudaStreamDestroy(c->s_lm);
+  if (c->s_dt) cudaStreamDestroy(c->s_dt);
+  if (c->epoch) cudaEventDestroy(c->epoch);
+  delete c;
+}
+
+// synthetic prompt id i of a request (oracle/workload.py: prompt_ids)
+static int prompt_id(uint64_t req_seed, int i, int text_vocab) {
+  return static_cast<int>(mix64(req_seed + 0x632BE59BD9B4E019ull * static_cast<uint64_t>(i + 1)) %
+                          static_cast<uint64_t>(text_vocab));
+}
+
+int vox_admit(VoxCtx* c, uint64_t req_seed, int32_t prompt_len, int32_t target_len,
+              const VoxSampling* params, int32_t* slot_out) {
+  if (!c || !params || !slot_out) return fail(c, VOX_ERR_INVALID, "null argument");
+  const VoxModelCfg& g = c->cfg;
+  if (prompt_len < 1) return fail(c, VOX_ERR_INVALID_TOKEN_COUNT, "prompt_tokens must be >= 1");
+  if (target_len < 1)
+    return fail(c, VOX_ERR_INVALID_TOKEN_COUNT, "target_output_tokens must be >= 1");
+  if (prompt_len + target_len > g.max_ctx)
+    return fail(c, VOX_ERR_PROMPT_TOO_LONG, "prompt + target exceeds the context capacity");
+  if (params->penalty_window < 0 || params->penalty_window > 256)
+    return fail(c, VOX_ERR_INVALID, "penalty_window must be in [0, 256]");
+  int slot = -1;
+  for (int s = 0; s < g.max_slots; ++s)
+    if (!c->slot_used[s]) {
+      slot = s;
+      break;
+    }
+  if (slot < 0) return fail(c, VOX_ERR_OUT_OF_MEMORY, "no free request slot");
+  const int need = (prompt_len + target_len + g.page_size - 1) / g.page_size;
+  if (need > static_cast<int>(c->free_pages.size()))
+    return fail(c, VOX_ERR_OUT_OF_MEMORY, "KV page pool exhausted");
+  std::vector<int> pages(need);
+  for (int i = 0; i < need; ++i) {
+    pages[i] = c->free_pages.back();
+    c->free_pages.pop_back();
+  }
+  std::vector<int> pt(c->max_pages_per_slot, 0);
+  std::copy(pages.begin(), pages.end(), pt.begin());
+  std::vector<int> prompt(prompt_len);
+  for (int i = 0; i < prompt_len; ++i) prompt[i] = prompt_id(req_seed, i, g.text_vocab);
+  cudaStream_t st = c->s_lm;
+  CK(cudaMemcpyAsync(c->page_table + static_cast<int64_t>(slot) * c->max_pages_per_slot,
+                     pt.data(), pt.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->token_store + static_cast<int64_t>(slot) * g.max_ctx, prompt.data(),
+                     prompt.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->slot_prompt + slot, &prompt_len, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->slot_seed + slot, &req_seed, 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->slot_params + slot, params, sizeof(VoxSampling), cudaMemcpyHostToDevice,
+                     st));
+  if (g.detok_enabled)
+    CK(cudaMemsetAsync(c->dstate + static_cast<int64_t>(slot) * 2 * c->dd.state_floats, 0,
+                       sizeof(float) * 2 * c->dd.state_floats, st));
+  CK(cudaStreamSynchronize(st));  // pageable sources
+  c->slot_used[slot] = 1;
+  c->slot_pages[slot] = pages;
+  c->h_prompt[slot] = prompt_len;
+  c->h_target[slot] = target_len;
+  c->slot_chunks[slot] = 0;
+  c->slot_covered[slot] = 0;
+  c->slot_last_fwd[slot] = -1;
+  c->h_seed[slot] = req_seed;
+  *slot_out = slot;
+  return VOX_OK;
+}
+
+int vox_release(VoxCtx* c, int32_t slot) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
+    return fail(c, VOX_ERR_CACHE_MISSING, "release of an unknown slot");
+  auto& pages = c->slot_pages[slot];
+  for (int i = static_cast<int>(pages.size()) - 1; i >= 0; --i) c->free_pages.push_back(pages[i]);
+  pages.clear();
+  c->slot_used[slot] = 0;
+  return VOX_OK;
+}
+
+int vox_page_table(VoxCtx* c, int32_t slot, int32_t* out, int32_t cap, int32_t* n_out) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
+    return fail(c, VOX_ERR_CACHE_MISSING, "unknown slot");
+  const auto& pages = c->slot_pages[slot];
+  const int n = static_cast<int>(pages.size());
+  std::vector<int> dev(c->max_pages_per_slot);
+  CK(cudaMemcpy(dev.data(), c->page_table + static_cast<int64_t>(slot) * c->max_pages_per_slot,
+                dev.size() * 4, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i)
+    if (dev[i] != pages[i]) return fail(c, VOX_ERR_CUDA, "device page table diverged from host");
+  for (int i = 0; i < n && i < cap; ++i) out[i] = dev[i];
+  if (n_out) *n_out = n;
+  return VOX_OK;
+}
+
+int vox_read_tokens(VoxCtx* c, int32_t slot, int32_t pos, int32_t n, int32_t* out) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || pos < 0 || n < 0 || pos + n > c->cfg.max_ctx)
+    return fail(c, VOX_ERR_INVALID, "bad token range");
+  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaMemcpy(out, c->token_store + static_cast<int64_t>(slot) * c->cfg.max_ctx + pos,
+                static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost));
+  return VOX_OK;
+}
+
+int vox_write_tokens(VoxCtx* c, int32_t slot, int32_t pos, int32_t n, const int32_t* ids) {
+  if (!c || !ids || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot] || pos < 0 ||
+      n < 0 || pos + n > c->cfg.max_ctx)
+    return fail(c, VOX_ERR_INVALID, "bad token range");
+  for (int i = 0; i < n; ++i)
+    if (ids[i] < 0 || ids[i] >= c->cfg.vocab) return fail(c, VOX_ERR_INVALID, "token id outside vocab");
+  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaMemcpy(c->token_store + static_cast<int64_t>(slot) * c->cfg.max_ctx + pos, ids,
+                static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
+  return VOX_OK;
+}
+
+int vox_slot_info(VoxCtx* c, int32_t slot, int32_t* prompt_len, int32_t* target_len) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
+    return fail(c, VOX_ERR_CACHE_MISSING, "unknown slot");
+  if (prompt_len) *prompt_len = c->h_prompt[slot];
+  if (target_len) *target_len = c->h_target[slot];
+  return VOX_OK;
+}
+
+int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float* logits_out,
+                int32_t* tokens_out) {
+  if (!c || (!rows && n > 0)) return fail(c, VOX_ERR_INVALID, "null argument");
+  const VoxModelCfg& g = c->cfg;
+  if (n <= 0) return fail(c, VOX_ERR_EMPTY_BATCH, "empty batch");
+  if (n > g.max_rows) return fail(c, VOX_ERR_BATCH_TOO_LARGE, "batch exceeds max_rows");
+  const bool want_logits = logits_out != nullptr;
+  const bool full = (flags & VOX_FWD_FULL_LOGITS) != 0 || want_logits;
+  if (want_logits && !(flags & VOX_FWD_FULL_LOGITS))
+    return fail(c, VOX_ERR_INVALID, "logits_out requires VOX_FWD_FULL_LOGITS");
+  int nsamp = 0;
+  for (int i = 0; i < n; ++i) {
+    const VoxRow& r = rows[i];
+    if (r.slot < 0 || r.slot >= g.max_slots || !c->slot_used[r.slot])
+      return fail(c, VOX_ERR_CACHE_MISSING, "row references an unknown slot");
+    const int cap = static_cast<int>(c->slot_pages[r.slot].size()) * g.page_size;
+    if (r.pos < 0 || r.pos + 1 >= g.max_ctx || r.pos >= cap)
+      return fail(c, VOX_ERR_INVALID, "row position outside the reserved KV range");
+    if (r.token >= g.vocab) return fail(c, VOX_ERR_INVALID, "token id outside the vocabulary");
+    if (r.sample) {
+      if (r.pos + 1 < c->h_prompt[r.slot])
+        return fail(c, VOX_ERR_INVALID, "sampling row inside the prompt");
+      ++nsamp;
+    }
+  }
+  if (full && nsamp > std::min(g.max_rows, 256))
+    return fail(c, VOX_ERR_BATCH_TOO_LARGE, "full-vocab logits limited to 256 rows");
+  int nrows = full ? n : bucket_of(n);
+  if (nrows < 0 || nrows > g.max_rows) nrows = n;  // no bucket fits: exact size
+  int ns = nsamp == 0 ? 0 : (full ? nsamp : bucket_of(nsamp));
+  if (ns < 0 || ns > nrows) ns = nsamp;
+  // pinned staging ring entry (wait for its previous user)
+  FwdStage& sg = c->stages[static_cast<size_t>(c->stage_seq++ % static_cast<int64_t>(c->stages.size()))];
+  if (sg.in_flight) {
+    CK(cudaEventSynchronize(sg.ev));
+    sg.in_flight = false;
+    if (*sg.err) {
+      const int e = *sg.err;
+      *sg.err = 0;
+      return check_err_value(c, e);
+    }
+  }
+  int k = 0;
+  double attn_bytes = 0;
+  for (int i = 0; i < nrows; ++i) {
+    if (i < n) {
+      sg.rows[i] = RowDev{rows[i].slot, rows[i].pos, rows[i].token, rows[i].sample};
+      attn_bytes += static_cast<double>(rows[i].pos + 1) * g.n_kv_heads * g.head_dim * 4;
+      if (rows[i].sample) {
+        sg.sample_rows[k] = i;
+        sg.out_index[i] = k++;
+      } else {
+        sg.out_index[i] = -1;
+      }
+    } else {
+      sg.rows[i] = RowDev{-1, 0, -1, 0};
+      sg.out_index[i] = -1;
+    }
+  }
+  for (int j = k; j < ns; ++j) sg.sample_rows[j] = -1;  // sampler skips padding
+  c->step_attn_bytes = attn_bytes;
+  cudaStream_t st = c->s_lm;
+  CK(cudaMemcpyAsync(c->d_rows, sg.rows, sizeof(RowDev) * nrows, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->d_out_index, sg.out_index, sizeof(int) * nrows, cudaMemcpyHostToDevice,
+                     st));
+  if (ns > 0)
+    CK(cudaMemcpyAsync(c->d_sample_rows, sg.sample_rows, sizeof(int) * ns,
+                       cudaMemcpyHostToDevice, st));
+  const bool use_graph = !(flags & VOX_FWD_NO_GRAPH) && !full && !c->timing;
+  int rc = VOX_OK;
+  if (use_graph) {
+    auto key = std::make_pair(nrows, ns);
+    auto it = c->graphs.find(key);
+    if (it == c->graphs.end()) {
+      // eager pass (executes this step and sets kernel attributes), then capture
+      rc = enqueue_forward(c, nrows, ns, false);
+      if (rc != VOX_OK) return rc;
+      CK(cudaStreamSynchronize(st));
+      const int64_t before = c->launches;
+      cudaGraph_t graph;
+      c->capturing = true;
+      CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_forward(c, nrows, ns, false);
+      cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      c->capturing = false;
+      if (rc != VOX_OK) return rc;
+      CK(ce);
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, graph, 0));
+      cudaGraphDestroy(graph);
+      c->graph_launches[key] = c->launches - before;
+      c->launches = before + c->graph_launches[key];  // the eager pass counted once
+      c->graphs[key] = ex;
+    } else {
+      CK(cudaGraphLaunch(it->second, st));
+      c->launches += c->graph_launches[key];
+    }
+  } else {
+    rc = enqueue_forward(c, nrows, ns, full);
+    if (rc != VOX_OK) return rc;
+  }
+  if (nsamp > 0)
+    CK(cudaMemcpyAsync(sg.tokens, c->d_tokens, sizeof(int) * nsamp, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(sg.err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(sg.ev, st));
+  sg.in_flight = true;
+  const int64_t seq = ++c->fwd_seq;
+  const int ei = static_cast<int>(seq % static_cast<int64_t>(c->fwd_events.size()));
+  CK(cudaEventRecord(c->fwd_events[ei], st));
+  c->fwd_event_seq[ei] = seq;
+  for (int i = 0; i < n; ++i)
+    if (rows[i].sample) c->slot_last_fwd[rows[i].slot] = seq;
+
+  const bool sync = (flags & VOX_FWD_SYNC) || tokens_out || logits_out;
+  if (sync) {
+    CK(cudaEventSynchronize(sg.ev));
+    sg.in_flight = false;
+    const int e = *sg.err;
+    *sg.err = 0;
+    rc = check_err_value(c, e);
+    if (rc != VOX_OK) return rc;
+    if (tokens_out)
+      for (int j = 0; j < nsamp; ++j) tokens_out[j] = sg.tokens[j];
+    if (logits_out)
+      CK(cudaMemcpy(logits_out, c->logits, sizeof(float) * static_cast<size_t>(nsamp) * g.vocab,
+                    cudaMemcpyDeviceToHost));
+  }
+  return VOX_OK;
+}
+
+int vox_sample_logits(VoxCtx* c, const float* logits, int32_t n, int32_t vocab,
+                      const VoxSampling* params, const int32_t* window_ids, int32_t wcap,
+                      const int32_t* window_len, const uint64_t* seeds, const uint64_t* steps,
+                      const int32_t* lo, const int32_t* hi, int32_t* tokens_out) {
+  if (!c || !logits || !params || !seeds || !steps || !tokens_out)
+    return fail(c, VOX_ERR_INVALID, "null argument");
+  if (n <= 0) return fail(c, VOX_ERR_EMPTY_BATCH, "empty batch");
+  if (wcap < 0 || wcap > 256) return fail(c, VOX_ERR_INVALID, "window capacity must be <= 256");
+  float* d_log = nullptr;
+  SampRowDesc* d_desc = nullptr;
+  int *d_win = nullptr, *d_out = nullptr;
+  std::vector<SampRowDesc> desc(n);
+  int max_span = 1;
+  for (int i = 0; i < n; ++i) {
+    SampRowDesc& s = desc[i];
+    s.logit_off = static_cast<int64_t>(i) * vocab;
+    s.col_base = 0;
+    s.lo = lo ? lo[i] : 0;
+    s.hi = hi ? hi[i] : vocab;
+    if (s.lo < 0 || s.hi > vocab || s.lo >= s.hi)
+      return fail(c, VOX_ERR_INVALID, "bad candidate range");
+    s.wlen = window_len ? std::min(window_len[i], wcap) : 0;
+    s.woff = i * wcap;
+    s.out_index = i;
+    s.seed = seeds[i];
+    s.step = steps[i];
+    s.params = params[i];
+    if (s.params.temperature < 0 || s.params.top_p <= 0 || s.params.top_p > 1 ||
+        s.params.repetition_penalty < 1 || s.params.top_k < 0)
+      return fail(c, VOX_ERR_INVALID, "invalid sampling parameters");
+    max_span = std::max(max_span, s.hi - s.lo);
+  }
+  cudaStream_t st = c->s_lm;
+  CK(dalloc(&d_log, static_cast<size_t>(n) * vocab));
+  CK(dalloc(&d_desc, static_cast<size_t>(n)));
+  CK(dalloc(&d_win, static_cast<size_t>(n) * std::max(wcap, 1)));
+  CK(dalloc(&d_out, static_cast<size_t>(n)));
+  CK(cudaMemcpyAsync(d_log, logits, sizeof(float) * n * static_cast<size_t>(vocab),
+                     cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_desc, desc.data(), sizeof(SampRowDesc) * n, cudaMemcpyHostToDevice, st));
+  if (window_ids && wcap > 0)
+    CK(cudaMemcpyAsync(d_win, window_ids, sizeof(int) * n * static_cast<size_t>(wcap),
+                       cudaMemcpyHostToDevice, st));
+  {
+    TimedLaunch tl(c, st, "sampler", static_cast<double>(n) * max_span * 4);
+    launch_sample_desc(d_log, d_desc, n, d_win, d_out, c->d_err, max_span, st);
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(tokens_out, d_out, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+  int errv = 0;
+  CK(cudaMemcpyAsync(&errv, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(d_log);
+  cudaFree(d_desc);
+  cudaFree(d_win);
+  cudaFree(d_out);
+  return check_err_value(c, errv);
+}
+
+// ---------------------------------------------------------------------------
+// detokenizer
+// ---------------------------------------------------------------------------
+static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
+  const DetokDims& dd = c->dd;
+  DetokW& w = c->dw;
+  cudaStream_t st = c->s_dt;
+  const DetokReq* reqs = reinterpret_cast<const DetokReq*>(c->d_dstage + 8);
+  const int L = dd.latent, D0 = dd.dec;
+  {
+    TimedLaunch tl(c, st, "detok_elt", static_cast<double>(n_lat) * L * 2);
+    launch_vq_dwconv(reqs, n_req, n_lat, c->token_store, w.tabs, w.in_dw_w, w.in_dw_b, c->dstate,
+                     dd, c->dbf, st);
+  }
+  std::map<int, CUtensorMap> xm;
+  if (!make_act_maps(c, xm, c->dbf, L, n_lat)) return fail(c, VOX_ERR_CUDA, "tmap detok act");
+  RET(run_gemm(c, w.tm_in_pw, xm, D0, n_lat, L, c->dx, D0, 1, w.in_pw_b, nullptr, 0, D0, st,
+               "detok_gemm"));
+  float* x = c->dx;
+  float* y = c->dy;
+  int up = 1;
+  const int dils[3] = {1, 3, 9};
+  for (int b = 0; b < 4; ++b) {
+    const int Ci = dd.ch[b], Co = dd.ch[b + 1], s = dd.rates[b];
+    const int rows = n_lat * up;
+    {
+      TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows) * Ci * 8);
+      launch_snake_upcat(reqs, n_req, rows, up, x, Ci, w.up_alpha[b], c->dstate, dd.off_up[b], dd,
+                         c->dbf, st);
+    }
+    std::map<int, CUtensorMap> um;
+    if (!make_act_maps(c, um, c->dbf, 2 * Ci, rows)) return fail(c, VOX_ERR_CUDA, "tmap up");
+    RET(run_gemm(c, w.tm_up[b], um, s * Co, rows, 2 * Ci, y, static_cast<int64_t>(s) * Co, 1,
+                 w.up_b[b], nullptr, 0, s * Co, st, "detok_gemm"));
+    std::swap(x, y);
+    up *= s;
+    const int rows2 = n_lat * up;
+    std::map<int, CUtensorMap> rm;
+    if (!make_act_maps(c, rm, c->dbf, Co, rows2)) return fail(c, VOX_ERR_CUDA, "tmap ru");
+    for (int u = 0; u < 3; ++u) {
+      {
+        TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows2) * Co * 6);
+        launch_ru_prep(reqs, n_req, rows2, up, x, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
+                       w.ru_dw_b[b][u], w.ru_a2[b][u], c->dstate, dd.off_ru[b][u], dd, c->dbf,
+                       st);
+      }
+      RET(run_gemm(c, w.tm_ru[b][u], rm, Co, rows2, Co, x, Co, 1, w.ru_pw_b[b][u], x, Co, Co, st,
+                   "detok_gemm"));
+    }
+  }
+  {
+    const int rows = n_lat * up;
+    TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows) * dd.ch[4] * 4);
+    launch_detok_out(reqs, n_req, rows, up, x, dd.ch[4], w.out_alpha, w.out_w, w.out_b, c->dstate,
+                     dd.off_out, dd, c->d_pcm, st);
+  }
+  CK(cudaGetLastError());
+  return VOX_OK;
+}
+
+int vox_detok(VoxCtx* c, const VoxWindow* win, int32_t n, float* pcm_out, int32_t* n_samples,
+              int64_t* ticket) {
+  if (!c || (!win && n > 0)) return fail(c, VOX_ERR_INVALID, "null argument");
+  const VoxModelCfg& g = c->cfg;
+  if (!g.detok_enabled) return fail(c, VOX_ERR_INVALID, "detokenizer disabled in this context");
+  if (n <= 0) return fail(c, VOX_ERR_EMPTY_BATCH, "empty detok batch");
+  const int ft = g.frame_tokens;
+  int hop = 1;
+  for (int b = 0; b < 4; ++b) hop *= g.rates[b];
+  const int frame_samples = 4 * hop;
+  // ticket (its pinned staging/PCM buffers are reused only after its event)
+  const int64_t tid = c->next_ticket;
+  Ticket& tk = c->tickets[static_cast<size_t>(tid % static_cast<int64_t>(c->tickets.size()))];
+  if (tk.id >= 0) CK(cudaEventSynchronize(tk.ev));
+  int32_t* hdr = reinterpret_cast<int32_t*>(tk.stage_host);
+  DetokReq* hr = reinterpret_cast<DetokReq*>(tk.stage_host + 8);
+  int lat = 0, pcm = 0;
+  int64_t wait_seq = -1;
+  std::vector<int> seen;
+  for (int i = 0; i < n; ++i) {
+    const VoxWindow& w = win[i];
+    if (w.slot < 0 || w.slot >= g.max_slots || !c->slot_used[w.slot])
+      return fail(c, VOX_ERR_CACHE_MISSING, "detokenize without cache for request slot");
+    if (std::find(seen.begin(), seen.end(), w.slot) != seen.end())
+      return fail(c, VOX_ERR_INVALID, "a request appears twice in one detok batch");
+    seen.push_back(w.slot);
+    if (w.new_tokens < 1 || w.new_tokens > w.length || w.start < 0)
+      return fail(c, VOX_ERR_WINDOW_RULE, "window new_tokens outside the window");
+    const int g0 = w.start + w.length - w.new_tokens;
+    if (g0 != c->slot_covered[w.slot] || g0 % ft != 0)
+      return fail(c, VOX_ERR_WINDOW_RULE,
+                  "stateful detokenizer needs in-order, frame-aligned windows");
+    if (w.start + w.length > c->h_target[w.slot])
+      return fail(c, VOX_ERR_WINDOW_RULE, "window beyond the request's generated tokens");
+    DetokReq& q = hr[i];
+    q.slot = w.slot;
+    q.f0 = g0 / ft;
+    q.nf = (w.new_tokens + ft - 1) / ft;
+    q.lat_off = lat;
+    q.parity = c->slot_chunks[w.slot] & 1;
+    q.prompt_len = c->h_prompt[w.slot];
+    q.n_tokens = w.start + w.length;
+    q.pcm_off = pcm;
+    q.n_samples = static_cast<int>((static_cast<int64_t>(w.new_tokens) * frame_samples) / ft);
+    lat += 4 * q.nf;
+    pcm += q.n_samples;
+    wait_seq = std::max(wait_seq, c->slot_last_fwd[w.slot]);
+    if (n_samples) n_samples[i] = q.n_samples;
+  }
+  if (lat > g.max_detok_frames)
+    return fail(c, VOX_ERR_BATCH_TOO_LARGE, "detok batch exceeds max_detok_frames");
+  hdr[0] = n;
+  hdr[1] = lat;
+  c->next_ticket++;
+  // LM -> detok dependency: the forward that produced the windows' last tokens
+  if (wait_seq >= 0) {
+    const int ei = static_cast<int>(wait_seq % static_cast<int64_t>(c->fwd_events.size()));
+    if (c->fwd_event_seq[ei] == wait_seq) CK(cudaStreamWaitEvent(c->s_dt, c->fwd_events[ei], 0));
+    else CK(cudaStreamWaitEvent(c->s_dt, c->fwd_events[c->fwd_seq % c->fwd_events.size()], 0));
+  }
+  const size_t stage_bytes = 8 + sizeof(DetokReq) * n;
+  CK(cudaMemcpyAsync(c->d_dstage, tk.stage_host, stage_bytes, cudaMemcpyHostToDevice, c->s_dt));
+  RET(enqueue_detok(c, n, lat));
+  CK(cudaMemcpyAsync(tk.pcm_host, c->d_pcm, sizeof(float) * pcm, cudaMemcpyDeviceToHost, c->s_dt));
+  CK(cudaEventRecord(tk.ev, c->s_dt));
+  tk.id = tid;
+  tk.total = pcm;
+  for (int i = 0; i < n; ++i) {
+    c->slot_chunks[win[i].slot] += 1;
+    c->slot_covered[win[i].slot] += win[i].new_tokens;
+  }
+  if (ticket) *ticket = tid;
+  if (pcm_out) {
+    CK(cudaEventSynchronize(tk.ev));
+    std::memcpy(pcm_out, tk.pcm_host, sizeof(float) * pcm);
+  }
+  return VOX_OK;
+}
+
+int vox_ticket_query(VoxCtx* c, int64_t ticket, int32_t* done, double* t_ms) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  Ticket& tk = c->tickets[static_cast<size_t>(ticket % static_cast<int64_t>(c->tickets.size()))];
+  if (tk.id != ticket) return fail(c, VOX_ERR_INVALID, "stale ticket");
+  cudaError_t e = cudaEventQuery(tk.ev);
+  if (e == cudaErrorNotReady) {
+    if (done) *done = 0;
+    return VOX_OK;
+  }
+  CK(e);
+  if (done) *done = 1;
+  if (t_ms) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->epoch, tk.ev));
+    *t_ms = ms;
+  }
+  return VOX_OK;
+}
+
+int vox_ticket_pcm(VoxCtx* c, int64_t ticket, const float** pcm, int32_t* total) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  Ticket& tk = c->tickets[static_cast<size_t>(ticket % static_cast<int64_t>(c->tickets.size()))];
+  if (tk.id != ticket) return fail(c, VOX_ERR_INVALID, "stale ticket");
+  CK(cudaEventSynchronize(tk.ev));
+  if (pcm) *pcm = tk.pcm_host;
+  if (total) *total = tk.total;
+  return VOX_OK;
+}
+
+int vox_clock_reset(VoxCtx* c) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  CK(cudaEventRecord(c->epoch, c->s_lm));
+  CK(cudaEventSynchronize(c->epoch));
+  return VOX_OK;
+}
+
+int vox_synchronize(VoxCtx* c) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaStreamSynchronize(c->s_dt));
+  for (auto& s : c->stages) {
+    if (s.in_flight) s.in_flight = false;
+    if (*s.err) {
+      const int e = *s.err;
+      *s.err = 0;
+      return check_err_value(c, e);
+    }
+  }
+  return VOX_OK;
+}
+
+int vox_streams(VoxCtx* c, void** lm, void** dt) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  if (lm) *lm = c->s_lm;
+  if (dt) *dt = c->s_dt;
+  return VOX_OK;
+}
+
+int vox_timing_enable(VoxCtx* c, int32_t on) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  for (auto& t : c->trecs) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  c->trecs.clear();
+  c->timing = on != 0;
+  return VOX_OK;
+}
+
+int vox_timing_read(VoxCtx* c, const char* name, double* total_ms, int64_t* launches,
+                    double* bytes) {
+  if (!c || !name) return fail(c, VOX_ERR_INVALID, "null argument");
+  CK(cudaDeviceSynchronize());
+  double ms = 0, by = 0;
+  int64_t cnt = 0;
+  for (auto& t : c->trecs) {
+    if (t.cls != name) continue;
+    float e = 0.f;
+    CK(cudaEventElapsedTime(&e, t.a, t.b));
+    ms += e;
+    by += t.bytes;
+    ++cnt;
+  }
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = cnt;
+  if (bytes) *bytes = by;
+  return VOX_OK;
+}
+
+int vox_launch_count(VoxCtx* c, int64_t* launches) {
+  if (!c || !launches) return fail(c, VOX_ERR_INVALID, "null argument");
+  *launches = c->launches;
+  return VOX_OK;
+}
+
+int vox_read_weight(VoxCtx* c, const char* name, int32_t layer, void* out, size_t bytes) {
+  if (!c || !name || !out) return fail(c, VOX_ERR_INVALID, "null argument");
+  const VoxModelCfg& g = c->cfg;
+  const int d = g.d_model;
+  const void* src = nullptr;
+  size_t avail = 0;
+  const std::string n(name);
+  const int64_t n_qkv = static_cast<int64_t>(c->nqkv) * d;
+  if (n == "emb") {
+    src = c->emb;
+    avail = static_cast<size_t>(g.vocab) * d * 2;
+  } else if (n == "qkv") {
+    src = c->w_qkv + layer * n_qkv;
+    avail = n_qkv * 2;
+  } else if (n == "norm_attn") {
+    src = c->norm_attn + static_cast<int64_t>(layer) * d;
+    avail = d * 4;
+  } else if (n == "vq_tab" && g.detok_enabled) {
+    src = c->dw.tabs;
+    avail = static_cast<size_t>(3) * g.codebook_size * g.latent_dim * 2;
+  } else {
+    return fail(c, VOX_ERR_INVALID, "unknown weight name");
+  }
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, src, std::min(bytes, avail), cudaMemcpyDeviceToHost));
+  return VOX_OK;
+}
+
+int vox_read_kv(VoxCtx* c, int32_t layer, int32_t slot, int32_t pos, float* k_out,
+                float* v_out) {
+  if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
+    return fail(c, VOX_ERR_CACHE_MISSING, "unknown slot");
+  const VoxModelCfg& g = c->cfg;
+  if (layer < 0 || layer >= g.n_layers || pos < 0 ||
+      pos >= static_cast<int>(c->slot_pages[slot].size()) * g.page_size)
+    return fail(c, VOX_ERR_INVALID, "bad kv coordinate");
+  CK(cudaDeviceSynchronize());
+  const int page = c->slot_pages[slot][pos / g.page_size], off = pos % g.page_size;
+  const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
+  std::vector<bf16> tmp(g.head_dim);
+  for (int h = 0; h < g.n_kv_heads; ++h) {
+    const size_t idx = layer * kv_layer +
+                       ((static_cast<size_t>(page) * g.n_kv_heads + h) * g.page_size + off) *
+                           g.head_dim;
+    CK(cudaMemcpy(tmp.data(), c->kc + idx, g.head_dim * 2, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < g.head_dim; ++e) k_out[h * g.head_dim + e] = __bfloat162float(tmp[e]);
+    CK(cudaMemcpy(tmp.data(), c->vc + idx, g.head_dim * 2, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < g.head_dim; ++e) v_out[h * g.head_dim + e] = __bfloat162float(tmp[e]);
+  }
+  return VOX_OK;
+}
+
+}  // extern "C"
