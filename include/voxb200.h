@@ -169,6 +169,20 @@ int vox_timing_read(VoxCtx* ctx, const char* name, double* total_ms, int64_t* la
                     double* bytes);
 int vox_launch_count(VoxCtx* ctx, int64_t* launches); /* our kernels launched so far */
 
+/* K3 alone (parity tests / roofline): out[n, m] = sum_k W[m, k] X[n, k] (+bias[m])
+ * with W [M, K], X [N, K] bf16 (raw uint16 bits), fp32 out [N, M]; K % 64 == 0.
+ * splits > 1 returns the split-K partial sum reduced on the host side of the
+ * call.  iters > 1 repeats the launch and reports the mean kernel time. */
+int vox_gemm_test(VoxCtx* ctx, const uint16_t* w, const uint16_t* x, const float* bias,
+                  int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters, float* out,
+                  double* mean_ms);
+
+/* test-only: copy the last detok stage output (fp32) and the bf16 GEMM operand
+ * buffer to the host, then make the next vox_detok stop after `stop_after`
+ * pipeline stages (<= 0: run to completion). */
+int vox_debug_detok(VoxCtx* ctx, int32_t stop_after, float* out, size_t n_floats,
+                    uint16_t* bf_out, size_t n_bf);
+
 /* weights / state introspection for parity tests (host copies) */
 int vox_read_weight(VoxCtx* ctx, const char* name, int32_t layer, void* out, size_t bytes);
 int vox_read_kv(VoxCtx* ctx, int32_t layer, int32_t slot, int32_t pos, float* k_out,

@@ -136,11 +136,12 @@ class DetokWeights:
                     a2=init_f32(Co, k(T_RU_A2, li), 0.5, 1.0),
                     dw_w=init_f32(7 * Co, k(T_RU_DW_W, li), np.sqrt(f32(3.0) / f32(7.0)), 0.0).reshape(Co, 7),
                     dw_b=init_f32(Co, k(T_RU_DW_B, li), 0.05, 0.0),
-                    pw_w=init_bf16(Co * Co, k(T_RU_PW_W, li), f32(0.5) * np.sqrt(f32(3.0) / f32(Co))).reshape(Co, Co),
+                    pw_w=init_bf16(Co * Co, k(T_RU_PW_W, li), f32(0.25) * np.sqrt(f32(3.0) / f32(Co))).reshape(Co, Co),
                     pw_b=init_f32(Co, k(T_RU_PW_B, li), 0.05, 0.0),
                 ))
             self.ru.append(units)
         C4 = ch[4]
         self.out_alpha = init_f32(C4, k(T_OUT_ALPHA), 0.5, 1.0)
-        self.out_w = init_f32(7 * C4, k(T_OUT_W), np.sqrt(f32(3.0) / (f32(7.0) * f32(C4))), 0.0).reshape(C4, 7)
+        self.out_w = init_f32(7 * C4, k(T_OUT_W), f32(0.15) * np.sqrt(f32(3.0) / (f32(7.0) * f32(C4))),
+                              0.0).reshape(C4, 7)
         self.out_b = init_f32(1, k(T_OUT_B), 0.05, 0.0)[0]

@@ -26,6 +26,12 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
+// per-tensor init key (oracle/weights.py:tensor_key mirrors this)
+__host__ __device__ __forceinline__ uint64_t tensor_key(uint64_t seed, uint64_t tid,
+                                                        uint64_t layer) {
+  return mix64(mix64(seed ^ (tid * 0xD1B54A32D192ED03ull)) ^ (layer * 0x8CB92BA72F3D8DD7ull));
+}
+
 // uniform in [-1, 1) with 24 random bits: exact in fp32 on both sides.
 __host__ __device__ __forceinline__ float unit_pm1(uint64_t h) {
   return (float)(int32_t)(h >> 40) * (1.0f / 8388608.0f) - 1.0f;

@@ -51,10 +51,6 @@ enum TensorId : uint64_t {
   T_OUT_B = 172,
 };
 
-inline uint64_t tensor_key(uint64_t seed, uint64_t tid, uint64_t layer) {
-  return mix64(mix64(seed ^ (tid * 0xD1B54A32D192ED03ull)) ^ (layer * 0x8CB92BA72F3D8DD7ull));
-}
-
 constexpr int kBuckets[] = {16, 32, 64, 128, 256, 512, 1024, 2048};
 
 struct TimingRec {
@@ -175,6 +171,9 @@ struct VoxCtx {
   std::vector<Ticket> tickets;
   int64_t next_ticket = 0;
   std::map<int, CUtensorMap> tm_dbf;  // placeholder (per call maps built on the fly)
+
+  int detok_stop = 1 << 30;  // debug: stop the detok pipeline after this many stages
+  float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
 
   // ---- timing / counting
   bool timing = false;
@@ -481,6 +480,7 @@ static int create_detok(VoxCtx* c) {
     float* tmp;
     CK(dalloc(&tmp, static_cast<size_t>(Co)));
     RET(init_f32(c, tmp, Co, T_UP_B + b, 0, 0.05f, 0.f));
+    CK(cudaStreamSynchronize(c->s_lm));  // init ran on the non-blocking LM stream
     CK(cudaMemcpy(bias_small.data(), tmp, Co * 4, cudaMemcpyDeviceToHost));
     cudaFree(tmp);
     for (int j = 0; j < s; ++j)
@@ -503,7 +503,7 @@ static int create_detok(VoxCtx* c) {
       RET(init_f32(c, w.ru_dw_w[b][u], 7LL * Co, T_RU_DW_W, li, std::sqrt(3.0f / 7.0f), 0.f));
       RET(init_f32(c, w.ru_dw_b[b][u], Co, T_RU_DW_B, li, 0.05f, 0.f));
       RET(init_bf16(c, w.ru_pw_w[b][u], static_cast<int64_t>(Co) * Co, T_RU_PW_W, li,
-                    0.5f * std::sqrt(3.0f / Co)));
+                    0.25f * std::sqrt(3.0f / Co)));
       RET(init_f32(c, w.ru_pw_b[b][u], Co, T_RU_PW_B, li, 0.05f, 0.f));
       if (!make_tmap_bf16(&w.tm_ru[b][u], w.ru_pw_w[b][u], Co, Co, Co * 2ull, 128))
         return fail(c, VOX_ERR_CUDA, "tmap detok ru");
@@ -513,11 +513,14 @@ static int create_detok(VoxCtx* c) {
   CK(dalloc(&w.out_alpha, static_cast<size_t>(C4)));
   CK(dalloc(&w.out_w, static_cast<size_t>(C4) * 7));
   RET(init_f32(c, w.out_alpha, C4, T_OUT_ALPHA, 0, 0.5f, 1.0f));
-  RET(init_f32(c, w.out_w, 7LL * C4, T_OUT_W, 0, std::sqrt(3.0f / (7.0f * C4)), 0.f));
+  // residual branches at 1/4 gain and a 0.15-gain output conv keep the random
+  // decoder contractive (well-conditioned for bf16 parity; pre-tanh rms ~0.3)
+  RET(init_f32(c, w.out_w, 7LL * C4, T_OUT_W, 0, 0.15f * std::sqrt(3.0f / (7.0f * C4)), 0.f));
   {
     float* tmp;
     CK(dalloc(&tmp, 1));
     RET(init_f32(c, tmp, 1, T_OUT_B, 0, 0.05f, 0.f));
+    CK(cudaStreamSynchronize(c->s_lm));
     CK(cudaMemcpy(&w.out_b, tmp, 4, cudaMemcpyDeviceToHost));
     cudaFree(tmp);
   }
@@ -875,7 +878,7 @@ int vox_write_tokens(VoxCtx* c, int32_t slot, int32_t pos, int32_t n, const int3
     return fail(c, VOX_ERR_INVALID, "bad token range");
   for (int i = 0; i < n; ++i)
     if (ids[i] < 0 || ids[i] >= c->cfg.vocab) return fail(c, VOX_ERR_INVALID, "token id outside vocab");
-  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaDeviceSynchronize());  // both streams may read the token store
   CK(cudaMemcpy(c->token_store + static_cast<int64_t>(slot) * c->cfg.max_ctx + pos, ids,
                 static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice));
   return VOX_OK;
@@ -1087,15 +1090,23 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
   cudaStream_t st = c->s_dt;
   const DetokReq* reqs = reinterpret_cast<const DetokReq*>(c->d_dstage + 8);
   const int L = dd.latent, D0 = dd.dec;
+  int stage = 0;
+#define DSTOP(buf)                                   \
+  do {                                               \
+    c->dbg_last = (buf);                             \
+    if (++stage >= c->detok_stop) return VOX_OK;     \
+  } while (0)
   {
     TimedLaunch tl(c, st, "detok_elt", static_cast<double>(n_lat) * L * 2);
     launch_vq_dwconv(reqs, n_req, n_lat, c->token_store, w.tabs, w.in_dw_w, w.in_dw_b, c->dstate,
                      dd, c->dbf, st);
   }
+  DSTOP(nullptr);
   std::map<int, CUtensorMap> xm;
   if (!make_act_maps(c, xm, c->dbf, L, n_lat)) return fail(c, VOX_ERR_CUDA, "tmap detok act");
   RET(run_gemm(c, w.tm_in_pw, xm, D0, n_lat, L, c->dx, D0, 1, w.in_pw_b, nullptr, 0, D0, st,
                "detok_gemm"));
+  DSTOP(c->dx);
   float* x = c->dx;
   float* y = c->dy;
   int up = 1;
@@ -1108,11 +1119,13 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
       launch_snake_upcat(reqs, n_req, rows, up, x, Ci, w.up_alpha[b], c->dstate, dd.off_up[b], dd,
                          c->dbf, st);
     }
+    DSTOP(nullptr);
     std::map<int, CUtensorMap> um;
     if (!make_act_maps(c, um, c->dbf, 2 * Ci, rows)) return fail(c, VOX_ERR_CUDA, "tmap up");
     RET(run_gemm(c, w.tm_up[b], um, s * Co, rows, 2 * Ci, y, static_cast<int64_t>(s) * Co, 1,
                  w.up_b[b], nullptr, 0, s * Co, st, "detok_gemm"));
     std::swap(x, y);
+    DSTOP(x);
     up *= s;
     const int rows2 = n_lat * up;
     std::map<int, CUtensorMap> rm;
@@ -1124,8 +1137,10 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
                        w.ru_dw_b[b][u], w.ru_a2[b][u], c->dstate, dd.off_ru[b][u], dd, c->dbf,
                        st);
       }
+      DSTOP(nullptr);
       RET(run_gemm(c, w.tm_ru[b][u], rm, Co, rows2, Co, x, Co, 1, w.ru_pw_b[b][u], x, Co, Co, st,
                    "detok_gemm"));
+      DSTOP(x);
     }
   }
   {
@@ -1311,6 +1326,69 @@ int vox_launch_count(VoxCtx* c, int64_t* launches) {
   if (!c || !launches) return fail(c, VOX_ERR_INVALID, "null argument");
   *launches = c->launches;
   return VOX_OK;
+}
+
+int vox_debug_detok(VoxCtx* c, int32_t stop_after, float* out, size_t n_floats, uint16_t* bf_out,
+                    size_t n_bf) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  CK(cudaDeviceSynchronize());
+  if (out && c->dbg_last) CK(cudaMemcpy(out, c->dbg_last, n_floats * 4, cudaMemcpyDeviceToHost));
+  if (bf_out) CK(cudaMemcpy(bf_out, c->dbf, n_bf * 2, cudaMemcpyDeviceToHost));
+  c->detok_stop = stop_after > 0 ? stop_after : (1 << 30);
+  return VOX_OK;
+}
+
+int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* bias, int32_t M,
+                  int32_t N, int32_t K, int32_t splits, int32_t iters, float* out,
+                  double* mean_ms) {
+  if (!c || !w || !x || !out) return fail(c, VOX_ERR_INVALID, "null argument");
+  if (M < 1 || N < 1 || K < 64 || K % 64 || splits < 1 || iters < 1)
+    return fail(c, VOX_ERR_INVALID, "bad GEMM shape");
+  bf16 *dw = nullptr, *dx = nullptr;
+  float *dout = nullptr, *db = nullptr;
+  CK(dalloc(&dw, static_cast<size_t>(M) * K));
+  CK(dalloc(&dx, static_cast<size_t>(N) * K));
+  CK(dalloc(&dout, static_cast<size_t>(splits) * N * M));
+  CK(cudaMemcpy(dw, w, static_cast<size_t>(M) * K * 2, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(dx, x, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
+  if (bias) {
+    CK(dalloc(&db, static_cast<size_t>(M)));
+    CK(cudaMemcpy(db, bias, static_cast<size_t>(M) * 4, cudaMemcpyHostToDevice));
+  }
+  CUtensorMap tw;
+  std::map<int, CUtensorMap> xm;
+  if (!make_tmap_bf16(&tw, dw, K, M, K * 2ull, 128) || !make_act_maps(c, xm, dx, K, N))
+    return fail(c, VOX_ERR_CUDA, "tensor map (gemm test)");
+  cudaEvent_t a, b;
+  CK(cudaEventCreate(&a));
+  CK(cudaEventCreate(&b));
+  int rc = VOX_OK;
+  for (int it = 0; it < iters && rc == VOX_OK; ++it) {
+    if (it == (iters > 1 ? 1 : 0)) CK(cudaEventRecord(a, c->s_lm));
+    rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
+                  c->s_lm);
+  }
+  CK(cudaEventRecord(b, c->s_lm));
+  CK(cudaEventSynchronize(b));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, a, b));
+  if (mean_ms) *mean_ms = ms / (iters > 1 ? iters - 1 : 1);
+  if (rc == VOX_OK) {
+    std::vector<float> tmp(static_cast<size_t>(splits) * N * M);
+    CK(cudaMemcpy(tmp.data(), dout, tmp.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < static_cast<size_t>(N) * M; ++i) {
+      float s = 0.f;
+      for (int k = 0; k < splits; ++k) s += tmp[k * static_cast<size_t>(N) * M + i];
+      out[i] = s;
+    }
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(dw);
+  cudaFree(dx);
+  cudaFree(dout);
+  if (db) cudaFree(db);
+  return rc;
 }
 
 int vox_read_weight(VoxCtx* c, const char* name, int32_t layer, void* out, size_t bytes) {

@@ -217,6 +217,20 @@ class VoxDevice:
         self._check(self.lib.vox_launch_count(self.ctx, C.byref(n)))
         return n.value
 
+    def gemm_test(self, w_bits: np.ndarray, x_bits: np.ndarray, bias=None, splits: int = 1, iters: int = 1):
+        """K3 alone: w_bits [M,K], x_bits [N,K] uint16 bf16 bits -> (out [N,M] fp32, mean ms)."""
+        w = np.ascontiguousarray(w_bits, dtype=np.uint16)
+        x = np.ascontiguousarray(x_bits, dtype=np.uint16)
+        M, K = w.shape
+        N = x.shape[0]
+        out = np.empty((N, M), np.float32)
+        ms = C.c_double()
+        b = None if bias is None else np.ascontiguousarray(bias, dtype=np.float32)
+        self._check(self.lib.vox_gemm_test(
+            self.ctx, w.ctypes.data_as(C.POINTER(C.c_uint16)), x.ctypes.data_as(C.POINTER(C.c_uint16)),
+            None if b is None else _ptr(b, C.c_float), M, N, K, splits, iters, _ptr(out, C.c_float), C.byref(ms)))
+        return out, ms.value
+
     def read_weight(self, name: str, layer: int, shape, dtype) -> np.ndarray:
         out = np.empty(shape, dtype=dtype)
         self._check(self.lib.vox_read_weight(self.ctx, name.encode(), layer, out.ctypes.data_as(C.c_void_p),

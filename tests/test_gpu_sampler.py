@@ -24,9 +24,9 @@ def _ref_greedy(row32, window, penalty, lo=None, hi=None):
         m = np.full_like(arr, -np.inf)
         m[lo:hi] = arr[lo:hi]
         arr = m
-    w = osamp.RingWindow(64, V)
+    w = model_api._RingWindow(64, V)
     for t in window:
-        w.append(t)
+        w.append(int(t))
     # the reference itself, on identical fp32-valued logits
     state = model_api.SamplingState(seed=0, rng=np.random.default_rng(0), windows=[w])
     p = model_api.SamplingParams(temperature=0.0, repetition_penalty=penalty)
