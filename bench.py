@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: Orpheus-3B-style streaming TTS serving on B200 (BASELINE.json config 2).
+
+Headline metric (BASELINE.json): req/s at >=99% streaming viability and p90
+TTFA <= 500 ms; audio-seconds per second per B200.
+
+* A "step" is one serving iteration of the StreamingEngine in steady state
+  over B concurrent streams (default B=256): the reference streaming-aware
+  scheduler's decision (scheduler.py:119-175) executed as one fused decode
+  step for the LM batch (tcgen05 GEMMs + paged attention + K1 sampler, CUDA
+  graph) plus the detokenization of that iteration's ready chunks (causal
+  SNAC-style decoder with cached left context) on the overlapped detok stream.
+* value = audio seconds represented by the tokens decoded in the timed
+  region / device time (CUDA events on both streams, max over ranks).
+* e2e  = the same metric on the host wall clock of the same steps, which
+  include every step's H2D row upload from pinned memory and the D2H of the
+  sampled ids and of the emitted PCM.
+* slo  = the paper's serving metric from a short Poisson load test through
+  the same engine: the highest offered rate whose pooled viability >= 0.99
+  and p90 TTFA <= 0.5 s (reference core.py metrics, unchanged).
+* --impl reference: the reference CPU path timed on this host (the oracle
+  port of the same arithmetic, numpy/BLAS on all cores; bounded sample).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+if (ROOT / "baseline" / "_ref").exists():
+    sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+
+import numpy as np  # noqa: E402
+
+METRIC = "req/s at >=99% streaming viability & p90 TTFA; audio-sec/sec per B200"
+UNIT = "audio-s/s"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def __enter__(self):
+        def loop():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._th = threading.Thread(target=loop, daemon=True)
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------- distributed
+def dist_setup(backend: str):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            import torch
+
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def reduce_max(x: float, ws: int, device=None) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def reduce_sum(xs, ws: int, device=None):
+    if ws == 1:
+        return list(xs)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor(list(xs), dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
+# ---------------------------------------------------------------------------- our arm
+def steady_state_steps(dev, B: int, steps: int, warmup: int, prompt: int, seed: int):
+    """Stagger B streams into steady state, then time `steps` engine iterations."""
+    import torch
+
+    from paper_2602_00269_b200._ref import scheduler, workload
+    from paper_2602_00269_b200.engine import StreamingEngine, orpheus_profile
+
+    prof = orpheus_profile(max_batch=B)
+    policy = scheduler.PolicyConfig(max_lm_batch=B, max_detok_batch=B, startup_concurrency_limit=B,
+                                    max_live_requests=4 * B)
+    eng = StreamingEngine(dev, prof, policy, seed)
+    target = 688
+    groups = 8
+    per = (B + groups - 1) // groups
+    rid = 0
+    dev.clock_reset()
+    eng._t0 = time.perf_counter()
+
+    def one_iter():
+        snap = eng._snapshot()
+        dec = scheduler.schedule(snap, eng.now_us(), policy)
+        if not dec.empty:
+            eng.run_iteration(dec)
+        eng._poll()
+
+    # staggered admission: group g joins at iteration g so chunk boundaries spread out
+    it = 0
+    while rid < B:
+        for _ in range(min(per, B - rid)):
+            eng.admit(rid, workload.ArrivalSpec(arrival_us=0, prompt_tokens=prompt, target_output_tokens=target))
+            rid += 1
+        one_iter()
+        it += 1
+    # run until every stream has its first chunk and the pipeline is warm
+    guard = 0
+    while any(r.req.first_chunk_us is None for r in eng.live.values()) and guard < 400:
+        one_iter()
+        guard += 1
+    for _ in range(warmup):
+        one_iter()
+    dev.synchronize()
+    lm_s, dt_s = dev.streams()
+    s_lm = torch.cuda.ExternalStream(lm_s)
+    s_dt = torch.cuda.ExternalStream(dt_s)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev_lm = torch.cuda.Event(enable_timing=True)
+    ev_dt = torch.cuda.Event(enable_timing=True)
+    st0 = eng.stats
+    dec0, chunks0, pcm0 = st0.decode_rows, len(eng.trace.chunks), st0.pcm_samples
+    rows0, dcalls0 = st0.lm_rows, st0.detok_calls
+    launches0 = dev.launch_count()
+    ev0.record(s_lm)
+    s_dt.wait_event(ev0)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one_iter()
+    ev_lm.record(s_lm)
+    ev_dt.record(s_dt)
+    torch.cuda.synchronize()
+    while eng._tickets:
+        eng._poll(block=True)
+    t_wall = time.perf_counter() - t0
+    dev_ms = max(ev0.elapsed_time(ev_lm), ev0.elapsed_time(ev_dt))
+    st = eng.stats
+    decoded = st.decode_rows - dec0
+    chunks = len(eng.trace.chunks) - chunks0
+    pcm = st.pcm_samples - pcm0
+    rows = st.lm_rows - rows0
+    out = dict(decoded=decoded, chunks=chunks, pcm_samples=pcm, dev_ms=dev_ms, wall_s=t_wall,
+               launches=dev.launch_count() - launches0, rows=rows, detok_calls=st.detok_calls - dcalls0,
+               token_rate=prof.token_rate, live=len(eng.live), host_s=st.host_s)
+    eng.shutdown()
+    return out
+
+
+def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: float):
+    """Per-kernel-class CUDA-event timing of eager decode steps at batch B (timing mode)."""
+    from paper_2602_00269_b200.device import Sampling
+
+    cfg = dev.cfg
+    ctx = prompt + 344  # mid-stream context (average over a 688-token request)
+    slots = []
+    for i in range(B):
+        slots.append(dev.admit(seed + i, prompt, 688, Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3)))
+    # fill KV for `ctx` positions with one big prefill-like pass per slot group
+    for a in range(0, B, 2):
+        rows = np.array([[s, p, -1, 0] for s in slots[a:a + 2] for p in range(ctx - 1)], np.int32)
+        dev.forward(rows, sample=False)
+    dev.synchronize()
+    rows = np.array([[s, ctx - 1, -1, 1] for s in slots], np.int32)
+    dev.forward(rows, graph=False)  # warm
+    dev.synchronize()
+    dev.timing(True)
+    n = 3
+    for _ in range(n):
+        dev.forward(rows, graph=False)
+    dev.synchronize()
+    classes = {}
+    for cls in ("gemm", "attn", "qkv_rope", "norm", "silu", "lm_head", "sampler"):
+        ms, cnt, by = dev.timing_read(cls)
+        classes[cls] = dict(ms=ms / n, launches=cnt // n, bytes=by / n)
+    dev.timing(False)
+    for s in slots:
+        dev.release(s)
+    step_ms = sum(v["ms"] for v in classes.values())
+    return classes, step_ms, ctx
+
+
+def run_slo(dev, rates, seconds: float, seed: int, prompt: int):
+    from paper_2602_00269_b200._ref import core, scheduler, workload
+    from paper_2602_00269_b200.engine import StreamingEngine, orpheus_profile
+
+    prof = orpheus_profile(max_batch=256)
+    out = []
+    for rate in rates:
+        spec = workload.WorkloadSpec(rate=rate, duration_s=seconds, prompt_dist=workload.fixed(prompt),
+                                     output_dist=workload.fixed(688), seed=seed)
+        arr = list(enumerate(workload.build_workload(spec)))
+        policy = scheduler.PolicyConfig(max_lm_batch=256, max_detok_batch=256, startup_concurrency_limit=16)
+        eng = StreamingEngine(dev, prof, policy, seed)
+        tr = eng.run(arr)
+        rep = core.build_report(tr)
+        out.append(dict(rate=rate, requests=len(arr), ttfa_p50=rep.ttfa_p50, ttfa_p90=rep.ttfa_p90,
+                        ttfa_p99=rep.ttfa_p99, viability=rep.viability_fraction, inverse_rtf=rep.inverse_rtf,
+                        audio_s=rep.audio_seconds_generated, completed=rep.requests_completed))
+        if not (rep.viability_fraction >= 0.99 and rep.ttfa_p90 <= 0.5):
+            break
+    ok = [r["rate"] for r in out if r["viability"] >= 0.99 and r["ttfa_p90"] <= 0.5]
+    return (max(ok) if ok else 0.0), out
+
+
+def cpu_port_sample(seconds_budget: float = 20.0):
+    """Oracle port of the same step on host cores (bounded sample); returns audio-s/s."""
+    from oracle.cpu_step import time_cpu_step
+
+    return time_cpu_step(budget_s=seconds_budget)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=64)
+    ap.add_argument("--warmup", type=int, default=8)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--prompt", type=int, default=50)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--slo-seconds", type=float, default=12.0)
+    ap.add_argument("--slo-rates", default="16,32,48,64")
+    ap.add_argument("--no-slo", action="store_true")
+    ap.add_argument("--no-roofline", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    if args.impl == "reference":
+        ws, rank, _ = dist_setup("gloo")
+        if rank != 0:
+            return
+        from oracle.cpu_step import time_cpu_step
+
+        r = time_cpu_step(budget_s=20.0, steps=args.steps, warmup=min(args.warmup, 1))
+        line = {"metric": METRIC, "value": r["audio_s_per_s"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": {"workload": "orpheus-3b-style decode+sample+detok step, oracle port",
+                                                "sample": r["sample"]},
+                "cpu_baseline": {"value": r["audio_s_per_s"], "unit": UNIT, "cores": r["cores"], "kind": "port",
+                                 "sample": r["sample"]},
+                "e2e": {"value": r["audio_s_per_s"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    ws, rank, local = dist_setup("nccl")
+    import torch
+
+    from paper_2602_00269_b200.build import build
+    from paper_2602_00269_b200.config import orpheus3b
+    from paper_2602_00269_b200.device import VoxDevice
+
+    if rank == 0:
+        build()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.set_device(local)
+    cfg = orpheus3b()
+    dev = VoxDevice(cfg, weight_seed=args.seed, device=local)
+    hbm, tfl, peak_kind = _peaks()
+
+    res = steady_state_steps(dev, args.batch, 3, args.warmup, args.prompt, args.seed + 1000 * rank)  # graphs warm
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        res = steady_state_steps(dev, args.batch, args.steps, args.warmup, args.prompt, args.seed + 1000 * rank)
+    dev_ms = reduce_max(res["dev_ms"], ws, torch.device("cuda", local))
+    wall_s = reduce_max(res["wall_s"], ws, torch.device("cuda", local))
+    decoded, chunks, pcm = reduce_sum([res["decoded"], res["chunks"], res["pcm_samples"]], ws,
+                                      torch.device("cuda", local))
+    audio_s = decoded / res["token_rate"]
+    value = audio_s / (dev_ms / 1000.0)
+    e2e = audio_s / wall_s
+
+    roof = None
+    if not args.no_roofline and rank == 0:
+        classes, step_ms, ctx = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77, hbm, tfl)
+        top = max(classes, key=lambda k: classes[k]["ms"])
+        c = classes[top]
+        per_launch_ms = c["ms"] / max(c["launches"], 1)
+        achieved = (c["bytes"] / max(c["launches"], 1)) / (per_launch_ms / 1000.0) / 1e9
+        prof_path = ROOT / "profiles" / "traffic_r01.json"
+        traffic = None
+        if prof_path.exists():
+            traffic = json.loads(prof_path.read_text()).get(top)
+        roof = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "classes_ms_per_step": {k: round(v["ms"], 4) for k, v in classes.items()},
+                "eager_step_ms": round(step_ms, 3), "ctx": ctx, "batch": args.batch}
+
+    slo = None
+    if not args.no_slo and rank == 0:
+        rates = [float(x) for x in args.slo_rates.split(",")]
+        best, sweep = run_slo(dev, rates, args.slo_seconds, args.seed, args.prompt)
+        slo = {"max_req_s_at_slo": best, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
+               "duration_s": args.slo_seconds, "sweep": sweep}
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        from oracle.cpu_step import time_cpu_step
+
+        r = time_cpu_step(budget_s=15.0, steps=2, warmup=1)
+        cpu = {"value": r["audio_s_per_s"], "unit": UNIT, "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+
+    if rank == 0:
+        steps = args.steps
+        h2d = (res["rows"] / steps) * 24 + 64
+        d2h = (res["decoded"] / steps) * 4 + (res["pcm_samples"] / steps) * 4 + 4
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": round(dev_ms / steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "orpheus-3b-style steady-state serving iteration (config 2)",
+                       "model": "orpheus-3b-style random-init", "concurrent_streams_per_gpu": args.batch,
+                       "prompt": args.prompt, "output_tokens": 688, "parallelism": f"dp{ws} (request-sharded replicas)",
+                       "l2": "inputs larger than L2 (6.6 GB weights + KV per step)"},
+            "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(res["launches"]),
+            "clocks": clk.summary(),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "slo": slo,
+            "detail": {"tokens_decoded": decoded, "chunks": chunks, "pcm_samples": pcm,
+                       "device_ms": round(dev_ms, 3), "wall_s": round(wall_s, 4),
+                       "req_s_equiv": round(decoded / res["token_rate"] / (688 / res["token_rate"]) / (dev_ms / 1000), 2)},
+        }
+        print(json.dumps(line))
+    dev.close()
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,11 @@ int vox_slot_info(VoxCtx* ctx, int32_t slot, int32_t* prompt_len, int32_t* targe
 int vox_forward(VoxCtx* ctx, const VoxRow* rows, int32_t n, uint32_t flags,
                 float* logits_out, int32_t* tokens_out);
 
+/* sequence number of the last issued vox_forward (1-based), and a host wait
+ * for forward `seq` to complete on the device (bounds host run-ahead) */
+int vox_forward_seq(VoxCtx* ctx, int64_t* seq);
+int vox_forward_wait(VoxCtx* ctx, int64_t seq);
+
 /* K1 alone over caller logits (host, [n, vocab] fp32): window_ids [n, wcap]
  * (window_len[i] valid entries, oldest first), seeds/steps drive the
  * counter-based RNG, lo/hi restrict the candidate range ([0,vocab) = none). */
@@ -153,6 +158,7 @@ int vox_sample_logits(VoxCtx* ctx, const float* logits, int32_t n, int32_t vocab
  * forward).  pcm_out (host, may be NULL): concatenated float PCM, request i
  * at offset sum(n_samples[:i]).  Returns a ticket usable with
  * vox_ticket_* when async (pcm_out == NULL). */
+#define VOX_TICKET_RING 32 /* a ticket stays valid for the next 31 vox_detok calls */
 int vox_detok(VoxCtx* ctx, const VoxWindow* w, int32_t n, float* pcm_out,
               int32_t* n_samples, int64_t* ticket);
 int vox_ticket_query(VoxCtx* ctx, int64_t ticket, int32_t* done, double* t_ms);

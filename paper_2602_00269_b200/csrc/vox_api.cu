@@ -52,6 +52,7 @@ enum TensorId : uint64_t {
 };
 
 constexpr int kBuckets[] = {16, 32, 64, 128, 256, 512, 1024, 2048};
+constexpr int kTicketRing = 32;  // in-flight detok calls (VOX_TICKET_RING in voxb200.h)
 
 struct TimingRec {
   std::string cls;
@@ -65,6 +66,12 @@ struct Ticket {
   float* pcm_host = nullptr;
   uint8_t* stage_host = nullptr;  // ReqHdr + DetokReq[] (pinned), reused after ev
   int32_t total = 0;
+};
+
+struct AdmitStage {  // pinned admission staging (page-table row, prompt, slot meta)
+  uint8_t* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool in_flight = false;
 };
 
 struct FwdStage {  // pinned per-call staging; reused only after `ev` completed
@@ -147,6 +154,9 @@ struct VoxCtx {
   int* d_tokens = nullptr;
   int* d_err = nullptr;
   std::vector<FwdStage> stages;  // ring
+  std::vector<AdmitStage> admit_stages;
+  int64_t admit_seq = 0;
+  size_t admit_seed_off = 0, admit_par_off = 0;
   int64_t stage_seq = 0;
   FwdStage* cur = nullptr;       // staging of the call being enqueued
   double step_attn_bytes = 0;    // per layer, for timing/roofline
@@ -413,6 +423,17 @@ static int create_buffers(VoxCtx* c) {
     *s.err = 0;
     CK(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
   }
+  {
+    const size_t ints = static_cast<size_t>(c->max_pages_per_slot) + g.max_ctx + 1;
+    c->admit_seed_off = (ints * 4 + 15) / 16 * 16;
+    c->admit_par_off = c->admit_seed_off + 16;
+    const size_t bytes = c->admit_par_off + sizeof(VoxSampling);
+    c->admit_stages.resize(64);
+    for (auto& a : c->admit_stages) {
+      CK(cudaHostAlloc(&a.host, bytes, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&a.ev, cudaEventDisableTiming));
+    }
+  }
   c->fwd_events.resize(64);
   c->fwd_event_seq.assign(64, -1);
   for (auto& e : c->fwd_events) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -545,7 +566,7 @@ static int create_detok(VoxCtx* c) {
   CK(dalloc(&c->d_dstage, stage_bytes));
   c->pcm_cap = static_cast<size_t>(F) * up;
   CK(dalloc(&c->d_pcm, c->pcm_cap));
-  c->tickets.resize(8);
+  c->tickets.resize(kTicketRing);
   for (auto& t : c->tickets) {
     CK(cudaEventCreate(&t.ev));
     CK(cudaHostAlloc(&t.pcm_host, c->pcm_cap * 4, cudaHostAllocDefault));
@@ -765,6 +786,10 @@ void vox_destroy(VoxCtx* c) {
       }
     }
   }
+  for (auto& a : c->admit_stages) {
+    if (a.host) cudaFreeHost(a.host);
+    if (a.ev) cudaEventDestroy(a.ev);
+  }
   for (auto& s : c->stages) {
     void* host_ptrs[] = {s.rows, s.sample_rows, s.out_index, s.tokens, s.err};
     for (void* p : host_ptrs)
@@ -813,19 +838,36 @@ int vox_admit(VoxCtx* c, uint64_t req_seed, int32_t prompt_len, int32_t target_l
   std::copy(pages.begin(), pages.end(), pt.begin());
   std::vector<int> prompt(prompt_len);
   for (int i = 0; i < prompt_len; ++i) prompt[i] = prompt_id(req_seed, i, g.text_vocab);
+  // Asynchronous admission: the slot's rows are copied from a pinned staging
+  // ring in LM-stream order (before any forward that uses the slot), so an
+  // arrival never stalls the host pipeline.
   cudaStream_t st = c->s_lm;
-  CK(cudaMemcpyAsync(c->page_table + static_cast<int64_t>(slot) * c->max_pages_per_slot,
-                     pt.data(), pt.size() * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->token_store + static_cast<int64_t>(slot) * g.max_ctx, prompt.data(),
+  AdmitStage& as = c->admit_stages[static_cast<size_t>(c->admit_seq++ %
+                                                       static_cast<int64_t>(c->admit_stages.size()))];
+  if (as.in_flight) CK(cudaEventSynchronize(as.ev));
+  int* h_pt = reinterpret_cast<int*>(as.host);
+  int* h_prompt = h_pt + c->max_pages_per_slot;
+  std::copy(pt.begin(), pt.end(), h_pt);
+  std::copy(prompt.begin(), prompt.end(), h_prompt);
+  int* h_plen = h_prompt + g.max_ctx;
+  *h_plen = prompt_len;
+  uint64_t* h_seed = reinterpret_cast<uint64_t*>(as.host + c->admit_seed_off);
+  *h_seed = req_seed;
+  VoxSampling* h_par = reinterpret_cast<VoxSampling*>(as.host + c->admit_par_off);
+  *h_par = *params;
+  CK(cudaMemcpyAsync(c->page_table + static_cast<int64_t>(slot) * c->max_pages_per_slot, h_pt,
+                     pt.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->token_store + static_cast<int64_t>(slot) * g.max_ctx, h_prompt,
                      prompt.size() * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->slot_prompt + slot, &prompt_len, 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->slot_seed + slot, &req_seed, 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(c->slot_params + slot, params, sizeof(VoxSampling), cudaMemcpyHostToDevice,
+  CK(cudaMemcpyAsync(c->slot_prompt + slot, h_plen, 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->slot_seed + slot, h_seed, 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(c->slot_params + slot, h_par, sizeof(VoxSampling), cudaMemcpyHostToDevice,
                      st));
   if (g.detok_enabled)
     CK(cudaMemsetAsync(c->dstate + static_cast<int64_t>(slot) * 2 * c->dd.state_floats, 0,
                        sizeof(float) * 2 * c->dd.state_floats, st));
-  CK(cudaStreamSynchronize(st));  // pageable sources
+  CK(cudaEventRecord(as.ev, st));
+  as.in_flight = true;
   c->slot_used[slot] = 1;
   c->slot_pages[slot] = pages;
   c->h_prompt[slot] = prompt_len;
@@ -854,6 +896,7 @@ int vox_page_table(VoxCtx* c, int32_t slot, int32_t* out, int32_t cap, int32_t* 
   const auto& pages = c->slot_pages[slot];
   const int n = static_cast<int>(pages.size());
   std::vector<int> dev(c->max_pages_per_slot);
+  CK(cudaStreamSynchronize(c->s_lm));  // admission copies are stream-ordered
   CK(cudaMemcpy(dev.data(), c->page_table + static_cast<int64_t>(slot) * c->max_pages_per_slot,
                 dev.size() * 4, cudaMemcpyDeviceToHost));
   for (int i = 0; i < n; ++i)
@@ -1019,6 +1062,24 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       CK(cudaMemcpy(logits_out, c->logits, sizeof(float) * static_cast<size_t>(nsamp) * g.vocab,
                     cudaMemcpyDeviceToHost));
   }
+  return VOX_OK;
+}
+
+int vox_forward_seq(VoxCtx* c, int64_t* seq) {
+  if (!c || !seq) return fail(c, VOX_ERR_INVALID, "null argument");
+  *seq = c->fwd_seq;
+  return VOX_OK;
+}
+
+int vox_forward_wait(VoxCtx* c, int64_t seq) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  if (seq <= 0) return VOX_OK;
+  const int ei = static_cast<int>(seq % static_cast<int64_t>(c->fwd_events.size()));
+  if (c->fwd_event_seq[ei] == seq) {
+    CK(cudaEventSynchronize(c->fwd_events[ei]));
+  } else if (seq > c->fwd_seq - static_cast<int64_t>(c->fwd_events.size())) {
+    return fail(c, VOX_ERR_INVALID, "unknown forward sequence number");
+  }  // older than the event ring: long complete (ring >> staging depth)
   return VOX_OK;
 }
 

@@ -134,6 +134,14 @@ class VoxDevice:
         self._check(self.lib.vox_forward(self.ctx, rp, n, flags, lp, tp))
         return toks, logits
 
+    def forward_seq(self) -> int:
+        s = C.c_int64()
+        self._check(self.lib.vox_forward_seq(self.ctx, C.byref(s)))
+        return s.value
+
+    def forward_wait(self, seq: int) -> None:
+        self._check(self.lib.vox_forward_wait(self.ctx, seq))
+
     def sample_logits(self, logits: np.ndarray, params: Sequence[Sampling], windows: Sequence[Sequence[int]],
                       seeds: Sequence[int], steps: Sequence[int], lo=None, hi=None) -> np.ndarray:
         logits = np.ascontiguousarray(logits, dtype=np.float32)
