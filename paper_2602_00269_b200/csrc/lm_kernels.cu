@@ -136,153 +136,6 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int spli
 }
 
 // ---------------------------------------------------------------------------
-// paged GQA decode attention.  One CTA per (row, kv head); the G = H/KV query
-// heads sharing the kv head are processed together so every K/V byte is read
-// once.  Each warp takes 4 tokens at a time (8 lanes per token, hd/8 dims per
-// lane, 16/32-byte vector loads, coalesced within the head-page), online
-// softmax in fp32, then a 4-warp merge through shared memory.
-// ---------------------------------------------------------------------------
-template <int HD, int G>
-__global__ void __launch_bounds__(128)
-    attn_decode_kernel(const RowDev* __restrict__ rows, const bf16* __restrict__ q,
-                       const bf16* __restrict__ kc, const bf16* __restrict__ vc,
-                       const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out) {
-  constexpr int DPL = HD / 8;  // dims per lane
-  __shared__ float s_m[4][G], s_l[4][G];
-  __shared__ float s_acc[4][G][HD];
-  const int r = blockIdx.x, kvh = blockIdx.y;
-  const RowDev rw = rows[r];
-  if (rw.slot < 0) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane >> 3, dl = (lane & 7) * DPL;
-  const int L = rw.pos + 1;
-  const float scale = 1.0f / sqrtf(static_cast<float>(HD));
-
-  float qv[G][DPL];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const bf16* qp = q + (static_cast<int64_t>(r) * dm.n_heads + kvh * G + g) * HD + dl;
-#pragma unroll
-    for (int j = 0; j < DPL; ++j) qv[g][j] = __bfloat162float(qp[j]);
-  }
-  float m[G], l[G], acc[G][DPL];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int j = 0; j < DPL; ++j) acc[g][j] = 0.f;
-  }
-  const int* pt = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
-  const int n_chunks = (L + 3) / 4;
-  for (int c = warp; c < n_chunks; c += 4) {
-    const int t = c * 4 + sub;
-    const bool valid = t < L;
-    float kf[DPL], vf[DPL];
-    if (valid) {
-      const int page = pt[t / dm.page_size];
-      const int64_t base =
-          ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + (t % dm.page_size)) *
-              HD +
-          dl;
-      const uint4* kp = reinterpret_cast<const uint4*>(kc + base);
-      const uint4* vp = reinterpret_cast<const uint4*>(vc + base);
-#pragma unroll
-      for (int j = 0; j < DPL / 8; ++j) {
-        const uint4 ku = kp[j], vu = vp[j];
-        const bf16* kb = reinterpret_cast<const bf16*>(&ku);
-        const bf16* vb = reinterpret_cast<const bf16*>(&vu);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          kf[j * 8 + e] = __bfloat162float(kb[e]);
-          vf[j * 8 + e] = __bfloat162float(vb[e]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) kf[j] = vf[j] = 0.f;
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float s = 0.f;
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) s = fmaf(qv[g][j], kf[j], s);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s = valid ? s * scale : -INFINITY;
-      float cm = fmaxf(s, __shfl_xor_sync(0xffffffffu, s, 8));
-      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
-      const float nm = fmaxf(m[g], cm);
-      const float corr = expf(m[g] - nm);  // m = -inf initially -> 0
-      const float pr = valid ? expf(s - nm) : 0.f;
-      l[g] = l[g] * corr + pr;
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) acc[g][j] = fmaf(pr, vf[j], acc[g][j] * corr);
-      m[g] = nm;
-    }
-  }
-  // merge the 4 token sub-groups inside the warp (same m per warp already)
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    l[g] += __shfl_xor_sync(0xffffffffu, l[g], 8);
-    l[g] += __shfl_xor_sync(0xffffffffu, l[g], 16);
-#pragma unroll
-    for (int j = 0; j < DPL; ++j) {
-      acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], 8);
-      acc[g][j] += __shfl_xor_sync(0xffffffffu, acc[g][j], 16);
-    }
-    if (lane == 0) {
-      s_m[warp][g] = m[g];
-      s_l[warp][g] = l[g];
-    }
-    if (sub == 0) {
-#pragma unroll
-      for (int j = 0; j < DPL; ++j) s_acc[warp][g][dl + j] = acc[g][j];
-    }
-  }
-  __syncthreads();
-  // merge the 4 warps: thread handles (g, dim) pairs
-  for (int idx = threadIdx.x; idx < G * HD; idx += 128) {
-    const int g = idx / HD, dd = idx % HD;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][g]);
-    float Ls = 0.f, A = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float f = (s_m[w][g] == -INFINITY) ? 0.f : expf(s_m[w][g] - M);
-      Ls += s_l[w][g] * f;
-      A += s_acc[w][g][dd] * f;
-    }
-    out[(static_cast<int64_t>(r) * dm.n_heads + kvh * G + g) * HD + dd] =
-        __float2bfloat16_rn(A / Ls);
-  }
-}
-
-template <int HD>
-static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16* kc,
-                            const bf16* vc, const int* pt, const LmDims& dm, bf16* out,
-                            cudaStream_t st) {
-  dim3 grid(n, dm.n_kv);
-  switch (dm.n_heads / dm.n_kv) {
-    case 1: attn_decode_kernel<HD, 1><<<grid, 128, 0, st>>>(rows, q, kc, vc, pt, dm, out); break;
-    case 2: attn_decode_kernel<HD, 2><<<grid, 128, 0, st>>>(rows, q, kc, vc, pt, dm, out); break;
-    case 3: attn_decode_kernel<HD, 3><<<grid, 128, 0, st>>>(rows, q, kc, vc, pt, dm, out); break;
-    case 4: attn_decode_kernel<HD, 4><<<grid, 128, 0, st>>>(rows, q, kc, vc, pt, dm, out); break;
-    default: break;  // rejected at vox_create
-  }
-}
-
-void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
-                        const int* page_table, const LmDims& dm, bf16* out, cudaStream_t st) {
-  if (dm.hd == 64)
-    attn_dispatch_g<64>(rows, n, q, kc, vc, page_table, dm, out, st);
-  else
-    attn_dispatch_g<128>(rows, n, q, kc, vc, page_table, dm, out, st);
-}
-
-// ---------------------------------------------------------------------------
 // split-K reduce + residual add + RMSNorm (optionally compacting output rows)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)

@@ -130,6 +130,7 @@ struct VoxCtx {
   bf16 *x = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr, *xf = nullptr;
   float* ws = nullptr;
   size_t ws_elems = 0;
+  float* attn_ws = nullptr;  // split-KV partials
   float* logits = nullptr;
   size_t logits_elems = 0;
   std::map<int, CUtensorMap> tm_x, tm_attn, tm_act, tm_xf;  // by BN
@@ -370,6 +371,12 @@ static int create_buffers(VoxCtx* c) {
   // split-K workspace: worst case splits * rows * max(N)
   const int maxN = std::max({c->nqkv, d, 2 * dff});
   c->ws_elems = static_cast<size_t>(16) * R * maxN;
+  {
+    const int grp = g.n_heads / g.n_kv_heads;
+    const size_t n = static_cast<size_t>(std::min(R, kAttnSplitRows)) * g.n_kv_heads *
+                     kAttnMaxSplits * grp * (g.head_dim + 2);
+    CK(dalloc(&c->attn_ws, n));
+  }
   CK(dalloc(&c->ws, c->ws_elems));
   const int head_cols = g.audio_base >= 0 ? c->head_audio_rows : g.vocab;
   const int full_rows = std::min(R, 256);
@@ -603,9 +610,10 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
                              c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
     }
     {
-      TimedLaunch tl(c, st, "attn", c->step_attn_bytes);
+      const int asp = attn_pick_splits(nrows, g.n_kv_heads);
+      TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
-                         c->page_table, dm, c->attn, st);
+                         c->page_table, dm, c->attn, c->attn_ws, asp, st);
     }
     RET(run_gemm(c, c->tm_o[l], c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st));
@@ -691,7 +699,7 @@ static int validate_cfg(const VoxModelCfg* g) {
   const int grp = g->n_heads / g->n_kv_heads;
   if (grp < 1 || grp > 4) return 0;
   if ((g->n_heads * g->head_dim) % 64) return 0;
-  if (g->page_size % 4 || g->max_rows < 1 || g->max_rows > 2048) return 0;
+  if (g->page_size % 8 || g->max_rows < 1 || g->max_rows > 2048) return 0;  // 8-token chunks
   if (g->max_slots < 1 || g->n_pages < 1 || g->max_ctx < 2) return 0;
   if (g->detok_enabled) {
     if (g->audio_base < 0 || g->n_rates != 4 || g->latent_dim % 64 || g->decoder_dim % 1024)
@@ -764,7 +772,7 @@ void vox_destroy(VoxCtx* c) {
   }
   void* dev_ptrs[] = {c->emb, c->norm_attn, c->norm_mlp, c->norm_final, c->w_qkv, c->w_o,
                       c->w_gu, c->w_down, c->inv_freq, c->h, c->x, c->xf, c->q, c->attn, c->act,
-                      c->ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
+                      c->ws, c->attn_ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
                       c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->d_sample_rows,
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
