@@ -28,6 +28,8 @@ __global__ void __launch_bounds__(128)
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
                        float* __restrict__ ws, int n_split) {
+  griddep_wait();
+  griddep_launch();
   constexpr int KSEG = HD / 32;  // 16-byte K segments per lane
   constexpr int VPL = HD / 32;   // output dims per lane
   __shared__ __align__(16) float s_q[G][HD];
@@ -208,6 +210,8 @@ template <int HD, int G>
 __global__ void __launch_bounds__(128)
     attn_combine_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, LmDims dm,
                         int n_split, bf16* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   const int r = blockIdx.x, kvh = blockIdx.y;
   if (rows[r].slot < 0) return;
   const float* base = ws + (static_cast<int64_t>(r) * dm.n_kv + kvh) * n_split * G * (HD + 2);
@@ -231,9 +235,9 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
                         const int* pt, const LmDims& dm, bf16* out, float* ws, int n_split,
                         cudaStream_t st) {
   dim3 grid(n, dm.n_kv, n_split);
-  attn_decode_kernel<HD, G><<<grid, 128, 0, st>>>(rows, q, kc, vc, pt, dm, out, ws, n_split);
+  launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(128), 0, st, rows, q, kc, vc, pt, dm, out, ws, n_split);
   if (n_split > 1)
-    attn_combine_kernel<HD, G><<<dim3(n, dm.n_kv), 128, 0, st>>>(rows, ws, dm, n_split, out);
+    launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split, out);
 }
 
 template <int HD>

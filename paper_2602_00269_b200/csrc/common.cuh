@@ -184,6 +184,11 @@ VOX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 VOX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Programmatic dependent launch: wait for the preceding grid's completion
+// (and memory flush) / allow the next grid to start its prologue.
+VOX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+VOX_DEV void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 VOX_DEV bool elect_one() {
   uint32_t pred = 0;
   asm volatile(

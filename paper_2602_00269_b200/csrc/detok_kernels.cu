@@ -67,6 +67,8 @@ __global__ void __launch_bounds__(256)
                      const int* __restrict__ token_store, const bf16* __restrict__ tabs,
                      const float* __restrict__ dw_w, const float* __restrict__ dw_b,
                      float* __restrict__ state, DetokDims dd, bf16* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x;
   if (row >= hdr->n_lat) return;
   const int ri = find_req(reqs, hdr->n_req, row);
@@ -96,7 +98,7 @@ void launch_vq_dwconv(const DetokReq* reqs, int n_req, int n_lat, const int* tok
                       const DetokDims& dd, bf16* out_bf16, cudaStream_t st) {
   const ReqHdr* hdr = reinterpret_cast<const ReqHdr*>(reqs) - 1;
   (void)n_req;
-  vq_dwconv_kernel<<<n_lat, 256, 0, st>>>(hdr, reqs, token_store, tabs, dw_w, dw_b, state, dd,
+  launch_k(vq_dwconv_kernel, dim3(n_lat), dim3(256), 0, st, hdr, reqs, token_store, tabs, dw_w, dw_b, state, dd,
                                           out_bf16);
 }
 
@@ -107,6 +109,8 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ x, int C, const float* __restrict__ alpha,
                        float* __restrict__ state, int64_t st_off, DetokDims dd,
                        bf16* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x;
   if (row >= hdr->n_lat * up) return;
   const int ri = find_req(reqs, hdr->n_req, row / up);
@@ -132,7 +136,7 @@ void launch_snake_upcat(const DetokReq* reqs, int n_req, int rows, int up_before
                         const DetokDims& dd, bf16* out_cat, cudaStream_t st) {
   const ReqHdr* hdr = reinterpret_cast<const ReqHdr*>(reqs) - 1;
   (void)n_req;
-  snake_upcat_kernel<<<rows, 256, 0, st>>>(hdr, reqs, up_before, x, C, alpha, state, st_off, dd,
+  launch_k(snake_upcat_kernel, dim3(rows), dim3(256), 0, st, hdr, reqs, up_before, x, C, alpha, state, st_off, dd,
                                            out_cat);
 }
 
@@ -144,6 +148,8 @@ __global__ void __launch_bounds__(128)
                    const float* __restrict__ dw_w, const float* __restrict__ dw_b,
                    const float* __restrict__ alpha2, float* __restrict__ state, int64_t st_off,
                    DetokDims dd, bf16* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   const int row = blockIdx.x;
   if (row >= hdr->n_lat * up) return;
   const int ri = find_req(reqs, hdr->n_req, row / up);
@@ -175,7 +181,7 @@ void launch_ru_prep(const DetokReq* reqs, int n_req, int rows, int up, const flo
                     bf16* out, cudaStream_t st) {
   const ReqHdr* hdr = reinterpret_cast<const ReqHdr*>(reqs) - 1;
   (void)n_req;
-  ru_prep_kernel<<<rows, 128, 0, st>>>(hdr, reqs, up, x, C, dil, alpha1, dw_w, dw_b, alpha2,
+  launch_k(ru_prep_kernel, dim3(rows), dim3(128), 0, st, hdr, reqs, up, x, C, dil, alpha1, dw_w, dw_b, alpha2,
                                        state, st_off, dd, out);
 }
 
@@ -186,6 +192,8 @@ __global__ void __launch_bounds__(256)
                      const float* __restrict__ x, int C, const float* __restrict__ alpha,
                      const float* __restrict__ w, float b, float* __restrict__ state,
                      int64_t st_off, DetokDims dd, float* __restrict__ pcm) {
+  griddep_wait();
+  griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + warp;
   if (row >= hdr->n_lat * up) return;
@@ -218,7 +226,7 @@ void launch_detok_out(const DetokReq* reqs, int n_req, int rows, int up, const f
                       const DetokDims& dd, float* pcm, cudaStream_t st) {
   const ReqHdr* hdr = reinterpret_cast<const ReqHdr*>(reqs) - 1;
   (void)n_req;
-  detok_out_kernel<<<(rows + 7) / 8, 256, 0, st>>>(hdr, reqs, up, x, C, alpha, w, b, state,
+  launch_k(detok_out_kernel, dim3((rows + 7) / 8), dim3(256), 0, st, hdr, reqs, up, x, C, alpha, w, b, state,
                                                    st_off, dd, pcm);
 }
 

@@ -66,13 +66,26 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  griddep_launch();  // let the next kernel start its own prologue
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
     const uint64_t pol_x = policy_evict_last();   // activations: re-read by every CTA
-    for (int i = 0; i < nkb; ++i) {
+    // Weights do not depend on the preceding kernel: fill the first stages'
+    // weight tiles BEFORE the grid-dependency wait (overlaps the previous
+    // kernel's tail), then load the activation tiles.
+    const int pre = nkb < C::kStages ? nkb : C::kStages;
+    for (int i = 0; i < pre; ++i) {
+      mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+      tma_load_2d(smem + i * C::kStageBytes, &tmW, &full[i], (kb0 + i) * 64, m0, pol_w);
+    }
+    griddep_wait();
+    for (int i = 0; i < pre; ++i)
+      tma_load_2d(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], (kb0 + i) * 64, n0,
+                  pol_x);
+    for (int i = pre; i < nkb; ++i) {
       const int s = i % C::kStages;
-      if (i >= C::kStages) mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
+      mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
       uint8_t* st = smem + s * C::kStageBytes;
       mbar_arrive_expect_tx(&full[s], C::kStageBytes);
       const int kx = (kb0 + i) * 64;
@@ -100,6 +113,7 @@ __global__ void __launch_bounds__(128, 1)
   __syncwarp();
 
   // ---------------- epilogue: TMEM -> registers -> global ----------------
+  griddep_wait();  // outputs may alias buffers the preceding kernel was reading
   mbar_wait(done, 0);
   tc_fence_after();
   const int m = m0 + warp * 32 + lane;
@@ -176,8 +190,7 @@ static cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const
     attr_set = true;
   }
   dim3 grid((a.M + 127) / 128, (a.N + BN - 1) / BN, splits);
-  gemm_bf16_tc_kernel<BN><<<grid, 128, C::kSmemBytes, st>>>(tw, tx, a);
-  return cudaGetLastError();
+  return launch_k(gemm_bf16_tc_kernel<BN>, grid, dim3(128), C::kSmemBytes, st, tw, tx, a);
 }
 
 int gemm_bn_for_rows(int rows) {
@@ -188,13 +201,25 @@ int gemm_bn_for_rows(int rows) {
   return 256;
 }
 
-// Split-K factor: fill ~2 CTAs per SM worth of tiles, each split >= 2 k-blocks.
+// Tile width over the activation rows (UMMA N).  Measured on B200 at the
+// Orpheus-3B shapes (scripts/gemm_sweep.py, profiles/gemm_sweep_r01.txt):
+// one 256-wide tile is L2/latency-limited (every CTA re-reads the whole
+// activation slab), so large batches use 128-wide tiles, and 64-wide ones
+// when the weight matrix has few 128-row tiles (d_model outputs).
+int gemm_plan_bn(int M, int rows) {
+  int bn = gemm_bn_for_rows(rows);
+  if (bn > 128) bn = 128;
+  if (rows >= 128 && M <= 4096) bn = 64;
+  return bn;
+}
+
+// Split-K factor: ~2 CTAs per SM (2 x 148 slots), each split >= 2 k-blocks.
 int gemm_pick_splits(int M, int N, int K, int max_splits) {
-  const int bn = gemm_bn_for_rows(N);
+  const int bn = gemm_plan_bn(M, N);
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int n_kb = K / 64;
   int best = 1;
-  const int target = bn >= 256 ? kNumSMs : 2 * kNumSMs;
+  const int target = 2 * kNumSMs;
   for (int s = 1; s <= max_splits; ++s) {
     const int per = (n_kb + s - 1) / s;
     if (per < 2) break;

@@ -11,6 +11,26 @@ namespace vox {
 
 using bf16 = __nv_bfloat16;
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// while its predecessor drains; every kernel calls griddep_wait() before it
+// touches data produced upstream.  Captured into CUDA graphs as programmatic
+// dependency edges.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- GEMM
 struct GemmArgs {
   int M, N, K;            // out features, rows, reduction
@@ -27,6 +47,7 @@ struct GemmArgs {
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                     uint64_t row_stride_bytes, uint32_t box_outer);
 int gemm_bn_for_rows(int rows);
+int gemm_plan_bn(int M, int rows);
 int gemm_pick_splits(int M, int N, int K, int max_splits);
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, cudaStream_t st);
@@ -52,7 +73,7 @@ struct LmDims {
 void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x, cudaStream_t st);
 void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int splits,
-                            int64_t split_stride, const LmDims& dm, const float* inv_freq,
+                            int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st);
 constexpr int kAttnMaxSplits = 8;    // split-KV factor cap

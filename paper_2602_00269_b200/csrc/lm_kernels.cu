@@ -1,5 +1,11 @@
-// lm_kernels.cu — the fused elementwise / attention kernels of one decode step.
+// lm_kernels.cu — fused elementwise kernels of one decode step (K5).
 //
+// Each follows a tcgen05 GEMM and folds its split-K reduction into the op
+// that consumes it, with 16-byte vector loads (one CTA per row, 256 threads):
+//   embed_norm        embedding gather + first RMSNorm
+//   qkv_rope_append   QKV split-K reduce + RoPE (table) + paged KV append
+//   resid_norm        O/down split-K reduce + residual add + RMSNorm
+//   silu_mul          gate|up split-K reduce + SiLU(gate) * up
 // Layouts (HBM):
 //   h        [rows, d]            fp32 residual stream
 //   x        [rows, d]            bf16 GEMM input (normalised)
@@ -14,22 +20,43 @@
 
 namespace vox {
 
-template <int NT>
-VOX_DEV float block_sum(float v, float* red) {
+VOX_DEV float block_sum256(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  float t = 0.f;
   if (threadIdx.x < 32) {
-    t = (l < NT / 32) ? red[l] : 0.f;
+    float t = (l < 8) ? red[l] : 0.f;
     t = warp_sum(t);
-    if (l == 0) red[32] = t;
+    if (l == 0) red[8] = t;
   }
   __syncthreads();
-  t = red[32];
-  __syncthreads();
-  return t;
+  return red[8];
+}
+
+VOX_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
+
+// sum of the split-K partial planes at float4 index i (fixed split order)
+VOX_DEV float4 sum_splits4(const float4* __restrict__ w, int splits, int64_t split_stride4,
+                           int64_t i) {
+  float4 a = w[i];
+  for (int s = 1; s < splits; ++s) a = add4(a, w[s * split_stride4 + i]);
+  return a;
+}
+
+VOX_DEV void store_bf16x4(bf16* dst, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
+  __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = u;
+}
+
+// x = bf16(h * inv * w) in the oracle's rounding order (two fp32 products)
+VOX_DEV void norm_store4(bf16* x, float4 h, float inv, float4 w) {
+  store_bf16x4(x, __fmul_rn(__fmul_rn(h.x, inv), w.x), __fmul_rn(__fmul_rn(h.y, inv), w.y),
+               __fmul_rn(__fmul_rn(h.z, inv), w.z), __fmul_rn(__fmul_rn(h.w, inv), w.w));
 }
 
 // ---------------------------------------------------------------------------
@@ -41,7 +68,9 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restric
                                                          const float* __restrict__ nw, int d,
                                                          float eps, float* __restrict__ h,
                                                          bf16* __restrict__ x) {
-  __shared__ float red[33];
+  griddep_wait();
+  griddep_launch();
+  __shared__ float red[9];
   const int r = blockIdx.x;
   const RowDev rw = rows[r];
   if (rw.slot < 0) return;
@@ -53,86 +82,98 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restric
     tok = *ts;
   }
   const bf16* e = emb + static_cast<int64_t>(tok) * d;
-  float* hr = h + static_cast<int64_t>(r) * d;
+  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
+  const int d4 = d / 4;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    const float v = __bfloat162float(e[i]);
-    hr[i] = v;
-    ss = fmaf(v, v, ss);
+  for (int i = threadIdx.x; i < d4; i += 256) {
+    const uint2 u = *reinterpret_cast<const uint2*>(e + 4 * i);
+    const bf16* b = reinterpret_cast<const bf16*>(&u);
+    const float4 v = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]),
+                                 __bfloat162float(b[2]), __bfloat162float(b[3]));
+    h4[i] = v;
+    ss = fmaf(v.x, v.x, ss);
+    ss = fmaf(v.y, v.y, ss);
+    ss = fmaf(v.z, v.z, ss);
+    ss = fmaf(v.w, v.w, ss);
   }
-  ss = block_sum<256>(ss, red);
+  ss = block_sum256(ss, red);
   const float inv = 1.0f / sqrtf(ss / static_cast<float>(d) + eps);
+  const float4* w4 = reinterpret_cast<const float4*>(nw);
   bf16* xr = x + static_cast<int64_t>(r) * d;
-  for (int i = threadIdx.x; i < d; i += 256)
-    xr[i] = __float2bfloat16_rn(__fmul_rn(__fmul_rn(hr[i], inv), nw[i]));
+  for (int i = threadIdx.x; i < d4; i += 256) norm_store4(xr + 4 * i, h4[i], inv, w4[i]);
 }
 
 void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x,
                        cudaStream_t st) {
-  embed_norm_kernel<<<n, 256, 0, st>>>(rows, token_store, max_ctx, emb, norm_w, dm.d, dm.eps, h,
-                                       x);
+  launch_k(embed_norm_kernel, dim3(n), dim3(256), 0, st, rows, token_store, max_ctx, emb, norm_w,
+           dm.d, dm.eps, h, x);
 }
 
 // ---------------------------------------------------------------------------
-// split-K reduce of the QKV projection + RoPE + paged KV append
+// split-K reduce of the QKV projection + RoPE + paged KV append.
+// rope[pos][i] = (cos, sin) of float(pos) * inv_freq[i] (fp64 -> fp32 table).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     qkv_rope_append_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws,
                            int splits, int64_t split_stride, LmDims dm,
-                           const float* __restrict__ inv_freq, const int* __restrict__ page_table,
+                           const float2* __restrict__ rope, const int* __restrict__ page_table,
                            bf16* __restrict__ kc, bf16* __restrict__ vc, bf16* __restrict__ q_out) {
+  griddep_wait();
+  griddep_launch();
   const int r = blockIdx.x;
   const RowDev rw = rows[r];
   if (rw.slot < 0) return;
   const int hd = dm.hd, half = hd / 2;
   const int nqkv = (dm.n_heads + 2 * dm.n_kv) * hd;
-  const float* wr = ws + static_cast<int64_t>(r) * nqkv;
+  const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * nqkv);
+  const int64_t ss4 = split_stride / 4;
   const int page = page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot +
                               rw.pos / dm.page_size];
   const int off = rw.pos % dm.page_size;
-  const int n_pairs = (dm.n_heads + dm.n_kv) * half;
-  for (int p = threadIdx.x; p < n_pairs; p += 256) {
-    const int head = p / half, i = p % half;
-    const int col = head * hd + i;
-    float x1 = 0.f, x2 = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      x1 += wr[s * split_stride + col];
-      x2 += wr[s * split_stride + col + half];
+  const float2* rp = rope + static_cast<int64_t>(rw.pos) * half;
+  // rotated heads (q then k): thread handles 4 consecutive pair indices i..i+3
+  const int q4 = half / 4;
+  const int n_items = (dm.n_heads + dm.n_kv) * q4;
+  for (int it = threadIdx.x; it < n_items; it += 256) {
+    const int head = it / q4, i = (it % q4) * 4;
+    const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
+    const float4 a = sum_splits4(w4, splits, ss4, c1);
+    const float4 b = sum_splits4(w4, splits, ss4, c2);
+    const float x1[4] = {a.x, a.y, a.z, a.w}, x2[4] = {b.x, b.y, b.z, b.w};
+    float o1[4], o2[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 cs = rp[i + e];
+      o1[e] = __fsub_rn(__fmul_rn(x1[e], cs.x), __fmul_rn(x2[e], cs.y));
+      o2[e] = __fadd_rn(__fmul_rn(x2[e], cs.x), __fmul_rn(x1[e], cs.y));
     }
-    const float ang = __fmul_rn(static_cast<float>(rw.pos), inv_freq[i]);
-    double sn, cs;
-    sincos(static_cast<double>(ang), &sn, &cs);
-    const float c = static_cast<float>(cs), sv = static_cast<float>(sn);
-    const float o1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sv));
-    const float o2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, sv));
+    bf16* dst;
     if (head < dm.n_heads) {
-      bf16* q = q_out + (static_cast<int64_t>(r) * dm.n_heads + head) * hd;
-      q[i] = __float2bfloat16_rn(o1);
-      q[i + half] = __float2bfloat16_rn(o2);
+      dst = q_out + (static_cast<int64_t>(r) * dm.n_heads + head) * hd;
     } else {
       const int kvh = head - dm.n_heads;
-      bf16* k = kc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + off) * hd;
-      k[i] = __float2bfloat16_rn(o1);
-      k[i + half] = __float2bfloat16_rn(o2);
+      dst = kc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + off) * hd;
     }
+    store_bf16x4(dst + i, o1[0], o1[1], o1[2], o1[3]);
+    store_bf16x4(dst + i + half, o2[0], o2[1], o2[2], o2[3]);
   }
-  const int vbase = (dm.n_heads + dm.n_kv) * hd;
-  for (int e = threadIdx.x; e < dm.n_kv * hd; e += 256) {
-    float v = 0.f;
-    for (int s = 0; s < splits; ++s) v += wr[s * split_stride + vbase + e];
-    const int kvh = e / hd, dd = e % hd;
-    vc[((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + off) * hd + dd] =
-        __float2bfloat16_rn(v);
+  const int vbase4 = (dm.n_heads + dm.n_kv) * hd / 4;
+  const int hd4 = hd / 4;
+  for (int e = threadIdx.x; e < dm.n_kv * hd4; e += 256) {
+    const float4 v = sum_splits4(w4, splits, ss4, vbase4 + e);
+    const int kvh = e / hd4, dd = (e % hd4) * 4;
+    store_bf16x4(vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + off) * hd + dd,
+                 v.x, v.y, v.z, v.w);
   }
 }
 
 void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int splits,
-                            int64_t split_stride, const LmDims& dm, const float* inv_freq,
+                            int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
-  qkv_rope_append_kernel<<<n, 256, 0, st>>>(rows, ws, splits, split_stride, dm, inv_freq,
-                                            page_table, kc, vc, q_out);
+  launch_k(qkv_rope_append_kernel, dim3(n), dim3(256), 0, st, rows, ws, splits, split_stride, dm,
+           rope, page_table, kc, vc, q_out);
 }
 
 // ---------------------------------------------------------------------------
@@ -143,59 +184,72 @@ __global__ void __launch_bounds__(256)
                       int64_t split_stride, int d, float eps, float* __restrict__ h,
                       const float* __restrict__ nw, bf16* __restrict__ x_out,
                       const int* __restrict__ out_index) {
-  __shared__ float red[33];
+  griddep_wait();
+  griddep_launch();
+  __shared__ float red[9];
   const int r = blockIdx.x;
   if (rows[r].slot < 0) return;
-  float* hr = h + static_cast<int64_t>(r) * d;
-  const float* wr = ws + static_cast<int64_t>(r) * d;
+  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
+  const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * d);
+  const int64_t ss4 = split_stride / 4;
+  const int d4 = d / 4;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += 256) {
-    float a = 0.f;
-    for (int s = 0; s < splits; ++s) a += wr[s * split_stride + i];
-    const float v = hr[i] + a;
-    hr[i] = v;
-    ss = fmaf(v, v, ss);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < d4; i += 256) {
+    const float4 v = add4(h4[i], sum_splits4(w4, splits, ss4, i));
+    h4[i] = v;
+    ss = fmaf(v.x, v.x, ss);
+    ss = fmaf(v.y, v.y, ss);
+    ss = fmaf(v.z, v.z, ss);
+    ss = fmaf(v.w, v.w, ss);
   }
-  ss = block_sum<256>(ss, red);
+  ss = block_sum256(ss, red);
   const int orow = out_index ? out_index[r] : r;
   if (orow < 0) return;
   const float inv = 1.0f / sqrtf(ss / static_cast<float>(d) + eps);
+  const float4* n4 = reinterpret_cast<const float4*>(nw);
   bf16* xr = x_out + static_cast<int64_t>(orow) * d;
-  for (int i = threadIdx.x; i < d; i += 256)
-    xr[i] = __float2bfloat16_rn(__fmul_rn(__fmul_rn(hr[i], inv), nw[i]));
+  for (int i = threadIdx.x; i < d4; i += 256) norm_store4(xr + 4 * i, h4[i], inv, n4[i]);
 }
 
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st) {
-  resid_norm_kernel<<<n, 256, 0, st>>>(rows, ws, splits, split_stride, dm.d, dm.eps, h, norm_w,
-                                       x_out, out_index);
+  launch_k(resid_norm_kernel, dim3(n), dim3(256), 0, st, rows, ws, splits, split_stride, dm.d,
+           dm.eps, h, norm_w, x_out, out_index);
 }
 
 // ---------------------------------------------------------------------------
 // split-K reduce of gate|up + SiLU(gate) * up
 // ---------------------------------------------------------------------------
+VOX_DEV float silu_mul1(float g, float u) {
+  return __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+}
+
 __global__ void __launch_bounds__(256)
     silu_mul_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, int splits,
                     int64_t split_stride, int dff, bf16* __restrict__ a_out) {
+  griddep_wait();
+  griddep_launch();
   const int r = blockIdx.x;
   if (rows[r].slot < 0) return;
-  const float* wr = ws + static_cast<int64_t>(r) * 2 * dff;
+  const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * 2 * dff);
+  const int64_t ss4 = split_stride / 4;
+  const int f4 = dff / 4;
   bf16* ar = a_out + static_cast<int64_t>(r) * dff;
-  for (int j = threadIdx.x; j < dff; j += 256) {
-    float g = 0.f, u = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      g += wr[s * split_stride + j];
-      u += wr[s * split_stride + dff + j];
-    }
-    const float sg = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    ar[j] = __float2bfloat16_rn(__fmul_rn(sg, u));
+#pragma unroll 4
+  for (int j = threadIdx.x; j < f4; j += 256) {
+    const float4 g = sum_splits4(w4, splits, ss4, j);
+    const float4 u = sum_splits4(w4, splits, ss4, f4 + j);
+    store_bf16x4(ar + 4 * j, silu_mul1(g.x, u.x), silu_mul1(g.y, u.y), silu_mul1(g.z, u.z),
+                 silu_mul1(g.w, u.w));
   }
 }
 
 void launch_silu_mul(const RowDev* rows, int n, const float* ws, int splits, int64_t split_stride,
                      const LmDims& dm, bf16* a_out, cudaStream_t st) {
-  silu_mul_kernel<<<n, 256, 0, st>>>(rows, ws, splits, split_stride, dm.dff, a_out);
+  launch_k(silu_mul_kernel, dim3(n), dim3(256), 0, st, rows, ws, splits, split_stride, dm.dff,
+           a_out);
 }
 
 }  // namespace vox

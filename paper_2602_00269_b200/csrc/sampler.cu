@@ -446,6 +446,8 @@ __global__ void __launch_bounds__(kST)
     sample_desc_kernel(const float* __restrict__ logits, const SampRowDesc* __restrict__ rows,
                        const int* __restrict__ window_ids, int* __restrict__ out,
                        int* __restrict__ err_flag) {
+  griddep_wait();
+  griddep_launch();
   extern __shared__ uint32_t dyn_bm[];
   __shared__ SampSmem S;
   const SampRowDesc d = rows[blockIdx.x];
@@ -455,6 +457,8 @@ __global__ void __launch_bounds__(kST)
 }
 
 __global__ void __launch_bounds__(kST) sample_fused_kernel(SampFusedArgs a) {
+  griddep_wait();
+  griddep_launch();
   extern __shared__ uint32_t dyn_bm[];
   __shared__ SampSmem S;
   __shared__ int wbuf[kMaxWin];
@@ -497,7 +501,7 @@ void launch_sample_fused(const SampFusedArgs& a, cudaStream_t st) {
   if (a.n_sample <= 0) return;
   const int span = a.audio_base >= 0 ? a.codebook_size : a.vocab;
   const size_t bm_bytes = static_cast<size_t>((span + 31) / 32) * 4;
-  sample_fused_kernel<<<a.n_sample, kST, bm_bytes, st>>>(a);
+  launch_k(sample_fused_kernel, dim3(a.n_sample), dim3(kST), bm_bytes, st, a);
 }
 
 void launch_sample_desc(const float* logits, const SampRowDesc* rows, int n,
@@ -505,7 +509,7 @@ void launch_sample_desc(const float* logits, const SampRowDesc* rows, int n,
                         cudaStream_t st) {
   if (n <= 0) return;
   const size_t bm_bytes = static_cast<size_t>((max_span + 31) / 32) * 4;
-  sample_desc_kernel<<<n, kST, bm_bytes, st>>>(logits, rows, window_ids, tokens_out, err_flag);
+  launch_k(sample_desc_kernel, dim3(n), dim3(kST), bm_bytes, st, logits, rows, window_ids, tokens_out, err_flag);
 }
 
 }  // namespace vox

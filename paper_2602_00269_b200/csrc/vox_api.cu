@@ -121,6 +121,7 @@ struct VoxCtx {
   float *norm_attn = nullptr, *norm_mlp = nullptr, *norm_final = nullptr;
   bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
   float* inv_freq = nullptr;
+  float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
   std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
   CUtensorMap tm_head_full{}, tm_head_audio{};
   int head_audio_rows = 0;
@@ -259,7 +260,11 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm") {
-  const int bn = gemm_bn_for_rows(rows);
+  int bn = gemm_plan_bn(M, rows);
+  if (const char* e = getenv("VOX_GEMM_BN_TEST")) {  // microbenchmarks only
+    const int f = atoi(e);
+    if (f == 16 || f == 32 || f == 64 || f == 128 || f == 256) bn = f;
+  }
   GemmArgs a{};
   a.M = M;
   a.N = rows;
@@ -332,6 +337,20 @@ static int create_backbone(VoxCtx* c) {
                                                (2.0 * i) / static_cast<double>(hd)));
   CK(dalloc(&c->inv_freq, inv.size()));
   CK(cudaMemcpy(c->inv_freq, inv.data(), inv.size() * 4, cudaMemcpyHostToDevice));
+  // (cos, sin) table: angle = float(pos) * inv_freq[i] in fp32, trig in fp64,
+  // rounded to fp32 (oracle/llama.py:rope computes the identical values)
+  {
+    std::vector<float2> tab(static_cast<size_t>(g.max_ctx) * (hd / 2));
+    for (int p = 0; p < g.max_ctx; ++p)
+      for (int i = 0; i < hd / 2; ++i) {
+        const float ang = static_cast<float>(p) * inv[i];
+        tab[static_cast<size_t>(p) * (hd / 2) + i] =
+            make_float2(static_cast<float>(std::cos(static_cast<double>(ang))),
+                        static_cast<float>(std::sin(static_cast<double>(ang))));
+      }
+    CK(dalloc(&c->rope_tab, tab.size()));
+    CK(cudaMemcpy(c->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+  }
 
   c->tm_qkv.resize(L);
   c->tm_o.resize(L);
@@ -606,7 +625,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * sp_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws, sp_qkv,
-                             static_cast<int64_t>(nrows) * c->nqkv, dm, c->inv_freq,
+                             static_cast<int64_t>(nrows) * c->nqkv, dm, c->rope_tab,
                              c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
     }
     {
@@ -771,7 +790,7 @@ void vox_destroy(VoxCtx* c) {
     cudaEventDestroy(t.b);
   }
   void* dev_ptrs[] = {c->emb, c->norm_attn, c->norm_mlp, c->norm_final, c->w_qkv, c->w_o,
-                      c->w_gu, c->w_down, c->inv_freq, c->h, c->x, c->xf, c->q, c->attn, c->act,
+                      c->w_gu, c->w_down, c->inv_freq, c->rope_tab, c->h, c->x, c->xf, c->q, c->attn, c->act,
                       c->ws, c->attn_ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
                       c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->d_sample_rows,
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
