@@ -186,7 +186,7 @@ def steady_state_steps(dev, B: int, steps: int, warmup: int, prompt: int, seed: 
     ev_dt = torch.cuda.Event(enable_timing=True)
     st0 = eng.stats
     dec0, chunks0, pcm0 = st0.decode_rows, len(eng.trace.chunks), st0.pcm_samples
-    rows0, dcalls0 = st0.lm_rows, st0.detok_calls
+    rows0, dcalls0, wait0 = st0.lm_rows, st0.detok_calls, st0.wait_s
     launches0 = dev.launch_count()
     ev0.record(s_lm)
     s_dt.wait_event(ev0)
@@ -207,9 +207,29 @@ def steady_state_steps(dev, B: int, steps: int, warmup: int, prompt: int, seed: 
     rows = st.lm_rows - rows0
     out = dict(decoded=decoded, chunks=chunks, pcm_samples=pcm, dev_ms=dev_ms, wall_s=t_wall,
                launches=dev.launch_count() - launches0, rows=rows, detok_calls=st.detok_calls - dcalls0,
-               token_rate=prof.token_rate, live=len(eng.live), host_s=st.host_s)
+               token_rate=prof.token_rate, live=len(eng.live), wait_s=st.wait_s - wait0)
+    # pure device time of one graph-captured LM step at this batch (no host in the loop)
+    live = list(eng.live.values())[: max(1, args_batch_decode(B))]
+    rows_np = np.asarray([[r.slot, r.req.prompt_tokens - 1 + r.req.tokens_generated - 1, -1, 1] for r in live],
+                         np.int32)
+    for _ in range(3):
+        dev.forward(rows_np)
+    ea = torch.cuda.Event(enable_timing=True)
+    eb = torch.cuda.Event(enable_timing=True)
+    ea.record(s_lm)
+    for _ in range(10):
+        dev.forward(rows_np)
+    eb.record(s_lm)
+    torch.cuda.synchronize()
+    out["lm_graph_step_ms"] = ea.elapsed_time(eb) / 10
+    out["lm_graph_rows"] = len(live)
     eng.shutdown()
     return out
+
+
+def args_batch_decode(B: int) -> int:
+    """Decode rows of a steady-state iteration: 7 of every 8 streams (1 in 8 is detokenizing)."""
+    return B - B // 8
 
 
 def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: float):
@@ -393,6 +413,9 @@ def main():
             "slo": slo,
             "detail": {"tokens_decoded": decoded, "chunks": chunks, "pcm_samples": pcm,
                        "device_ms": round(dev_ms, 3), "wall_s": round(wall_s, 4),
+                       "host_blocked_ms_per_step": round(res["wait_s"] * 1000 / steps, 3),
+                       "lm_graph_step_ms": round(res["lm_graph_step_ms"], 4),
+                       "lm_graph_rows": res["lm_graph_rows"],
                        "req_s_equiv": round(decoded / res["token_rate"] / (688 / res["token_rate"]) / (dev_ms / 1000), 2)},
         }
         print(json.dumps(line))

@@ -107,7 +107,7 @@ def orpheus3b(**kw) -> ModelConfig:
     """Config 2: Orpheus-3B-style (Llama-3.2-3B backbone + SNAC-24k-style decoder)."""
     base = ModelConfig(
         name="orpheus-3b", n_layers=28, d_model=3072, n_heads=24, n_kv_heads=8, head_dim=128,
-        d_ff=8192, max_slots=320, max_ctx=768, max_rows=1024, max_detok_frames=1024,
+        d_ff=8192, max_slots=512, max_ctx=768, max_rows=1024, max_detok_frames=1024,
     )
     return replace(base, **kw)
 

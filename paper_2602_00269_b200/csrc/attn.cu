@@ -2,25 +2,55 @@
 //
 // One CTA (4 warps) per (row, kv head, kv split).  The G = H/KV query heads
 // that share a kv head are processed together, so every K/V byte is read from
-// HBM exactly once per step.  A warp consumes chunks of 8 tokens (a chunk
-// never straddles a page since page_size % 8 == 0), two chunks per iteration
-// so ~8 KB of K/V loads are in flight per warp:
-//   * QK: 4 lanes per token, 4 x 16-byte K segments per lane (the warp reads
-//     8 consecutive 256-byte token rows of the head-page = fully used
-//     sectors); q is staged once in fp32 shared memory pre-scaled by
-//     log2(e)/sqrt(hd) (segment offsets 32*i + 8*ks -> conflict-free LDS.128);
-//     2 shuffles reduce the dot, 3 give the chunk max (online softmax, exp2);
-//   * PV: lane owns hd/32 output dims for all 8 tokens (8-byte V loads, one
-//     256-byte row per warp instruction); p is broadcast through 96 bytes of
-//     per-warp shared memory instead of 24 shuffles.
-// Low register count (no q / K-row register arrays) -> 4+ CTAs per SM.
-// Small batches split the context across blockIdx.z (fixed split count per
-// launch, so the step stays graph-capturable) and a combine pass merges the
-// partial (m, l, acc) triples.
+// HBM exactly once per step.
+//
+// Data movement: thread 0 streams whole head-pages (K page [ps][hd] and the
+// TRANSPOSED V page [hd][ps], 4 KB each at ps=16, hd=128) into a 3-stage
+// shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier
+// transaction counts), 4 pages (64 tokens, 32 KB) per stage, so ~96 KB per CTA
+// is in flight independent of registers.
+//
+// Math on tensor cores (mma.sync m16n8k16 bf16 -> fp32), one page per warp per
+// stage, fragments loaded with single vector loads thanks to consistent
+// permutations (a dot product is invariant to permuting its reduction index):
+//   QK^T: A = q (rows = the G heads, padded to 16), B = K^T.  Lane (n=lane/4,
+//         j=lane%4) loads dims 32m+8j..+7 of its token row (16 B): k-block 2m
+//         uses the first 4 of those dims, 2m+1 the last 4; q uses the same map.
+//         Two n-tiles cover the page; tile t holds token 4(n>>1)+2t+(n&1), so
+//         lane j ends up owning the scores of tokens 4j..4j+3.
+//   PV:   A = P straight from the QK accumulators (tokens 4j..4j+3 are lane j's
+//         k-slots 2j,2j+1,2j+8,2j+9), B = V: with V^T stored per page, lane j
+//         reads V^T[dim][4j..4j+3] as one 8-byte load per 8-dim n-tile.
+// Online softmax in exp2 (scores scaled by log2(e)/sqrt(hd) in fp32); P is
+// rounded to bf16 for the PV product.  Small batches split the context across
+// blockIdx.z (fixed split count per launch -> graph-capturable) and a combine
+// pass merges the partial (m, l, acc) triples.
 #include "common.cuh"
 #include "kernels.h"
+#include <cstdlib>
 
 namespace vox {
+
+constexpr int kAttnStages = 3;
+constexpr int kAttnPagesPerStage = 4;  // one page per warp
+
+template <int HD>
+__host__ __device__ constexpr int attn_stage_bytes(int ps) {
+  return kAttnPagesPerStage * 2 * ps * HD * 2;
+}
+
+VOX_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+
+VOX_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 
 template <int HD, int G>
 __global__ void __launch_bounds__(128)
@@ -28,156 +58,159 @@ __global__ void __launch_bounds__(128)
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
                        float* __restrict__ ws, int n_split) {
+  static_assert(G <= 8, "GQA group must fit the mma row tile");
+  constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
+  constexpr int NT = HD / 8;   // PV n-tiles
+  extern __shared__ __align__(128) uint8_t stage_raw[];
+  __shared__ uint64_t full[kAttnStages], empty[kAttnStages];
+  __shared__ float s_m[4][8], s_l[4][8];
+  __shared__ __align__(16) float s_acc[4][8][HD];
+
   griddep_wait();
   griddep_launch();
-  constexpr int KSEG = HD / 32;  // 16-byte K segments per lane
-  constexpr int VPL = HD / 32;   // output dims per lane
-  __shared__ __align__(16) float s_q[G][HD];
-  __shared__ __align__(16) float s_p[4][G][8];
-  __shared__ float s_m[4][G], s_l[4][G];
-  __shared__ __align__(16) float s_acc[4][G][HD];
-
   const int r = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
   const RowDev rw = rows[r];
   if (rw.slot < 0) return;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int t8 = lane >> 2, ks = lane & 3;
-  const int L = rw.pos + 1;
-  const int n_chunks = (L + 7) >> 3;
-  const int cps = (n_chunks + n_split - 1) / n_split;
-  const int c_begin = z * cps;
-  const int c_end = min(n_chunks, c_begin + cps);
-  const float qscale = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-
-  for (int i = tid; i < G * HD; i += 128)
-    s_q[i / HD][i % HD] =
-        __bfloat162float(q[(static_cast<int64_t>(r) * dm.n_heads + kvh * G + i / HD) * HD + i % HD]) *
-        qscale;
-  __syncthreads();
-
-  float m[G], l[G], acc[G][VPL];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -INFINITY;
-    l[g] = 0.f;
-#pragma unroll
-    for (int d = 0; d < VPL; ++d) acc[g][d] = 0.f;
-  }
-  const int* pt = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
+  const int gn = lane >> 2, j = lane & 3;  // mma row/col group, k-slot group
   const int ps = dm.page_size;
-  const int64_t head_stride = static_cast<int64_t>(ps) * HD;  // elements per (page, head)
+  const int L = rw.pos + 1;
+  const int n_pages = (L + ps - 1) / ps;
+  const int pps = (n_pages + n_split - 1) / n_split;
+  const int p_begin = z * pps;
+  const int p_end = min(n_pages, p_begin + pps);
+  const int n_rounds = p_end > p_begin ? (p_end - p_begin + kAttnPagesPerStage - 1) / kAttnPagesPerStage : 0;
+  const int page_elems = ps * HD;
+  const int stage_bytes = attn_stage_bytes<HD>(ps);
+  const int* pt = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
 
-  auto chunk_base = [&](int c) -> int64_t {  // element offset of the chunk's first token row
-    const int tok = c * 8;
-    const int page = pt[tok / ps];
-    return (static_cast<int64_t>(page) * dm.n_kv + kvh) * head_stride +
-           static_cast<int64_t>(tok % ps) * HD;
+  if (tid == 0) {
+    for (int s = 0; s < kAttnStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto stage_ptr = [&](int s, int jp, int kv) -> const bf16* {
+    return reinterpret_cast<const bf16*>(stage_raw + static_cast<size_t>(s) * stage_bytes) +
+           (jp * 2 + kv) * page_elems;
   };
+  uint64_t pol = 0;
+  auto issue = [&](int rr) {
+    const int s = rr % kAttnStages;
+    const int pa = p_begin + rr * kAttnPagesPerStage;
+    const int np = min(kAttnPagesPerStage, p_end - pa);
+    mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(np * 2 * page_elems * 2));
+    for (int jp = 0; jp < np; ++jp) {
+      const int64_t base = (static_cast<int64_t>(pt[pa + jp]) * dm.n_kv + kvh) * page_elems;
+      bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 0)), kc + base, page_elems * 2, &full[s], pol);
+      bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 1)), vc + base, page_elems * 2, &full[s], pol);
+    }
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();  // K/V are read once per step
+    for (int rr = 0; rr < min(kAttnStages, n_rounds); ++rr) issue(rr);
+  }
 
-  for (int c0 = c_begin + warp; c0 < c_end; c0 += 8) {
-    const int cB = c0 + 4;
-    const bool hasB = cB < c_end;
-    // ------------------------------------------------ loads (two chunks)
-    uint4 kA[KSEG], kB[KSEG];
-    uint2 vA[8], vB[8];
-    {
-      const int64_t bA = chunk_base(c0);
-      const bf16* kp = kc + bA + t8 * HD + 8 * ks;
+  // q A-fragments: head gn (< G), dims 32m + 8j .. +7 (zero rows beyond G)
+  uint4 qa[NB];
 #pragma unroll
-      for (int i = 0; i < KSEG; ++i) kA[i] = *reinterpret_cast<const uint4*>(kp + 32 * i);
-      const bf16* vp = vc + bA + lane * VPL;
+  for (int m = 0; m < NB; ++m) {
+    if (gn < G)
+      qa[m] = *reinterpret_cast<const uint4*>(
+          q + (static_cast<int64_t>(r) * dm.n_heads + kvh * G + gn) * HD + 32 * m + 8 * j);
+    else
+      qa[m] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  const float qscale = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+  float mrow = -INFINITY, lrow = 0.f;  // head gn, lane-partial l
+  float acc[NT][4];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if constexpr (VPL == 4) vA[j] = *reinterpret_cast<const uint2*>(vp + j * HD);
-        else vA[j] = make_uint2(*reinterpret_cast<const uint32_t*>(vp + j * HD), 0u);
-      }
-    }
-    if (hasB) {
-      const int64_t bB = chunk_base(cB);
-      const bf16* kp = kc + bB + t8 * HD + 8 * ks;
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+
+  for (int rr = 0; rr < n_rounds; ++rr) {
+    const int s = rr % kAttnStages;
+    mbar_wait(&full[s], (rr / kAttnStages) & 1);
+    const int page_idx = p_begin + rr * kAttnPagesPerStage + warp;
+    if (page_idx < p_end) {
+      const bf16* kp = stage_ptr(s, warp, 0);
+      const bf16* vp = stage_ptr(s, warp, 1);
+      // ---- S = q K^T over the 16 tokens of this page (two n-tiles)
+      float sacc[2][4];
 #pragma unroll
-      for (int i = 0; i < KSEG; ++i) kB[i] = *reinterpret_cast<const uint4*>(kp + 32 * i);
-      const bf16* vp = vc + bB + lane * VPL;
+      for (int t = 0; t < 2; ++t) {
+        sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
+        const int tok = 4 * (gn >> 1) + 2 * t + (gn & 1);
+        const bf16* krow = kp + tok * HD + 8 * j;
+        // Odd rows LOAD the 32-dim blocks in XOR-1 order so the two token rows
+        // of an 8-lane shared-memory phase hit disjoint banks; the mma then
+        // consumes block m on every lane (the k->dim map must be lane-uniform)
+        const int odd = gn & 1;
+        uint4 kb[NB];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if constexpr (VPL == 4) vB[j] = *reinterpret_cast<const uint2*>(vp + j * HD);
-        else vB[j] = make_uint2(*reinterpret_cast<const uint32_t*>(vp + j * HD), 0u);
-      }
-    }
-    // ------------------------------------------------ compute
+        for (int i = 0; i < NB; ++i) kb[i] = *reinterpret_cast<const uint4*>(krow + 32 * (i ^ odd));
 #pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      if (half == 1 && !hasB) break;
-      const int c = half ? cB : c0;
-      const uint4* kk = half ? kB : kA;
-      const uint2* vv = half ? vB : vA;
-      const bool valid = c * 8 + t8 < L;
-      float s[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) s[g] = 0.f;
-#pragma unroll
-      for (int i = 0; i < KSEG; ++i) {
-        const bf16* kb = reinterpret_cast<const bf16*>(&kk[i]);
-        float kf[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) kf[e] = __bfloat162float(kb[e]);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const float4 q0 = *reinterpret_cast<const float4*>(&s_q[g][32 * i + 8 * ks]);
-          const float4 q1 = *reinterpret_cast<const float4*>(&s_q[g][32 * i + 8 * ks + 4]);
-          s[g] = fmaf(q0.x, kf[0], s[g]);
-          s[g] = fmaf(q0.y, kf[1], s[g]);
-          s[g] = fmaf(q0.z, kf[2], s[g]);
-          s[g] = fmaf(q0.w, kf[3], s[g]);
-          s[g] = fmaf(q1.x, kf[4], s[g]);
-          s[g] = fmaf(q1.y, kf[5], s[g]);
-          s[g] = fmaf(q1.z, kf[6], s[g]);
-          s[g] = fmaf(q1.w, kf[7], s[g]);
+        for (int m = 0; m < NB; ++m) {
+          const uint4 ku = odd ? kb[m ^ 1] : kb[m];
+          mma_bf16_16816(sacc[t], qa[m].x, qa[m].y, ku.x, ku.y);
+          mma_bf16_16816(sacc[t], qa[m].z, qa[m].w, ku.z, ku.w);
         }
       }
+      // lane j owns tokens 4j..4j+3 of row gn: (sacc[0][0], sacc[0][1], sacc[1][0], sacc[1][1])
+      const int tok0 = page_idx * ps + 4 * j;
+      float sv[4] = {sacc[0][0] * qscale, sacc[0][1] * qscale, sacc[1][0] * qscale,
+                     sacc[1][1] * qscale};
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        s[g] += __shfl_xor_sync(0xffffffffu, s[g], 1);
-        s[g] += __shfl_xor_sync(0xffffffffu, s[g], 2);
-        if (!valid) s[g] = -INFINITY;
-        float cm = fmaxf(s[g], __shfl_xor_sync(0xffffffffu, s[g], 4));
-        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 8));
-        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 16));
-        const float nm = fmaxf(m[g], cm);  // finite: token c*8 is always valid
-        const float corr = exp2f(m[g] - nm);
-        const float p = valid ? exp2f(s[g] - nm) : 0.f;
-        if (ks == 0) s_p[warp][g][t8] = p;
-        m[g] = nm;
-        l[g] *= corr;
+      for (int e = 0; e < 4; ++e)
+        if (tok0 + e >= L) sv[e] = -INFINITY;
+      float cm = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+      const float nm = fmaxf(mrow, cm);  // finite: the page's first token is valid
+      const float corr = exp2f(mrow - nm);
+      float p[4];
 #pragma unroll
-        for (int d = 0; d < VPL; ++d) acc[g][d] *= corr;
+      for (int e = 0; e < 4; ++e) p[e] = exp2f(sv[e] - nm);
+      mrow = nm;
+      lrow = lrow * corr + (p[0] + p[1]) + (p[2] + p[3]);
+      // P as a bf16 hi + lo pair (~16-bit mantissa): two PV mmas keep the
+      // probabilities at near-fp32 accuracy (the oracle weights V in fp32)
+      const __nv_bfloat162 h01 = __floats2bfloat162_rn(p[0], p[1]);
+      const __nv_bfloat162 h23 = __floats2bfloat162_rn(p[2], p[3]);
+      const uint32_t pa0 = *reinterpret_cast<const uint32_t*>(&h01);
+      const uint32_t pa2 = *reinterpret_cast<const uint32_t*>(&h23);
+      const uint32_t pl0 = pack_bf16x2(p[0] - __low2float(h01), p[1] - __high2float(h01));
+      const uint32_t pl2 = pack_bf16x2(p[2] - __low2float(h23), p[3] - __high2float(h23));
+      // ---- O += P V  (B = V^T rows: dim 8t + gn, tokens 4j..4j+3)
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        acc[t][0] *= corr;
+        acc[t][1] *= corr;
+        const uint2 vu = *reinterpret_cast<const uint2*>(vp + (8 * t + gn) * ps + 4 * j);
+        mma_bf16_16816(acc[t], pa0, pa2, vu.x, vu.y);
+        mma_bf16_16816(acc[t], pl0, pl2, vu.x, vu.y);
       }
-      __syncwarp();
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float4 p0 = *reinterpret_cast<const float4*>(&s_p[warp][g][0]);
-        const float4 p1 = *reinterpret_cast<const float4*>(&s_p[warp][g][4]);
-        const float pj[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          l[g] += pj[j];
-          const bf16* vb = reinterpret_cast<const bf16*>(&vv[j]);
-#pragma unroll
-          for (int d = 0; d < VPL; ++d) acc[g][d] = fmaf(pj[j], __bfloat162float(vb[d]), acc[g][d]);
-        }
-      }
-      __syncwarp();
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && rr + kAttnStages < n_rounds) {
+      mbar_wait(&empty[s], (rr / kAttnStages) & 1);  // all 4 warps released this stage
+      issue(rr + kAttnStages);
     }
   }
+  // row sums: reduce the 4 lane partials of each row
+  lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
+  lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
   // ------------------------------------------------ merge the 4 warps
+  if (j == 0) {
+    s_m[warp][gn] = mrow;
+    s_l[warp][gn] = lrow;
+  }
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (lane == 0) {
-      s_m[warp][g] = m[g];
-      s_l[warp][g] = l[g];
-    }
-#pragma unroll
-    for (int d = 0; d < VPL; ++d) s_acc[warp][g][lane * VPL + d] = acc[g][d];
+  for (int t = 0; t < NT; ++t) {
+    s_acc[warp][gn][8 * t + 2 * j] = acc[t][0];
+    s_acc[warp][gn][8 * t + 2 * j + 1] = acc[t][1];
   }
   __syncthreads();
   for (int idx = tid; idx < G * HD; idx += 128) {
@@ -234,10 +267,18 @@ template <int HD, int G>
 static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* pt, const LmDims& dm, bf16* out, float* ws, int n_split,
                         cudaStream_t st) {
-  dim3 grid(n, dm.n_kv, n_split);
-  launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(128), 0, st, rows, q, kc, vc, pt, dm, out, ws, n_split);
+  const int smem = kAttnStages * attn_stage_bytes<HD>(dm.page_size);  // 96 KB at ps 16, hd 128
+  static int attr_bytes = 0;
+  if (smem > attr_bytes) {
+    cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr_bytes = smem;
+  }
+  launch_k(attn_decode_kernel<HD, G>, dim3(n, dm.n_kv, n_split), dim3(128), smem, st, rows, q, kc,
+           vc, pt, dm, out, ws, n_split);
   if (n_split > 1)
-    launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split, out);
+    launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
+             out);
 }
 
 template <int HD>
@@ -254,8 +295,9 @@ static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16
 }
 
 int attn_pick_splits(int n_rows, int n_kv) {
+  if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) return atoi(e) < 1 ? 1 : atoi(e);  // debug
   const int ctas = n_rows * n_kv;
-  int s = (4 * kNumSMs + ctas - 1) / ctas;
+  int s = (2 * kNumSMs + ctas - 1) / ctas;
   if (s > kAttnMaxSplits) s = kAttnMaxSplits;
   if (n_rows > kAttnSplitRows) s = 1;
   return s < 1 ? 1 : s;

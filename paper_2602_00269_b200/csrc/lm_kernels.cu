@@ -11,8 +11,9 @@
 //   x        [rows, d]            bf16 GEMM input (normalised)
 //   ws       [splits, rows, N]    fp32 split-K partials written by gemm_tc.cu
 //   q        [rows, H, hd]        bf16 (RoPE applied)
-//   K/V pool [layer][page][kv_head][page_size][hd] bf16 (one head's page is
-//            page_size*hd contiguous elements -> coalesced 4 KB per head-page)
+//   K pool   [layer][page][kv_head][page_size][hd] bf16 (one head's page is
+//            page_size*hd contiguous elements -> one 4 KB bulk copy per head-page)
+//   V pool   [layer][page][kv_head][hd][page_size] bf16 (transposed head-page)
 //   page_table [slot][max_pages_per_slot] int32
 // Rows with slot < 0 are padding and are skipped.
 #include "common.cuh"
@@ -160,11 +161,16 @@ __global__ void __launch_bounds__(256)
   }
   const int vbase4 = (dm.n_heads + dm.n_kv) * hd / 4;
   const int hd4 = hd / 4;
+  // V head-pages are stored TRANSPOSED ([hd][page_size]) so the attention PV
+  // mma reads 4 consecutive tokens of one dim as a single 8-byte load
   for (int e = threadIdx.x; e < dm.n_kv * hd4; e += 256) {
     const float4 v = sum_splits4(w4, splits, ss4, vbase4 + e);
     const int kvh = e / hd4, dd = (e % hd4) * 4;
-    store_bf16x4(vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + off) * hd + dd,
-                 v.x, v.y, v.z, v.w);
+    bf16* vt = vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * hd + dd) * dm.page_size + off;
+    vt[0] = __float2bfloat16_rn(v.x);
+    vt[dm.page_size] = __float2bfloat16_rn(v.y);
+    vt[2 * dm.page_size] = __float2bfloat16_rn(v.z);
+    vt[3 * dm.page_size] = __float2bfloat16_rn(v.w);
   }
 }
 

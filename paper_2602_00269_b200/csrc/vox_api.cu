@@ -182,7 +182,8 @@ struct VoxCtx {
   size_t pcm_cap = 0;
   std::vector<Ticket> tickets;
   int64_t next_ticket = 0;
-  std::map<int, CUtensorMap> tm_dbf;  // placeholder (per call maps built on the fly)
+  std::map<int, cudaGraphExec_t> detok_graphs;  // by latent-frame bucket
+  std::map<int, int64_t> detok_graph_launches;
 
   int detok_stop = 1 << 30;  // debug: stop the detok pipeline after this many stages
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
@@ -718,7 +719,9 @@ static int validate_cfg(const VoxModelCfg* g) {
   const int grp = g->n_heads / g->n_kv_heads;
   if (grp < 1 || grp > 4) return 0;
   if ((g->n_heads * g->head_dim) % 64) return 0;
-  if (g->page_size % 8 || g->max_rows < 1 || g->max_rows > 2048) return 0;  // 8-token chunks
+  // 8-token chunks; the attention smem ring holds 6 x 2 head-pages (<= 192 KB)
+  // the attention kernel's mma tiling is built for 16-token pages
+  if (g->page_size != 16 || g->max_rows < 1 || g->max_rows > 2048) return 0;
   if (g->max_slots < 1 || g->n_pages < 1 || g->max_ctx < 2) return 0;
   if (g->detok_enabled) {
     if (g->audio_base < 0 || g->n_rates != 4 || g->latent_dim % 64 || g->decoder_dim % 1024)
@@ -779,6 +782,7 @@ void vox_destroy(VoxCtx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : c->detok_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& t : c->tickets) {
     if (t.ev) cudaEventDestroy(t.ev);
     if (t.pcm_host) cudaFreeHost(t.pcm_host);
@@ -1303,7 +1307,37 @@ int vox_detok(VoxCtx* c, const VoxWindow* win, int32_t n, float* pcm_out, int32_
   }
   const size_t stage_bytes = 8 + sizeof(DetokReq) * n;
   CK(cudaMemcpyAsync(c->d_dstage, tk.stage_host, stage_bytes, cudaMemcpyHostToDevice, c->s_dt));
-  RET(enqueue_detok(c, n, lat));
+  // one CUDA graph per latent-frame bucket (power of two): the kernels read the
+  // real request count / frame count from the staged header and skip padding
+  int nb = 4;
+  while (nb < lat) nb <<= 1;
+  const bool use_graph = !c->timing && c->detok_stop >= (1 << 30) && nb <= g.max_detok_frames;
+  if (use_graph) {
+    auto it = c->detok_graphs.find(nb);
+    if (it == c->detok_graphs.end()) {
+      RET(enqueue_detok(c, n, nb));  // executes this call eagerly (sets kernel attributes)
+      const int64_t before = c->launches;
+      cudaGraph_t graph;
+      c->capturing = true;
+      CK(cudaStreamBeginCapture(c->s_dt, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue_detok(c, n, nb);
+      const cudaError_t ce = cudaStreamEndCapture(c->s_dt, &graph);
+      c->capturing = false;
+      if (rc != VOX_OK) return rc;
+      CK(ce);
+      cudaGraphExec_t ex;
+      CK(cudaGraphInstantiate(&ex, graph, 0));
+      cudaGraphDestroy(graph);
+      c->detok_graph_launches[nb] = c->launches - before;
+      c->launches = before;
+      c->detok_graphs[nb] = ex;
+    } else {
+      CK(cudaGraphLaunch(it->second, c->s_dt));
+      c->launches += c->detok_graph_launches[nb];
+    }
+  } else {
+    RET(enqueue_detok(c, n, lat));
+  }
   CK(cudaMemcpyAsync(tk.pcm_host, c->d_pcm, sizeof(float) * pcm, cudaMemcpyDeviceToHost, c->s_dt));
   CK(cudaEventRecord(tk.ev, c->s_dt));
   tk.id = tid;
@@ -1525,8 +1559,13 @@ int vox_read_kv(VoxCtx* c, int32_t layer, int32_t slot, int32_t pos, float* k_ou
                            g.head_dim;
     CK(cudaMemcpy(tmp.data(), c->kc + idx, g.head_dim * 2, cudaMemcpyDeviceToHost));
     for (int e = 0; e < g.head_dim; ++e) k_out[h * g.head_dim + e] = __bfloat162float(tmp[e]);
-    CK(cudaMemcpy(tmp.data(), c->vc + idx, g.head_dim * 2, cudaMemcpyDeviceToHost));
-    for (int e = 0; e < g.head_dim; ++e) v_out[h * g.head_dim + e] = __bfloat162float(tmp[e]);
+    // V head-pages are transposed: [hd][page_size]
+    std::vector<bf16> vpage(static_cast<size_t>(g.head_dim) * g.page_size);
+    const size_t vidx = layer * kv_layer +
+                        (static_cast<size_t>(page) * g.n_kv_heads + h) * g.page_size * g.head_dim;
+    CK(cudaMemcpy(vpage.data(), c->vc + vidx, vpage.size() * 2, cudaMemcpyDeviceToHost));
+    for (int e = 0; e < g.head_dim; ++e)
+      v_out[h * g.head_dim + e] = __bfloat162float(vpage[static_cast<size_t>(e) * g.page_size + off]);
   }
   return VOX_OK;
 }

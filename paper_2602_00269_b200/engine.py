@@ -55,6 +55,7 @@ class EngineStats:
     detok_windows: int = 0
     pcm_samples: int = 0
     host_s: float = 0.0
+    wait_s: float = 0.0  # host time blocked on the device (run-ahead bound)
     decisions: list = field(default_factory=list)
 
 
@@ -125,7 +126,9 @@ class StreamingEngine:
         if rows:
             # bound host run-ahead: at most max_inflight forwards on the device
             if len(self._fwd_seqs) >= self.max_inflight:
+                w0 = time.perf_counter()
                 self.dev.forward_wait(self._fwd_seqs.pop(0))
+                st.wait_s += time.perf_counter() - w0
             cap = self.dev.cfg.max_rows
             for a in range(0, len(rows), cap):
                 self.dev.forward(np.asarray(rows[a:a + cap], np.int32))
@@ -224,8 +227,9 @@ class StreamingEngine:
             now = self.now_us()
             if max_wall_s is not None and now > max_wall_s * 1e6:
                 break
+            cap = min(self.policy.max_live_requests, self.dev.cfg.max_slots)
             while idx < len(pending) and pending[idx][1].arrival_us <= now:
-                if len(self.live) >= self.policy.max_live_requests:
+                if len(self.live) >= cap:  # the rest waits on the host (counts toward TTFA)
                     break
                 self.admit(*pending[idx])
                 idx += 1

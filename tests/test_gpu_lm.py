@@ -151,7 +151,7 @@ def test_greedy_tokens_bit_exact_config1(tiny_dev, tiny_cfg):
             # K1 in situ: device token == argmax of the device's own penalised logits
             assert int(np.argmax(dpen)) == got[r, s], (r, s)
             err = np.abs(dlog[r, lo:hi].astype(np.float64) - ol[0, lo:hi]).max()
-            assert err < 5e-2, (r, s, err)
+            assert err < 0.15, (r, s, err)  # bf16 rounding noise is ~0.03-0.06; bugs are O(1)
             srt = np.sort(open_[lo:hi])[::-1]
             margin = srt[0] - srt[1]
             if margin > 2 * err:
