@@ -109,9 +109,20 @@ def dist_setup(backend: str):
         if backend == "nccl":
             import torch
 
+            n_dev = max(torch.cuda.device_count(), 1)
+            if n_dev < ws:
+                # more ranks than GPUs (functional testing of the multi-rank path on one
+                # device): NCCL refuses duplicate devices, so reduce metrics over gloo
+                backend = "gloo"
+            local = local % n_dev
             torch.cuda.set_device(local)
         dist.init_process_group(backend=backend)
+        global _DIST_DEVICE
+        _DIST_DEVICE = None if backend == "gloo" else "cuda"
     return ws, rank, local
+
+
+_DIST_DEVICE = "cuda"
 
 
 def reduce_max(x: float, ws: int, device=None) -> float:
@@ -265,8 +276,11 @@ def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: flo
     return classes, step_ms, ctx
 
 
-def run_slo(dev, rates, seconds: float, seed: int, prompt: int):
-    from paper_2602_00269_b200._ref import core, scheduler, workload
+def run_slo(dev, rates, seconds: float, seed: int, prompt: int, ws: int = 1, rank: int = 0):
+    """Poisson load test (config 5): offered rate r is the WHOLE-JOB rate; requests are
+    routed to the ws replicas with the reference router, metrics pooled at the end."""
+    from paper_2602_00269_b200 import dp
+    from paper_2602_00269_b200._ref import scheduler, workload
     from paper_2602_00269_b200.engine import StreamingEngine, orpheus_profile
 
     prof = orpheus_profile(max_batch=256)
@@ -275,14 +289,15 @@ def run_slo(dev, rates, seconds: float, seed: int, prompt: int):
         spec = workload.WorkloadSpec(rate=rate, duration_s=seconds, prompt_dist=workload.fixed(prompt),
                                      output_dist=workload.fixed(688), seed=seed)
         arr = list(enumerate(workload.build_workload(spec)))
+        mine = dp.route(arr, ws, seed)[rank]
         policy = scheduler.PolicyConfig(max_lm_batch=256, max_detok_batch=256, startup_concurrency_limit=16)
         eng = StreamingEngine(dev, prof, policy, seed)
-        tr = eng.run(arr)
-        rep = core.build_report(tr)
-        out.append(dict(rate=rate, requests=len(arr), ttfa_p50=rep.ttfa_p50, ttfa_p90=rep.ttfa_p90,
-                        ttfa_p99=rep.ttfa_p99, viability=rep.viability_fraction, inverse_rtf=rep.inverse_rtf,
-                        audio_s=rep.audio_seconds_generated, completed=rep.requests_completed))
-        if not (rep.viability_fraction >= 0.99 and rep.ttfa_p90 <= 0.5):
+        tr = eng.run(mine)
+        rep = dp.gather_pool(dp.local_summary(tr), ws)
+        out.append(dict(rate=rate, requests=len(arr), ttfa_p50=rep["ttfa_p50"], ttfa_p90=rep["ttfa_p90"],
+                        ttfa_p99=rep["ttfa_p99"], viability=rep["viability"], inverse_rtf=rep["inverse_rtf"],
+                        audio_s=rep["audio_s"], completed=rep["completed"]))
+        if not (rep["viability"] >= 0.99 and rep["ttfa_p90"] <= 0.5):
             break
     ok = [r["rate"] for r in out if r["viability"] >= 0.99 and r["ttfa_p90"] <= 0.5]
     return (max(ok) if ok else 0.0), out
@@ -305,7 +320,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=50)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--slo-seconds", type=float, default=12.0)
-    ap.add_argument("--slo-rates", default="16,32,48,64")
+    ap.add_argument("--slo-rates", default="32,40,48,56,64")
     ap.add_argument("--no-slo", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -355,10 +370,10 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         res = steady_state_steps(dev, args.batch, args.steps, args.warmup, args.prompt, args.seed + 1000 * rank)
-    dev_ms = reduce_max(res["dev_ms"], ws, torch.device("cuda", local))
-    wall_s = reduce_max(res["wall_s"], ws, torch.device("cuda", local))
+    dev_ms = reduce_max(res["dev_ms"], ws, (torch.device("cuda", local) if _DIST_DEVICE else None))
+    wall_s = reduce_max(res["wall_s"], ws, (torch.device("cuda", local) if _DIST_DEVICE else None))
     decoded, chunks, pcm = reduce_sum([res["decoded"], res["chunks"], res["pcm_samples"]], ws,
-                                      torch.device("cuda", local))
+                                      (torch.device("cuda", local) if _DIST_DEVICE else None))
     audio_s = decoded / res["token_rate"]
     value = audio_s / (dev_ms / 1000.0)
     e2e = audio_s / wall_s
@@ -380,11 +395,12 @@ def main():
                 "eager_step_ms": round(step_ms, 3), "ctx": ctx, "batch": args.batch}
 
     slo = None
-    if not args.no_slo and rank == 0:
-        rates = [float(x) for x in args.slo_rates.split(",")]
-        best, sweep = run_slo(dev, rates, args.slo_seconds, args.seed, args.prompt)
-        slo = {"max_req_s_at_slo": best, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
-               "duration_s": args.slo_seconds, "sweep": sweep}
+    if not args.no_slo:
+        rates = [float(x) * ws for x in args.slo_rates.split(",")]  # whole-job offered rate
+        best, sweep = run_slo(dev, rates, args.slo_seconds, args.seed, args.prompt, ws, rank)
+        slo = {"max_req_s_at_slo": best, "per_gpu": best / ws, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
+               "duration_s": args.slo_seconds, "routing": "reference route_dp (seeded uniform), replicas",
+               "sweep": sweep}
 
     cpu = None
     if not args.no_cpu and rank == 0:
