@@ -411,7 +411,7 @@ def main():
 
     if rank == 0:
         steps = args.steps
-        h2d = (res["rows"] / steps) * 24 + 64
+        h2d = (res["rows"] / steps) * 40 + 64  # RowDev (32 B) + out_index + sample_rows per row
         d2h = (res["decoded"] / steps) * 4 + (res["pcm_samples"] / steps) * 4 + 4
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": steps,

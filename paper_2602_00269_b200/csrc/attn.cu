@@ -33,6 +33,7 @@ namespace vox {
 
 constexpr int kAttnStages = 3;
 constexpr int kAttnPagesPerStage = 4;  // one page per warp
+constexpr int kAttnPtSmem = 512;       // page ids staged in smem (8192 tokens at ps 16)
 
 template <int HD>
 __host__ __device__ constexpr int attn_stage_bytes(int ps) {
@@ -64,13 +65,20 @@ __global__ void __launch_bounds__(128)
   extern __shared__ __align__(128) uint8_t stage_raw[];
   __shared__ uint64_t full[kAttnStages], empty[kAttnStages];
   __shared__ float s_m[4][8], s_l[4][8];
-  __shared__ __align__(16) float s_acc[4][8][HD];
+  // the 4 warps' partial outputs are merged through the (then idle) K/V ring
+  float (*s_acc)[8][HD] = reinterpret_cast<float (*)[8][HD]>(stage_raw);
 
-  griddep_wait();
-  griddep_launch();
+  // rows / page table are uploaded before the step's first kernel and K/V of
+  // positions < pos were appended by earlier steps: none of it depends on the
+  // preceding kernel, so the prologue and the first K/V copies overlap its
+  // tail (PDL); only q and the page holding `pos` wait for griddep_wait.
   const int r = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
   const RowDev rw = rows[r];
-  if (rw.slot < 0) return;
+  if (rw.slot < 0) {
+    griddep_wait();
+    griddep_launch();
+    return;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gn = lane >> 2, j = lane & 3;  // mma row/col group, k-slot group
   const int ps = dm.page_size;
@@ -82,7 +90,14 @@ __global__ void __launch_bounds__(128)
   const int n_rounds = p_end > p_begin ? (p_end - p_begin + kAttnPagesPerStage - 1) / kAttnPagesPerStage : 0;
   const int page_elems = ps * HD;
   const int stage_bytes = attn_stage_bytes<HD>(ps);
-  const int* pt = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
+  const int* pt_g = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
+  // this split's page ids, staged once (a dependent global load per bulk copy
+  // would serialise the issue loop on load latency)
+  __shared__ int s_pt[kAttnPtSmem];
+  const bool pt_in_smem = (p_end - p_begin) <= kAttnPtSmem;
+  if (pt_in_smem)
+    for (int i = tid; i < p_end - p_begin; i += 128) s_pt[i] = pt_g[p_begin + i];
+  auto page_id = [&](int pg) { return pt_in_smem ? s_pt[pg - p_begin] : pt_g[pg]; };
 
   if (tid == 0) {
     for (int s = 0; s < kAttnStages; ++s) {
@@ -103,15 +118,28 @@ __global__ void __launch_bounds__(128)
     const int np = min(kAttnPagesPerStage, p_end - pa);
     mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(np * 2 * page_elems * 2));
     for (int jp = 0; jp < np; ++jp) {
-      const int64_t base = (static_cast<int64_t>(pt[pa + jp]) * dm.n_kv + kvh) * page_elems;
+      const int64_t base = (static_cast<int64_t>(page_id(pa + jp)) * dm.n_kv + kvh) * page_elems;
       bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 0)), kc + base, page_elems * 2, &full[s], pol);
       bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 1)), vc + base, page_elems * 2, &full[s], pol);
     }
   };
+  // stages whose pages all precede the first page this forward appends to
+  // (rw.fresh, written by the preceding kernel) are issued before the
+  // grid-dependency wait
+  const int last_page = rw.fresh / ps;
+  const int pre = min(kAttnStages, n_rounds);
+  int n_early = 0;
+  while (n_early < pre && p_begin + (n_early + 1) * kAttnPagesPerStage - 1 < last_page &&
+         p_begin + (n_early + 1) * kAttnPagesPerStage <= p_end)
+    ++n_early;
   if (tid == 0) {
     pol = policy_evict_first();  // K/V are read once per step
-    for (int rr = 0; rr < min(kAttnStages, n_rounds); ++rr) issue(rr);
+    for (int rr = 0; rr < n_early; ++rr) issue(rr);
   }
+  griddep_wait();
+  griddep_launch();
+  if (tid == 0)
+    for (int rr = n_early; rr < pre; ++rr) issue(rr);
 
   // q A-fragments: head gn (< G), dims 32m + 8j .. +7 (zero rows beyond G)
   uint4 qa[NB];
@@ -203,6 +231,7 @@ __global__ void __launch_bounds__(128)
   lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
   lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
   // ------------------------------------------------ merge the 4 warps
+  __syncthreads();  // every warp is done reading the ring before it is reused
   if (j == 0) {
     s_m[warp][gn] = mrow;
     s_l[warp][gn] = lrow;

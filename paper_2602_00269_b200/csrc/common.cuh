@@ -42,6 +42,17 @@ VOX_DEV float unit_open01(uint64_t h) {
   return ((float)(uint32_t)(h >> 40) + 0.5f) * (1.0f / 16777216.0f);
 }
 
+// sin(x) for the Snake activations: one Cody-Waite reduction to [-pi, pi]
+// (two FMAs with a split 2*pi) and the SFU sine.  Absolute error ~1e-6 for
+// |x| < 1e4 (vs ~2 ulp for libdevice sinf at ~8x the instruction count); far
+// below the bf16 rounding of the GEMM operands that follow.
+VOX_DEV float snake_sin(float x) {
+  const float k = rintf(x * 0.15915494309189535f);
+  float r = fmaf(-k, 6.28318548202514648f, x);
+  r = fmaf(-k, -1.7484556e-07f, r);
+  return __sinf(r);
+}
+
 VOX_DEV float bf16_to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 VOX_DEV __nv_bfloat16 f32_to_bf16(float v) { return __float2bfloat16_rn(v); }
 

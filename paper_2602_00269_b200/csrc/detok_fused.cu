@@ -1,0 +1,338 @@
+// detok_fused.cu — K4 fine levels: one kernel per residual unit, and a tiled
+// output head.
+//
+// At the fine decoder levels (C = 64 / 128 channels, 2^17..2^18 rows per
+// steady-state detok call) the residual unit
+//     y1 = Snake(x; a1);  u = b + dwconv7_dil(y1) (causal);  v = Snake(u; a2)
+//     x' = x + pw_b + v . W^T                                  (1x1 conv)
+// is memory/latency bound, not FLOP bound (K = C is tiny).  ru_fused_kernel
+// does it in one pass over a 128-row tile:
+//   1. y1 for rows [r0 - 6*dil, r0 + 128) into shared memory (Snake computed
+//      once per element; rows before the request's first row come from its
+//      cached left context, state[parity]; the new context is written to
+//      state[parity ^ 1]),
+//   2. v = Snake(dwconv(y1)) for the tile's 128 rows, rounded to bf16 straight
+//      into the 128B-swizzled K-major UMMA operand layout in shared memory,
+//   3. one elected thread issues tcgen05.mma (M = 128 rows, N = C, K = C;
+//      W^T staged in shared memory in the same layout), accumulator in TMEM,
+//   4. tcgen05.ld -> shared staging -> coalesced x + pw_b + acc -> y.
+// The intermediate v never touches global memory and the unit is one launch
+// instead of two.  A tile never straddles two requests: request row ranges
+// are multiples of 4*up rows and 4*up >= 1024 at these levels (host checks).
+// Arithmetic and rounding points are those of ru_prep_kernel + the GEMM
+// (oracle/snac.py: bf16 GEMM operands, fp32 everything else).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace vox {
+
+namespace {
+
+struct ReqHdrF {
+  int32_t n_req, n_lat;
+};
+
+VOX_DEV int find_req_f(const DetokReq* reqs, int n_req, int lat_row) {
+  int lo = 0, hi = n_req - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (reqs[mid].lat_off <= lat_row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+VOX_DEV float snake_f(float x, float a) {
+  const float s = snake_sin(__fmul_rn(a, x));
+  return __fadd_rn(x, __fmul_rn(__fdiv_rn(1.0f, __fadd_rn(a, 1e-9f)), __fmul_rn(s, s)));
+}
+// same value with the per-channel reciprocal 1 / (a + 1e-9) precomputed
+VOX_DEV float snake_r(float x, float a, float inv) {
+  const float s = snake_sin(__fmul_rn(a, x));
+  return __fadd_rn(x, __fmul_rn(inv, __fmul_rn(s, s)));
+}
+VOX_DEV float snake_inv(float a) { return __fdiv_rn(1.0f, __fadd_rn(a, 1e-9f)); }
+
+VOX_DEV float* slot_state_f(float* state, const DetokDims& dd, int slot, int parity) {
+  return state + (static_cast<int64_t>(slot) * 2 + parity) * dd.state_floats;
+}
+
+// byte offset of element (row r, k) in a K-major SWIZZLE_128B operand whose
+// 64-element k-regions are stored one after another (rows x 128 B each)
+VOX_DEV uint32_t swz_off(int r, int k, int rows) {
+  const int kr = k >> 6, kk = k & 63;
+  const int chunk = (kk >> 3) ^ (r & 7);
+  return static_cast<uint32_t>(kr * rows * 128 + r * 128 + chunk * 16 + (kk & 7) * 2);
+}
+
+}  // namespace
+
+constexpr int kRuRows = 128;  // rows per tile (UMMA M)
+// threads: 4 warps per 32 columns of the tile (C = 128 runs 1 CTA per SM, so
+// it gets 16 warps to hide the Snake / dwconv latency chains)
+template <int C>
+__host__ __device__ constexpr int ru_threads() { return C == 64 ? 256 : 512; }
+
+template <int C>
+struct RuSmem {
+  static constexpr int kMaxHalo = 6 * 9;
+  static constexpr int kY1Floats = (kRuRows + kMaxHalo) * C;
+  static constexpr int kStage = kRuRows * (C + 1);  // epilogue staging (reuses y1)
+  static constexpr int kY1Bytes = (kY1Floats > kStage ? kY1Floats : kStage) * 4;
+  static constexpr int kABytes = kRuRows * C * 2;
+  static constexpr int kBBytes = C * C * 2;
+  static constexpr int kAOff = (kY1Bytes + 1023) / 1024 * 1024;
+  static constexpr int kBOff = kAOff + kABytes;
+  static constexpr int kBarOff = kBOff + kBBytes;
+  static constexpr int kBytes = kBarOff + 64 + 1024;  // + alignment slack
+};
+
+template <int C>
+__global__ void __launch_bounds__(ru_threads<C>())
+    ru_fused_kernel(const ReqHdrF* hdr, const DetokReq* __restrict__ reqs, int up,
+                    const float* __restrict__ x, float* __restrict__ y, int dil,
+                    const float* __restrict__ alpha1, const float* __restrict__ dw_w,
+                    const float* __restrict__ dw_b, const float* __restrict__ alpha2,
+                    const bf16* __restrict__ pw_w, const float* __restrict__ pw_b,
+                    float* __restrict__ state, int64_t st_off, DetokDims dd) {
+  using L = RuSmem<C>;
+  constexpr int kRuThreads = ru_threads<C>();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  float* y1s = reinterpret_cast<float*>(smem);
+  uint8_t* sa = smem + L::kAOff;
+  uint8_t* sb = smem + L::kBOff;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int r0 = blockIdx.x * kRuRows;
+
+  // weights do not depend on the preceding kernel: stage W (K-major, swizzled)
+  for (int e = tid; e < C * C / 8; e += kRuThreads) {
+    const int n = e / (C / 8), k = (e % (C / 8)) * 8;
+    *reinterpret_cast<uint4*>(sb + swz_off(n, k, C)) =
+        *reinterpret_cast<const uint4*>(pw_w + static_cast<int64_t>(n) * C + k);
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, C);
+  griddep_wait();
+  griddep_launch();
+  const int n_rows = hdr->n_lat * up;
+  const bool active = r0 < n_rows;
+
+  // ---------------- 1. y1 = Snake(x) for the tile + causal halo ----------------
+  const int H = 6 * dil;
+  int t0 = 0, n = 0;
+  const float* hin = nullptr;
+  float* hout = nullptr;
+  if (active) {
+    const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+    t0 = r0 - q.lat_off * up;  // local row of the tile's first row
+    n = 4 * q.nf * up;         // rows of this request at this level
+    hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
+    hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+    const int nr = kRuRows + H;
+    for (int e = tid; e < nr * C; e += kRuThreads) {
+      const int i = e / C, ch = e % C;
+      const int t = t0 - H + i;  // local row
+      float v;
+      if (t >= 0) {
+        const float a = alpha1[ch];
+        v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], a, snake_inv(a));
+        if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
+      } else {
+        v = hin[(H + t) * C + ch];
+      }
+      y1s[i * C + ch] = v;
+    }
+    // short requests (n < H): shift the old context
+    for (int e = tid; e < kRuRows * C; e += kRuThreads) {
+      const int i = e / C, ch = e % C, t = t0 + i;
+      for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
+    }
+  }
+  __syncthreads();
+
+  // ---------------- 2. v = Snake(dwconv(y1)) -> bf16 UMMA operand ----------------
+  if (active) {
+    for (int e = tid; e < kRuRows * (C / 2); e += kRuThreads) {
+      const int i = e / (C / 2), ch = (e % (C / 2)) * 2;
+      float o[2];
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c2 = ch + cc;
+        float acc = dw_b[c2];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) acc = fmaf(dw_w[c2 * 7 + k], y1s[(H + i - (6 - k) * dil) * C + c2], acc);
+        o[cc] = snake_f(acc, alpha2[c2]);
+      }
+      const __nv_bfloat162 pr = __floats2bfloat162_rn(o[0], o[1]);
+      *reinterpret_cast<__nv_bfloat162*>(sa + swz_off(i, ch, kRuRows)) = pr;
+    }
+  }
+  fence_proxy_async();  // generic-proxy smem writes -> visible to tcgen05 (async proxy)
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // ---------------- 3. tcgen05.mma: acc[128 x C] = v[128 x C] . W^T ----------------
+  if (active && tid == 0) {
+    constexpr uint32_t idesc = make_idesc_bf16(128, C);
+    const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+#pragma unroll
+    for (int kr = 0; kr < C / 64; ++kr)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        umma_bf16(tmem, make_desc_k128(a0 + kr * kRuRows * 128 + k * 32),
+                  make_desc_k128(b0 + kr * C * 128 + k * 32), idesc, (kr | k) ? 1u : 0u);
+    umma_commit(bar);
+  }
+  if (active) {
+    mbar_wait(bar, 0);
+    tc_fence_after();
+    // ---------------- 4. epilogue: TMEM -> smem staging -> coalesced y ----------------
+    float* stg = y1s;  // y1 is dead now
+    const int quarter = warp & 3, part = warp >> 2;  // 32 columns per part
+    const int row = quarter * 32 + lane;
+    {
+      const int col = part * 32;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + col, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[row * (C + 1) + col + j] = __uint_as_float(r[j]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (active) {
+    const float* stg = y1s;
+    for (int e = tid; e < kRuRows * C; e += kRuThreads) {
+      const int i = e / C, ch = e % C;
+      const int64_t gi = static_cast<int64_t>(r0 + i) * C + ch;
+      y[gi] = (stg[i * (C + 1) + ch] + pw_b[ch]) + x[gi];
+    }
+  }
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C);
+  }
+}
+
+template <int C>
+static void ru_fused_launch(const DetokReq* reqs, int rows, int up, const float* x, float* y,
+                            int dil, const float* a1, const float* dw_w, const float* dw_b,
+                            const float* a2, const bf16* pw_w, const float* pw_b, float* state,
+                            int64_t st_off, const DetokDims& dd, cudaStream_t st) {
+  const ReqHdrF* hdr = reinterpret_cast<const ReqHdrF*>(reqs) - 1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ru_fused_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         RuSmem<C>::kBytes);
+    attr = true;
+  }
+  launch_k(ru_fused_kernel<C>, dim3((rows + kRuRows - 1) / kRuRows), dim3(ru_threads<C>()),
+           RuSmem<C>::kBytes, st, hdr, reqs, up, x, y, dil, a1, dw_w, dw_b, a2, pw_w, pw_b, state,
+           st_off, dd);
+}
+
+bool ru_fused_supported(int C, int up) { return (C == 64 || C == 128) && (4 * up) % kRuRows == 0; }
+
+void launch_ru_fused(const DetokReq* reqs, int rows, int up, const float* x, float* y, int C,
+                     int dil, const float* alpha1, const float* dw_w, const float* dw_b,
+                     const float* alpha2, const bf16* pw_w, const float* pw_b, float* state,
+                     int64_t st_off, const DetokDims& dd, cudaStream_t st) {
+  if (C == 64)
+    ru_fused_launch<64>(reqs, rows, up, x, y, dil, alpha1, dw_w, dw_b, alpha2, pw_w, pw_b, state,
+                        st_off, dd, st);
+  else
+    ru_fused_launch<128>(reqs, rows, up, x, y, dil, alpha1, dw_w, dw_b, alpha2, pw_w, pw_b, state,
+                         st_off, dd, st);
+}
+
+// ---------------------------------------------------------------------------
+// Output head, tiled: Snake once per element into shared memory (tile + 6-row
+// causal halo from the cached context), then one thread per output sample:
+// pcm[t] = tanh(b + sum_{c,k} w[c][k] * s[t-6+k][c]).
+// ---------------------------------------------------------------------------
+constexpr int kOutRows = 128;
+
+template <int C>
+__global__ void __launch_bounds__(kOutRows)
+    detok_out_tiled_kernel(const ReqHdrF* hdr, const DetokReq* __restrict__ reqs, int up,
+                           const float* __restrict__ x, const float* __restrict__ alpha,
+                           const float* __restrict__ w, float b, float* __restrict__ state,
+                           int64_t st_off, DetokDims dd, float* __restrict__ pcm) {
+  __shared__ float s[(kOutRows + 6) * (C + 1)];
+  __shared__ float ws[C * 7];
+  const int tid = threadIdx.x;
+  for (int e = tid; e < C * 7; e += kOutRows) ws[e] = w[e];
+  griddep_wait();
+  griddep_launch();
+  const int r0 = blockIdx.x * kOutRows;
+  if (r0 >= hdr->n_lat * up) return;
+  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const int t0 = r0 - q.lat_off * up;
+  const int n = 4 * q.nf * up;
+  constexpr int H = 6;
+  const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
+  float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+  for (int e = tid; e < (kOutRows + H) * C; e += kOutRows) {
+    const int i = e / C, ch = e % C;
+    const int t = t0 - H + i;
+    float v;
+    if (t >= 0) {
+      v = snake_f(x[static_cast<int64_t>(r0 - H + i) * C + ch], alpha[ch]);
+      if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;
+    } else {
+      v = hin[(H + t) * C + ch];
+    }
+    s[i * (C + 1) + ch] = v;
+  }
+  for (int e = tid; e < kOutRows * C; e += kOutRows) {
+    const int i = e / C, ch = e % C, t = t0 + i;
+    for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
+  }
+  __syncthreads();
+  const int t = t0 + tid;
+  float acc = 0.f;
+  // same per-lane accumulation order as detok_out_kernel: channel c's 7 taps
+  // are summed into lane (c % 32)'s partial, then a warp reduction (here: the
+  // 32 partials summed in the same butterfly order)
+  float part[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) part[l] = 0.f;
+#pragma unroll
+  for (int ch = 0; ch < C; ++ch) {
+    float a = part[ch & 31];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) a = fmaf(ws[ch * 7 + k], s[(tid + k) * (C + 1) + ch], a);
+    part[ch & 31] = a;
+  }
+  // butterfly (xor 16, 8, 4, 2, 1) as warp_sum: lane 0's result
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+      if (l < o) part[l] = part[l] + part[l + o];
+  acc = part[0];
+  if (t < q.n_samples && t < n) pcm[q.pcm_off + t] = tanhf(acc + b);
+}
+
+void launch_detok_out_tiled(const DetokReq* reqs, int rows, int up, const float* x, int C,
+                            const float* alpha, const float* w, float b, float* state,
+                            int64_t st_off, const DetokDims& dd, float* pcm, cudaStream_t st) {
+  const ReqHdrF* hdr = reinterpret_cast<const ReqHdrF*>(reqs) - 1;
+  if (C == 64)
+    launch_k(detok_out_tiled_kernel<64>, dim3((rows + kOutRows - 1) / kOutRows), dim3(kOutRows), 0,
+             st, hdr, reqs, up, x, alpha, w, b, state, st_off, dd, pcm);
+}
+
+bool detok_out_tiled_supported(int C, int up) { return C == 64 && (4 * up) % kOutRows == 0; }
+
+}  // namespace vox

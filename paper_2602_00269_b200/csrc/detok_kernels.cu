@@ -29,7 +29,7 @@ VOX_DEV int find_req(const DetokReq* reqs, int n_req, int lat_row) {
 }
 
 VOX_DEV float snake(float x, float a) {
-  const float s = sinf(__fmul_rn(a, x));
+  const float s = snake_sin(__fmul_rn(a, x));
   return __fadd_rn(x, __fmul_rn(__fdiv_rn(1.0f, __fadd_rn(a, 1e-9f)), __fmul_rn(s, s)));
 }
 

@@ -14,25 +14,33 @@
 // warps run the epilogue (tcgen05.ld 32x32b -> registers -> coalesced stores).
 #include "common.cuh"
 #include "kernels.h"
+#include <cstdlib>
 
 namespace vox {
 
-template <int BN>
+template <int BN, int MT>
 struct GemmCfg {
-  static constexpr int kABytes = 128 * 64 * 2;
+  // MT = 128-row weight sub-tiles per CTA (1 or 2).  MT = 2 computes a 256 x BN
+  // output tile as two M=128 UMMAs that share one activation (B) stage: the
+  // activation slab is re-read from L2 half as often (it is re-read once per
+  // weight tile), which is what bounds the swap-AB decode GEMM at large batch.
+  static constexpr int kABytes = MT * 128 * 64 * 2;
   static constexpr int kBBytes = BN * 64 * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages =
-      BN >= 256 ? 4 : (96 * 1024 / kStageBytes > 8 ? 8 : 96 * 1024 / kStageBytes);
-  static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kBudget = MT == 2 ? 192 * 1024 : 96 * 1024;
+  static constexpr int kStages0 = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
+  static constexpr int kStages = (MT == 1 && BN >= 256) ? 4 : kStages0;
+  static constexpr int kTmemCols0 = MT * BN < 32 ? 32 : MT * BN;
+  // power of two >= 32 (tcgen05.alloc granularity)
+  static constexpr int kTmemCols = kTmemCols0 <= 32 ? 32 : kTmemCols0 <= 64 ? 64 : kTmemCols0 <= 128 ? 128 : kTmemCols0 <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
-template <int BN>
+template <int BN, int MT>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmX, GemmArgs p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, MT>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -43,8 +51,10 @@ __global__ void __launch_bounds__(128, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * 128;
-  const int n0 = blockIdx.y * BN;
+  // n-tiles vary fastest so the CTAs that share a weight tile run in the same
+  // wave: each weight byte comes from HBM once (then L2) per split.
+  const int m0 = blockIdx.y * (128 * MT);
+  const int n0 = blockIdx.x * BN;
   const int split = blockIdx.z;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.n_kb, kb0 + p.kb_per_split);
@@ -77,7 +87,16 @@ __global__ void __launch_bounds__(128, 1)
     const int pre = nkb < C::kStages ? nkb : C::kStages;
     for (int i = 0; i < pre; ++i) {
       mbar_arrive_expect_tx(&full[i], C::kStageBytes);
-      tma_load_2d(smem + i * C::kStageBytes, &tmW, &full[i], (kb0 + i) * 64, m0, pol_w);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        if (p.w_packed != nullptr)
+          bulk_load(smem + i * C::kStageBytes + mt * 16384,
+                    p.w_packed + (static_cast<int64_t>(m0 / 128 + mt) * p.n_kb + kb0 + i) * 8192,
+                    16384, &full[i], pol_w);
+        else
+          tma_load_2d(smem + i * C::kStageBytes + mt * 16384, &tmW, &full[i], (kb0 + i) * 64,
+                      m0 + mt * 128, pol_w);
+      }
     }
     griddep_wait();
     for (int i = 0; i < pre; ++i)
@@ -89,7 +108,15 @@ __global__ void __launch_bounds__(128, 1)
       uint8_t* st = smem + s * C::kStageBytes;
       mbar_arrive_expect_tx(&full[s], C::kStageBytes);
       const int kx = (kb0 + i) * 64;
-      tma_load_2d(st, &tmW, &full[s], kx, m0, pol_w);
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        if (p.w_packed != nullptr)
+          bulk_load(st + mt * 16384,
+                    p.w_packed + (static_cast<int64_t>(m0 / 128 + mt) * p.n_kb + kb0 + i) * 8192,
+                    16384, &full[s], pol_w);
+        else
+          tma_load_2d(st + mt * 16384, &tmW, &full[s], kx, m0 + mt * 128, pol_w);
+      }
       tma_load_2d(st + C::kABytes, &tmX, &full[s], kx, n0, pol_x);
     }
   } else if (warp == 1 && lane == 0) {
@@ -103,8 +130,10 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t b_addr = a_addr + C::kABytes;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 4 x UMMA_K(16) per 64-wide k-block
-        umma_bf16(tmem, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + k * 32), idesc,
-                  (i > 0 || k > 0) ? 1u : 0u);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)  // accumulator mt lives at TMEM columns [mt*BN, mt*BN+BN)
+          umma_bf16(tmem + mt * BN, make_desc_k128(a_addr + mt * 16384 + k * 32),
+                    make_desc_k128(b_addr + k * 32), idesc, (i > 0 || k > 0) ? 1u : 0u);
       }
       umma_commit(&empty[s]);  // frees the smem stage once these MMAs retire
     }
@@ -116,23 +145,26 @@ __global__ void __launch_bounds__(128, 1)
   griddep_wait();  // outputs may alias buffers the preceding kernel was reading
   mbar_wait(done, 0);
   tc_fence_after();
-  const int m = m0 + warp * 32 + lane;
   float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
-  const bool m_ok = m < p.m_valid;
-  const float b = (p.bias != nullptr && m_ok) ? p.bias[m] : 0.f;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
-    tmem_ld_wait();
-    if (m_ok) {
+  for (int mt = 0; mt < MT; ++mt) {
+    const int m = m0 + mt * 128 + warp * 32 + lane;
+    const bool m_ok = m < p.m_valid;
+    const float b = (p.bias != nullptr && m_ok) ? p.bias[m] : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * BN + c, r);
+      tmem_ld_wait();
+      if (m_ok) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c + j;
-        if ((c + j) < BN && n < p.N) {
-          float v = __uint_as_float(r[j]) + b;
-          if (p.resid != nullptr) v += p.resid[static_cast<int64_t>(n) * p.ldr + m];
-          outp[static_cast<int64_t>(n) * p.ldo + m] = v;
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + c + j;
+          if ((c + j) < BN && n < p.N) {
+            float v = __uint_as_float(r[j]) + b;
+            if (p.resid != nullptr) v += p.resid[static_cast<int64_t>(n) * p.ldr + m];
+            outp[static_cast<int64_t>(n) * p.ldo + m] = v;
+          }
         }
       }
     }
@@ -177,20 +209,20 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
   return r == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int MT>
 static cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a,
                              int splits, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, MT>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_bf16_tc_kernel<BN, MT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grid((a.M + 127) / 128, (a.N + BN - 1) / BN, splits);
-  return launch_k(gemm_bf16_tc_kernel<BN>, grid, dim3(128), C::kSmemBytes, st, tw, tx, a);
+  dim3 grid((a.N + BN - 1) / BN, (a.M + 128 * MT - 1) / (128 * MT), splits);
+  return launch_k(gemm_bf16_tc_kernel<BN, MT>, grid, dim3(128), C::kSmemBytes, st, tw, tx, a);
 }
 
 int gemm_bn_for_rows(int rows) {
@@ -201,46 +233,59 @@ int gemm_bn_for_rows(int rows) {
   return 256;
 }
 
-// Tile width over the activation rows (UMMA N).  Measured on B200 at the
-// Orpheus-3B shapes (scripts/gemm_sweep.py, profiles/gemm_sweep_r01.txt):
-// one 256-wide tile is L2/latency-limited (every CTA re-reads the whole
-// activation slab), so large batches use 128-wide tiles, and 64-wide ones
-// when the weight matrix has few 128-row tiles (d_model outputs).
-int gemm_plan_bn(int M, int rows) {
-  int bn = gemm_bn_for_rows(rows);
-  if (bn > 128) bn = 128;
-  if (rows >= 128 && M <= 4096) bn = 64;
-  return bn;
-}
-
-// Split-K factor: ~2 CTAs per SM (2 x 148 slots), each split >= 2 k-blocks.
-int gemm_pick_splits(int M, int N, int K, int max_splits) {
-  const int bn = gemm_plan_bn(M, N);
-  const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+// Tile plan for out[rows, M] = X[rows, K] W[M, K]^T.
+// One 128 x BN tile per CTA (BN = rows rounded up to a power of two, capped at
+// 128; 64 for the d_model-wide outputs at >= 128 rows), ~2 CTAs per SM and
+// split-K to fill the machine: at decode sizes the GEMM streams weights, and
+// every SM must keep loads in flight (measured, profiles/gemm_sweep_r01.txt:
+// 256 x 256 tiles (MT = 2) leave SMs idle and lose 2x at 224 rows).
+GemmPlan gemm_plan(int M, int rows, int K) {
+  GemmPlan g{};
   const int n_kb = K / 64;
+  g.bn = gemm_bn_for_rows(rows);
+  if (g.bn > 128) g.bn = 128;
+  if (rows >= 128 && M <= 4096) g.bn = 64;
+  g.mt = 1;
+  if (const char* e = getenv("VOX_GEMM_BN_TEST")) {  // microbenchmarks only
+    const int f = atoi(e);
+    if (f == 16 || f == 32 || f == 64 || f == 128 || f == 256) g.bn = f;
+  }
+  if (const char* e = getenv("VOX_GEMM_MT_TEST")) g.mt = atoi(e) == 2 ? 2 : 1;
+  const int tiles = ((M + 128 * g.mt - 1) / (128 * g.mt)) * ((rows + g.bn - 1) / g.bn);
+  const int slots = (g.mt == 2 ? 1 : 2) * kNumSMs;
   int best = 1;
-  const int target = 2 * kNumSMs;
-  for (int s = 1; s <= max_splits; ++s) {
+  for (int s = 1; s <= kGemmMaxSplits; ++s) {
     const int per = (n_kb + s - 1) / s;
     if (per < 2) break;
     if ((n_kb + per - 1) / per != s) continue;  // every split non-empty
-    if (tiles * s > target) break;
+    if (tiles * s > slots) break;
     best = s;
   }
-  return best;
+  g.splits = best;
+  if (const char* e = getenv("VOX_GEMM_SPLITS_TEST")) g.splits = atoi(e) < 1 ? 1 : atoi(e);
+  return g;
 }
 
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
-                        int bn, cudaStream_t st) {
+                        int bn, int mt, cudaStream_t st) {
   a.n_kb = a.K / 64;
   a.kb_per_split = (a.n_kb + splits - 1) / splits;
   splits = (a.n_kb + a.kb_per_split - 1) / a.kb_per_split;
+  if (mt == 2) {
+    switch (bn) {
+      case 16: return launch_bn<16, 2>(tw, tx, a, splits, st);
+      case 32: return launch_bn<32, 2>(tw, tx, a, splits, st);
+      case 64: return launch_bn<64, 2>(tw, tx, a, splits, st);
+      case 128: return launch_bn<128, 2>(tw, tx, a, splits, st);
+      default: return launch_bn<256, 2>(tw, tx, a, splits, st);
+    }
+  }
   switch (bn) {
-    case 16: return launch_bn<16>(tw, tx, a, splits, st);
-    case 32: return launch_bn<32>(tw, tx, a, splits, st);
-    case 64: return launch_bn<64>(tw, tx, a, splits, st);
-    case 128: return launch_bn<128>(tw, tx, a, splits, st);
-    default: return launch_bn<256>(tw, tx, a, splits, st);
+    case 16: return launch_bn<16, 1>(tw, tx, a, splits, st);
+    case 32: return launch_bn<32, 1>(tw, tx, a, splits, st);
+    case 64: return launch_bn<64, 1>(tw, tx, a, splits, st);
+    case 128: return launch_bn<128, 1>(tw, tx, a, splits, st);
+    default: return launch_bn<256, 1>(tw, tx, a, splits, st);
   }
 }
 

@@ -42,19 +42,32 @@ struct GemmArgs {
   const float* resid;     // [N, ldr] or null (only with 1 split)
   int64_t ldr;
   int m_valid;            // columns m >= m_valid are not stored
+  const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
+                          // copies of contiguous 16 KB tiles instead of the tensor map
 };
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer,
                     uint64_t row_stride_bytes, uint32_t box_outer);
 int gemm_bn_for_rows(int rows);
-int gemm_plan_bn(int M, int rows);
-int gemm_pick_splits(int M, int N, int K, int max_splits);
+constexpr int kGemmMaxSplits = 16;
+struct GemmPlan {
+  int bn;      // activation rows per tile (UMMA N)
+  int mt;      // 128-row weight sub-tiles per CTA (1 or 2)
+  int splits;  // split-K factor (fp32 partial planes)
+};
+GemmPlan gemm_plan(int M, int rows, int K);
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
-                        int bn, cudaStream_t st);
+                        int bn, int mt, cudaStream_t st);
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).
 void launch_init_bf16(bf16* w, int64_t n, uint64_t key, float scale, cudaStream_t st);
+// packed-tile variant (see init.cu); buffer holds roundup(M, 128) * K elements
+void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t key,
+                             float scale, cudaStream_t st);
+void launch_pack_bf16(const bf16* src, bf16* dst, int64_t M, int64_t K, cudaStream_t st);
+inline int64_t packed_elems(int64_t M, int64_t K) { return (M + 127) / 128 * 128 * K; }
+void launch_l2_flush(const void* buf, size_t bytes, uint32_t* sink, cudaStream_t st);
 // fp32 variant: w[i] = offset + unit_pm1(mix64(key+i)) * scale rounded through bf16.
 void launch_init_f32(float* w, int64_t n, uint64_t key, float scale, float offset,
                      cudaStream_t st);
@@ -62,6 +75,9 @@ void launch_init_f32(float* w, int64_t n, uint64_t key, float scale, float offse
 // ---------------------------------------------------------------- LM step
 struct RowDev {
   int32_t slot, pos, token, sample;
+  int32_t fresh;  // lowest position of this slot whose K/V this forward appends: pages
+                  // below fresh / page_size are complete before the forward starts
+  int32_t pad_[3];
 };
 
 struct LmDims {
@@ -158,5 +174,16 @@ void launch_ru_prep(const DetokReq* reqs, int n_req, int rows, int up, const flo
 void launch_detok_out(const DetokReq* reqs, int n_req, int rows, int up, const float* x, int C,
                       const float* alpha, const float* w, float b, float* state, int64_t st_off,
                       const DetokDims& dd, float* pcm, cudaStream_t st);
+
+// fused residual unit / tiled output head (detok_fused.cu)
+bool ru_fused_supported(int C, int up);
+void launch_ru_fused(const DetokReq* reqs, int rows, int up, const float* x, float* y, int C,
+                     int dil, const float* alpha1, const float* dw_w, const float* dw_b,
+                     const float* alpha2, const bf16* pw_w, const float* pw_b, float* state,
+                     int64_t st_off, const DetokDims& dd, cudaStream_t st);
+bool detok_out_tiled_supported(int C, int up);
+void launch_detok_out_tiled(const DetokReq* reqs, int rows, int up, const float* x, int C,
+                            const float* alpha, const float* w, float b, float* state,
+                            int64_t st_off, const DetokDims& dd, float* pcm, cudaStream_t st);
 
 }  // namespace vox

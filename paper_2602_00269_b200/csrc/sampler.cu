@@ -80,6 +80,43 @@ VOX_DEV T block_reduce_sum(T v, T* red, T* out_slot) {
   return *out_slot;
 }
 
+// Descending-bin scan by one warp (replaces a serial loop over the bins):
+// visits bins nb-1 .. 0, skipping empty ones (cnt == 0), and stops at the
+// first bin whose inclusive cumulative weight reaches `target`.  Returns that
+// bin (or the lowest non-empty bin if the target is never reached) and, in
+// *before, the cumulative weight of the bins strictly above it (or the full
+// total when the target is never reached, matching the serial loop).
+// weight(b) is the bin's mass (top-p) or count (top-k) as float/int.
+template <typename T, typename WF, typename CF>
+VOX_DEV int warp_scan_desc(int nb, T target, WF weight, CF nonempty, T* before) {
+  const int lane = threadIdx.x & 31;
+  T acc = 0;
+  int last_nz = -1;
+  for (int base = nb - 1; base >= 0; base -= 32) {
+    const int b = base - lane;
+    const bool ne = b >= 0 && nonempty(b);
+    const T m = ne ? weight(b) : T(0);
+    T incl = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const T t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const T tot = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t hit = __ballot_sync(0xffffffffu, ne && acc + incl >= target);
+    if (hit) {
+      const int l = __ffs(hit) - 1;
+      *before = acc + __shfl_sync(0xffffffffu, incl - m, l);
+      return base - l;
+    }
+    const uint32_t nz = __ballot_sync(0xffffffffu, ne);
+    if (nz) last_nz = base - (31 - __clz(nz));
+    acc += tot;
+  }
+  *before = acc;
+  return last_nz;
+}
+
 struct RowCtx {
   const float* row;  // row[id - col_base]
   int col_base, lo, hi;
@@ -288,17 +325,16 @@ VOX_DEV int sample_row(SampSmem& S, uint32_t* bm, const float* row, int col_base
     int rank = prm.top_k;  // rank-th largest
     for (int lv = 0; lv < 3; ++lv) {
       hist_pass<false>(c, S, prefix, mask, shifts[lv], nbits[lv], ymax, 0u, INT32_MAX);
-      if (tid == 0) {
-        int acc = 0;
-        for (int b = (1 << nbits[lv]) - 1; b >= 0; --b) {
-          const int cnt = static_cast<int>(S.hcnt[b]);
-          if (acc + cnt >= rank) {
-            S.u_a = static_cast<uint32_t>(b);
-            S.i_a = rank - acc;
-            S.i_b = cnt;
-            break;
-          }
-          acc += cnt;
+      if (tid < 32) {
+        int before = 0;
+        const int r0 = rank;
+        const int b = warp_scan_desc<int>(
+            1 << nbits[lv], r0, [&](int x) { return static_cast<int>(S.hcnt[x]); },
+            [&](int) { return true; }, &before);
+        if (tid == 0) {
+          S.u_a = static_cast<uint32_t>(b < 0 ? 0 : b);
+          S.i_a = rank - before;
+          S.i_b = b < 0 ? 0 : static_cast<int>(S.hcnt[b]);
         }
       }
       __syncthreads();
@@ -329,28 +365,24 @@ VOX_DEV int sample_row(SampSmem& S, uint32_t* bm, const float* row, int col_base
         hist_pass<true>(c, S, prefix, mask, shifts[lv], nbits[lv], ymax, kb_key, kb_tie_idx);
       else
         hist_pass<false>(c, S, prefix, mask, shifts[lv], nbits[lv], ymax, kb_key, kb_tie_idx);
-      if (tid == 0) {
-        if (lv == 0) {
-          float Z = 0.f;
-          for (int b = 0; b < kBins; ++b) Z += S.hmass[b];
-          S.f_b = static_cast<float>(prm.top_p) * Z;
-        }
+      if (lv == 0) {
+        float z = 0.f;
+        for (int b = tid; b < kBins; b += kST) z += S.hmass[b];
+        z = block_reduce_sum<float>(z, S.redf, &S.f_b);
+        if (tid == 0) S.f_b = static_cast<float>(prm.top_p) * z;
       }
       __syncthreads();
       if (lv == 0) target = S.f_b;
       if (lv < 2) {
-        if (tid == 0) {
-          float acc = 0.f;
-          int sel = -1;
-          for (int b = (1 << nbits[lv]) - 1; b >= 0; --b) {
-            const float mb = S.hmass[b];
-            if (mb <= 0.f) continue;
-            sel = b;
-            if (acc + mb >= target) break;
-            acc += mb;
+        if (tid < 32) {
+          float before = 0.f;
+          const int sel = warp_scan_desc<float>(
+              1 << nbits[lv], target, [&](int x) { return S.hmass[x]; },
+              [&](int x) { return S.hmass[x] > 0.f; }, &before);
+          if (tid == 0) {
+            S.u_a = static_cast<uint32_t>(sel < 0 ? 0 : sel);
+            S.f_a = before;
           }
-          S.u_a = static_cast<uint32_t>(sel < 0 ? 0 : sel);
-          S.f_a = acc;
         }
         __syncthreads();
         prefix |= S.u_a << shifts[lv];
@@ -360,23 +392,24 @@ VOX_DEV int sample_row(SampSmem& S, uint32_t* bm, const float* row, int col_base
         __syncthreads();
       } else {
         // last digit: per-bin element value is exact (full key known)
-        if (tid == 0) {
-          float acc = 0.f;
-          int sel = -1, cnt_sel = 0;
-          for (int b = (1 << nbits[lv]) - 1; b >= 0; --b) {
-            int cnt = static_cast<int>(S.hcnt[b]);
-            if (cnt == 0) continue;
-            const uint32_t kk = prefix | static_cast<uint32_t>(b);
+        if (tid < 32) {
+          // ties at the top-k boundary key count only up to the kept number
+          auto cnt_of = [&](int x) {
+            int cnt = static_cast<int>(S.hcnt[x]);
+            const uint32_t kk = prefix | static_cast<uint32_t>(x);
             if (kk == kb_key && kb_ties_kept > 0 && cnt > kb_ties_kept) cnt = kb_ties_kept;
-            const float w = expf(key2f(kk) - ymax);
-            sel = b;
-            cnt_sel = cnt;
-            if (acc + w * cnt >= target) break;
-            acc += w * cnt;
+            return cnt;
+          };
+          float before = 0.f;
+          const int sel = warp_scan_desc<float>(
+              1 << nbits[lv], target,
+              [&](int x) { return expf(key2f(prefix | static_cast<uint32_t>(x)) - ymax) * cnt_of(x); },
+              [&](int x) { return S.hcnt[x] != 0u; }, &before);
+          if (tid == 0) {
+            S.u_a = static_cast<uint32_t>(sel < 0 ? 0 : sel);
+            S.f_a = before;
+            S.i_a = sel < 0 ? 0 : cnt_of(sel);
           }
-          S.u_a = static_cast<uint32_t>(sel < 0 ? 0 : sel);
-          S.f_a = acc;
-          S.i_a = cnt_sel;
         }
         __syncthreads();
         prefix |= S.u_a;

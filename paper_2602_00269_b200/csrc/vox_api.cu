@@ -122,8 +122,8 @@ struct VoxCtx {
   bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
   float* inv_freq = nullptr;
   float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
-  std::vector<CUtensorMap> tm_qkv, tm_o, tm_gu, tm_down;
-  CUtensorMap tm_head_full{}, tm_head_audio{};
+  bf16* w_head_audio = nullptr;  // packed copy of the tied head's audio rows
+  CUtensorMap tm_head_full{};
   int head_audio_rows = 0;
 
   // ---- activations [max_rows, ...]
@@ -186,6 +186,7 @@ struct VoxCtx {
   std::map<int, int64_t> detok_graph_launches;
 
   int detok_stop = 1 << 30;  // debug: stop the detok pipeline after this many stages
+  bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
 
   // ---- timing / counting
@@ -257,15 +258,13 @@ static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* 
 }
 
 // GEMM over `rows` activation rows of buffer map set `xm`.
+// `wp` non-null: W is in the packed tile layout (init.cu) and `tw` is unused.
 static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>& xm, int M,
                     int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
-                    const char* cls = "gemm") {
-  int bn = gemm_plan_bn(M, rows);
-  if (const char* e = getenv("VOX_GEMM_BN_TEST")) {  // microbenchmarks only
-    const int f = atoi(e);
-    if (f == 16 || f == 32 || f == 64 || f == 128 || f == 256) bn = f;
-  }
+                    const char* cls = "gemm", const bf16* wp = nullptr) {
+  const GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
+  const int bn = plan.bn;
   GemmArgs a{};
   a.M = M;
   a.N = rows;
@@ -277,10 +276,11 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.resid = resid;
   a.ldr = ldr;
   a.m_valid = m_valid;
+  a.w_packed = wp;
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
-  cudaError_t e = gemm_launch(tw, xm.at(bn), a, splits, bn, st);
+  cudaError_t e = gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
 }
@@ -311,8 +311,9 @@ static int create_backbone(VoxCtx* c) {
   const int L = g.n_layers, d = g.d_model, hd = g.head_dim, H = g.n_heads, KV = g.n_kv_heads;
   const int dff = g.d_ff, V = g.vocab;
   c->nqkv = (H + 2 * KV) * hd;
-  const int64_t n_qkv = static_cast<int64_t>(c->nqkv) * d, n_o = static_cast<int64_t>(d) * H * hd;
-  const int64_t n_gu = static_cast<int64_t>(2) * dff * d, n_dn = static_cast<int64_t>(d) * dff;
+  // projection weights live in the packed tile layout (init.cu) the GEMM streams
+  const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, H * hd);
+  const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
   CK(dalloc(&c->emb, static_cast<size_t>(V) * d));
   CK(dalloc(&c->norm_attn, static_cast<size_t>(L) * d));
   CK(dalloc(&c->norm_mlp, static_cast<size_t>(L) * d));
@@ -322,13 +323,23 @@ static int create_backbone(VoxCtx* c) {
   CK(dalloc(&c->w_gu, static_cast<size_t>(L * n_gu)));
   CK(dalloc(&c->w_down, static_cast<size_t>(L * n_dn)));
   RET(init_bf16(c, c->emb, static_cast<int64_t>(V) * d, T_EMB, 0, g.embed_scale));
+  auto packed = [&](bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t tid, uint64_t layer,
+                    float scale) {
+    launch_init_bf16_packed(w, M, K, row0, tensor_key(c->seed, tid, layer), scale, c->s_lm);
+    return cudaGetLastError() == cudaSuccess ? VOX_OK : fail(c, VOX_ERR_CUDA, "init packed");
+  };
   for (int l = 0; l < L; ++l) {
     RET(init_f32(c, c->norm_attn + static_cast<int64_t>(l) * d, d, T_NORM_ATTN, l, 0.25f, 1.0f));
     RET(init_f32(c, c->norm_mlp + static_cast<int64_t>(l) * d, d, T_NORM_MLP, l, 0.25f, 1.0f));
-    RET(init_bf16(c, c->w_qkv + l * n_qkv, n_qkv, T_QKV, l, std::sqrt(3.0f / d)));
-    RET(init_bf16(c, c->w_o + l * n_o, n_o, T_O, l, std::sqrt(3.0f / (H * hd))));
-    RET(init_bf16(c, c->w_gu + l * n_gu, n_gu, T_GU, l, std::sqrt(3.0f / d)));
-    RET(init_bf16(c, c->w_down + l * n_dn, n_dn, T_DOWN, l, std::sqrt(3.0f / dff)));
+    RET(packed(c->w_qkv + l * n_qkv, c->nqkv, d, 0, T_QKV, l, std::sqrt(3.0f / d)));
+    RET(packed(c->w_o + l * n_o, d, H * hd, 0, T_O, l, std::sqrt(3.0f / (H * hd))));
+    RET(packed(c->w_gu + l * n_gu, 2 * dff, d, 0, T_GU, l, std::sqrt(3.0f / d)));
+    RET(packed(c->w_down + l * n_dn, d, dff, 0, T_DOWN, l, std::sqrt(3.0f / dff)));
+  }
+  if (g.audio_base >= 0) {  // packed copy of the audio rows of the tied head
+    const int rows = g.frame_tokens * g.codebook_size;
+    CK(dalloc(&c->w_head_audio, static_cast<size_t>(packed_elems(rows, d))));
+    RET(packed(c->w_head_audio, rows, d, g.audio_base, T_EMB, 0, g.embed_scale));
   }
   RET(init_f32(c, c->norm_final, d, T_NORM_FINAL, 0, 0.25f, 1.0f));
   // RoPE inverse frequencies, fp64 -> fp32 (oracle: identical table)
@@ -353,24 +364,11 @@ static int create_backbone(VoxCtx* c) {
     CK(cudaMemcpy(c->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
 
-  c->tm_qkv.resize(L);
-  c->tm_o.resize(L);
-  c->tm_gu.resize(L);
-  c->tm_down.resize(L);
-  for (int l = 0; l < L; ++l) {
-    bool ok = make_tmap_bf16(&c->tm_qkv[l], c->w_qkv + l * n_qkv, d, c->nqkv, d * 2ull, 128) &&
-              make_tmap_bf16(&c->tm_o[l], c->w_o + l * n_o, H * hd, d, H * hd * 2ull, 128) &&
-              make_tmap_bf16(&c->tm_gu[l], c->w_gu + l * n_gu, d, 2 * dff, d * 2ull, 128) &&
-              make_tmap_bf16(&c->tm_down[l], c->w_down + l * n_dn, dff, d, dff * 2ull, 128);
-    if (!ok) return fail(c, VOX_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
-  }
   if (!make_tmap_bf16(&c->tm_head_full, c->emb, d, V, d * 2ull, 128))
     return fail(c, VOX_ERR_CUDA, "tensor map (lm head)");
   if (g.audio_base >= 0) {
     c->head_audio_rows = g.frame_tokens * g.codebook_size;
-    if (!make_tmap_bf16(&c->tm_head_audio, c->emb + static_cast<int64_t>(g.audio_base) * d, d,
-                        c->head_audio_rows, d * 2ull, 128))
-      return fail(c, VOX_ERR_CUDA, "tensor map (audio head)");
+
   }
   return VOX_OK;
 }
@@ -615,14 +613,17 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     launch_embed_norm(c->d_rows, nrows, c->token_store, g.max_ctx, c->emb, c->norm_attn, dm, c->h,
                       c->x, st);
   }
-  const int sp_qkv = gemm_pick_splits(c->nqkv, nrows, d, 16);
-  const int sp_o = gemm_pick_splits(d, nrows, Hhd, 16);
-  const int sp_gu = gemm_pick_splits(2 * dff, nrows, d, 16);
-  const int sp_dn = gemm_pick_splits(d, nrows, dff, 16);
+  const int sp_qkv = gemm_plan(c->nqkv, nrows, d).splits;
+  const int sp_o = gemm_plan(d, nrows, Hhd).splits;
+  const int sp_gu = gemm_plan(2 * dff, nrows, d).splits;
+  const int sp_dn = gemm_plan(d, nrows, dff).splits;
   const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
+  const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
+  const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
+  const CUtensorMap& tw_unused = c->tm_head_full;  // packed weights: the W map is not read
   for (int l = 0; l < L; ++l) {
-    RET(run_gemm(c, c->tm_qkv[l], c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
-                 nullptr, 0, c->nqkv, st));
+    RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
+                 nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv));
     {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * sp_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws, sp_qkv,
@@ -635,22 +636,22 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
                          c->page_table, dm, c->attn, c->attn_ws, asp, st);
     }
-    RET(run_gemm(c, c->tm_o[l], c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
-                 st));
+    RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
+                 st, "gemm", c->w_o + l * n_o));
     {
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_o + 10));
       launch_resid_norm(c->d_rows, nrows, c->ws, sp_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
-    RET(run_gemm(c, c->tm_gu[l], c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
-                 nullptr, 0, 2 * dff, st));
+    RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
+                 nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu));
     {
       TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
       launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
     }
-    RET(run_gemm(c, c->tm_down[l], c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
-                 d, st));
+    RET(run_gemm(c, tw_unused, c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
+                 d, st, "gemm", c->w_down + l * n_dn));
     {
       const bool last = (l == L - 1);
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_dn + 10));
@@ -662,8 +663,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
   if (nsamp > 0) {
     const bool audio = (g.audio_base >= 0) && !full_logits;
     const int M = audio ? c->head_audio_rows : g.vocab;
-    RET(run_gemm(c, audio ? c->tm_head_audio : c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits,
-                 M, 1, nullptr, nullptr, 0, M, st, "lm_head"));
+    RET(run_gemm(c, c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits, M, 1, nullptr, nullptr, 0,
+                 M, st, "lm_head", audio ? c->w_head_audio : nullptr));
     SampFusedArgs a{};
     a.rows = c->d_rows;
     a.sample_rows = c->d_sample_rows;
@@ -794,7 +795,7 @@ void vox_destroy(VoxCtx* c) {
     cudaEventDestroy(t.b);
   }
   void* dev_ptrs[] = {c->emb, c->norm_attn, c->norm_mlp, c->norm_final, c->w_qkv, c->w_o,
-                      c->w_gu, c->w_down, c->inv_freq, c->rope_tab, c->h, c->x, c->xf, c->q, c->attn, c->act,
+                      c->w_gu, c->w_down, c->w_head_audio, c->inv_freq, c->rope_tab, c->h, c->x, c->xf, c->q, c->attn, c->act,
                       c->ws, c->attn_ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
                       c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->d_sample_rows,
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
@@ -1010,9 +1011,18 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
   }
   int k = 0;
   double attn_bytes = 0;
+  // lowest position appended per slot in this forward (attention may read the
+  // pages below it before the grid-dependency wait)
+  std::map<int, int> fresh;
+  for (int i = 0; i < n; ++i) {
+    auto it = fresh.find(rows[i].slot);
+    if (it == fresh.end()) fresh.emplace(rows[i].slot, rows[i].pos);
+    else it->second = std::min(it->second, static_cast<int>(rows[i].pos));
+  }
   for (int i = 0; i < nrows; ++i) {
     if (i < n) {
-      sg.rows[i] = RowDev{rows[i].slot, rows[i].pos, rows[i].token, rows[i].sample};
+      sg.rows[i] = RowDev{rows[i].slot, rows[i].pos, rows[i].token, rows[i].sample,
+                          fresh[rows[i].slot], {0, 0, 0}};
       attn_bytes += static_cast<double>(rows[i].pos + 1) * g.n_kv_heads * g.head_dim * 4;
       if (rows[i].sample) {
         sg.sample_rows[k] = i;
@@ -1021,7 +1031,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
         sg.out_index[i] = -1;
       }
     } else {
-      sg.rows[i] = RowDev{-1, 0, -1, 0};
+      sg.rows[i] = RowDev{-1, 0, -1, 0, 0, {0, 0, 0}};
       sg.out_index[i] = -1;
     }
   }
@@ -1223,6 +1233,16 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
     std::map<int, CUtensorMap> rm;
     if (!make_act_maps(c, rm, c->dbf, Co, rows2)) return fail(c, VOX_ERR_CUDA, "tmap ru");
     for (int u = 0; u < 3; ++u) {
+      if (ru_fused_supported(Co, up) && !c->detok_unfused) {
+        TimedLaunch tl(c, st, "detok_ru", static_cast<double>(rows2) * Co * 8);
+        launch_ru_fused(reqs, rows2, up, x, y, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
+                        w.ru_dw_b[b][u], w.ru_a2[b][u], w.ru_pw_w[b][u], w.ru_pw_b[b][u],
+                        c->dstate, dd.off_ru[b][u], dd, st);
+        std::swap(x, y);
+        DSTOP(nullptr);
+        DSTOP(x);
+        continue;
+      }
       {
         TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows2) * Co * 6);
         launch_ru_prep(reqs, n_req, rows2, up, x, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
@@ -1238,8 +1258,12 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
   {
     const int rows = n_lat * up;
     TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows) * dd.ch[4] * 4);
-    launch_detok_out(reqs, n_req, rows, up, x, dd.ch[4], w.out_alpha, w.out_w, w.out_b, c->dstate,
-                     dd.off_out, dd, c->d_pcm, st);
+    if (detok_out_tiled_supported(dd.ch[4], up) && !c->detok_unfused)
+      launch_detok_out_tiled(reqs, rows, up, x, dd.ch[4], w.out_alpha, w.out_w, w.out_b,
+                             c->dstate, dd.off_out, dd, c->d_pcm, st);
+    else
+      launch_detok_out(reqs, n_req, rows, up, x, dd.ch[4], w.out_alpha, w.out_w, w.out_b,
+                       c->dstate, dd.off_out, dd, c->d_pcm, st);
   }
   CK(cudaGetLastError());
   return VOX_OK;
@@ -1481,20 +1505,42 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   std::map<int, CUtensorMap> xm;
   if (!make_tmap_bf16(&tw, dw, K, M, K * 2ull, 128) || !make_act_maps(c, xm, dx, K, N))
     return fail(c, VOX_ERR_CUDA, "tensor map (gemm test)");
+  // Each timed iteration starts with L2 flushed (a 512 MB read between
+  // iterations, outside the event pair): weights stream from HBM as they do
+  // inside a decode step, where 6.6 GB of weights pass through a 126 MB L2.
+  void* flush = nullptr;
+  uint32_t* sink = nullptr;
+  const size_t flush_bytes = 512ull << 20;
+  CK(cudaMalloc(&flush, flush_bytes));
+  CK(cudaMemset(flush, 0, flush_bytes));
+  CK(cudaMalloc(&sink, 148 * 8 * 4));
+  // VOX_GEMM_PACKED_TEST=1: stream W from the packed tile layout (the decode path)
+  bf16* wpk = nullptr;
+  if (getenv("VOX_GEMM_PACKED_TEST") && atoi(getenv("VOX_GEMM_PACKED_TEST")) == 1) {
+    CK(dalloc(&wpk, static_cast<size_t>(packed_elems(M, K))));
+    launch_pack_bf16(dw, wpk, M, K, c->s_lm);
+    CK(cudaStreamSynchronize(c->s_lm));
+  }
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   int rc = VOX_OK;
+  double total_ms = 0.0;
   for (int it = 0; it < iters && rc == VOX_OK; ++it) {
-    if (it == (iters > 1 ? 1 : 0)) CK(cudaEventRecord(a, c->s_lm));
+    launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
+    CK(cudaEventRecord(a, c->s_lm));
     rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm);
+                  c->s_lm, "gemm", wpk);
+    CK(cudaEventRecord(b, c->s_lm));
+    CK(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    if (it > 0 || iters == 1) total_ms += ms;
   }
-  CK(cudaEventRecord(b, c->s_lm));
-  CK(cudaEventSynchronize(b));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, a, b));
-  if (mean_ms) *mean_ms = ms / (iters > 1 ? iters - 1 : 1);
+  if (mean_ms) *mean_ms = total_ms / (iters > 1 ? iters - 1 : 1);
+  cudaFree(flush);
+  cudaFree(sink);
+  if (wpk) cudaFree(wpk);
   if (rc == VOX_OK) {
     std::vector<float> tmp(static_cast<size_t>(splits) * N * M);
     CK(cudaMemcpy(tmp.data(), dout, tmp.size() * 4, cudaMemcpyDeviceToHost));
@@ -1524,9 +1570,22 @@ int vox_read_weight(VoxCtx* c, const char* name, int32_t layer, void* out, size_
   if (n == "emb") {
     src = c->emb;
     avail = static_cast<size_t>(g.vocab) * d * 2;
-  } else if (n == "qkv") {
-    src = c->w_qkv + layer * n_qkv;
-    avail = n_qkv * 2;
+  } else if (n == "qkv") {  // stored packed (init.cu): unpack to the logical [nqkv, d]
+    if (layer < 0 || layer >= g.n_layers) return fail(c, VOX_ERR_INVALID, "bad layer");
+    const int64_t np = packed_elems(c->nqkv, d);
+    std::vector<uint16_t> pk(static_cast<size_t>(np));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(pk.data(), c->w_qkv + layer * np, np * 2, cudaMemcpyDeviceToHost));
+    const size_t want = std::min(bytes, static_cast<size_t>(n_qkv) * 2) / 2;
+    uint16_t* o = static_cast<uint16_t*>(out);
+    const int n_kb = d / 64;
+    for (size_t i = 0; i < want; ++i) {
+      const int64_t m = static_cast<int64_t>(i) / d, k = static_cast<int64_t>(i) % d;
+      const int64_t t = (m / 128) * n_kb + k / 64;
+      const int r = static_cast<int>(m % 128), ch = static_cast<int>((k % 64) / 8) ^ (r & 7);
+      o[i] = pk[static_cast<size_t>(t * 8192 + r * 64 + ch * 8 + k % 8)];
+    }
+    return VOX_OK;
   } else if (n == "norm_attn") {
     src = c->norm_attn + static_cast<int64_t>(layer) * d;
     avail = d * 4;

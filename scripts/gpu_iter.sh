@@ -1,0 +1,6 @@
+set -x
+python -c "from paper_2602_00269_b200.build import build; build()"
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --no-slo --no-cpu > gpurun_out/bench_prof.json 2> gpurun_out/bench_prof.err
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py --batch 224 --ctx 394 --steps 2 > gpurun_out/launch_run.log 2>&1
+python scripts/launch_summary.py gpurun_out/launches.csv 30 > gpurun_out/launches_summary.txt

@@ -1,9 +1,14 @@
 """Profiling driver: eager Orpheus-3B-style decode steps at batch B, context ctx.
 
-Used under ncu (one GPU):  ncu ... python scripts/profile_step.py --batch 256 --ctx 394
+Used under ncu (one GPU), with the profiled region bracketed by
+cudaProfilerStart/Stop so the KV-fill prefill passes are not captured:
+
+  ncu --profile-from-start off --metrics gpu__time_duration.sum ... \
+      python scripts/profile_step.py --batch 224 --ctx 394
+
 The KV cache is filled by prefill forwards first; then --steps eager decode
-steps (no CUDA graph, so every kernel is a separate launch) and one detok
-call per 8 streams (steady-state chunk rate) run back to back.
+steps (no CUDA graph, so every kernel is a separate launch) and, with
+--detok N, one steady-state detok call over N streams run inside the range.
 """
 
 import argparse
@@ -22,11 +27,14 @@ from paper_2602_00269_b200.device import Sampling, VoxDevice  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=224)
     ap.add_argument("--ctx", type=int, default=394)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--detok", type=int, default=32)
+    ap.add_argument("--graph", action="store_true", help="graph-captured decode steps")
     a = ap.parse_args()
+    import torch
+
     dev = VoxDevice(orpheus3b(max_slots=max(a.batch, 8)), 0)
     prm = Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3)
     P = 50
@@ -35,23 +43,23 @@ def main():
     for i in range(0, a.batch, per):
         rows = np.array([[s, p, -1, 0] for s in slots[i:i + per] for p in range(a.ctx - 1)], np.int32)
         dev.forward(rows, sample=False)
-    dev.synchronize()
-    print("kv filled", flush=True)
-    for step in range(a.steps):
-        rows = np.array([[s, a.ctx - 1 + step, -1, 1] for s in slots], np.int32)
-        dev.forward(rows, graph=False)
-    dev.synchronize()
-    # detok: first windows need >= 28 generated tokens; generate into a few slots
+    # tokens for a detok window (first chunk: 28 generated tokens) in the first k slots
     k = min(a.detok, a.batch)
-    for step in range(a.steps, 28):
+    for step in range(28 if k > 0 else 0):
         rows = np.array([[s, a.ctx - 1 + step, -1, 1] for s in slots[:k]], np.int32)
         dev.forward(rows)
+    rows = np.array([[s, a.ctx - 1 + 28, -1, 1] for s in slots], np.int32)
+    dev.forward(rows, graph=a.graph)  # warm
     dev.synchronize()
-    # (the windows index generated tokens; decode rows started at ctx-1, so
-    #  generated index g lives at position P + g: make the store consistent)
-    w = np.array([[s, 1, 0, 28, 28, 0] for s in slots[:k]], np.int32)
-    dev.detok(w)
+    print("kv filled", flush=True)
+    torch.cuda.profiler.start()
+    for step in range(a.steps):
+        rows = np.array([[s, a.ctx - 1 + 28 + step, -1, 1] for s in slots], np.int32)
+        dev.forward(rows, graph=a.graph)
+    if k > 0:
+        dev.detok(np.array([[s, 1, 0, 28, 28, 0] for s in slots[:k]], np.int32))
     dev.synchronize()
+    torch.cuda.profiler.stop()
     print("done", flush=True)
 
 

@@ -17,7 +17,10 @@ def _bits(a):
     (512, 64, 768, 3), (200, 100, 1024, 1), (1024, 128, 2048, 8), (64, 300, 64, 1),
     (4096, 257, 2048, 1), (128, 1024, 256, 1), (156940 // 10, 7, 256, 1),
 ])
-def test_gemm_matches_numpy(tiny_dev, M, N, K, splits):
+@pytest.mark.parametrize("packed", [0, 1])
+def test_gemm_matches_numpy(tiny_dev, monkeypatch, M, N, K, splits, packed):
+    # packed=1 streams W from the packed 16 KB tile layout (init.cu), the decode path
+    monkeypatch.setenv("VOX_GEMM_PACKED_TEST", str(packed))
     rng = np.random.default_rng(M * 7 + N)
     w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
     x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
