@@ -33,7 +33,7 @@ namespace vox {
 
 constexpr int kAttnStages = 3;
 constexpr int kAttnPagesPerStage = 4;  // one page per warp
-constexpr int kAttnPtSmem = 512;       // page ids staged in smem (8192 tokens at ps 16)
+constexpr int kAttnQSlot = 1024;       // per-stage q slot (G * hd * 2 <= 1 KB)
 
 template <int HD>
 __host__ __device__ constexpr int attn_stage_bytes(int ps) {
@@ -53,51 +53,63 @@ VOX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Work item = (row, kv head, kv split), item = ((row * n_kv) + kvh) * n_split + z.
+// Persistent CTAs (2 per SM), warp-specialised: warps 0-3 consume one K/V
+// head-page each per stage; warp 4 is the producer.  The producer pulls items
+// from a device counter ONE ITEM AHEAD (counter, row descriptor and the item's
+// page ids, loaded lane-parallel into shared memory, are ready before they are
+// needed) and walks a flat sequence of stages across items, so the ring keeps
+// streaming through item boundaries.  Everything the consumers need about an
+// item travels in the stage descriptor (no global loads on their side).
+struct StageMeta {
+  int item;  // -1: no more work
+  int rr;    // round within the item
+  int np;    // pages in this stage (0: empty split)
+  int last;  // last round of the item
+  int row, kvh, z;
+  int L;      // context length (pos + 1)
+  int begin;  // first page of this item's split
+  int pad_[3];
+};
+
+struct AttnItem {
+  int item, row, kvh, z, slot, L, begin, end, nr, rr;
+};
+
+VOX_DEV void attn_item_decode(int item, int n_kv, int n_split, int& r, int& kvh, int& z) {
+  z = item % n_split;
+  const int t = item / n_split;
+  kvh = t % n_kv;
+  r = t / n_kv;
+}
+
+VOX_DEV void named_bar_consumers() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+constexpr int kAttnThreads = 160;
+constexpr int kAttnItemPages = 64;  // page ids staged per item (1024 tokens at ps 16)
+
 template <int HD, int G>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(kAttnThreads, 2)
     attn_decode_kernel(const RowDev* __restrict__ rows, const bf16* __restrict__ q,
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
-                       float* __restrict__ ws, int n_split) {
+                       float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched) {
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
   constexpr int NT = HD / 8;   // PV n-tiles
+  constexpr int kP = kAttnPagesPerStage;
+  constexpr int kQBytes = G * HD * 2;
   extern __shared__ __align__(128) uint8_t stage_raw[];
   __shared__ uint64_t full[kAttnStages], empty[kAttnStages];
-  __shared__ float s_m[4][8], s_l[4][8];
-  // the 4 warps' partial outputs are merged through the (then idle) K/V ring
-  float (*s_acc)[8][HD] = reinterpret_cast<float (*)[8][HD]>(stage_raw);
+  __shared__ __align__(16) StageMeta meta[kAttnStages];
+  __shared__ float s_m[4][G], s_l[4][G];
+  __shared__ __align__(16) float s_acc[4][G][HD];
+  __shared__ int s_pt[2][kAttnItemPages];
 
-  // rows / page table are uploaded before the step's first kernel and K/V of
-  // positions < pos were appended by earlier steps: none of it depends on the
-  // preceding kernel, so the prologue and the first K/V copies overlap its
-  // tail (PDL); only q and the page holding `pos` wait for griddep_wait.
-  const int r = blockIdx.x, kvh = blockIdx.y, z = blockIdx.z;
-  const RowDev rw = rows[r];
-  if (rw.slot < 0) {
-    griddep_wait();
-    griddep_launch();
-    return;
-  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int gn = lane >> 2, j = lane & 3;  // mma row/col group, k-slot group
   const int ps = dm.page_size;
-  const int L = rw.pos + 1;
-  const int n_pages = (L + ps - 1) / ps;
-  const int pps = (n_pages + n_split - 1) / n_split;
-  const int p_begin = z * pps;
-  const int p_end = min(n_pages, p_begin + pps);
-  const int n_rounds = p_end > p_begin ? (p_end - p_begin + kAttnPagesPerStage - 1) / kAttnPagesPerStage : 0;
   const int page_elems = ps * HD;
   const int stage_bytes = attn_stage_bytes<HD>(ps);
-  const int* pt_g = page_table + static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot;
-  // this split's page ids, staged once (a dependent global load per bulk copy
-  // would serialise the issue loop on load latency)
-  __shared__ int s_pt[kAttnPtSmem];
-  const bool pt_in_smem = (p_end - p_begin) <= kAttnPtSmem;
-  if (pt_in_smem)
-    for (int i = tid; i < p_end - p_begin; i += 128) s_pt[i] = pt_g[p_begin + i];
-  auto page_id = [&](int pg) { return pt_in_smem ? s_pt[pg - p_begin] : pt_g[pg]; };
 
   if (tid == 0) {
     for (int s = 0; s < kAttnStages; ++s) {
@@ -107,163 +119,262 @@ __global__ void __launch_bounds__(128)
     fence_mbar_init();
   }
   __syncthreads();
-  auto stage_ptr = [&](int s, int jp, int kv) -> const bf16* {
-    return reinterpret_cast<const bf16*>(stage_raw + static_cast<size_t>(s) * stage_bytes) +
+  auto stage_ptr = [&](int s, int jp, int kv) -> bf16* {
+    return reinterpret_cast<bf16*>(stage_raw + static_cast<size_t>(s) * stage_bytes) +
            (jp * 2 + kv) * page_elems;
   };
-  uint64_t pol = 0;
-  auto issue = [&](int rr) {
-    const int s = rr % kAttnStages;
-    const int pa = p_begin + rr * kAttnPagesPerStage;
-    const int np = min(kAttnPagesPerStage, p_end - pa);
-    mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(np * 2 * page_elems * 2));
-    for (int jp = 0; jp < np; ++jp) {
-      const int64_t base = (static_cast<int64_t>(page_id(pa + jp)) * dm.n_kv + kvh) * page_elems;
-      bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 0)), kc + base, page_elems * 2, &full[s], pol);
-      bulk_load(const_cast<bf16*>(stage_ptr(s, jp, 1)), vc + base, page_elems * 2, &full[s], pol);
-    }
+  auto q_slot = [&](int s) -> bf16* {
+    return reinterpret_cast<bf16*>(stage_raw + static_cast<size_t>(kAttnStages) * stage_bytes +
+                                   static_cast<size_t>(s) * kAttnQSlot);
   };
-  // stages whose pages all precede the first page this forward appends to
-  // (rw.fresh, written by the preceding kernel) are issued before the
-  // grid-dependency wait
-  const int last_page = rw.fresh / ps;
-  const int pre = min(kAttnStages, n_rounds);
-  int n_early = 0;
-  while (n_early < pre && p_begin + (n_early + 1) * kAttnPagesPerStage - 1 < last_page &&
-         p_begin + (n_early + 1) * kAttnPagesPerStage <= p_end)
-    ++n_early;
-  if (tid == 0) {
-    pol = policy_evict_first();  // K/V are read once per step
-    for (int rr = 0; rr < n_early; ++rr) issue(rr);
-  }
-  griddep_wait();
-  griddep_launch();
-  if (tid == 0)
-    for (int rr = n_early; rr < pre; ++rr) issue(rr);
 
-  // q A-fragments: head gn (< G), dims 32m + 8j .. +7 (zero rows beyond G)
-  uint4 qa[NB];
-#pragma unroll
-  for (int m = 0; m < NB; ++m) {
-    if (gn < G)
-      qa[m] = *reinterpret_cast<const uint4*>(
-          q + (static_cast<int64_t>(r) * dm.n_heads + kvh * G + gn) * HD + 32 * m + 8 * j);
-    else
-      qa[m] = make_uint4(0u, 0u, 0u, 0u);
-  }
-  const float qscale = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
-  float mrow = -INFINITY, lrow = 0.f;  // head gn, lane-partial l
-  float acc[NT][4];
-#pragma unroll
-  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
-
-  for (int rr = 0; rr < n_rounds; ++rr) {
-    const int s = rr % kAttnStages;
-    mbar_wait(&full[s], (rr / kAttnStages) & 1);
-    const int page_idx = p_begin + rr * kAttnPagesPerStage + warp;
-    if (page_idx < p_end) {
-      const bf16* kp = stage_ptr(s, warp, 0);
-      const bf16* vp = stage_ptr(s, warp, 1);
-      // ---- S = q K^T over the 16 tokens of this page (two n-tiles)
-      float sacc[2][4];
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
-        const int tok = 4 * (gn >> 1) + 2 * t + (gn & 1);
-        const bf16* krow = kp + tok * HD + 8 * j;
-        // Odd rows LOAD the 32-dim blocks in XOR-1 order so the two token rows
-        // of an 8-lane shared-memory phase hit disjoint banks; the mma then
-        // consumes block m on every lane (the k->dim map must be lane-uniform)
-        const int odd = gn & 1;
-        uint4 kb[NB];
-#pragma unroll
-        for (int i = 0; i < NB; ++i) kb[i] = *reinterpret_cast<const uint4*>(krow + 32 * (i ^ odd));
-#pragma unroll
-        for (int m = 0; m < NB; ++m) {
-          const uint4 ku = odd ? kb[m ^ 1] : kb[m];
-          mma_bf16_16816(sacc[t], qa[m].x, qa[m].y, ku.x, ku.y);
-          mma_bf16_16816(sacc[t], qa[m].z, qa[m].w, ku.z, ku.w);
+  if (warp == 4) {
+    // ====================== producer warp ======================
+    // The counter is zeroed by the last CTA of the previous launch; every kernel
+    // between two attention launches does griddep_wait before griddep_launch,
+    // so the previous attention grid has completed when this one starts.
+    const uint64_t pol = policy_evict_first();  // K/V are read once per step
+    auto fetch = [&](AttnItem& it, int buf) {
+      int v[9] = {-1, 0, 0, 0, 0, 0, 0, 0, 0};
+      if (lane == 0) {
+        for (;;) {
+          const int idx = atomicAdd(&sched[0], 1);
+          if (idx >= n_items) break;
+          int r, kvh, z;
+          attn_item_decode(idx, dm.n_kv, n_split, r, kvh, z);
+          const RowDev rw = rows[r];
+          if (rw.slot < 0) continue;  // bucket padding
+          const int n_pages = (rw.pos + 1 + ps - 1) / ps;
+          const int pps = (n_pages + n_split - 1) / n_split;
+          const int b = min(n_pages, z * pps);
+          const int e = min(n_pages, b + pps);
+          v[0] = idx; v[1] = r; v[2] = kvh; v[3] = z; v[4] = rw.slot; v[5] = rw.pos + 1;
+          v[6] = b; v[7] = e; v[8] = max(1, (e - b + kP - 1) / kP);
+          break;
         }
       }
-      // lane j owns tokens 4j..4j+3 of row gn: (sacc[0][0], sacc[0][1], sacc[1][0], sacc[1][1])
-      const int tok0 = page_idx * ps + 4 * j;
-      float sv[4] = {sacc[0][0] * qscale, sacc[0][1] * qscale, sacc[1][0] * qscale,
-                     sacc[1][1] * qscale};
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (tok0 + e >= L) sv[e] = -INFINITY;
-      float cm = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-      cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-      const float nm = fmaxf(mrow, cm);  // finite: the page's first token is valid
-      const float corr = exp2f(mrow - nm);
-      float p[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) p[e] = exp2f(sv[e] - nm);
-      mrow = nm;
-      lrow = lrow * corr + (p[0] + p[1]) + (p[2] + p[3]);
-      // P as a bf16 hi + lo pair (~16-bit mantissa): two PV mmas keep the
-      // probabilities at near-fp32 accuracy (the oracle weights V in fp32)
-      const __nv_bfloat162 h01 = __floats2bfloat162_rn(p[0], p[1]);
-      const __nv_bfloat162 h23 = __floats2bfloat162_rn(p[2], p[3]);
-      const uint32_t pa0 = *reinterpret_cast<const uint32_t*>(&h01);
-      const uint32_t pa2 = *reinterpret_cast<const uint32_t*>(&h23);
-      const uint32_t pl0 = pack_bf16x2(p[0] - __low2float(h01), p[1] - __high2float(h01));
-      const uint32_t pl2 = pack_bf16x2(p[2] - __low2float(h23), p[3] - __high2float(h23));
-      // ---- O += P V  (B = V^T rows: dim 8t + gn, tokens 4j..4j+3)
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        acc[t][0] *= corr;
-        acc[t][1] *= corr;
-        const uint2 vu = *reinterpret_cast<const uint2*>(vp + (8 * t + gn) * ps + 4 * j);
-        mma_bf16_16816(acc[t], pa0, pa2, vu.x, vu.y);
-        mma_bf16_16816(acc[t], pl0, pl2, vu.x, vu.y);
+      for (int k = 0; k < 9; ++k) v[k] = __shfl_sync(0xffffffffu, v[k], 0);
+      it = AttnItem{v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], 0};
+      if (it.item >= 0) {
+        const int* pt = page_table + static_cast<int64_t>(it.slot) * dm.max_pages_per_slot + it.begin;
+        const int n = min(it.end - it.begin, kAttnItemPages);
+        for (int i = lane; i < n; i += 32) s_pt[buf][i] = pt[i];
+      }
+      __syncwarp();
+    };
+    AttnItem cur, nxt;
+    int buf = 0;
+    fetch(cur, 0);
+    fetch(nxt, 1);
+    // issue the next stage of `cur` into slot s (q optionally deferred)
+    auto issue = [&](int s, bool with_q) {
+      if (cur.item < 0) {
+        if (lane == 0) {
+          meta[s] = StageMeta{-1, 0, 0, 0, 0, 0, 0, 0, 0, {0, 0, 0}};
+          mbar_arrive(&full[s]);  // terminator: completes the phase without data
+        }
+        return;
+      }
+      const int pa = cur.begin + cur.rr * kP;
+      const int np = max(0, min(kP, cur.end - pa));
+      if (lane == 0) {
+        meta[s] = StageMeta{cur.item, cur.rr, np, cur.rr == cur.nr - 1, cur.row, cur.kvh, cur.z,
+                            cur.L, cur.begin, {0, 0, 0}};
+        const uint32_t q_bytes = cur.rr == 0 ? kQBytes : 0u;
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(np * 2 * page_elems * 2) + q_bytes);
+      }
+      __syncwarp();
+      // lanes 0..np-1 copy K pages, lanes 4..4+np-1 the matching V pages, lane 8 q
+      if (lane < 2 * kP && (lane & (kP - 1)) < np) {
+        const int jp = lane & (kP - 1), kv = lane / kP;
+        const int off = pa - cur.begin + jp;
+        const int pid = off < kAttnItemPages
+                            ? s_pt[buf][off]
+                            : page_table[static_cast<int64_t>(cur.slot) * dm.max_pages_per_slot + pa + jp];
+        const int64_t base = (static_cast<int64_t>(pid) * dm.n_kv + cur.kvh) * page_elems;
+        bulk_load(stage_ptr(s, jp, kv), (kv ? vc : kc) + base, page_elems * 2, &full[s], pol);
+      } else if (lane == 2 * kP && cur.rr == 0 && with_q) {
+        bulk_load(q_slot(s), q + (static_cast<int64_t>(cur.row) * dm.n_heads + cur.kvh * G) * HD,
+                  kQBytes, &full[s], pol);
+      }
+      __syncwarp();
+      if (++cur.rr == cur.nr) {  // next item (prefetched); refill the look-ahead
+        cur = nxt;
+        buf ^= 1;
+        fetch(nxt, buf ^ 1);
+      }
+    };
+    // ---- prologue: stages of the first item whose pages all precede the first
+    // page this forward appends to (RowDev::fresh; written by the preceding
+    // kernel) go out before griddep_wait; q (written by it) after it.
+    int g = 0, deferred_q = -1;
+    if (cur.item >= 0) {
+      const int fresh_page = rows[cur.row].fresh / ps;
+      const int first = cur.item;
+      while (g < kAttnStages && cur.item == first) {
+        const int pa = cur.begin + cur.rr * kP;
+        const int np = max(0, min(kP, cur.end - pa));
+        if (np == 0 || pa + np > fresh_page) break;
+        if (cur.rr == 0) deferred_q = g;
+        issue(g++, false);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (tid == 0 && rr + kAttnStages < n_rounds) {
-      mbar_wait(&empty[s], (rr / kAttnStages) & 1);  // all 4 warps released this stage
-      issue(rr + kAttnStages);
+    griddep_wait();
+    griddep_launch();
+    if (deferred_q >= 0 && lane == 0) {
+      const StageMeta m = meta[deferred_q];
+      bulk_load(q_slot(deferred_q), q + (static_cast<int64_t>(m.row) * dm.n_heads + m.kvh * G) * HD,
+                kQBytes, &full[deferred_q], pol);
+    }
+    for (;; ++g) {
+      const int s = g % kAttnStages;
+      if (g >= kAttnStages) mbar_wait(&empty[s], ((g / kAttnStages) - 1) & 1);
+      const bool done = cur.item < 0;
+      issue(s, true);
+      if (done) break;
+    }
+  } else {
+    // ====================== consumer warps 0-3 ======================
+    griddep_wait();
+    griddep_launch();
+    const int gn = lane >> 2, j = lane & 3;  // mma row/col group, k-slot group
+    const float qscale = 1.4426950408889634f / sqrtf(static_cast<float>(HD));
+    uint4 qa[NB];
+    float mrow = -INFINITY, lrow = 0.f;  // head gn, lane-partial l
+    float acc[NT][4];
+    for (int g = 0;; ++g) {
+      const int s = g % kAttnStages;
+      mbar_wait(&full[s], (g / kAttnStages) & 1);
+      const StageMeta m = meta[s];
+      if (m.item < 0) break;
+      if (m.rr == 0) {  // new item: q from the stage, reset the online softmax
+        const bf16* qs = q_slot(s);
+#pragma unroll
+        for (int mb = 0; mb < NB; ++mb)
+          qa[mb] = gn < G ? *reinterpret_cast<const uint4*>(qs + gn * HD + 32 * mb + 8 * j)
+                          : make_uint4(0u, 0u, 0u, 0u);
+        mrow = -INFINITY;
+        lrow = 0.f;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+      }
+      if (warp < m.np) {
+        const int page_idx = m.begin + m.rr * kP + warp;
+        const bf16* kp = stage_ptr(s, warp, 0);
+        const bf16* vp = stage_ptr(s, warp, 1);
+        // ---- S = q K^T over the 16 tokens of this page (two n-tiles)
+        float sacc[2][4];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          sacc[t][0] = sacc[t][1] = sacc[t][2] = sacc[t][3] = 0.f;
+          const int tok = 4 * (gn >> 1) + 2 * t + (gn & 1);
+          const bf16* krow = kp + tok * HD + 8 * j;
+          // Odd rows LOAD the 32-dim blocks in XOR-1 order so the two token rows
+          // of an 8-lane shared-memory phase hit disjoint banks; the mma then
+          // consumes block m on every lane (the k->dim map must be lane-uniform)
+          const int odd = gn & 1;
+          uint4 kb[NB];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) kb[i] = *reinterpret_cast<const uint4*>(krow + 32 * (i ^ odd));
+#pragma unroll
+          for (int mb = 0; mb < NB; ++mb) {
+            const uint4 ku = odd ? kb[mb ^ 1] : kb[mb];
+            mma_bf16_16816(sacc[t], qa[mb].x, qa[mb].y, ku.x, ku.y);
+            mma_bf16_16816(sacc[t], qa[mb].z, qa[mb].w, ku.z, ku.w);
+          }
+        }
+        // lane j owns tokens 4j..4j+3 of row gn: (sacc[0][0], sacc[0][1], sacc[1][0], sacc[1][1])
+        const int tok0 = page_idx * ps + 4 * j;
+        float sv[4] = {sacc[0][0] * qscale, sacc[0][1] * qscale, sacc[1][0] * qscale,
+                       sacc[1][1] * qscale};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (tok0 + e >= m.L) sv[e] = -INFINITY;
+        float cm = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+        const float nm = fmaxf(mrow, cm);  // finite: the page's first token is valid
+        const float corr = exp2f(mrow - nm);
+        float p[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p[e] = exp2f(sv[e] - nm);
+        mrow = nm;
+        lrow = lrow * corr + (p[0] + p[1]) + (p[2] + p[3]);
+        // P as a bf16 hi + lo pair (~16-bit mantissa): two PV mmas keep the
+        // probabilities at near-fp32 accuracy (the oracle weights V in fp32)
+        const __nv_bfloat162 h01 = __floats2bfloat162_rn(p[0], p[1]);
+        const __nv_bfloat162 h23 = __floats2bfloat162_rn(p[2], p[3]);
+        const uint32_t pa0 = *reinterpret_cast<const uint32_t*>(&h01);
+        const uint32_t pa2 = *reinterpret_cast<const uint32_t*>(&h23);
+        const uint32_t pl0 = pack_bf16x2(p[0] - __low2float(h01), p[1] - __high2float(h01));
+        const uint32_t pl2 = pack_bf16x2(p[2] - __low2float(h23), p[3] - __high2float(h23));
+        // ---- O += P V  (B = V^T rows: dim 8t + gn, tokens 4j..4j+3)
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          acc[t][0] *= corr;
+          acc[t][1] *= corr;
+          const uint2 vu = *reinterpret_cast<const uint2*>(vp + (8 * t + gn) * ps + 4 * j);
+          mma_bf16_16816(acc[t], pa0, pa2, vu.x, vu.y);
+          mma_bf16_16816(acc[t], pl0, pl2, vu.x, vu.y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (m.last) {
+        // ---------------- finalize the item: merge the 4 warps ----------------
+        float lr = lrow;
+        lr += __shfl_xor_sync(0xffffffffu, lr, 1);
+        lr += __shfl_xor_sync(0xffffffffu, lr, 2);
+        if (gn < G) {
+          if (j == 0) {
+            s_m[warp][gn] = mrow;
+            s_l[warp][gn] = lr;
+          }
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            s_acc[warp][gn][8 * t + 2 * j] = acc[t][0];
+            s_acc[warp][gn][8 * t + 2 * j + 1] = acc[t][1];
+          }
+        }
+        named_bar_consumers();
+        for (int idx = tid; idx < G * HD; idx += 128) {
+          const int gg = idx / HD, dd = idx % HD;
+          float M = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][gg]);
+          float Ls = 0.f, A = 0.f;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const float f = (s_m[w][gg] == -INFINITY) ? 0.f : exp2f(s_m[w][gg] - M);
+            Ls += s_l[w][gg] * f;
+            A += s_acc[w][gg][dd] * f;
+          }
+          if (n_split == 1) {
+            out[(static_cast<int64_t>(m.row) * dm.n_heads + m.kvh * G + gg) * HD + dd] =
+                __float2bfloat16_rn(A / Ls);
+          } else {
+            float* wp =
+                ws + ((static_cast<int64_t>(m.row) * dm.n_kv + m.kvh) * n_split + m.z) * G * (HD + 2);
+            wp[gg * (HD + 2) + dd] = A;
+            if (dd == 0) {
+              wp[gg * (HD + 2) + HD] = M;
+              wp[gg * (HD + 2) + HD + 1] = Ls;
+            }
+          }
+        }
+        named_bar_consumers();  // s_acc / s_m / s_l are reused by the next item
+      }
     }
   }
-  // row sums: reduce the 4 lane partials of each row
-  lrow += __shfl_xor_sync(0xffffffffu, lrow, 1);
-  lrow += __shfl_xor_sync(0xffffffffu, lrow, 2);
-  // ------------------------------------------------ merge the 4 warps
-  __syncthreads();  // every warp is done reading the ring before it is reused
-  if (j == 0) {
-    s_m[warp][gn] = mrow;
-    s_l[warp][gn] = lrow;
-  }
-#pragma unroll
-  for (int t = 0; t < NT; ++t) {
-    s_acc[warp][gn][8 * t + 2 * j] = acc[t][0];
-    s_acc[warp][gn][8 * t + 2 * j + 1] = acc[t][1];
-  }
+  // self-resetting scheduler: the last CTA to finish zeroes the counters
   __syncthreads();
-  for (int idx = tid; idx < G * HD; idx += 128) {
-    const int g = idx / HD, dd = idx % HD;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][g]);
-    float Ls = 0.f, A = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float f = (s_m[w][g] == -INFINITY) ? 0.f : exp2f(s_m[w][g] - M);
-      Ls += s_l[w][g] * f;
-      A += s_acc[w][g][dd] * f;
-    }
-    if (n_split == 1) {
-      out[(static_cast<int64_t>(r) * dm.n_heads + kvh * G + g) * HD + dd] =
-          __float2bfloat16_rn(A / Ls);
-    } else {
-      float* wp = ws + ((static_cast<int64_t>(r) * dm.n_kv + kvh) * n_split + z) * G * (HD + 2);
-      wp[g * (HD + 2) + dd] = A;
-      if (dd == 0) {
-        wp[g * (HD + 2) + HD] = M;
-        wp[g * (HD + 2) + HD + 1] = Ls;
-      }
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&sched[1], 1) == static_cast<int>(gridDim.x) - 1) {
+      sched[0] = 0;
+      sched[1] = 0;
+      __threadfence();
     }
   }
 }
@@ -295,16 +406,19 @@ __global__ void __launch_bounds__(128)
 template <int HD, int G>
 static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* pt, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        cudaStream_t st) {
-  const int smem = kAttnStages * attn_stage_bytes<HD>(dm.page_size);  // 96 KB at ps 16, hd 128
+                        int* sched, cudaStream_t st) {
+  // K/V ring + one q slot per stage (96 KB + 3 KB at ps 16, hd 128): 2 CTAs per SM
+  const int smem = kAttnStages * (attn_stage_bytes<HD>(dm.page_size) + kAttnQSlot);
   static int attr_bytes = 0;
   if (smem > attr_bytes) {
     cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
     attr_bytes = smem;
   }
-  launch_k(attn_decode_kernel<HD, G>, dim3(n, dm.n_kv, n_split), dim3(128), smem, st, rows, q, kc,
-           vc, pt, dm, out, ws, n_split);
+  const int n_items = n * dm.n_kv * n_split;
+  const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
+  launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), smem, st, rows, q, kc, vc, pt, dm,
+           out, ws, n_split, n_items, sched);
   if (n_split > 1)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
              out);
@@ -313,12 +427,12 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
 template <int HD>
 static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16* kc,
                             const bf16* vc, const int* pt, const LmDims& dm, bf16* out, float* ws,
-                            int n_split, cudaStream_t st) {
+                            int n_split, int* sched, cudaStream_t st) {
   switch (dm.n_heads / dm.n_kv) {
-    case 1: attn_launch<HD, 1>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, st); break;
-    case 2: attn_launch<HD, 2>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, st); break;
-    case 3: attn_launch<HD, 3>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, st); break;
-    case 4: attn_launch<HD, 4>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, st); break;
+    case 1: attn_launch<HD, 1>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 2: attn_launch<HD, 2>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 3: attn_launch<HD, 3>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 4: attn_launch<HD, 4>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
     default: break;  // rejected at vox_create
   }
 }
@@ -334,11 +448,11 @@ int attn_pick_splits(int n_rows, int n_kv) {
 
 void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* page_table, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        cudaStream_t st) {
+                        int* sched, cudaStream_t st) {
   if (dm.hd == 64)
-    attn_dispatch_g<64>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, st);
+    attn_dispatch_g<64>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st);
   else
-    attn_dispatch_g<128>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, st);
+    attn_dispatch_g<128>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st);
 }
 
 }  // namespace vox

@@ -96,9 +96,10 @@ constexpr int kAttnMaxSplits = 8;    // split-KV factor cap
 constexpr int kAttnSplitRows = 128;  // split-KV only for batches up to this many rows
 int attn_pick_splits(int n_rows, int n_kv);
 // ws: split-KV partials [rows][kv][n_split][G][hd + 2] (unused when n_split == 1)
+// sched: 2 zeroed ints (work counter, done counter), self-resetting per launch
 void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* page_table, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        cudaStream_t st);
+                        int* sched, cudaStream_t st);
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st);

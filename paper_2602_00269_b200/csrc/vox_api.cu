@@ -151,6 +151,7 @@ struct VoxCtx {
 
   // ---- per-step staging
   RowDev* d_rows = nullptr;
+  int* attn_sched = nullptr;  // persistent attention work counters (self-resetting)
   int* d_sample_rows = nullptr;
   int* d_out_index = nullptr;
   int* d_tokens = nullptr;
@@ -433,6 +434,8 @@ static int create_buffers(VoxCtx* c) {
   c->h_seed.assign(g.max_slots, 0);
 
   CK(dalloc(&c->d_rows, static_cast<size_t>(R)));
+  CK(dalloc(&c->attn_sched, 2));
+  CK(cudaMemset(c->attn_sched, 0, 2 * sizeof(int)));
   CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
   CK(dalloc(&c->d_out_index, static_cast<size_t>(R)));
   CK(dalloc(&c->d_tokens, static_cast<size_t>(R)));
@@ -634,7 +637,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
       const int asp = attn_pick_splits(nrows, g.n_kv_heads);
       TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
-                         c->page_table, dm, c->attn, c->attn_ws, asp, st);
+                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st, "gemm", c->w_o + l * n_o));
@@ -797,7 +800,7 @@ void vox_destroy(VoxCtx* c) {
   void* dev_ptrs[] = {c->emb, c->norm_attn, c->norm_mlp, c->norm_final, c->w_qkv, c->w_o,
                       c->w_gu, c->w_down, c->w_head_audio, c->inv_freq, c->rope_tab, c->h, c->x, c->xf, c->q, c->attn, c->act,
                       c->ws, c->attn_ws, c->logits, c->kc, c->vc, c->token_store, c->page_table,
-                      c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->d_sample_rows,
+                      c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->attn_sched, c->d_sample_rows,
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w};
