@@ -38,7 +38,7 @@ __global__ void init_f32_kernel(float* __restrict__ w, int64_t n, uint64_t key, 
 __global__ void init_bf16_packed_kernel(bf16* __restrict__ w, int64_t M, int64_t K,
                                         int64_t row0, uint64_t key, float scale) {
   const int64_t n_kb = K / 64;
-  const int64_t total = (M + 127) / 128 * 128 * K;
+  const int64_t total = (M + 255) / 256 * 256 * K;  // = packed_elems(M, K)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < total;
        j += stride) {
@@ -63,7 +63,7 @@ void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64
 __global__ void pack_bf16_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, int64_t M,
                                  int64_t K) {
   const int64_t n_kb = K / 64;
-  const int64_t total = (M + 127) / 128 * 128 * K;
+  const int64_t total = (M + 255) / 256 * 256 * K;  // = packed_elems(M, K)
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < total;
        j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = j >> 13, within = j & 8191;

@@ -42,6 +42,8 @@ struct GemmArgs {
   const float* resid;     // [N, ldr] or null (only with 1 split)
   int64_t ldr;
   int m_valid;            // columns m >= m_valid are not stored
+  int k_rotate;           // rotate each CTA's k-block order by its weight tile
+  int probe;              // microbenchmarks only: 1 = MMA-only, 2 = loads-only
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };
@@ -51,6 +53,7 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 int gemm_bn_for_rows(int rows);
 constexpr int kGemmMaxSplits = 16;
 struct GemmPlan {
+  int pair;    // 1: CTA-pair kernel (cta_group::2, 256 weight rows x bn rows per 2 CTAs)
   int bn;      // activation rows per tile (UMMA N)
   int mt;      // 128-row weight sub-tiles per CTA (1 or 2)
   int splits;  // split-K factor (fp32 partial planes)
@@ -58,6 +61,10 @@ struct GemmPlan {
 GemmPlan gemm_plan(int M, int rows, int K);
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, int mt, cudaStream_t st);
+// pair kernel: tw_packed from make_tmap_packed, tx_half = activation map with box bnp / 2
+cudaError_t gemm_launch_pair(const CUtensorMap& tw_packed, const CUtensorMap& tx_half, GemmArgs a,
+                             int splits, int bnp, cudaStream_t st);
+bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K);
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).
@@ -66,7 +73,8 @@ void launch_init_bf16(bf16* w, int64_t n, uint64_t key, float scale, cudaStream_
 void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t key,
                              float scale, cudaStream_t st);
 void launch_pack_bf16(const bf16* src, bf16* dst, int64_t M, int64_t K, cudaStream_t st);
-inline int64_t packed_elems(int64_t M, int64_t K) { return (M + 127) / 128 * 128 * K; }
+// rows padded to 256 so CTA pairs (256 weight rows) never read past the buffer
+inline int64_t packed_elems(int64_t M, int64_t K) { return (M + 255) / 256 * 256 * K; }
 void launch_l2_flush(const void* buf, size_t bytes, uint32_t* sink, cudaStream_t st);
 // fp32 variant: w[i] = offset + unit_pm1(mix64(key+i)) * scale rounded through bf16.
 void launch_init_f32(float* w, int64_t n, uint64_t key, float scale, float offset,

@@ -123,6 +123,9 @@ struct VoxCtx {
   float* inv_freq = nullptr;
   float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
   bf16* w_head_audio = nullptr;  // packed copy of the tied head's audio rows
+  // 2-D tensor maps over the packed tiles (CTA-pair GEMM)
+  std::vector<CUtensorMap> tp_qkv, tp_o, tp_gu, tp_down;
+  CUtensorMap tp_head{};
   CUtensorMap tm_head_full{};
   int head_audio_rows = 0;
 
@@ -188,6 +191,8 @@ struct VoxCtx {
 
   int detok_stop = 1 << 30;  // debug: stop the detok pipeline after this many stages
   bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
+  int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
+  int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
 
   // ---- timing / counting
@@ -259,12 +264,18 @@ static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* 
 }
 
 // GEMM over `rows` activation rows of buffer map set `xm`.
-// `wp` non-null: W is in the packed tile layout (init.cu) and `tw` is unused.
+// `wp` non-null: W is in the packed tile layout (init.cu) and `tw` is unused;
+// `twp` is the 2-D tensor map over the packed tiles (CTA-pair kernel).
 static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>& xm, int M,
                     int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
-                    const char* cls = "gemm", const bf16* wp = nullptr) {
-  const GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
+                    const char* cls = "gemm", const bf16* wp = nullptr,
+                    const CUtensorMap* twp = nullptr) {
+  GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
+  if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
+    plan.pair = 0;
+    plan.bn = (rows >= 128 && M <= 4096) ? 64 : 128;
+  }
   const int bn = plan.bn;
   GemmArgs a{};
   a.M = M;
@@ -278,10 +289,13 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.ldr = ldr;
   a.m_valid = m_valid;
   a.w_packed = wp;
+  a.k_rotate = c->gemm_k_rotate;
+  a.probe = c->gemm_probe;
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
-  cudaError_t e = gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
+  cudaError_t e = plan.pair ? gemm_launch_pair(*twp, xm.at(bn / 2), a, splits, bn, st)
+                            : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
 }
@@ -365,6 +379,20 @@ static int create_backbone(VoxCtx* c) {
     CK(cudaMemcpy(c->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
 
+  c->tp_qkv.resize(L);
+  c->tp_o.resize(L);
+  c->tp_gu.resize(L);
+  c->tp_down.resize(L);
+  for (int l = 0; l < L; ++l) {
+    if (!make_tmap_packed(&c->tp_qkv[l], c->w_qkv + l * n_qkv, c->nqkv, d) ||
+        !make_tmap_packed(&c->tp_o[l], c->w_o + l * n_o, d, H * hd) ||
+        !make_tmap_packed(&c->tp_gu[l], c->w_gu + l * n_gu, 2 * dff, d) ||
+        !make_tmap_packed(&c->tp_down[l], c->w_down + l * n_dn, d, dff))
+      return fail(c, VOX_ERR_CUDA, "tensor map (packed weights)");
+  }
+  if (g.audio_base >= 0 &&
+      !make_tmap_packed(&c->tp_head, c->w_head_audio, g.frame_tokens * g.codebook_size, d))
+    return fail(c, VOX_ERR_CUDA, "tensor map (packed audio head)");
   if (!make_tmap_bf16(&c->tm_head_full, c->emb, d, V, d * 2ull, 128))
     return fail(c, VOX_ERR_CUDA, "tensor map (lm head)");
   if (g.audio_base >= 0) {
@@ -626,7 +654,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
   const CUtensorMap& tw_unused = c->tm_head_full;  // packed weights: the W map is not read
   for (int l = 0; l < L; ++l) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
-                 nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv));
+                 nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv, &c->tp_qkv[l]));
     {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * sp_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws, sp_qkv,
@@ -640,21 +668,21 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
                          c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
-                 st, "gemm", c->w_o + l * n_o));
+                 st, "gemm", c->w_o + l * n_o, &c->tp_o[l]));
     {
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_o + 10));
       launch_resid_norm(c->d_rows, nrows, c->ws, sp_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
-                 nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu));
+                 nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
     {
       TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
       launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
-                 d, st, "gemm", c->w_down + l * n_dn));
+                 d, st, "gemm", c->w_down + l * n_dn, &c->tp_down[l]));
     {
       const bool last = (l == L - 1);
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_dn + 10));
@@ -667,7 +695,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     const bool audio = (g.audio_base >= 0) && !full_logits;
     const int M = audio ? c->head_audio_rows : g.vocab;
     RET(run_gemm(c, c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits, M, 1, nullptr, nullptr, 0,
-                 M, st, "lm_head", audio ? c->w_head_audio : nullptr));
+                 M, st, "lm_head", audio ? c->w_head_audio : nullptr, audio ? &c->tp_head : nullptr));
     SampFusedArgs a{};
     a.rows = c->d_rows;
     a.sample_rows = c->d_sample_rows;
@@ -1519,10 +1547,12 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   CK(cudaMalloc(&sink, 148 * 8 * 4));
   // VOX_GEMM_PACKED_TEST=1: stream W from the packed tile layout (the decode path)
   bf16* wpk = nullptr;
+  CUtensorMap tpk{};
   if (getenv("VOX_GEMM_PACKED_TEST") && atoi(getenv("VOX_GEMM_PACKED_TEST")) == 1) {
     CK(dalloc(&wpk, static_cast<size_t>(packed_elems(M, K))));
     launch_pack_bf16(dw, wpk, M, K, c->s_lm);
     CK(cudaStreamSynchronize(c->s_lm));
+    if (!make_tmap_packed(&tpk, wpk, M, K)) return fail(c, VOX_ERR_CUDA, "tensor map (packed test)");
   }
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
@@ -1533,7 +1563,7 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
     CK(cudaEventRecord(a, c->s_lm));
     rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm, "gemm", wpk);
+                  c->s_lm, "gemm", wpk, wpk ? &tpk : nullptr);
     CK(cudaEventRecord(b, c->s_lm));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;
