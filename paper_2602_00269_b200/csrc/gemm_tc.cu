@@ -155,6 +155,45 @@ __global__ void __launch_bounds__(128, 1)
   griddep_wait();  // outputs may alias buffers the preceding kernel was reading
   mbar_wait(done, 0);
   tc_fence_after();
+  if (MT == 1 && p.epi == 1) {
+    // fused SiLU(gate) * up: TMEM lanes 0-63 hold gate, 64-127 up of features
+    // f = 64 * tile + (lane % 64); warps 2-3 hand `up` to warps 0-1 through
+    // shared memory (the pipeline stages are idle once `done` has fired)
+    float* stg = reinterpret_cast<float*>(smem);  // [64][BN + 1]
+    const int f0 = (m0 / 128) * 64;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
+      tmem_ld_wait();
+      if (warp >= 2) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stg[((warp - 2) * 32 + lane) * (BN + 1) + c + j] = __uint_as_float(r[j]);
+      }
+      __syncthreads();
+      if (warp < 2) {
+        const int f = f0 + warp * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int n = n0 + c + j;
+          if ((c + j) < BN && n < p.N) {
+            const float g = __uint_as_float(r[j]);
+            const float u = stg[(warp * 32 + lane) * (BN + 1) + c + j];
+            p.act[static_cast<int64_t>(n) * p.ld_act + f] =
+                __float2bfloat16_rn(__fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u));
+          }
+        }
+      }
+      __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+      tc_fence_after();
+      tmem_dealloc(tmem, C::kTmemCols);
+    }
+    return;
+  }
   float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
 #pragma unroll 1
   for (int mt = 0; mt < MT; ++mt) {

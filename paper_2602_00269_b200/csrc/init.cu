@@ -35,8 +35,17 @@ __global__ void init_f32_kernel(float* __restrict__ w, int64_t n, uint64_t key, 
 //   stored at chunk c ^ (r & 7)).  Rows beyond M (tile padding) are zero.
 // One k-block of one 128-row tile is then a single contiguous 16 KB bulk copy
 // (sequential DRAM bursts) instead of 128 strided 128-byte rows.
+// half > 0: gate|up interleave -- packed row r of tile t holds logical row
+// (r < 64 ? 64 t + r : half + 64 t + r - 64), so each 128-row tile carries the
+// gate and up rows of the same 64 features (fused SiLU(gate) * up epilogue).
+__device__ __forceinline__ int64_t packed_logical_row(int64_t m, int64_t half) {
+  if (half <= 0) return m;
+  const int64_t t = m >> 7, r = m & 127;
+  return r < 64 ? 64 * t + r : half + 64 * t + (r - 64);
+}
+
 __global__ void init_bf16_packed_kernel(bf16* __restrict__ w, int64_t M, int64_t K,
-                                        int64_t row0, uint64_t key, float scale) {
+                                        int64_t row0, uint64_t key, float scale, int64_t half) {
   const int64_t n_kb = K / 64;
   const int64_t total = (M + 255) / 256 * 256 * K;  // = packed_elems(M, K)
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -49,14 +58,17 @@ __global__ void init_bf16_packed_kernel(bf16* __restrict__ w, int64_t M, int64_t
     const int64_t m = (t / n_kb) * 128 + r;
     const int64_t k = (t % n_kb) * 64 + c * 8 + e;
     float v = 0.f;
-    if (m < M) v = __fmul_rn(unit_pm1(mix64(key + static_cast<uint64_t>((row0 + m) * K + k))), scale);
+    if (m < M) {
+      const int64_t ml = packed_logical_row(m, half);
+      v = __fmul_rn(unit_pm1(mix64(key + static_cast<uint64_t>((row0 + ml) * K + k))), scale);
+    }
     w[j] = __float2bfloat16_rn(v);
   }
 }
 
 void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t key,
-                             float scale, cudaStream_t st) {
-  init_bf16_packed_kernel<<<148 * 64, 256, 0, st>>>(w, M, K, row0, key, scale);
+                             float scale, cudaStream_t st, int64_t interleave_half) {
+  init_bf16_packed_kernel<<<148 * 64, 256, 0, st>>>(w, M, K, row0, key, scale, interleave_half);
 }
 
 // logical [M][K] -> packed tiles (same layout as init_bf16_packed_kernel)

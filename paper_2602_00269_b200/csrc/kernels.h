@@ -44,6 +44,11 @@ struct GemmArgs {
   int m_valid;            // columns m >= m_valid are not stored
   int k_rotate;           // rotate each CTA's k-block order by its weight tile
   int probe;              // microbenchmarks only: 1 = MMA-only, 2 = loads-only
+  // epi == 1 (gate|up GEMM, 1 split, interleaved weight tiles): instead of fp32
+  // out, write act[n][f] = bf16(SiLU(gate) * up) for the tile's 64 features
+  int epi;
+  bf16* act;
+  int64_t ld_act;
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };
@@ -71,7 +76,7 @@ bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K);
 void launch_init_bf16(bf16* w, int64_t n, uint64_t key, float scale, cudaStream_t st);
 // packed-tile variant (see init.cu); buffer holds roundup(M, 128) * K elements
 void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t key,
-                             float scale, cudaStream_t st);
+                             float scale, cudaStream_t st, int64_t interleave_half = 0);
 void launch_pack_bf16(const bf16* src, bf16* dst, int64_t M, int64_t K, cudaStream_t st);
 // rows padded to 256 so CTA pairs (256 weight rows) never read past the buffer
 inline int64_t packed_elems(int64_t M, int64_t K) { return (M + 255) / 256 * 256 * K; }

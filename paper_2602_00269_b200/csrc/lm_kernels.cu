@@ -243,10 +243,14 @@ __global__ void __launch_bounds__(256)
   const int64_t ss4 = split_stride / 4;
   const int f4 = dff / 4;
   bf16* ar = a_out + static_cast<int64_t>(r) * dff;
+  // gate|up columns are interleaved per 128 (the packed weight tiles): feature
+  // f's gate at column 128 (f / 64) + f % 64, its up 64 columns later
 #pragma unroll 4
   for (int j = threadIdx.x; j < f4; j += 256) {
-    const float4 g = sum_splits4(w4, splits, ss4, j);
-    const float4 u = sum_splits4(w4, splits, ss4, f4 + j);
+    const int f = 4 * j;
+    const int cg = ((f >> 6) << 7) + (f & 63);
+    const float4 g = sum_splits4(w4, splits, ss4, cg / 4);
+    const float4 u = sum_splits4(w4, splits, ss4, (cg + 64) / 4);
     store_bf16x4(ar + 4 * j, silu_mul1(g.x, u.x), silu_mul1(g.y, u.y), silu_mul1(g.z, u.z),
                  silu_mul1(g.w, u.w));
   }

@@ -193,6 +193,7 @@ struct VoxCtx {
   bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
+  bool silu_unfused = getenv("VOX_SILU_UNFUSED") != nullptr;  // A/B: separate SiLU kernel
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
 
   // ---- timing / counting
@@ -270,7 +271,8 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm", const bf16* wp = nullptr,
-                    const CUtensorMap* twp = nullptr) {
+                    const CUtensorMap* twp = nullptr, bf16* act_out = nullptr,
+                    int64_t ld_act = 0) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
   if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
     plan.pair = 0;
@@ -291,6 +293,11 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.w_packed = wp;
   a.k_rotate = c->gemm_k_rotate;
   a.probe = c->gemm_probe;
+  a.epi = act_out != nullptr ? 1 : 0;
+  a.act = act_out;
+  a.ld_act = ld_act;
+  if (a.epi == 1 && (splits != 1 || plan.pair || plan.mt != 1))
+    return fail(c, VOX_ERR_INVALID, "fused SiLU epilogue needs one split, 1-CTA tiles");
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
@@ -339,8 +346,9 @@ static int create_backbone(VoxCtx* c) {
   CK(dalloc(&c->w_down, static_cast<size_t>(L * n_dn)));
   RET(init_bf16(c, c->emb, static_cast<int64_t>(V) * d, T_EMB, 0, g.embed_scale));
   auto packed = [&](bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t tid, uint64_t layer,
-                    float scale) {
-    launch_init_bf16_packed(w, M, K, row0, tensor_key(c->seed, tid, layer), scale, c->s_lm);
+                    float scale, int64_t interleave_half = 0) {
+    launch_init_bf16_packed(w, M, K, row0, tensor_key(c->seed, tid, layer), scale, c->s_lm,
+                            interleave_half);
     return cudaGetLastError() == cudaSuccess ? VOX_OK : fail(c, VOX_ERR_CUDA, "init packed");
   };
   for (int l = 0; l < L; ++l) {
@@ -348,7 +356,8 @@ static int create_backbone(VoxCtx* c) {
     RET(init_f32(c, c->norm_mlp + static_cast<int64_t>(l) * d, d, T_NORM_MLP, l, 0.25f, 1.0f));
     RET(packed(c->w_qkv + l * n_qkv, c->nqkv, d, 0, T_QKV, l, std::sqrt(3.0f / d)));
     RET(packed(c->w_o + l * n_o, d, H * hd, 0, T_O, l, std::sqrt(3.0f / (H * hd))));
-    RET(packed(c->w_gu + l * n_gu, 2 * dff, d, 0, T_GU, l, std::sqrt(3.0f / d)));
+    // gate|up rows interleaved per 128-row tile (64 gate + the same 64 up rows)
+    RET(packed(c->w_gu + l * n_gu, 2 * dff, d, 0, T_GU, l, std::sqrt(3.0f / d), dff));
     RET(packed(c->w_down + l * n_dn, d, dff, 0, T_DOWN, l, std::sqrt(3.0f / dff)));
   }
   if (g.audio_base >= 0) {  // packed copy of the audio rows of the tied head
@@ -646,7 +655,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
   }
   const int sp_qkv = gemm_plan(c->nqkv, nrows, d).splits;
   const int sp_o = gemm_plan(d, nrows, Hhd).splits;
-  const int sp_gu = gemm_plan(2 * dff, nrows, d).splits;
+  const GemmPlan gu_plan = gemm_plan(2 * dff, nrows, d);
+  const int sp_gu = gu_plan.splits;
   const int sp_dn = gemm_plan(d, nrows, dff).splits;
   const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
   const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
@@ -674,9 +684,12 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
       launch_resid_norm(c->d_rows, nrows, c->ws, sp_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
-    RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
-                 nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
-    {
+    if (sp_gu == 1 && !gu_plan.pair && !c->silu_unfused) {  // SiLU(gate) * up in the epilogue
+      RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, 1, nullptr, nullptr,
+                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l], c->act, dff));
+    } else {
+      RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
+                   nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
       TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
       launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
