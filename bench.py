@@ -276,6 +276,51 @@ def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: flo
     return classes, step_ms, ctx
 
 
+def roofline_summary(cfg, classes, B: int, ctx: int, hbm: float, tfl: float, peak_kind: str):
+    """Roofline of the dominant kernel class (by device time per step).
+
+    achieved = algorithmic work per launch / mean launch time (CUDA events on the
+    launching stream, eager timing mode).  Work per unit:
+      gemm (K3, the 4 per-layer projections): FLOPs = 2 * params_layer * B rows;
+           bytes = weights + activations + fp32 outputs (the larger of the two
+           roofline times decides the bound: tensor at B >= ~214 rows)
+      attn (K2): bytes = sum over rows of (pos + 1) * n_kv * hd * 2 (K and V) * 2 B
+    traffic = dram read + write bytes per launch from the committed ncu --set full
+    capture (profiles/traffic_r01.json), or null."""
+    d, H, KV, hd, dff, L = cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.d_ff, cfg.n_layers
+    params_layer = (H + 2 * KV) * hd * d + d * H * hd + 2 * dff * d + d * dff
+    out = {}
+    for name, c in classes.items():
+        if c["launches"] <= 0 or c["ms"] <= 0:
+            continue
+        per_launch_s = c["ms"] / c["launches"] / 1e3
+        bytes_l = c["bytes"] / c["launches"]
+        e = {"ms_per_step": round(c["ms"], 4), "launches": c["launches"],
+             "hbm_gbs": round(bytes_l / per_launch_s / 1e9, 1)}
+        t_hbm = bytes_l / (hbm * 1e9)
+        t_tc = 0.0
+        if name == "gemm":
+            flops_l = 2.0 * params_layer * B / 4  # mean over the 4 projections of a layer
+            e["tflops"] = round(flops_l / per_launch_s / 1e12, 1)
+            t_tc = flops_l / (tfl * 1e12)
+        e["bound"] = "tensor" if t_tc > t_hbm else "hbm"
+        e["frac"] = round(max(t_hbm, t_tc) / per_launch_s, 4)
+        out[name] = e
+    top = max(out, key=lambda k: out[k]["ms_per_step"])
+    t = out[top]
+    traffic = None
+    prof_path = ROOT / "profiles" / "traffic_r01.json"
+    if prof_path.exists():
+        traffic = json.loads(prof_path.read_text()).get(top)
+    if t["bound"] == "tensor":
+        ach, peak, unit = t["tflops"], tfl, "TFLOP/s"
+    else:
+        ach, peak, unit = t["hbm_gbs"], hbm, "GB/s"
+    return {"bound": t["bound"], "kernel": top, "achieved": ach, "peak": peak, "unit": unit,
+            "frac": round(ach / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+            "classes": out, "ctx": ctx, "batch": B}
+
+
 def run_slo(dev, rates, seconds: float, seed: int, prompt: int, ws: int = 1, rank: int = 0):
     """Poisson load test (config 5): offered rate r is the WHOLE-JOB rate; requests are
     routed to the ws replicas with the reference router, metrics pooled at the end."""
@@ -320,7 +365,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=50)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--slo-seconds", type=float, default=12.0)
-    ap.add_argument("--slo-rates", default="32,40,48,56,64")
+    ap.add_argument("--slo-rates", default="48,64,72,80,88,96,112")
     ap.add_argument("--no-slo", action="store_true")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -381,18 +426,8 @@ def main():
     roof = None
     if not args.no_roofline and rank == 0:
         classes, step_ms, ctx = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77, hbm, tfl)
-        top = max(classes, key=lambda k: classes[k]["ms"])
-        c = classes[top]
-        per_launch_ms = c["ms"] / max(c["launches"], 1)
-        achieved = (c["bytes"] / max(c["launches"], 1)) / (per_launch_ms / 1000.0) / 1e9
-        prof_path = ROOT / "profiles" / "traffic_r01.json"
-        traffic = None
-        if prof_path.exists():
-            traffic = json.loads(prof_path.read_text()).get(top)
-        roof = {"bound": "hbm", "kernel": top, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": traffic, "peak_kind": peak_kind,
-                "classes_ms_per_step": {k: round(v["ms"], 4) for k, v in classes.items()},
-                "eager_step_ms": round(step_ms, 3), "ctx": ctx, "batch": args.batch}
+        roof = roofline_summary(cfg, classes, args.batch, ctx, hbm, tfl, peak_kind)
+        roof["eager_step_ms"] = round(step_ms, 3)
 
     slo = None
     if not args.no_slo:

@@ -791,8 +791,15 @@ int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx*
   c->cfg = *cfg;
   c->seed = weight_seed;
   CK(cudaSetDevice(device));
-  CK(cudaStreamCreateWithFlags(&c->s_lm, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&c->s_dt, cudaStreamNonBlocking));
+  // The LM step is the throughput-critical path (every live stream waits on it);
+  // detokenization has a chunk of playback time as slack.  With the LM stream
+  // at the higher priority the CTA scheduler fills SMs from it first and detok
+  // CTAs soak up the gaps (VOX_STREAM_PRIO=0: equal priorities, for A/B).
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  const bool prio = !(getenv("VOX_STREAM_PRIO") && atoi(getenv("VOX_STREAM_PRIO")) == 0);
+  CK(cudaStreamCreateWithPriority(&c->s_lm, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+  CK(cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, prio_lo));
   CK(cudaEventCreate(&c->epoch));
   c->dm.d = cfg->d_model;
   c->dm.n_heads = cfg->n_heads;
