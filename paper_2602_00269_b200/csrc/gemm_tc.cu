@@ -195,27 +195,60 @@ __global__ void __launch_bounds__(128, 1)
     return;
   }
   float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
+  // Staged epilogue: 32 accumulator columns (= 32 output rows n) at a time go
+  // TMEM -> registers -> shared memory (transposed to [n][m]) -> 16-byte
+  // coalesced stores along m.  (Thread-per-m scalar stores issue 4x the store
+  // instructions and serialise on the per-SM store path.)
+  float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4], pipeline smem is idle now
+  constexpr int kSt = 128 + 4;
 #pragma unroll 1
   for (int mt = 0; mt < MT; ++mt) {
-    const int m = m0 + mt * 128 + warp * 32 + lane;
-    const bool m_ok = m < p.m_valid;
-    const float b = (p.bias != nullptr && m_ok) ? p.bias[m] : 0.f;
+    const int mb = m0 + mt * 128;
+    const bool full_m = mb + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
+                        (p.resid == nullptr || (p.ldr & 3) == 0) &&
+                        (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * BN + c, r);
       tmem_ld_wait();
-      if (m_ok) {
+      const int ml = warp * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + c + j;
-          if ((c + j) < BN && n < p.N) {
-            float v = __uint_as_float(r[j]) + b;
-            if (p.resid != nullptr) v += p.resid[static_cast<int64_t>(n) * p.ldr + m];
-            outp[static_cast<int64_t>(n) * p.ldo + m] = v;
+      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
+      __syncthreads();
+      // 32 rows n x 128 m: 1024 float4, 8 per thread
+#pragma unroll 2
+      for (int e = threadIdx.x; e < 32 * 32; e += 128) {
+        const int j = e >> 5, q = (e & 31) * 4;
+        const int n = n0 + c + j;
+        if ((c + j) < BN && n < p.N) {
+          float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
+          const int m = mb + q;
+          if (full_m) {
+            if (p.bias != nullptr) {
+              const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
+              v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
+            }
+            if (p.resid != nullptr) {
+              const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
+              v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
+            }
+            *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (m + t < p.m_valid) {
+                float o = vv[t];
+                if (p.bias != nullptr) o += p.bias[m + t];
+                if (p.resid != nullptr) o += p.resid[static_cast<int64_t>(n) * p.ldr + m + t];
+                outp[static_cast<int64_t>(n) * p.ldo + m + t] = o;
+              }
+            }
           }
         }
       }
+      __syncthreads();
     }
   }
 

@@ -133,10 +133,12 @@ __global__ void __launch_bounds__(256)
                               rw.pos / dm.page_size];
   const int off = rw.pos % dm.page_size;
   const float2* rp = rope + static_cast<int64_t>(rw.pos) * half;
-  // rotated heads (q then k): thread handles 4 consecutive pair indices i..i+3
+  // rotated heads (q then k): thread handles 4 consecutive pair indices i..i+3;
+  // gridDim.y CTAs share a row (interleaved items) for more loads in flight
   const int q4 = half / 4;
   const int n_items = (dm.n_heads + dm.n_kv) * q4;
-  for (int it = threadIdx.x; it < n_items; it += 256) {
+  const int cta_stride = 256 * gridDim.y;
+  for (int it = threadIdx.x + 256 * blockIdx.y; it < n_items; it += cta_stride) {
     const int head = it / q4, i = (it % q4) * 4;
     const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
     const float4 a = sum_splits4(w4, splits, ss4, c1);
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(256)
   const int hd4 = hd / 4;
   // V head-pages are stored TRANSPOSED ([hd][page_size]) so the attention PV
   // mma reads 4 consecutive tokens of one dim as a single 8-byte load
-  for (int e = threadIdx.x; e < dm.n_kv * hd4; e += 256) {
+  for (int e = threadIdx.x + 256 * blockIdx.y; e < dm.n_kv * hd4; e += cta_stride) {
     const float4 v = sum_splits4(w4, splits, ss4, vbase4 + e);
     const int kvh = e / hd4, dd = (e % hd4) * 4;
     bf16* vt = vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * hd + dd) * dm.page_size + off;
@@ -178,7 +180,7 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int spli
                             int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
-  launch_k(qkv_rope_append_kernel, dim3(n), dim3(256), 0, st, rows, ws, splits, split_stride, dm,
+  launch_k(qkv_rope_append_kernel, dim3(n, 2), dim3(256), 0, st, rows, ws, splits, split_stride, dm,
            rope, page_table, kc, vc, q_out);
 }
 
