@@ -64,6 +64,18 @@ __global__ void __launch_bounds__(128, 1)
   // hammering the same L2 lines (each activation line is read by every CTA)
   const int krot = p.k_rotate ? static_cast<int>((blockIdx.y * 7u) % static_cast<unsigned>(nkb)) : 0;
   auto kbi = [&](int i) { const int t = i + krot; return kb0 + (t >= nkb ? t - nkb : t); };
+  // activations in the packed tile layout: the BN rows of one k-block are
+  // contiguous (BN * 128 B) inside a 128-row tile, so one bulk copy per 128 rows
+  auto load_x_packed = [&](uint8_t* dst, int kb, uint64_t* bar, uint64_t pol) {
+#pragma unroll
+    for (int h = 0; h < (BN + 127) / 128; ++h) {
+      const int nr = n0 + h * 128;
+      const int rows = BN < 128 ? BN : 128;
+      bulk_load(dst + h * 16384,
+                p.x_packed + (static_cast<int64_t>(nr / 128) * p.n_kb + kb) * 8192 + (nr % 128) * 64,
+                rows * 128, bar, pol);
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmW);
@@ -105,7 +117,10 @@ __global__ void __launch_bounds__(128, 1)
     }
     griddep_wait();
     for (int i = 0; i < pre; ++i)
-      tma_load_2d(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], kbi(i) * 64, n0,
+      if (p.x_packed != nullptr)
+        load_x_packed(smem + i * C::kStageBytes + C::kABytes, kbi(i), &full[i], pol_x);
+      else
+        tma_load_2d(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], kbi(i) * 64, n0,
                   pol_x);
     for (int i = pre; i < nkb; ++i) {
       const int s = i % C::kStages;
@@ -126,7 +141,10 @@ __global__ void __launch_bounds__(128, 1)
         else
           tma_load_2d(st + mt * 16384, &tmW, &full[s], kx, m0 + mt * 128, pol_w);
       }
-      tma_load_2d(st + C::kABytes, &tmX, &full[s], kx, n0, pol_x);
+      if (p.x_packed != nullptr)
+        load_x_packed(st + C::kABytes, kbi(i), &full[s], pol_x);
+      else
+        tma_load_2d(st + C::kABytes, &tmX, &full[s], kx, n0, pol_x);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer (single thread) ----------------

@@ -49,6 +49,7 @@ struct GemmArgs {
   int epi;
   bf16* act;
   int64_t ld_act;
+  const bf16* x_packed;   // non-null: activations in the packed tile layout (bulk copies)
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };

@@ -192,6 +192,7 @@ struct VoxCtx {
   int detok_stop = 1 << 30;  // debug: stop the detok pipeline after this many stages
   bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
+  const bf16* test_x_packed = nullptr;  // gemm_test only: packed activations
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
   bool silu_unfused = getenv("VOX_SILU_UNFUSED") != nullptr;  // A/B: separate SiLU kernel
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
@@ -291,6 +292,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.ldr = ldr;
   a.m_valid = m_valid;
   a.w_packed = wp;
+  a.x_packed = c->test_x_packed;
   a.k_rotate = c->gemm_k_rotate;
   a.probe = c->gemm_probe;
   a.epi = act_out != nullptr ? 1 : 0;
@@ -1567,7 +1569,14 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   CK(cudaMalloc(&sink, 148 * 8 * 4));
   // VOX_GEMM_PACKED_TEST=1: stream W from the packed tile layout (the decode path)
   bf16* wpk = nullptr;
+  bf16* xpk = nullptr;
   CUtensorMap tpk{};
+  if (getenv("VOX_GEMM_XPACKED_TEST") && atoi(getenv("VOX_GEMM_XPACKED_TEST")) == 1) {
+    CK(dalloc(&xpk, static_cast<size_t>(packed_elems(N, K))));
+    launch_pack_bf16(dx, xpk, N, K, c->s_lm);
+    CK(cudaStreamSynchronize(c->s_lm));
+    c->test_x_packed = xpk;
+  }
   if (getenv("VOX_GEMM_PACKED_TEST") && atoi(getenv("VOX_GEMM_PACKED_TEST")) == 1) {
     CK(dalloc(&wpk, static_cast<size_t>(packed_elems(M, K))));
     launch_pack_bf16(dw, wpk, M, K, c->s_lm);
@@ -1594,6 +1603,8 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   cudaFree(flush);
   cudaFree(sink);
   if (wpk) cudaFree(wpk);
+  if (xpk) cudaFree(xpk);
+  c->test_x_packed = nullptr;
   if (rc == VOX_OK) {
     std::vector<float> tmp(static_cast<size_t>(splits) * N * M);
     CK(cudaMemcpy(tmp.data(), dout, tmp.size() * 4, cudaMemcpyDeviceToHost));
