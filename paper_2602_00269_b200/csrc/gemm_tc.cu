@@ -175,31 +175,41 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   if (MT == 1 && p.epi == 1) {
     // fused SiLU(gate) * up: TMEM lanes 0-63 hold gate, 64-127 up of features
-    // f = 64 * tile + (lane % 64); warps 2-3 hand `up` to warps 0-1 through
-    // shared memory (the pipeline stages are idle once `done` has fired)
-    float* stg = reinterpret_cast<float*>(smem);  // [64][BN + 1]
+    // f = 64 * tile + (lane % 64).  32 accumulator columns (rows n) at a time are
+    // staged transposed in the idle pipeline smem, then each thread turns 8
+    // features of one row into 8 bf16 and writes them with one 16-byte store.
+    float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4]
+    constexpr int kSt = 128 + 4;
     const int f0 = (m0 / 128) * 64;
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
       tmem_ld_wait();
-      if (warp >= 2) {
+      const int ml = warp * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) stg[((warp - 2) * 32 + lane) * (BN + 1) + c + j] = __uint_as_float(r[j]);
-      }
+      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
       __syncthreads();
-      if (warp < 2) {
-        const int f = f0 + warp * 32 + lane;
+#pragma unroll 2
+      for (int e = threadIdx.x; e < 32 * 8; e += 128) {
+        const int j = e >> 3, q = (e & 7) * 8;
+        const int n = n0 + c + j;
+        if ((c + j) < BN && n < p.N) {
+          uint32_t pk[4];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int n = n0 + c + j;
-          if ((c + j) < BN && n < p.N) {
-            const float g = __uint_as_float(r[j]);
-            const float u = stg[(warp * 32 + lane) * (BN + 1) + c + j];
-            p.act[static_cast<int64_t>(n) * p.ld_act + f] =
-                __float2bfloat16_rn(__fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u));
+          for (int t = 0; t < 4; ++t) {
+            float o[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float g = stg[j * kSt + q + 2 * t + h];
+              const float u = stg[j * kSt + 64 + q + 2 * t + h];
+              o[h] = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+            }
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(o[0], o[1]);
+            pk[t] = *reinterpret_cast<const uint32_t*>(&b2);
           }
+          *reinterpret_cast<uint4*>(p.act + static_cast<int64_t>(n) * p.ld_act + f0 + q) =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
       }
       __syncthreads();
@@ -493,6 +503,10 @@ static cudaError_t launch_pair(const CUtensorMap& tw, const CUtensorMap& tx, con
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (getenv("VOX_PAIR_NOPDL")) {  // debug: cluster launch without the PDL edge
+    at[0] = at[1];
+    cfg.numAttrs = 1;
+  }
   return cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BNP, DEEP>, tw, tx, a);
 }
 

@@ -193,6 +193,7 @@ struct VoxCtx {
   bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
   const bf16* test_x_packed = nullptr;  // gemm_test only: packed activations
+  bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;  // debug: eager decode steps
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
   bool silu_unfused = getenv("VOX_SILU_UNFUSED") != nullptr;  // A/B: separate SiLU kernel
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
@@ -1097,7 +1098,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
   if (ns > 0)
     CK(cudaMemcpyAsync(c->d_sample_rows, sg.sample_rows, sizeof(int) * ns,
                        cudaMemcpyHostToDevice, st));
-  const bool use_graph = !(flags & VOX_FWD_NO_GRAPH) && !full && !c->timing;
+  const bool use_graph = !(flags & VOX_FWD_NO_GRAPH) && !full && !c->timing && !c->no_graphs;
   int rc = VOX_OK;
   if (use_graph) {
     auto key = std::make_pair(nrows, ns);
