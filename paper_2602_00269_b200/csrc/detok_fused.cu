@@ -136,13 +136,17 @@ __global__ void __launch_bounds__(ru_threads<C>())
     hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
     hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
     const int nr = kRuRows + H;
-    for (int e = tid; e < nr * C; e += kRuThreads) {
-      const int i = e / C, ch = e % C;
+    // each thread owns one channel (kRuThreads % C == 0): per-channel constants
+    // once, rows strided by kRuThreads / C, 4 independent loads in flight
+    constexpr int kRowStep = kRuThreads / C;
+    const int ch = tid % C;
+    const float a1 = alpha1[ch], inv1 = snake_inv(a1);
+#pragma unroll 4
+    for (int i = tid / C; i < nr; i += kRowStep) {
       const int t = t0 - H + i;  // local row
       float v;
       if (t >= 0) {
-        const float a = alpha1[ch];
-        v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], a, snake_inv(a));
+        v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], a1, inv1);
         if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
       } else {
         v = hin[(H + t) * C + ch];
@@ -159,18 +163,28 @@ __global__ void __launch_bounds__(ru_threads<C>())
 
   // ---------------- 2. v = Snake(dwconv(y1)) -> bf16 UMMA operand ----------------
   if (active) {
-    for (int e = tid; e < kRuRows * (C / 2); e += kRuThreads) {
-      const int i = e / (C / 2), ch = (e % (C / 2)) * 2;
-      float o[2];
+    // each thread owns a channel pair (kRuThreads % (C / 2) == 0)
+    constexpr int kRowStep2 = kRuThreads / (C / 2);
+    const int ch = (tid % (C / 2)) * 2;
+    float w0[7], w1[7];
 #pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c2 = ch + cc;
-        float acc = dw_b[c2];
+    for (int k = 0; k < 7; ++k) {
+      w0[k] = dw_w[ch * 7 + k];
+      w1[k] = dw_w[(ch + 1) * 7 + k];
+    }
+    const float b0 = dw_b[ch], b1 = dw_b[ch + 1];
+    const float a20 = alpha2[ch], a21 = alpha2[ch + 1];
+    const float i20 = snake_inv(a20), i21 = snake_inv(a21);
+#pragma unroll 2
+    for (int i = tid / (C / 2); i < kRuRows; i += kRowStep2) {
+      float acc0 = b0, acc1 = b1;
 #pragma unroll
-        for (int k = 0; k < 7; ++k) acc = fmaf(dw_w[c2 * 7 + k], y1s[(H + i - (6 - k) * dil) * C + c2], acc);
-        o[cc] = snake_f(acc, alpha2[c2]);
+      for (int k = 0; k < 7; ++k) {
+        const float* yr = y1s + (H + i - (6 - k) * dil) * C + ch;
+        acc0 = fmaf(w0[k], yr[0], acc0);
+        acc1 = fmaf(w1[k], yr[1], acc1);
       }
-      const __nv_bfloat162 pr = __floats2bfloat162_rn(o[0], o[1]);
+      const __nv_bfloat162 pr = __floats2bfloat162_rn(snake_r(acc0, a20, i20), snake_r(acc1, a21, i21));
       *reinterpret_cast<__nv_bfloat162*>(sa + swz_off(i, ch, kRuRows)) = pr;
     }
   }
@@ -212,10 +226,13 @@ __global__ void __launch_bounds__(ru_threads<C>())
   __syncthreads();
   if (active) {
     const float* stg = y1s;
-    for (int e = tid; e < kRuRows * C; e += kRuThreads) {
-      const int i = e / C, ch = e % C;
+    constexpr int kRowStep = kRuThreads / C;
+    const int ch = tid % C;
+    const float pb = pw_b[ch];
+#pragma unroll 4
+    for (int i = tid / C; i < kRuRows; i += kRowStep) {
       const int64_t gi = static_cast<int64_t>(r0 + i) * C + ch;
-      y[gi] = (stg[i * (C + 1) + ch] + pw_b[ch]) + x[gi];
+      y[gi] = (stg[i * (C + 1) + ch] + pb) + x[gi];
     }
   }
   if (warp == 0) {
@@ -282,12 +299,15 @@ __global__ void __launch_bounds__(kOutRows)
   constexpr int H = 6;
   const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
   float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+  const int chx = tid % C;
+  const float ax = alpha[chx], ix = snake_inv(ax);
+#pragma unroll 4
   for (int e = tid; e < (kOutRows + H) * C; e += kOutRows) {
-    const int i = e / C, ch = e % C;
+    const int i = e / C, ch = chx;  // kOutRows % C == 0: fixed channel per thread
     const int t = t0 - H + i;
     float v;
     if (t >= 0) {
-      v = snake_f(x[static_cast<int64_t>(r0 - H + i) * C + ch], alpha[ch]);
+      v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], ax, ix);
       if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;
     } else {
       v = hin[(H + t) * C + ch];
@@ -334,5 +354,81 @@ void launch_detok_out_tiled(const DetokReq* reqs, int rows, int up, const float*
 }
 
 bool detok_out_tiled_supported(int C, int up) { return C == 64 && (4 * up) % kOutRows == 0; }
+
+// ---------------------------------------------------------------------------
+// Snake + transposed-conv operand [s(x_t) | s(x_{t-1})] (bf16), tiled: a CTA
+// walks R consecutive rows of one request, each thread owning channels, so
+// Snake is evaluated once per element (s(x_{t-1}) is carried in a register)
+// and every access is coalesced along channels.  History = 1 row of s(x).
+// ---------------------------------------------------------------------------
+template <int CPT>  // channels per thread
+__global__ void __launch_bounds__(256)
+    snake_upcat_tiled_kernel(const ReqHdrF* hdr, const DetokReq* __restrict__ reqs, int up, int R,
+                             const float* __restrict__ x, int C, const float* __restrict__ alpha,
+                             float* __restrict__ state, int64_t st_off, DetokDims dd,
+                             bf16* __restrict__ out) {
+  const int tid = threadIdx.x;
+  float a[CPT], inv[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int ch = tid + k * blockDim.x;
+    a[k] = ch < C ? alpha[ch] : 1.f;
+    inv[k] = snake_inv(a[k]);
+  }
+  griddep_wait();
+  griddep_launch();
+  const int r0 = blockIdx.x * R;
+  if (r0 >= hdr->n_lat * up) return;
+  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const int t0 = r0 - q.lat_off * up;
+  const int n = 4 * q.nf * up;
+  const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
+  float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+  float prev[CPT];
+#pragma unroll
+  for (int k = 0; k < CPT; ++k) {
+    const int ch = tid + k * blockDim.x;
+    if (ch < C)
+      prev[k] = t0 > 0 ? snake_r(x[static_cast<int64_t>(r0 - 1) * C + ch], a[k], inv[k]) : hin[ch];
+  }
+  for (int i = 0; i < R; ++i) {
+    const int r = r0 + i;
+    const float* xr = x + static_cast<int64_t>(r) * C;
+    bf16* o = out + static_cast<int64_t>(r) * 2 * C;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int ch = tid + k * blockDim.x;
+      if (ch < C) {
+        const float cur = snake_r(xr[ch], a[k], inv[k]);
+        o[ch] = __float2bfloat16_rn(cur);
+        o[C + ch] = __float2bfloat16_rn(prev[k]);
+        if (t0 + i == n - 1) hout[ch] = cur;
+        prev[k] = cur;
+      }
+    }
+  }
+}
+
+bool snake_upcat_tiled_supported(int up_before) { return up_before >= 1; }
+
+void launch_snake_upcat_tiled(const DetokReq* reqs, int rows, int up_before, const float* x, int C,
+                              const float* alpha, float* state, int64_t st_off, const DetokDims& dd,
+                              bf16* out_cat, cudaStream_t st) {
+  const ReqHdrF* hdr = reinterpret_cast<const ReqHdrF*>(reqs) - 1;
+  // rows per CTA: a request spans 4 * nf * up_before rows at this level
+  const int R = (4 * up_before) < 16 ? 4 * up_before : 16;
+  const int threads = C < 256 ? C : 256;
+  const int cpt = (C + threads - 1) / threads;
+  const dim3 grid((rows + R - 1) / R);
+  if (cpt <= 1)
+    launch_k(snake_upcat_tiled_kernel<1>, grid, dim3(threads), 0, st, hdr, reqs, up_before, R, x, C,
+             alpha, state, st_off, dd, out_cat);
+  else if (cpt <= 2)
+    launch_k(snake_upcat_tiled_kernel<2>, grid, dim3(threads), 0, st, hdr, reqs, up_before, R, x, C,
+             alpha, state, st_off, dd, out_cat);
+  else
+    launch_k(snake_upcat_tiled_kernel<4>, grid, dim3(threads), 0, st, hdr, reqs, up_before, R, x, C,
+             alpha, state, st_off, dd, out_cat);
+}
 
 }  // namespace vox

@@ -197,6 +197,10 @@ void launch_ru_fused(const DetokReq* reqs, int rows, int up, const float* x, flo
                      const float* alpha2, const bf16* pw_w, const float* pw_b, float* state,
                      int64_t st_off, const DetokDims& dd, cudaStream_t st);
 bool detok_out_tiled_supported(int C, int up);
+bool snake_upcat_tiled_supported(int up_before);
+void launch_snake_upcat_tiled(const DetokReq* reqs, int rows, int up_before, const float* x, int C,
+                              const float* alpha, float* state, int64_t st_off, const DetokDims& dd,
+                              bf16* out_cat, cudaStream_t st);
 void launch_detok_out_tiled(const DetokReq* reqs, int rows, int up, const float* x, int C,
                             const float* alpha, const float* w, float b, float* state,
                             int64_t st_off, const DetokDims& dd, float* pcm, cudaStream_t st);

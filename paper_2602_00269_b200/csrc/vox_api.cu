@@ -1272,8 +1272,12 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
     const int rows = n_lat * up;
     {
       TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows) * Ci * 8);
-      launch_snake_upcat(reqs, n_req, rows, up, x, Ci, w.up_alpha[b], c->dstate, dd.off_up[b], dd,
-                         c->dbf, st);
+      if (snake_upcat_tiled_supported(up) && !c->detok_unfused)
+        launch_snake_upcat_tiled(reqs, rows, up, x, Ci, w.up_alpha[b], c->dstate, dd.off_up[b], dd,
+                                 c->dbf, st);
+      else
+        launch_snake_upcat(reqs, n_req, rows, up, x, Ci, w.up_alpha[b], c->dstate, dd.off_up[b], dd,
+                           c->dbf, st);
     }
     DSTOP(nullptr);
     std::map<int, CUtensorMap> um;
