@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(ru_threads<C>())
   using L = RuSmem<C>;
   constexpr int kRuThreads = ru_threads<C>();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by pointer arithmetic on the __shared__ array (an
+  // integer round-trip would turn every smem access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* y1s = reinterpret_cast<float*>(smem);
   uint8_t* sa = smem + L::kAOff;
   uint8_t* sb = smem + L::kBOff;
@@ -141,17 +142,26 @@ __global__ void __launch_bounds__(ru_threads<C>())
     constexpr int kRowStep = kRuThreads / C;
     const int ch = tid % C;
     const float a1 = alpha1[ch], inv1 = snake_inv(a1);
-#pragma unroll 4
-    for (int i = tid / C; i < nr; i += kRowStep) {
-      const int t = t0 - H + i;  // local row
-      float v;
-      if (t >= 0) {
-        v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], a1, inv1);
-        if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
-      } else {
-        v = hin[(H + t) * C + ch];
+    // 4 rows per round: all loads first (independent), then the Snakes
+    for (int i0 = tid / C; i0 < nr; i0 += 4 * kRowStep) {
+      float xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kRowStep;
+        const int t = t0 - H + i;
+        xv[u] = 0.f;
+        if (i < nr) xv[u] = t >= 0 ? x[static_cast<int64_t>(r0 - H + i) * C + ch] : hin[(H + t) * C + ch];
       }
-      y1s[i * C + ch] = v;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = i0 + u * kRowStep;
+        const int t = t0 - H + i;
+        if (i < nr) {
+          const float v = t >= 0 ? snake_r(xv[u], a1, inv1) : xv[u];
+          if (t >= 0 && i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
+          y1s[i * C + ch] = v;
+        }
+      }
     }
     // short requests (n < H): shift the old context
     for (int e = tid; e < kRuRows * C; e += kRuThreads) {

@@ -42,8 +42,9 @@ __global__ void __launch_bounds__(128, 1)
                         const __grid_constant__ CUtensorMap tmX, GemmArgs p) {
   using C = GemmCfg<BN, MT>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by pointer arithmetic on the __shared__ array (an
+  // integer round-trip would turn every smem access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* done = empty + C::kStages;
@@ -321,8 +322,9 @@ __global__ void __launch_bounds__(128, 1)
                      GemmArgs p) {
   using C = PairCfg<BNP, DEEP>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // align to 1024 B by pointer arithmetic on the __shared__ array (an
+  // integer round-trip would turn every smem access into a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* empty = full + C::kStages;
   uint64_t* done = empty + C::kStages;
