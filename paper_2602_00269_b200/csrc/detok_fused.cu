@@ -330,27 +330,16 @@ __global__ void __launch_bounds__(kOutRows)
   }
   __syncthreads();
   const int t = t0 + tid;
-  float acc = 0.f;
-  // same per-lane accumulation order as detok_out_kernel: channel c's 7 taps
-  // are summed into lane (c % 32)'s partial, then a warp reduction (here: the
-  // 32 partials summed in the same butterfly order)
-  float part[32];
-#pragma unroll
-  for (int l = 0; l < 32; ++l) part[l] = 0.f;
-#pragma unroll
+  // 4 interleaved partial sums (channel c -> c % 4): short FMA chains, few registers
+  float part[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
   for (int ch = 0; ch < C; ++ch) {
-    float a = part[ch & 31];
+    float a = part[ch & 3];
 #pragma unroll
     for (int k = 0; k < 7; ++k) a = fmaf(ws[ch * 7 + k], s[(tid + k) * (C + 1) + ch], a);
-    part[ch & 31] = a;
+    part[ch & 3] = a;
   }
-  // butterfly (xor 16, 8, 4, 2, 1) as warp_sum: lane 0's result
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-    for (int l = 0; l < 32; ++l)
-      if (l < o) part[l] = part[l] + part[l + o];
-  acc = part[0];
+  const float acc = (part[0] + part[1]) + (part[2] + part[3]);
   if (t < q.n_samples && t < n) pcm[q.pcm_off + t] = tanhf(acc + b);
 }
 
@@ -420,6 +409,94 @@ __global__ void __launch_bounds__(256)
 }
 
 bool snake_upcat_tiled_supported(int up_before) { return up_before >= 1; }
+
+// ---------------------------------------------------------------------------
+// Residual-unit prologue for the wide levels (C >= 256), tiled: a CTA owns TR
+// rows x 64 channels of one request; y1 = Snake(x) for the rows plus the
+// 6*dil causal halo is computed once into shared memory (ru_prep_kernel
+// recomputes it for each of the 7 taps), then v = bf16(Snake(dwconv(y1))) is
+// written for the 1x1 GEMM.  Cached left context as in ru_prep_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kPrepCh = 64;
+
+__global__ void __launch_bounds__(256)
+    ru_prep_tiled_kernel(const ReqHdrF* hdr, const DetokReq* __restrict__ reqs, int up, int TR,
+                         const float* __restrict__ x, int C, int dil,
+                         const float* __restrict__ alpha1, const float* __restrict__ dw_w,
+                         const float* __restrict__ dw_b, const float* __restrict__ alpha2,
+                         float* __restrict__ state, int64_t st_off, DetokDims dd,
+                         bf16* __restrict__ out) {
+  extern __shared__ float y1s[];  // [TR + 6 dil][kPrepCh]
+  const int tid = threadIdx.x;
+  const int cl = tid % kPrepCh;                 // channel within the tile
+  const int ch = blockIdx.y * kPrepCh + cl;     // channel
+  const int rstep = 256 / kPrepCh;              // rows per pass
+  const float a1 = alpha1[ch], i1 = snake_inv(a1);
+  const float a2 = alpha2[ch], i2 = snake_inv(a2);
+  float w[7];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) w[k] = dw_w[ch * 7 + k];
+  const float bias = dw_b[ch];
+  griddep_wait();
+  griddep_launch();
+  const int r0 = blockIdx.x * TR;
+  if (r0 >= hdr->n_lat * up) return;
+  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const int t0 = r0 - q.lat_off * up;
+  const int n = 4 * q.nf * up;
+  const int H = 6 * dil;
+  const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
+  float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+  const int nr = TR + H;
+  for (int i0 = tid / kPrepCh; i0 < nr; i0 += 4 * rstep) {
+    float xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * rstep, t = t0 - H + i;
+      xv[u] = 0.f;
+      if (i < nr) xv[u] = t >= 0 ? x[static_cast<int64_t>(r0 - H + i) * C + ch] : hin[(H + t) * C + ch];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * rstep, t = t0 - H + i;
+      if (i < nr) {
+        const float v = t >= 0 ? snake_r(xv[u], a1, i1) : xv[u];
+        if (t >= 0 && i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;
+        y1s[i * kPrepCh + cl] = v;
+      }
+    }
+  }
+  for (int i = tid / kPrepCh; i < TR; i += rstep) {  // short requests (n < H)
+    const int t = t0 + i;
+    for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int i = tid / kPrepCh; i < TR; i += rstep) {
+    float acc = bias;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc = fmaf(w[k], y1s[(H + i - (6 - k) * dil) * kPrepCh + cl], acc);
+    out[static_cast<int64_t>(r0 + i) * C + ch] = __float2bfloat16_rn(snake_r(acc, a2, i2));
+  }
+}
+
+bool ru_prep_tiled_supported(int C, int up) { return C % kPrepCh == 0 && C >= 256 && 4 * up >= 16; }
+
+void launch_ru_prep_tiled(const DetokReq* reqs, int rows, int up, const float* x, int C, int dil,
+                          const float* alpha1, const float* dw_w, const float* dw_b,
+                          const float* alpha2, float* state, int64_t st_off, const DetokDims& dd,
+                          bf16* out, cudaStream_t st) {
+  const ReqHdrF* hdr = reinterpret_cast<const ReqHdrF*>(reqs) - 1;
+  const int TR = 4 * up < 64 ? 4 * up : 64;  // a request spans 4 * nf * up rows
+  const size_t smem = static_cast<size_t>(TR + 6 * dil) * kPrepCh * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ru_prep_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  launch_k(ru_prep_tiled_kernel, dim3((rows + TR - 1) / TR, C / kPrepCh), dim3(256), smem, st, hdr,
+           reqs, up, TR, x, C, dil, alpha1, dw_w, dw_b, alpha2, state, st_off, dd, out);
+}
 
 void launch_snake_upcat_tiled(const DetokReq* reqs, int rows, int up_before, const float* x, int C,
                               const float* alpha, float* state, int64_t st_off, const DetokDims& dd,

@@ -198,6 +198,11 @@ void launch_ru_fused(const DetokReq* reqs, int rows, int up, const float* x, flo
                      int64_t st_off, const DetokDims& dd, cudaStream_t st);
 bool detok_out_tiled_supported(int C, int up);
 bool snake_upcat_tiled_supported(int up_before);
+bool ru_prep_tiled_supported(int C, int up);
+void launch_ru_prep_tiled(const DetokReq* reqs, int rows, int up, const float* x, int C, int dil,
+                          const float* alpha1, const float* dw_w, const float* dw_b,
+                          const float* alpha2, float* state, int64_t st_off, const DetokDims& dd,
+                          bf16* out, cudaStream_t st);
 void launch_snake_upcat_tiled(const DetokReq* reqs, int rows, int up_before, const float* x, int C,
                               const float* alpha, float* state, int64_t st_off, const DetokDims& dd,
                               bf16* out_cat, cudaStream_t st);

@@ -1303,9 +1303,14 @@ static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
       }
       {
         TimedLaunch tl(c, st, "detok_elt", static_cast<double>(rows2) * Co * 6);
-        launch_ru_prep(reqs, n_req, rows2, up, x, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
-                       w.ru_dw_b[b][u], w.ru_a2[b][u], c->dstate, dd.off_ru[b][u], dd, c->dbf,
-                       st);
+        if (ru_prep_tiled_supported(Co, up) && !c->detok_unfused)
+          launch_ru_prep_tiled(reqs, rows2, up, x, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
+                               w.ru_dw_b[b][u], w.ru_a2[b][u], c->dstate, dd.off_ru[b][u], dd,
+                               c->dbf, st);
+        else
+          launch_ru_prep(reqs, n_req, rows2, up, x, Co, dils[u], w.ru_a1[b][u], w.ru_dw_w[b][u],
+                         w.ru_dw_b[b][u], w.ru_a2[b][u], c->dstate, dd.off_ru[b][u], dd, c->dbf,
+                         st);
       }
       DSTOP(nullptr);
       RET(run_gemm(c, w.tm_ru[b][u], rm, Co, rows2, Co, x, Co, 1, w.ru_pw_b[b][u], x, Co, Co, st,
