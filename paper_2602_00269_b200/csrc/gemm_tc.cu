@@ -116,6 +116,15 @@ __global__ void __launch_bounds__(128, 1)
                       m0 + mt * 128, pol_w);
       }
     }
+    // ... and pull the rest of this CTA's weight slice into L2 while the
+    // preceding kernel finishes (HBM is otherwise idle during the small
+    // elementwise kernels between GEMMs); the ring then refills from L2.
+    if (p.w_packed != nullptr && p.l2_prefetch)
+      for (int i = pre; i < nkb; ++i)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          prefetch_l2_bulk(p.w_packed + (static_cast<int64_t>(m0 / 128 + mt) * p.n_kb + kbi(i)) * 8192,
+                           16384);
     griddep_wait();
     for (int i = 0; i < pre; ++i)
       if (p.x_packed != nullptr)

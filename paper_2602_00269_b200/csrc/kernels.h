@@ -44,6 +44,7 @@ struct GemmArgs {
   int m_valid;            // columns m >= m_valid are not stored
   int k_rotate;           // rotate each CTA's k-block order by its weight tile
   int probe;              // microbenchmarks only: 1 = MMA-only, 2 = loads-only
+  int l2_prefetch;        // prefetch the CTA's remaining weight tiles into L2 before griddep_wait
   // epi == 1 (gate|up GEMM, 1 split, interleaved weight tiles): instead of fp32
   // out, write act[n][f] = bf16(SiLU(gate) * up) for the tile's 64 features
   int epi;

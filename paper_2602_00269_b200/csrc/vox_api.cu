@@ -194,6 +194,7 @@ struct VoxCtx {
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
   const bf16* test_x_packed = nullptr;  // gemm_test only: packed activations
   bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;  // debug: eager decode steps
+  int gemm_l2_prefetch = getenv("VOX_GEMM_L2PF") ? atoi(getenv("VOX_GEMM_L2PF")) : 0;  // measured slower (profiles/gemm_l2_prefetch_ab_r01.txt)
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
   bool silu_unfused = getenv("VOX_SILU_UNFUSED") != nullptr;  // A/B: separate SiLU kernel
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
@@ -296,6 +297,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.x_packed = c->test_x_packed;
   a.k_rotate = c->gemm_k_rotate;
   a.probe = c->gemm_probe;
+  a.l2_prefetch = c->gemm_l2_prefetch;
   a.epi = act_out != nullptr ? 1 : 0;
   a.act = act_out;
   a.ld_act = ld_act;
