@@ -119,12 +119,17 @@ __global__ void __launch_bounds__(128, 1)
     // ... and pull the rest of this CTA's weight slice into L2 while the
     // preceding kernel finishes (HBM is otherwise idle during the small
     // elementwise kernels between GEMMs); the ring then refills from L2.
-    if (p.w_packed != nullptr && p.l2_prefetch)
-      for (int i = pre; i < nkb; ++i)
+    // l2_prefetch = D > 0: a sliding window -- keep the weight tiles of the next
+    // D k-blocks beyond the smem ring in flight towards L2 (more memory-level
+    // parallelism than the ring alone; the ring then refills from L2)
+    auto pf = [&](int i) {
+      if (p.w_packed != nullptr && p.l2_prefetch > 0 && i < nkb)
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
           prefetch_l2_bulk(p.w_packed + (static_cast<int64_t>(m0 / 128 + mt) * p.n_kb + kbi(i)) * 8192,
                            16384);
+    };
+    for (int i = pre; i < pre + p.l2_prefetch; ++i) pf(i);
     griddep_wait();
     for (int i = 0; i < pre; ++i)
       if (p.x_packed != nullptr)
@@ -135,6 +140,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int i = pre; i < nkb; ++i) {
       const int s = i % C::kStages;
       mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
+      pf(i + p.l2_prefetch);
       uint8_t* st = smem + s * C::kStageBytes;
       if (p.probe == 1) {  // microbenchmark: MMA-only (re-use the resident stage data)
         mbar_arrive(&full[s]);
@@ -413,26 +419,54 @@ __global__ void __launch_bounds__(128, 1)
   griddep_wait();
   mbar_wait(done, 0);
   tc_fence_after();
-  const int m = mw + warp * 32 + lane;
   float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
-  const bool m_ok = m < p.m_valid;
-  const float b = (p.bias != nullptr && m_ok) ? p.bias[m] : 0.f;
+  // staged through the idle pipeline smem: [32 rows n][128 m] then 16-byte stores
+  float* stg = reinterpret_cast<float*>(smem);
+  constexpr int kSt = 128 + 4;
+  const bool full_m = mw + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
+                      (p.resid == nullptr || (p.ldr & 3) == 0) &&
+                      (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
 #pragma unroll 1
   for (int c = 0; c < BNP; c += 32) {
     uint32_t r[32];
     tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
     tmem_ld_wait();
-    if (m_ok) {
+    const int ml = warp * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int n = n0 + c + j;
-        if (n < p.N) {
-          float v = __uint_as_float(r[j]) + b;
-          if (p.resid != nullptr) v += p.resid[static_cast<int64_t>(n) * p.ldr + m];
-          outp[static_cast<int64_t>(n) * p.ldo + m] = v;
+    for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
+    __syncthreads();
+#pragma unroll 2
+    for (int e = threadIdx.x; e < 32 * 32; e += 128) {
+      const int j = e >> 5, q = (e & 31) * 4;
+      const int n = n0 + c + j;
+      if (n < p.N) {
+        float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
+        const int m = mw + q;
+        if (full_m) {
+          if (p.bias != nullptr) {
+            const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
+            v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
+          }
+          if (p.resid != nullptr) {
+            const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
+            v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
+          }
+          *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (m + t < p.m_valid) {
+              float o = vv[t];
+              if (p.bias != nullptr) o += p.bias[m + t];
+              if (p.resid != nullptr) o += p.resid[static_cast<int64_t>(n) * p.ldr + m + t];
+              outp[static_cast<int64_t>(n) * p.ldo + m + t] = o;
+            }
+          }
         }
       }
     }
+    __syncthreads();
   }
   tc_fence_before();
   cluster_sync();  // both CTAs done with TMEM before the pair deallocates
