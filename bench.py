@@ -321,21 +321,23 @@ def roofline_summary(cfg, classes, B: int, ctx: int, hbm: float, tfl: float, pea
             "classes": out, "ctx": ctx, "batch": B}
 
 
-def run_slo(dev, rates, seconds: float, seed: int, prompt: int, ws: int = 1, rank: int = 0):
+def run_slo(dev, rates, seconds: float, seed: int, prompt: int, ws: int = 1, rank: int = 0,
+            max_batch: int = 256, startup_limit: int = 16):
     """Poisson load test (config 5): offered rate r is the WHOLE-JOB rate; requests are
     routed to the ws replicas with the reference router, metrics pooled at the end."""
     from paper_2602_00269_b200 import dp
     from paper_2602_00269_b200._ref import scheduler, workload
     from paper_2602_00269_b200.engine import StreamingEngine, orpheus_profile
 
-    prof = orpheus_profile(max_batch=256)
+    prof = orpheus_profile(max_batch=max_batch)
     out = []
     for rate in rates:
         spec = workload.WorkloadSpec(rate=rate, duration_s=seconds, prompt_dist=workload.fixed(prompt),
                                      output_dist=workload.fixed(688), seed=seed)
         arr = list(enumerate(workload.build_workload(spec)))
         mine = dp.route(arr, ws, seed)[rank]
-        policy = scheduler.PolicyConfig(max_lm_batch=256, max_detok_batch=256, startup_concurrency_limit=16)
+        policy = scheduler.PolicyConfig(max_lm_batch=max_batch, max_detok_batch=max_batch,
+                                        startup_concurrency_limit=startup_limit)
         eng = StreamingEngine(dev, prof, policy, seed)
         tr = eng.run(mine)
         rep = dp.gather_pool(dp.local_summary(tr), ws)
@@ -365,8 +367,10 @@ def main():
     ap.add_argument("--prompt", type=int, default=50)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--slo-seconds", type=float, default=12.0)
-    ap.add_argument("--slo-rates", default="48,64,72,80,88,96,112")
+    ap.add_argument("--slo-rates", default="64,72,80,88,96,112")
     ap.add_argument("--no-slo", action="store_true")
+    ap.add_argument("--slo-max-batch", type=int, default=256, help="LM batch cap of the load test")
+    ap.add_argument("--slo-startup-limit", type=int, default=16, help="scheduler startup concurrency")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -432,8 +436,10 @@ def main():
     slo = None
     if not args.no_slo:
         rates = [float(x) * ws for x in args.slo_rates.split(",")]  # whole-job offered rate
-        best, sweep = run_slo(dev, rates, args.slo_seconds, args.seed, args.prompt, ws, rank)
-        slo = {"max_req_s_at_slo": best, "per_gpu": best / ws, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
+        best, sweep = run_slo(dev, rates, args.slo_seconds, args.seed, args.prompt, ws, rank,
+                              args.slo_max_batch, args.slo_startup_limit)
+        slo = {"max_req_s_at_slo": best, "per_gpu": best / ws, "max_lm_batch": args.slo_max_batch,
+               "startup_concurrency_limit": args.slo_startup_limit, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
                "duration_s": args.slo_seconds, "routing": "reference route_dp (seeded uniform), replicas",
                "sweep": sweep}
 
