@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           if (idx >= n_items) break;
           int r, kvh, z;
           attn_item_decode(idx, dm.n_kv, n_split, r, kvh, z);
+          r = rows[r].attn_row;  // longest contexts first
           const RowDev rw = rows[r];
           if (rw.slot < 0) continue;  // bucket padding
           const int n_pages = (rw.pos + 1 + ps - 1) / ps;

@@ -92,7 +92,9 @@ struct RowDev {
   int32_t slot, pos, token, sample;
   int32_t fresh;  // lowest position of this slot whose K/V this forward appends: pages
                   // below fresh / page_size are complete before the forward starts
-  int32_t pad_[3];
+  int32_t attn_row;  // attention work order: the i-th row to schedule is rows[rows[i].attn_row]
+                     // (longest context first, so the persistent grid's tail is short)
+  int32_t pad_[2];
 };
 
 struct LmDims {

@@ -1078,7 +1078,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
   for (int i = 0; i < nrows; ++i) {
     if (i < n) {
       sg.rows[i] = RowDev{rows[i].slot, rows[i].pos, rows[i].token, rows[i].sample,
-                          fresh[rows[i].slot], {0, 0, 0}};
+                          fresh[rows[i].slot], i, {0, 0}};
       attn_bytes += static_cast<double>(rows[i].pos + 1) * g.n_kv_heads * g.head_dim * 4;
       if (rows[i].sample) {
         sg.sample_rows[k] = i;
@@ -1087,11 +1087,18 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
         sg.out_index[i] = -1;
       }
     } else {
-      sg.rows[i] = RowDev{-1, 0, -1, 0, 0, {0, 0, 0}};
+      sg.rows[i] = RowDev{-1, 0, -1, 0, 0, i, {0, 0}};
       sg.out_index[i] = -1;
     }
   }
   for (int j = k; j < ns; ++j) sg.sample_rows[j] = -1;  // sampler skips padding
+  {  // attention order: longest context first (LPT), padding rows last
+    std::vector<int> ord(n);
+    for (int i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](int a, int b) { return rows[a].pos > rows[b].pos; });
+    for (int i = 0; i < n; ++i) sg.rows[i].attn_row = ord[i];
+  }
   c->step_attn_bytes = attn_bytes;
   cudaStream_t st = c->s_lm;
   CK(cudaMemcpyAsync(c->d_rows, sg.rows, sizeof(RowDev) * nrows, cudaMemcpyHostToDevice, st));
