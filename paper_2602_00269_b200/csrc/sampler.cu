@@ -29,7 +29,10 @@ constexpr int kST = 512;      // threads per row
 constexpr int kBins = 2048;   // radix histogram bins (11 bits)
 constexpr int kMaxWin = 256;
 
+constexpr int kFastE = 8;     // register-resident elements per thread (span <= 4096)
+
 struct SampSmem {
+  float part[2][kST / 32][8];  // fast path: per-warp partial sums of the 7 probes
   float hmass[kBins];
   uint32_t hcnt[kBins];
   int win[kMaxWin];
@@ -203,6 +206,187 @@ VOX_DEV int select_tie_index(const RowCtx& c, SampSmem& S, uint32_t kk, int rank
   return c.lo + static_cast<int>(prefix);
 }
 
+// ---------------------------------------------------------------------------
+// Stochastic path for spans of <= kST * kFastE candidates (the Orpheus 4096-id
+// frame slot): every thread keeps its 8 penalised/tempered values, keys and
+// softmax weights in registers, and the top-k / top-p boundaries are found by
+// an 8-ary search over the 32-bit key space with deterministic block
+// reductions (fixed-order warp shuffles + per-warp partials) -- no shared-
+// memory atomics (the radix histogram's hot bins serialise) and no re-reads
+// of the logits.  Same boundary semantics as the histogram path below.
+// ---------------------------------------------------------------------------
+VOX_DEV int sample_row_fast(SampSmem& S, const RowCtx& c, float ymax, int nfin, uint64_t seed,
+                            uint64_t step, const VoxSampling& prm, int* err_flag) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  float y[kFastE], w[kFastE];
+  uint32_t key[kFastE];
+  bool valid[kFastE];
+#pragma unroll
+  for (int e = 0; e < kFastE; ++e) {
+    const int id = c.lo + tid + e * kST;
+    y[e] = id < c.hi ? yval(c, id) : -INFINITY;
+    valid[e] = y[e] > -INFINITY;
+    key[e] = f2key(y[e]);
+    w[e] = valid[e] ? expf(y[e] - ymax) : 0.f;
+  }
+  int rnd = 0;
+  // F(b) = sum of wt over masked elements with key >= b, for 7 probes at once
+  auto probe_sums = [&](const uint32_t (&b)[7], const bool (&m)[kFastE], bool counts, float (&out)[7]) {
+    float acc[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      float a = 0.f;
+#pragma unroll
+      for (int e = 0; e < kFastE; ++e)
+        if (m[e] && key[e] >= b[j]) a += counts ? 1.f : w[e];
+      acc[j] = warp_sum(a);
+    }
+    float (*P)[8] = S.part[rnd & 1];
+    if (lane == 0)
+#pragma unroll
+      for (int j = 0; j < 7; ++j) P[wid][j] = acc[j];
+    __syncthreads();
+    // every warp reduces the kST/32 partials lane-parallel (fixed shuffle
+    // tree: deterministic, identical in all warps) instead of each thread
+    // summing them serially
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      float t = lane < kST / 32 ? P[lane][j] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      out[j] = t;
+    }
+    ++rnd;  // next round writes the other buffer (no WAR barrier needed)
+  };
+  // largest key b with F(b) >= target (F non-increasing; F(0) >= target)
+  auto search = [&](const bool (&m)[kFastE], bool counts, float target) -> uint32_t {
+    uint32_t lo = 0u, hi = 0xFFFFFFFFu;
+    while (lo < hi) {
+      const uint64_t len = static_cast<uint64_t>(hi) - lo + 1;
+      uint32_t b[7];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) b[j] = lo + static_cast<uint32_t>((len * (j + 1)) / 8);
+      float f[7];
+      probe_sums(b, m, counts, f);
+      uint32_t nlo = lo, nhi = hi;
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        if (b[j] <= nlo) continue;
+        if (f[j] >= target) {
+          nlo = b[j];
+        } else {
+          nhi = b[j] - 1;
+          break;
+        }
+      }
+      lo = nlo;
+      hi = nhi;
+    }
+    return lo;
+  };
+  // F at a single key, plus the count of masked elements equal to it
+  auto mass_gt_and_ties = [&](const bool (&m)[kFastE], bool counts, uint32_t tau, float& gt,
+                              float& ties) {
+    uint32_t b[7];
+    for (int j = 0; j < 7; ++j) b[j] = tau;
+    if (tau != 0xFFFFFFFFu) b[0] = tau + 1;
+    float f[7];
+    probe_sums(b, m, counts, f);
+    gt = tau != 0xFFFFFFFFu ? f[0] : 0.f;
+    bool eqm[kFastE];
+#pragma unroll
+    for (int e = 0; e < kFastE; ++e) eqm[e] = m[e] && key[e] == tau;
+    uint32_t z[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    probe_sums(z, eqm, true, f);
+    ties = f[0];
+  };
+
+  // ---- top-k: keep keys > kb_key, and ties at kb_key with id <= kb_tie_idx
+  bool kset = false;
+  uint32_t kb_key = 0u;
+  int kb_tie_idx = INT32_MAX;
+  int kb_ties_kept = 0;
+  bool in_k[kFastE];
+#pragma unroll
+  for (int e = 0; e < kFastE; ++e) in_k[e] = valid[e];
+  if (prm.top_k > 0 && prm.top_k < nfin) {
+    const uint32_t tau = search(valid, true, static_cast<float>(prm.top_k));
+    float gt, ties;
+    mass_gt_and_ties(valid, true, tau, gt, ties);
+    kset = true;
+    kb_key = tau;
+    kb_ties_kept = prm.top_k - static_cast<int>(gt);
+    if (kb_ties_kept < static_cast<int>(ties)) kb_tie_idx = select_tie_index(c, S, tau, kb_ties_kept);
+#pragma unroll
+    for (int e = 0; e < kFastE; ++e) {
+      const int id = c.lo + tid + e * kST;
+      in_k[e] = valid[e] && (key[e] > kb_key || (key[e] == kb_key && id <= kb_tie_idx));
+    }
+  }
+  uint32_t fb_key = kset ? kb_key : 0u;
+  int fb_tie_idx = kb_tie_idx;
+  bool kept[kFastE];
+#pragma unroll
+  for (int e = 0; e < kFastE; ++e) kept[e] = in_k[e];
+  if (prm.top_p < 1.0) {
+    // ---- top-p inside the top-k set: minimal prefix whose mass reaches p * Z
+    uint32_t z[7] = {0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    float f[7];
+    probe_sums(z, in_k, false, f);
+    const float target = static_cast<float>(prm.top_p) * f[0];
+    const uint32_t tau = search(in_k, false, target);
+    float gt, ties;
+    mass_gt_and_ties(in_k, false, tau, gt, ties);
+    const float w_tau = expf(key2f(tau) - ymax);
+    const int n_ties = static_cast<int>(ties);
+    int keep = (w_tau > 0.f) ? static_cast<int>(ceilf((target - gt) / w_tau)) : n_ties;
+    if (keep < 1) keep = 1;
+    if (keep > n_ties) keep = n_ties;
+    fb_key = tau;
+    if (keep < n_ties)
+      fb_tie_idx = select_tie_index(c, S, tau, keep);  // lowest ids first (<= kb_tie_idx)
+    else
+      fb_tie_idx = (kset && tau == kb_key) ? kb_tie_idx : INT32_MAX;
+#pragma unroll
+    for (int e = 0; e < kFastE; ++e) {
+      const int id = c.lo + tid + e * kST;
+      kept[e] = in_k[e] && (key[e] > fb_key || (key[e] == fb_key && id <= fb_tie_idx));
+    }
+  }
+  // ---- Gumbel-max draw over the kept set (counter RNG keyed by seed, step, id)
+  const uint64_t rkey = mix64(seed ^ (step * 0xD1B54A32D192ED03ull));
+  float gv = -INFINITY;
+  int gi = -1;
+#pragma unroll
+  for (int e = 0; e < kFastE; ++e) {
+    if (!kept[e]) continue;
+    const int id = c.lo + tid + e * kST;
+    const float u = unit_open01(mix64(rkey + static_cast<uint64_t>(id)));
+    better(gv, gi, y[e] - logf(-logf(u)), id);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v2 = __shfl_xor_sync(0xffffffffu, gv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, gi, o);
+    better(gv, gi, v2, i2);
+  }
+  __syncthreads();
+  if (lane == 0) {
+    S.redf[wid] = gv;
+    S.redi[wid] = gi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float v = S.redf[0];
+    int i = S.redi[0];
+    for (int k = 1; k < kST / 32; ++k) better(v, i, S.redf[k], S.redi[k]);
+    if (i < 0) atomicMax(err_flag, static_cast<int>(VOX_ERR_DEGENERATE));
+    S.i_b = i;
+  }
+  __syncthreads();
+  return S.i_b;
+}
+
 // Whole-CTA sampling of one row.  Returns the token id (same in all threads).
 VOX_DEV int sample_row(SampSmem& S, uint32_t* bm, const float* row, int col_base, int lo, int hi,
                        const int* win, int wlen, uint64_t seed, uint64_t step,
@@ -312,6 +496,7 @@ VOX_DEV int sample_row(SampSmem& S, uint32_t* bm, const float* row, int col_base
     if (tid == 0) atomicMax(err_flag, static_cast<int>(VOX_ERR_DEGENERATE));
     return -1;
   }
+  if (n <= kST * kFastE) return sample_row_fast(S, c, ymax, nfin, seed, step, prm, err_flag);
   // boundary of the admissible (top-k) set: keys > kb_key, plus ties at
   // kb_key with index <= kb_tie_idx.  Default: everything finite.
   uint32_t kb_key = f2key(-INFINITY) + 1u;
