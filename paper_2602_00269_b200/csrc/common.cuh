@@ -266,6 +266,30 @@ VOX_DEV void umma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Cluster multicast (1-CTA MMAs, activations shared across a cluster): one
+// CTA's TMA load lands at the same smem offset in every CTA of `mask` and
+// completes tx bytes on each destination CTA's mbarrier at `bar`'s offset.
+// ---------------------------------------------------------------------------
+VOX_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                            uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
+      "cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask),
+      "l"(policy)
+      : "memory");
+}
+// arrive (once) on the mbarrier at this smem offset in every CTA of `mask`
+// when all previously issued cta_group::1 MMAs of this thread have completed
+VOX_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+      "[%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // Programmatic dependent launch: wait for the preceding grid's completion
 // (and memory flush) / allow the next grid to start its prologue.
 VOX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

@@ -36,6 +36,116 @@ struct GemmCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 };
 
+// ---------------------------------------------------------------------------
+// Epilogue shared by the GEMM kernels: TMEM accumulator (128 lanes = weight
+// rows m, BN columns = activation rows n) -> registers -> smem (transposed)
+// -> 16-byte coalesced global stores.  `smem` is the idle pipeline ring.
+// ---------------------------------------------------------------------------
+template <int BN, int MT>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, uint32_t tmem,
+                                              int warp, int lane, int m0, int n0, int split) {
+  if (MT == 1 && p.epi == 1) {
+    // fused SiLU(gate) * up: TMEM lanes 0-63 hold gate, 64-127 up of features
+    // f = 64 * tile + (lane % 64).  32 accumulator columns (rows n) at a time are
+    // staged transposed in the idle pipeline smem, then each thread turns 8
+    // features of one row into 8 bf16 and writes them with one 16-byte store.
+    float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4]
+    constexpr int kSt = 128 + 4;
+    const int f0 = (m0 / 128) * 64;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
+      tmem_ld_wait();
+      const int ml = warp * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
+      __syncthreads();
+#pragma unroll 2
+      for (int e = threadIdx.x; e < 32 * 8; e += 128) {
+        const int j = e >> 3, q = (e & 7) * 8;
+        const int n = n0 + c + j;
+        if ((c + j) < BN && n < p.N) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float o[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float g = stg[j * kSt + q + 2 * t + h];
+              const float u = stg[j * kSt + 64 + q + 2 * t + h];
+              o[h] = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
+            }
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn(o[0], o[1]);
+            pk[t] = *reinterpret_cast<const uint32_t*>(&b2);
+          }
+          *reinterpret_cast<uint4*>(p.act + static_cast<int64_t>(n) * p.ld_act + f0 + q) =
+              make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
+  // Staged epilogue: 32 accumulator columns (= 32 output rows n) at a time go
+  // TMEM -> registers -> shared memory (transposed to [n][m]) -> 16-byte
+  // coalesced stores along m.  (Thread-per-m scalar stores issue 4x the store
+  // instructions and serialise on the per-SM store path.)
+  float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4], pipeline smem is idle now
+  constexpr int kSt = 128 + 4;
+#pragma unroll 1
+  for (int mt = 0; mt < MT; ++mt) {
+    const int mb = m0 + mt * 128;
+    const bool full_m = mb + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
+                        (p.resid == nullptr || (p.ldr & 3) == 0) &&
+                        (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * BN + c, r);
+      tmem_ld_wait();
+      const int ml = warp * 32 + lane;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
+      __syncthreads();
+      // 32 rows n x 128 m: 1024 float4, 8 per thread
+#pragma unroll 2
+      for (int e = threadIdx.x; e < 32 * 32; e += 128) {
+        const int j = e >> 5, q = (e & 31) * 4;
+        const int n = n0 + c + j;
+        if ((c + j) < BN && n < p.N) {
+          float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
+          const int m = mb + q;
+          if (full_m) {
+            if (p.bias != nullptr) {
+              const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
+              v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
+            }
+            if (p.resid != nullptr) {
+              const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
+              v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
+            }
+            *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
+          } else {
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              if (m + t < p.m_valid) {
+                float o = vv[t];
+                if (p.bias != nullptr) o += p.bias[m + t];
+                if (p.resid != nullptr) o += p.resid[static_cast<int64_t>(n) * p.ldr + m + t];
+                outp[static_cast<int64_t>(n) * p.ldo + m + t] = o;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 template <int BN, int MT>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW,
@@ -189,115 +299,282 @@ __global__ void __launch_bounds__(128, 1)
   griddep_wait();  // outputs may alias buffers the preceding kernel was reading
   mbar_wait(done, 0);
   tc_fence_after();
-  if (MT == 1 && p.epi == 1) {
-    // fused SiLU(gate) * up: TMEM lanes 0-63 hold gate, 64-127 up of features
-    // f = 64 * tile + (lane % 64).  32 accumulator columns (rows n) at a time are
-    // staged transposed in the idle pipeline smem, then each thread turns 8
-    // features of one row into 8 bf16 and writes them with one 16-byte store.
-    float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4]
-    constexpr int kSt = 128 + 4;
-    const int f0 = (m0 / 128) * 64;
+  gemm_epilogue<BN, MT>(p, smem, tmem, warp, lane, m0, n0, split);
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::kTmemCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decode-step GEMM ("mc" kernel: one n-tile, optional cluster multicast).
+//
+// One CTA covers ALL activation rows of the step (BN = the row bucket, a single
+// n-tile), so every weight byte is read from HBM exactly once; the 1-CTA kernel
+// above tiles the rows (BN <= 128) and re-reads each weight tile per n-tile.
+// One CTA per SM with a deep ring (~200 KB): measured per-CTA phase stamps
+// (VOX_GEMM_DBG, profiles/gemm_mc_phases_r01.txt) show the k-loop streaming
+// weights at ~6.2 TB/s aggregate; what remains is the first-load latency and
+// the epilogue.  Optional (VOX_GEMM_CS_TEST): a cluster of CS CTAs along M
+// shares each activation k-block -- CTA r loads rows [r*BN/CS, (r+1)*BN/CS)
+// and multicasts them into the same smem offset of every CTA, and each CTA's
+// MMA commit is multicast to every CTA's `empty` barrier (count CS).  It cuts
+// activation L2 reads by CS but measured slower (activation reads are not the
+// bound once the rows are a single n-tile).
+// ---------------------------------------------------------------------------
+// Direct epilogue of the multicast kernel (8 warps).  TMEM lane = weight row
+// m, so for one accumulator column (activation row n) the 32 lanes of a warp
+// hold 32 consecutive m: each column is one fully coalesced 128-byte warp
+// store straight from registers -- no smem staging, no block barriers.  Warps
+// w and w + 4 read the same TMEM lane quarter (w % 4) and split the 32-column
+// chunks between them.  The loop body is kept to a compare, a store and a
+// pointer bump: with one or two warps per SMSP the epilogue is bound by the
+// issue latency of its instruction chain (ncu: the first version spent ~37
+// instructions per store on 64-bit index math and per-element guards and took
+// longer than the whole k-loop).
+// epi == 1 (fused SiLU(gate) * up, gate|up rows interleaved per tile): gate
+// (lanes 0-63) and up (lanes 64-127) are parked in smem [n][64] fp32, then
+// each warp forms bf16(SiLU(g) * u) for whole rows: 32 threads x 2 features
+// = one 128-byte store per row.
+template <int BN>
+__device__ __forceinline__ void mc_epilogue(const GemmArgs& p, uint8_t* smem, uint32_t tmem,
+                                            int warp, int lane, int m0, int n0, int split) {
+  constexpr int kChunks = (BN + 31) / 32;
+  const int q = warp & 3, h = warp >> 2;
+  const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
+  const int nv = min(BN, p.N - n0);  // valid columns of this tile
+  if (p.epi == 1) {
+    float* sg = reinterpret_cast<float*>(smem);  // [BN][64] gate, then [BN][64] up
+    float* dst = sg + (q >= 2 ? BN * 64 : 0) + (q & 1) * 32 + lane;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int ch = h; ch < kChunks; ch += 2) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
+      tmem_ld_32x32b_x32(tbase + ch * 32, r);
       tmem_ld_wait();
-      const int ml = warp * 32 + lane;
+      float* d = dst + ch * 32 * 64;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
-      __syncthreads();
-#pragma unroll 2
-      for (int e = threadIdx.x; e < 32 * 8; e += 128) {
-        const int j = e >> 3, q = (e & 7) * 8;
-        const int n = n0 + c + j;
-        if ((c + j) < BN && n < p.N) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            float o[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const float g = stg[j * kSt + q + 2 * t + h];
-              const float u = stg[j * kSt + 64 + q + 2 * t + h];
-              o[h] = __fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), u);
-            }
-            const __nv_bfloat162 b2 = __floats2bfloat162_rn(o[0], o[1]);
-            pk[t] = *reinterpret_cast<const uint32_t*>(&b2);
-          }
-          *reinterpret_cast<uint4*>(p.act + static_cast<int64_t>(n) * p.ld_act + f0 + q) =
-              make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
-      }
-      __syncthreads();
+      for (int j = 0; j < 32; ++j) d[j * 64] = __uint_as_float(r[j]);
     }
-    tc_fence_before();
     __syncthreads();
-    if (warp == 2) {
-      tc_fence_after();
-      tmem_dealloc(tmem, C::kTmemCols);
+    const float* su = sg + BN * 64;
+    const int fp = lane * 2;
+    __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(p.act + static_cast<int64_t>(n0) * p.ld_act +
+                                                            (m0 / 128) * 64 + fp);
+    const int64_t step = p.ld_act / 2;  // in bf16x2 units
+#pragma unroll 4
+    for (int j = warp; j < nv; j += 8) {
+      const float2 g = *reinterpret_cast<const float2*>(&sg[j * 64 + fp]);
+      const float2 u = *reinterpret_cast<const float2*>(&su[j * 64 + fp]);
+      const float o0 = __fmul_rn(__fdiv_rn(g.x, __fadd_rn(1.0f, expf(-g.x))), u.x);
+      const float o1 = __fmul_rn(__fdiv_rn(g.y, __fadd_rn(1.0f, expf(-g.y))), u.y);
+      out[j * step] = __floats2bfloat162_rn(o0, o1);
     }
     return;
   }
-  float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
-  // Staged epilogue: 32 accumulator columns (= 32 output rows n) at a time go
-  // TMEM -> registers -> shared memory (transposed to [n][m]) -> 16-byte
-  // coalesced stores along m.  (Thread-per-m scalar stores issue 4x the store
-  // instructions and serialise on the per-SM store path.)
-  float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4], pipeline smem is idle now
-  constexpr int kSt = 128 + 4;
+  const int m = m0 + q * 32 + lane;
+  const bool mok = m < p.m_valid;
+  float* o = p.out + static_cast<int64_t>(split) * p.split_stride + static_cast<int64_t>(n0) * p.ldo + m;
+  const int64_t ldo = p.ldo;
+  if (p.bias == nullptr && p.resid == nullptr) {
 #pragma unroll 1
-  for (int mt = 0; mt < MT; ++mt) {
-    const int mb = m0 + mt * 128;
-    const bool full_m = mb + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
-                        (p.resid == nullptr || (p.ldr & 3) == 0) &&
-                        (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
-#pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int ch = h; ch < kChunks; ch += 2) {
       uint32_t r[32];
-      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * BN + c, r);
+      tmem_ld_32x32b_x32(tbase + ch * 32, r);
       tmem_ld_wait();
-      const int ml = warp * 32 + lane;
+      if (!mok) continue;
+      float* oc = o + ch * 32 * ldo;
+      const int lim = nv - ch * 32;
+      if (lim >= 32) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
-      __syncthreads();
-      // 32 rows n x 128 m: 1024 float4, 8 per thread
-#pragma unroll 2
-      for (int e = threadIdx.x; e < 32 * 32; e += 128) {
-        const int j = e >> 5, q = (e & 31) * 4;
-        const int n = n0 + c + j;
-        if ((c + j) < BN && n < p.N) {
-          float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
-          const int m = mb + q;
-          if (full_m) {
-            if (p.bias != nullptr) {
-              const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
-              v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
-            }
-            if (p.resid != nullptr) {
-              const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
-              v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
-            }
-            *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
-          } else {
-            const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int j = 0; j < 32; ++j) { *oc = __uint_as_float(r[j]); oc += ldo; }
+      } else {
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              if (m + t < p.m_valid) {
-                float o = vv[t];
-                if (p.bias != nullptr) o += p.bias[m + t];
-                if (p.resid != nullptr) o += p.resid[static_cast<int64_t>(n) * p.ldr + m + t];
-                outp[static_cast<int64_t>(n) * p.ldo + m + t] = o;
-              }
-            }
-          }
-        }
+        for (int j = 0; j < 32; ++j) { if (j < lim) *oc = __uint_as_float(r[j]); oc += ldo; }
       }
-      __syncthreads();
+    }
+    return;
+  }
+  const float b = (p.bias != nullptr && mok) ? p.bias[m] : 0.f;
+#pragma unroll 1
+  for (int ch = h; ch < kChunks; ch += 2) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(tbase + ch * 32, r);
+    tmem_ld_wait();
+    if (!mok) continue;
+#pragma unroll 4
+    for (int j = 0; j < 32; ++j) {
+      const int n = ch * 32 + j;
+      if (n < nv) {
+        float v = __uint_as_float(r[j]) + b;
+        if (p.resid != nullptr) v += p.resid[static_cast<int64_t>(n0 + n) * p.ldr + m];
+        o[n * ldo] = v;
+      }
+    }
+  }
+}
+
+static int gemm_mc_budget_kb() {
+  static int b = -1;
+  if (b < 0) {
+    const char* e = getenv("VOX_GEMM_MC_BUDGET_KB");
+    b = e ? atoi(e) : 150;  // measured on the serving step: 150 (3 x 48 KB stages at 256 rows) > 200 > 100
+    if (b < 32) b = 32;
+    if (b > 220) b = 220;
+  }
+  return b;
+}
+
+template <int BN>
+struct McCfg {
+  static constexpr int kABytes = 128 * 64 * 2;
+  static constexpr int kBBytes = BN * 64 * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  // ring depth from a smem budget (KB): ~200 = one CTA per SM, deep; ~100 lets
+  // the next kernel's CTA co-reside (PDL prologue overlap)
+  static int stages(int budget_kb) {
+    int n = budget_kb * 1024 / kStageBytes;
+    return n > 8 ? 8 : (n < 2 ? 2 : n);
+  }
+  // the fused-SiLU epilogue parks gate and up ([BN][64] fp32 each) in the ring
+  __host__ __device__ static int ring_bytes(int st, int epi) {
+    const int r = st * kStageBytes, e = epi == 1 ? 2 * BN * 64 * 4 : 0;
+    return r > e ? r : e;
+  }
+  static int smem_bytes(int st, int epi) { return ring_bytes(st, epi) + 1024 + 256; }
+  static constexpr int kSmemMax = 8 * kStageBytes + 1024 + 256 > 227 * 1024 ? 227 * 1024 : 8 * kStageBytes + 1024 + 256;
+};
+
+template <int BN, int CS>
+__global__ void __launch_bounds__(256, 1)
+    gemm_mc_kernel(const __grid_constant__ CUtensorMap tmXs, GemmArgs p) {
+  using C = McCfg<BN>;
+  const long long t_entry = clock64();
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+  constexpr int kSlice = BN / CS;  // activation rows this CTA multicasts (multiple of 8)
+  static_assert(kSlice % 8 == 0, "multicast slices must be whole 1024-B swizzle atoms");
+  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CS) - 1u);
+  const int nst = p.stages;  // ring depth (runtime: smem budget chosen by the host)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ring_bytes(nst, p.epi));
+  uint64_t* empty = full + nst;
+  uint64_t* done = empty + nst;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
+  const int m0 = blockIdx.y * 128;
+  const int n0 = blockIdx.x * BN;
+  const int split = blockIdx.z;
+  const int kb0 = split * p.kb_per_split;
+  const int kb1 = min(p.n_kb, kb0 + p.kb_per_split);
+  const int nkb = kb1 - kb0;  // host guarantees >= 1
+  // k-block order rotated per CLUSTER (its CTAs share every activation stage)
+  const int krot = p.k_rotate ? static_cast<int>(((blockIdx.y / CS) * 7u) % static_cast<unsigned>(nkb)) : 0;
+  auto kbi = [&](int i) { const int t = i + krot; return kb0 + (t >= nkb ? t - nkb : t); };
+  const bf16* wt = p.w_packed + static_cast<int64_t>(m0 / 128) * p.n_kb * 8192;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmXs);
+    for (int s = 0; s < nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CS);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
+  tc_fence_before();
+  if (CS > 1) cluster_sync(); else __syncthreads();  // peers' barriers exist before any multicast
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const long long t_setup = clock64();
+  long long t_first = 0, t_lastmma = 0;
+
+  griddep_launch();
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer: own weight tile + this CTA's activation slice ----------------
+    const uint64_t pol_w = policy_evict_first();
+    const uint64_t pol_x = policy_evict_last();
+    const int pre = nkb < nst ? nkb : nst;
+    for (int i = 0; i < pre; ++i) {  // weights do not depend on the preceding kernel
+      mbar_arrive_expect_tx(&full[i], C::kStageBytes);
+      bulk_load(smem + i * C::kStageBytes, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[i],
+                pol_w);
+    }
+    griddep_wait();
+    const int xoff = C::kABytes + rank * kSlice * 128;
+    for (int i = 0; i < pre; ++i) {
+      if (CS > 1)
+        tma_load_2d_mc(smem + i * C::kStageBytes + xoff, &tmXs, &full[i], kbi(i) * 64,
+                       n0 + rank * kSlice, kMask, pol_x);
+      else
+        tma_load_2d(smem + i * C::kStageBytes + xoff, &tmXs, &full[i], kbi(i) * 64, n0, pol_x);
+    }
+    for (int i = pre; i < nkb; ++i) {
+      const int s = i % nst;
+      mbar_wait(&empty[s], ((i / nst) - 1) & 1);  // all CS consumers retired stage s
+      uint8_t* st = smem + s * C::kStageBytes;
+      mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+      bulk_load(st, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[s], pol_w);
+      if (CS > 1)
+        tma_load_2d_mc(st + xoff, &tmXs, &full[s], kbi(i) * 64, n0 + rank * kSlice, kMask, pol_x);
+      else
+        tma_load_2d(st + xoff, &tmXs, &full[s], kbi(i) * 64, n0, pol_x);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % nst;
+      mbar_wait(&full[s], (i / nst) & 1);
+      if (i == 0) t_first = clock64();
+      tc_fence_after();
+      const uint32_t a_addr = smem_u32(smem + s * C::kStageBytes);
+      const uint32_t b_addr = a_addr + C::kABytes;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        umma_bf16(tmem, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + k * 32), idesc,
+                  (i > 0 || k > 0) ? 1u : 0u);
+      if (i == nkb - 1) t_lastmma = clock64();
+      if (CS > 1)
+        umma_commit_mc(&empty[s], kMask);  // stage s retired in this CTA: tell every producer
+      else
+        umma_commit(&empty[s]);
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+
+  griddep_wait();
+  mbar_wait(done, 0);
+  const long long t_done = clock64();
+  tc_fence_after();
+  mc_epilogue<BN>(p, smem, tmem, warp, lane, m0, n0, split);
+  if (p.dbg != nullptr) {
+    const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    unsigned long long* d = p.dbg + cta * 8;
+    if (threadIdx.x == 32) { d[2] = t_first - t_entry; d[3] = t_lastmma - t_entry; }
+    if (threadIdx.x == 0) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      d[0] = g_entry; d[1] = t_setup - t_entry; d[4] = t_done - t_entry; d[5] = clock64() - t_entry;
+      d[6] = gt;
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      d[7] = smid;
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  // no CTA leaves while a peer's commit may still arrive on its barriers
+  if (CS > 1) cluster_sync(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
@@ -523,6 +800,120 @@ static cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const
   return launch_k(gemm_bf16_tc_kernel<BN, MT>, grid, dim3(128), C::kSmemBytes, st, tw, tx, a);
 }
 
+template <int BN, int CS>
+static cudaError_t launch_mc(const CUtensorMap& txs, const GemmArgs& a, int splits, cudaStream_t st) {
+  using C = McCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_mc_kernel<BN, CS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  GemmArgs a2 = a;
+  a2.stages = C::stages(gemm_mc_budget_kb());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.N + BN - 1) / BN, (a.M + 127) / 128, splits);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = C::smem_bytes(a2.stages, a2.epi);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeClusterDimension;
+  at[1].val.clusterDim.x = 1;
+  at[1].val.clusterDim.y = CS;
+  at[1].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = CS > 1 ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, gemm_mc_kernel<BN, CS>, txs, a2);
+}
+
+template <int BN>
+static cudaError_t launch_mc_cs(const CUtensorMap& txs, const GemmArgs& a, int splits, int cs,
+                                cudaStream_t st) {
+  constexpr bool k8 = (BN / 8) % 8 == 0, k4 = (BN / 4) % 8 == 0, k2 = (BN / 2) % 8 == 0;
+  if (cs == 8) {
+    if constexpr (k8) return launch_mc<BN, 8>(txs, a, splits, st);
+  } else if (cs == 4) {
+    if constexpr (k4) return launch_mc<BN, 4>(txs, a, splits, st);
+  } else if (cs == 2) {
+    if constexpr (k2) return launch_mc<BN, 2>(txs, a, splits, st);
+  } else if (cs == 1) {
+    return launch_mc<BN, 1>(txs, a, splits, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+// CTAs of gemm_mc_kernel<BN, CS> that can be co-resident (whole clusters:
+// a cluster's CTAs must share one GPC, so clusters of 8 one-CTA-per-SM blocks
+// leave some SMs of each GPC idle).  Queried once per instantiation.
+template <int BN, int CS>
+static int mc_capacity_t() {
+  static int cap = 0;
+  if (cap == 0) {
+    using C = McCfg<BN>;
+    cudaFuncSetAttribute(gemm_mc_kernel<BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmemMax);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, CS * 64, 1);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = C::smem_bytes(C::stages(gemm_mc_budget_kb()), 0);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = CS;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, gemm_mc_kernel<BN, CS>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = kNumSMs / CS;
+    }
+    cap = n * CS;
+  }
+  return cap;
+}
+template <int BN>
+static int mc_capacity_bn(int cs) {
+  constexpr bool k8 = (BN / 8) % 8 == 0, k4 = (BN / 4) % 8 == 0, k2 = (BN / 2) % 8 == 0;
+  if constexpr (k8) if (cs == 8) return mc_capacity_t<BN, 8>();
+  if constexpr (k4) if (cs == 4) return mc_capacity_t<BN, 4>();
+  if constexpr (k2) if (cs == 2) return mc_capacity_t<BN, 2>();
+  return mc_capacity_t<BN, 1>();
+}
+int gemm_mc_capacity(int bn, int cs) {
+  switch (bn) {
+    case 16: return mc_capacity_bn<16>(cs);
+    case 32: return mc_capacity_bn<32>(cs);
+    case 64: return mc_capacity_bn<64>(cs);
+    case 128: return mc_capacity_bn<128>(cs);
+    case 192: return mc_capacity_bn<192>(cs);
+    case 224: return mc_capacity_bn<224>(cs);
+    default: return mc_capacity_bn<256>(cs);
+  }
+}
+
+// BN in {16, 32, 64, 128, 192, 224, 256}; txs = activation map with box rows BN / cs
+cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
+                           cudaStream_t st) {
+  if (a.w_packed == nullptr || (a.M + 127) / 128 % cs != 0) return cudaErrorInvalidValue;
+  a.n_kb = a.K / 64;
+  a.kb_per_split = (a.n_kb + splits - 1) / splits;
+  splits = (a.n_kb + a.kb_per_split - 1) / a.kb_per_split;
+  switch (bn) {
+    case 16: return launch_mc_cs<16>(txs, a, splits, cs, st);
+    case 32: return launch_mc_cs<32>(txs, a, splits, cs, st);
+    case 64: return launch_mc_cs<64>(txs, a, splits, cs, st);
+    case 128: return launch_mc_cs<128>(txs, a, splits, cs, st);
+    case 192: return launch_mc_cs<192>(txs, a, splits, cs, st);
+    case 224: return launch_mc_cs<224>(txs, a, splits, cs, st);
+    case 256: return launch_mc_cs<256>(txs, a, splits, cs, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int BNP, bool DEEP>
 static cudaError_t launch_pair(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a,
                                int splits, cudaStream_t st) {
@@ -602,10 +993,12 @@ int gemm_bn_for_rows(int rows) {
 // split-K to fill the machine: at decode sizes the GEMM streams weights, and
 // every SM must keep loads in flight (measured, profiles/gemm_sweep_r01.txt:
 // 256 x 256 tiles (MT = 2) leave SMs idle and lose 2x at 224 rows).
-GemmPlan gemm_plan(int M, int rows, int K) {
+GemmPlan gemm_plan_1cta(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
   g.pair = 0;
+  g.mc = 0;
+  g.cs = 1;
   g.bn = gemm_bn_for_rows(rows);
   if (g.bn > 128) g.bn = 128;
   if (rows >= 128 && M <= 4096) g.bn = 64;
@@ -641,6 +1034,52 @@ GemmPlan gemm_plan(int M, int rows, int K) {
   g.splits = best;
   if (const char* e = getenv("VOX_GEMM_SPLITS_TEST")) g.splits = atoi(e) < 1 ? 1 : atoi(e);
   return g;
+}
+
+GemmPlan gemm_plan(int M, int rows, int K) {
+  GemmPlan g{};
+  const int n_kb = K / 64;
+  g.pair = 0;
+  g.mc = 0;
+  g.cs = 1;
+  // Decode-sized row counts: the cluster-multicast kernel (one n-tile covering
+  // every row, activations multicast across CS CTAs along M, split-K to fill
+  // the co-resident CTA slots).  Callers fall back to the plan below when the
+  // weights are not in the packed layout.
+  const char* mce = getenv("VOX_GEMM_MC");
+  if (rows >= 64 && rows <= 256 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
+    int bn = 256;
+    for (int b : {16, 32, 64, 128, 192, 224, 256})
+      if (rows <= b) { bn = b; break; }
+    const int mtiles = (M + 127) / 128;
+    // Multicast is measured SLOWER than cs = 1 on every decode shape
+    // (profiles/gemm_mc_sweep_r01.txt): with one n-tile the activation L2
+    // reads are not the bound -- the k-loop already streams weights at HBM
+    // rate -- and clusters add co-scheduling constraints and couple each
+    // stage's release to the slowest CTA of the cluster.  Kept as an option.
+    int cs = 1;
+    if (const char* e = getenv("VOX_GEMM_CS_TEST")) {
+      const int f = atoi(e);
+      if ((f == 1 || f == 2 || f == 4 || f == 8) && mtiles % f == 0 && (bn / f) % 8 == 0) cs = f;
+    }
+    const int cap = gemm_mc_capacity(bn, cs);
+    int best = 1;
+    for (int s2 = 1; s2 <= kGemmMaxSplits; ++s2) {
+      const int per = (n_kb + s2 - 1) / s2;
+      if (per < 2) break;
+      if ((n_kb + per - 1) / per != s2) continue;  // every split non-empty
+      if (mtiles * s2 > cap) break;
+      best = s2;
+    }
+    g.mc = 1;
+    g.cs = cs;
+    g.bn = bn;
+    g.mt = 1;
+    g.splits = best;
+    if (const char* e = getenv("VOX_GEMM_SPLITS_TEST")) g.splits = atoi(e) < 1 ? 1 : atoi(e);
+    return g;
+  }
+  return gemm_plan_1cta(M, rows, K);
 }
 
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,

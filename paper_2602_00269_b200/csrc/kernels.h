@@ -51,6 +51,8 @@ struct GemmArgs {
   bf16* act;
   int64_t ld_act;
   const bf16* x_packed;   // non-null: activations in the packed tile layout (bulk copies)
+  int stages;             // mc kernel: smem ring depth (set by the launcher)
+  unsigned long long* dbg; // gemm_test only: per-CTA clock64 stamps (VOX_GEMM_DBG=1)
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };
@@ -64,14 +66,21 @@ struct GemmPlan {
   int bn;      // activation rows per tile (UMMA N)
   int mt;      // 128-row weight sub-tiles per CTA (1 or 2)
   int splits;  // split-K factor (fp32 partial planes)
+  int mc;      // 1: cluster-multicast kernel (one n-tile of bn >= rows, packed weights)
+  int cs;      // mc: CTAs per cluster along M sharing each activation k-block
 };
 GemmPlan gemm_plan(int M, int rows, int K);
+GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA / pair kernels only
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, int mt, cudaStream_t st);
 // pair kernel: tw_packed from make_tmap_packed, tx_half = activation map with box bnp / 2
 cudaError_t gemm_launch_pair(const CUtensorMap& tw_packed, const CUtensorMap& tx_half, GemmArgs a,
                              int splits, int bnp, cudaStream_t st);
 bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K);
+// cluster-multicast kernel: txs = activation map with box rows bn / cs
+cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
+                           cudaStream_t st);
+int gemm_mc_capacity(int bn, int cs);
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).

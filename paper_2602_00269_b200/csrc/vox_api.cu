@@ -193,6 +193,7 @@ struct VoxCtx {
   bool detok_unfused = getenv("VOX_DETOK_UNFUSED") != nullptr;  // A/B: two-kernel residual units
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
   const bf16* test_x_packed = nullptr;  // gemm_test only: packed activations
+  unsigned long long* test_dbg = nullptr;  // gemm_test only: per-CTA stamps
   bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;  // debug: eager decode steps
   int gemm_l2_prefetch = getenv("VOX_GEMM_L2PF") ? atoi(getenv("VOX_GEMM_L2PF")) : 0;  // measured slower (profiles/gemm_l2_prefetch_ab_r01.txt)
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
@@ -259,7 +260,8 @@ struct TimedLaunch {  // RAII event pair around a launch (eager + timing only)
 
 static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* base, int K,
                           int rows) {
-  for (int bn : {16, 32, 64, 128, 256}) {
+  // box rows: the 1-CTA tiles (16..256) and the multicast slices (bn / cs)
+  for (int bn : {8, 16, 24, 28, 32, 48, 56, 64, 96, 112, 128, 192, 224, 256}) {
     CUtensorMap t;
     if (!make_tmap_bf16(&t, base, K, rows, static_cast<uint64_t>(K) * 2, bn)) return false;
     m[bn] = t;
@@ -277,6 +279,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     const CUtensorMap* twp = nullptr, bf16* act_out = nullptr,
                     int64_t ld_act = 0) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
+  if (plan.mc && wp == nullptr) plan = gemm_plan_1cta(M, rows, K);  // mc streams packed tiles only
   if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
     plan.pair = 0;
     plan.bn = (rows >= 128 && M <= 4096) ? 64 : 128;
@@ -295,6 +298,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.m_valid = m_valid;
   a.w_packed = wp;
   a.x_packed = c->test_x_packed;
+  a.dbg = c->test_dbg;
   a.k_rotate = c->gemm_k_rotate;
   a.probe = c->gemm_probe;
   a.l2_prefetch = c->gemm_l2_prefetch;
@@ -306,8 +310,9 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
-  cudaError_t e = plan.pair ? gemm_launch_pair(*twp, xm.at(bn / 2), a, splits, bn, st)
-                            : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
+  cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn / plan.cs), a, splits, bn, plan.cs, st)
+                  : plan.pair ? gemm_launch_pair(*twp, xm.at(bn / 2), a, splits, bn, st)
+                              : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
 }
@@ -1602,6 +1607,13 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     CK(cudaStreamSynchronize(c->s_lm));
     if (!make_tmap_packed(&tpk, wpk, M, K)) return fail(c, VOX_ERR_CUDA, "tensor map (packed test)");
   }
+  unsigned long long* dbg = nullptr;
+  const size_t dbg_n = 8ull * 4096;
+  if (getenv("VOX_GEMM_DBG") && atoi(getenv("VOX_GEMM_DBG")) == 1) {
+    CK(cudaMalloc(&dbg, dbg_n * 8));
+    CK(cudaMemset(dbg, 0, dbg_n * 8));
+    c->test_dbg = dbg;
+  }
   cudaEvent_t a, b;
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
@@ -1619,6 +1631,32 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     if (it > 0 || iters == 1) total_ms += ms;
   }
   if (mean_ms) *mean_ms = total_ms / (iters > 1 ? iters - 1 : 1);
+  if (dbg) {  // per-CTA stamps of the last launch: mean deltas (cycles) + SM spread
+    std::vector<unsigned long long> h(dbg_n);
+    CK(cudaMemcpy(h.data(), dbg, dbg_n * 8, cudaMemcpyDeviceToHost));
+    double sum[6] = {0}, ghz = 0;
+    int n = 0;
+    unsigned long long gmin = ~0ull, gmax = 0, dmax = 0, g0 = ~0ull;
+    for (size_t i = 0; i < dbg_n / 8; ++i) {
+      if (h[i * 8 + 6] == 0) continue;
+      ++n;
+      for (int k = 1; k < 6; ++k) sum[k] += static_cast<double>(h[i * 8 + k]);
+      g0 = std::min(g0, h[i * 8]);
+      ghz += static_cast<double>(h[i * 8 + 5]) / static_cast<double>(h[i * 8 + 6] - h[i * 8]);
+      gmin = std::min(gmin, h[i * 8 + 6]);
+      gmax = std::max(gmax, h[i * 8 + 6]);
+      dmax = std::max(dmax, h[i * 8 + 5]);
+    }
+    if (n > 0)
+      fprintf(stderr,
+              "gemm dbg M=%d N=%d K=%d ctas=%d cyc: setup %.0f first_full %.0f last_mma %.0f "
+              "done %.0f end %.0f (max end %llu); end spread %.2f us; first entry -> last end "
+              "%.2f us; SM clock %.2f GHz\n",
+              M, N, K, n, sum[1] / n, sum[2] / n, sum[3] / n, sum[4] / n, sum[5] / n, dmax,
+              (gmax - gmin) * 1e-3, (gmax - g0) * 1e-3, ghz / n);
+    cudaFree(dbg);
+    c->test_dbg = nullptr;
+  }
   cudaFree(flush);
   cudaFree(sink);
   if (wpk) cudaFree(wpk);

@@ -1,0 +1,26 @@
+"""Per-CTA phase stamps of the cluster-multicast GEMM (VOX_GEMM_DBG=1). GPU only."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, '.')
+from paper_2602_00269_b200.config import tiny  # noqa: E402
+from paper_2602_00269_b200.device import VoxDevice  # noqa: E402
+
+os.environ["VOX_GEMM_PACKED_TEST"] = "1"
+os.environ["VOX_GEMM_DBG"] = "1"
+dev = VoxDevice(tiny(max_slots=2, detok_enabled=False), 1)
+rng = np.random.default_rng(0)
+for name, M, K, N, cs, s in [("gu", 16384, 3072, 224, 1, 1), ("gu", 16384, 3072, 224, 8, 1),
+                             ("gu", 16384, 3072, 16, 1, 1), ("qkv", 5120, 3072, 224, 1, 3),
+                             ("qkv", 5120, 3072, 224, 1, 1), ("down", 3072, 8192, 224, 1, 5),
+                             ("gu", 16384, 12288, 224, 1, 1), ("gu", 4096, 3072, 224, 1, 1),
+                             ("gu", 4096, 12288, 224, 1, 1), ("gu", 4096, 12288, 128, 1, 1),
+                             ("gu", 4096, 12288, 64, 1, 1)]:
+    os.environ["VOX_GEMM_CS_TEST"] = str(cs)
+    w = rng.integers(0, 65535, size=(M, K), dtype=np.uint16) & 0x3FFF
+    x = rng.integers(0, 65535, size=(N, K), dtype=np.uint16) & 0x3FFF
+    _, ms = dev.gemm_test(w, x, None, s, iters=4)
+    print(name, M, K, N, "cs", cs, "s", s, "%.1f us" % (ms * 1000), "%.0f GB/s" % (M * K * 2 / ms / 1e6),
+          "%.0f TF" % (2 * M * N * K / ms / 1e9), flush=True)

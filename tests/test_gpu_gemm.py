@@ -31,3 +31,22 @@ def test_gemm_matches_numpy(tiny_dev, monkeypatch, M, N, K, splits, packed):
         ref += bias
     err = np.abs(out - ref).max()
     assert err < 1e-3 * np.sqrt(K), (err, np.unravel_index(np.argmax(np.abs(out - ref)), out.shape))
+
+
+@pytest.mark.parametrize("M,N,K,splits", [
+    (1024, 224, 512, 1), (1024, 256, 1024, 3), (2048, 16, 256, 2), (512, 64, 768, 1),
+    (1024, 100, 256, 1), (1024, 192, 512, 2),
+])
+@pytest.mark.parametrize("cs", [1, 2, 4, 8])
+def test_gemm_cluster_multicast(tiny_dev, monkeypatch, M, N, K, splits, cs):
+    """Cluster-multicast kernel (gemm_mc_kernel): each CTA multicasts a slice of
+    the activation k-block to the CS CTAs of its cluster; every CTA covers all rows."""
+    monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
+    monkeypatch.setenv("VOX_GEMM_CS_TEST", str(cs))
+    rng = np.random.default_rng(M + N * 3 + cs)
+    w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
+    x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
+    out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), None, splits)
+    ref = x.astype(np.float64) @ w.astype(np.float64).T
+    err = np.abs(out - ref).max()
+    assert err < 1e-3 * np.sqrt(K), err
