@@ -175,6 +175,13 @@ int vox_timing_read(VoxCtx* ctx, const char* name, double* total_ms, int64_t* la
                     double* bytes);
 int vox_launch_count(VoxCtx* ctx, int64_t* launches); /* our kernels launched so far */
 
+/* in-graph kernel tracer (diagnostics): vox_trace_arm allocates room for
+ * `capacity` records and arms every instrumented kernel; vox_trace_read
+ * synchronizes, copies up to `max_records` records {u32 tag, u32 smid,
+ * u64 t_start_ns, u64 t_end_ns} (one per CTA, %globaltimer) and disarms. */
+int vox_trace_arm(VoxCtx* ctx, int64_t capacity);
+int vox_trace_read(VoxCtx* ctx, void* records, int64_t max_records, int64_t* n_records);
+
 /* K3 alone (parity tests / roofline): out[n, m] = sum_k W[m, k] X[n, k] (+bias[m])
  * with W [M, K], X [N, K] bf16 (raw uint16 bits), fp32 out [N, M]; K % 64 == 0.
  * splits > 1 returns the split-K partial sum reduced on the host side of the

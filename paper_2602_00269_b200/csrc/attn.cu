@@ -30,6 +30,8 @@
 #include <cstdlib>
 
 namespace vox {
+VOX_TRACE_TU(trace_set_attn)
+
 
 constexpr int kAttnStages = 3;
 constexpr int kAttnPagesPerStage = 4;  // one page per warp
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
                        float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched) {
+  VOX_TRACE(kTrAttn);
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
   constexpr int NT = HD / 8;   // PV n-tiles
@@ -384,6 +387,7 @@ template <int HD, int G>
 __global__ void __launch_bounds__(128)
     attn_combine_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, LmDims dm,
                         int n_split, bf16* __restrict__ out) {
+  VOX_TRACE(kTrAttnCombine);
   griddep_wait();
   griddep_launch();
   const int r = blockIdx.x, kvh = blockIdx.y;

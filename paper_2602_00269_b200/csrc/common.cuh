@@ -307,4 +307,57 @@ VOX_DEV bool elect_one() {
   return pred != 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// In-graph kernel tracer (diagnostics, vox_trace_*): when a trace buffer is
+// armed, thread 0 of every CTA of an instrumented kernel appends
+// {tag, smid, globaltimer at CTA start, at CTA end}.  buf[0] is the record
+// counter, records start at buf[2].  One pointer per translation unit
+// (no relocatable device code); off = one predicated global load per CTA.
+// ---------------------------------------------------------------------------
+struct TraceRec {
+  uint32_t tag, smid;
+  unsigned long long t0, t1;
+};
+#define VOX_TRACE_TU(setter)                                                              \
+  static __device__ unsigned long long* g_vox_trace = nullptr;                            \
+  void setter(unsigned long long* buf) {                                                  \
+    cudaMemcpyToSymbol(g_vox_trace, &buf, sizeof(buf));                                    \
+  }
+VOX_DEV unsigned long long vox_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct TraceScope {
+  unsigned long long* buf;
+  unsigned long long t0;
+  uint32_t tag;
+  // tag | (CTAs in the grid << 8): separates back-to-back launches of one kernel
+  __device__ __forceinline__ TraceScope(unsigned long long* b, uint32_t tg)
+      : buf(b), t0(0), tag(tg | ((gridDim.x * gridDim.y * gridDim.z) << 8)) {
+    if (buf != nullptr && threadIdx.x == 0) t0 = vox_now();
+  }
+  __device__ __forceinline__ ~TraceScope() {
+    if (buf != nullptr && threadIdx.x == 0) {
+      const unsigned long long t1 = vox_now();
+      const unsigned long long i = atomicAdd(buf, 1ull);
+      if (i < buf[1]) {
+        uint32_t sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        TraceRec* r = reinterpret_cast<TraceRec*>(buf + 2) + i;
+        r->tag = tag;
+        r->smid = sm;
+        r->t0 = t0;
+        r->t1 = t1;
+      }
+    }
+  }
+};
+#define VOX_TRACE(tag) TraceScope vox_trace_scope_(g_vox_trace, (tag))
+enum TraceTag : uint32_t {
+  kTrGemm = 1, kTrGemmMc = 2, kTrAttn = 3, kTrAttnCombine = 4, kTrQkvRope = 5, kTrResidNorm = 6,
+  kTrEmbedNorm = 7, kTrSilu = 8, kTrSampler = 9, kTrDetok = 10, kTrPair = 11
+};
+
 }  // namespace vox

@@ -25,6 +25,8 @@
 #include "kernels.h"
 
 namespace vox {
+VOX_TRACE_TU(trace_set_detok_fused)
+
 
 namespace {
 
@@ -94,6 +96,7 @@ __global__ void __launch_bounds__(ru_threads<C>())
                     const float* __restrict__ dw_b, const float* __restrict__ alpha2,
                     const bf16* __restrict__ pw_w, const float* __restrict__ pw_b,
                     float* __restrict__ state, int64_t st_off, DetokDims dd) {
+  VOX_TRACE(kTrDetok);
   using L = RuSmem<C>;
   constexpr int kRuThreads = ru_threads<C>();
   extern __shared__ uint8_t smem_raw[];
@@ -295,6 +298,7 @@ __global__ void __launch_bounds__(kOutRows)
                            const float* __restrict__ x, const float* __restrict__ alpha,
                            const float* __restrict__ w, float b, float* __restrict__ state,
                            int64_t st_off, DetokDims dd, float* __restrict__ pcm) {
+  VOX_TRACE(kTrDetok);
   __shared__ float s[(kOutRows + 6) * (C + 1)];
   __shared__ float ws[C * 7];
   const int tid = threadIdx.x;
@@ -366,6 +370,7 @@ __global__ void __launch_bounds__(256)
                              const float* __restrict__ x, int C, const float* __restrict__ alpha,
                              float* __restrict__ state, int64_t st_off, DetokDims dd,
                              bf16* __restrict__ out) {
+  VOX_TRACE(kTrDetok);
   const int tid = threadIdx.x;
   float a[CPT], inv[CPT];
 #pragma unroll
@@ -426,6 +431,7 @@ __global__ void __launch_bounds__(256)
                          const float* __restrict__ dw_b, const float* __restrict__ alpha2,
                          float* __restrict__ state, int64_t st_off, DetokDims dd,
                          bf16* __restrict__ out) {
+  VOX_TRACE(kTrDetok);
   extern __shared__ float y1s[];  // [TR + 6 dil][kPrepCh]
   const int tid = threadIdx.x;
   const int cl = tid % kPrepCh;                 // channel within the tile

@@ -14,6 +14,8 @@
 #include "kernels.h"
 
 namespace vox {
+VOX_TRACE_TU(trace_set_detok)
+
 
 struct ReqHdr {  // first bytes of the uploaded detok staging block
   int32_t n_req, n_lat;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(256)
                      const int* __restrict__ token_store, const bf16* __restrict__ tabs,
                      const float* __restrict__ dw_w, const float* __restrict__ dw_b,
                      float* __restrict__ state, DetokDims dd, bf16* __restrict__ out) {
+  VOX_TRACE(kTrDetok);
   griddep_wait();
   griddep_launch();
   const int row = blockIdx.x;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(256)
                        const float* __restrict__ x, int C, const float* __restrict__ alpha,
                        float* __restrict__ state, int64_t st_off, DetokDims dd,
                        bf16* __restrict__ out) {
+  VOX_TRACE(kTrDetok);
   griddep_wait();
   griddep_launch();
   const int row = blockIdx.x;
@@ -148,6 +152,7 @@ __global__ void __launch_bounds__(128)
                    const float* __restrict__ dw_w, const float* __restrict__ dw_b,
                    const float* __restrict__ alpha2, float* __restrict__ state, int64_t st_off,
                    DetokDims dd, bf16* __restrict__ out) {
+  VOX_TRACE(kTrDetok);
   griddep_wait();
   griddep_launch();
   const int row = blockIdx.x;
@@ -192,6 +197,7 @@ __global__ void __launch_bounds__(256)
                      const float* __restrict__ x, int C, const float* __restrict__ alpha,
                      const float* __restrict__ w, float b, float* __restrict__ state,
                      int64_t st_off, DetokDims dd, float* __restrict__ pcm) {
+  VOX_TRACE(kTrDetok);
   griddep_wait();
   griddep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -17,6 +17,8 @@
 #include <cstdlib>
 
 namespace vox {
+VOX_TRACE_TU(trace_set_gemm)
+
 
 template <int BN, int MT>
 struct GemmCfg {
@@ -150,6 +152,7 @@ template <int BN, int MT>
 __global__ void __launch_bounds__(128, 1)
     gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmW,
                         const __grid_constant__ CUtensorMap tmX, GemmArgs p) {
+  VOX_TRACE(kTrGemm);
   using C = GemmCfg<BN, MT>;
   extern __shared__ uint8_t smem_raw[];
   // align to 1024 B by pointer arithmetic on the __shared__ array (an
@@ -451,6 +454,7 @@ struct McCfg {
 template <int BN, int CS>
 __global__ void __launch_bounds__(256, 1)
     gemm_mc_kernel(const __grid_constant__ CUtensorMap tmXs, GemmArgs p) {
+  VOX_TRACE(kTrGemmMc);
   using C = McCfg<BN>;
   const long long t_entry = clock64();
   unsigned long long g_entry;
@@ -612,6 +616,7 @@ template <int BNP, bool DEEP>
 __global__ void __launch_bounds__(128, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                      GemmArgs p) {
+  VOX_TRACE(kTrPair);
   using C = PairCfg<BNP, DEEP>;
   extern __shared__ uint8_t smem_raw[];
   // align to 1024 B by pointer arithmetic on the __shared__ array (an
@@ -889,13 +894,15 @@ int gemm_mc_capacity(int bn, int cs) {
     case 32: return mc_capacity_bn<32>(cs);
     case 64: return mc_capacity_bn<64>(cs);
     case 128: return mc_capacity_bn<128>(cs);
+    case 96: return mc_capacity_bn<96>(cs);
+    case 160: return mc_capacity_bn<160>(cs);
     case 192: return mc_capacity_bn<192>(cs);
     case 224: return mc_capacity_bn<224>(cs);
     default: return mc_capacity_bn<256>(cs);
   }
 }
 
-// BN in {16, 32, 64, 128, 192, 224, 256}; txs = activation map with box rows BN / cs
+// BN in {16, 32, 64, 96, 128, 160, 192, 224, 256}; txs = activation map with box rows BN / cs
 cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
                            cudaStream_t st) {
   if (a.w_packed == nullptr || (a.M + 127) / 128 % cs != 0) return cudaErrorInvalidValue;
@@ -907,6 +914,8 @@ cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int b
     case 32: return launch_mc_cs<32>(txs, a, splits, cs, st);
     case 64: return launch_mc_cs<64>(txs, a, splits, cs, st);
     case 128: return launch_mc_cs<128>(txs, a, splits, cs, st);
+    case 96: return launch_mc_cs<96>(txs, a, splits, cs, st);
+    case 160: return launch_mc_cs<160>(txs, a, splits, cs, st);
     case 192: return launch_mc_cs<192>(txs, a, splits, cs, st);
     case 224: return launch_mc_cs<224>(txs, a, splits, cs, st);
     case 256: return launch_mc_cs<256>(txs, a, splits, cs, st);
@@ -1049,7 +1058,7 @@ GemmPlan gemm_plan(int M, int rows, int K) {
   const char* mce = getenv("VOX_GEMM_MC");
   if (rows >= 64 && rows <= 256 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
     int bn = 256;
-    for (int b : {16, 32, 64, 128, 192, 224, 256})
+    for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
       if (rows <= b) { bn = b; break; }
     const int mtiles = (M + 127) / 128;
     // Multicast is measured SLOWER than cs = 1 on every decode shape

@@ -20,6 +20,8 @@
 #include "kernels.h"
 
 namespace vox {
+VOX_TRACE_TU(trace_set_lm)
+
 
 VOX_DEV float block_sum256(float v, float* red) {
   v = warp_sum(v);
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restric
                                                          const float* __restrict__ nw, int d,
                                                          float eps, float* __restrict__ h,
                                                          bf16* __restrict__ x) {
+  VOX_TRACE(kTrEmbedNorm);
   griddep_wait();
   griddep_launch();
   __shared__ float red[9];
@@ -120,6 +123,7 @@ __global__ void __launch_bounds__(256)
                            int splits, int64_t split_stride, LmDims dm,
                            const float2* __restrict__ rope, const int* __restrict__ page_table,
                            bf16* __restrict__ kc, bf16* __restrict__ vc, bf16* __restrict__ q_out) {
+  VOX_TRACE(kTrQkvRope);
   griddep_wait();
   griddep_launch();
   const int r = blockIdx.x;
@@ -192,6 +196,7 @@ __global__ void __launch_bounds__(256)
                       int64_t split_stride, int d, float eps, float* __restrict__ h,
                       const float* __restrict__ nw, bf16* __restrict__ x_out,
                       const int* __restrict__ out_index) {
+  VOX_TRACE(kTrResidNorm);
   griddep_wait();
   griddep_launch();
   __shared__ float red[9];
@@ -237,6 +242,7 @@ VOX_DEV float silu_mul1(float g, float u) {
 __global__ void __launch_bounds__(256)
     silu_mul_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, int splits,
                     int64_t split_stride, int dff, bf16* __restrict__ a_out) {
+  VOX_TRACE(kTrSilu);
   griddep_wait();
   griddep_launch();
   const int r = blockIdx.x;

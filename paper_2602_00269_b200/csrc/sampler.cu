@@ -24,6 +24,8 @@
 #include "kernels.h"
 
 namespace vox {
+VOX_TRACE_TU(trace_set_sampler)
+
 
 constexpr int kST = 512;      // threads per row
 constexpr int kBins = 2048;   // radix histogram bins (11 bits)
@@ -664,6 +666,7 @@ __global__ void __launch_bounds__(kST)
     sample_desc_kernel(const float* __restrict__ logits, const SampRowDesc* __restrict__ rows,
                        const int* __restrict__ window_ids, int* __restrict__ out,
                        int* __restrict__ err_flag) {
+  VOX_TRACE(kTrSampler);
   griddep_wait();
   griddep_launch();
   extern __shared__ uint32_t dyn_bm[];
@@ -675,6 +678,7 @@ __global__ void __launch_bounds__(kST)
 }
 
 __global__ void __launch_bounds__(kST) sample_fused_kernel(SampFusedArgs a) {
+  VOX_TRACE(kTrSampler);
   griddep_wait();
   griddep_launch();
   extern __shared__ uint32_t dyn_bm[];

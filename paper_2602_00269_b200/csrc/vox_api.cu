@@ -51,7 +51,10 @@ enum TensorId : uint64_t {
   T_OUT_B = 172,
 };
 
-constexpr int kBuckets[] = {16, 32, 64, 128, 256, 512, 1024, 2048};
+// decode-step row buckets (one CUDA graph each): steps of 32 rows between 64
+// and 256 so a step pays at most 31 padding rows of tensor work -- at ~224 rows
+// the projections are at the tensor/HBM ridge
+constexpr int kBuckets[] = {16, 32, 64, 96, 128, 160, 192, 224, 256, 512, 1024, 2048};
 constexpr int kTicketRing = 32;  // in-flight detok calls (VOX_TICKET_RING in voxb200.h)
 
 struct TimingRec {
@@ -194,6 +197,8 @@ struct VoxCtx {
   int gemm_k_rotate = getenv("VOX_GEMM_KROT") ? atoi(getenv("VOX_GEMM_KROT")) : 1;
   const bf16* test_x_packed = nullptr;  // gemm_test only: packed activations
   unsigned long long* test_dbg = nullptr;  // gemm_test only: per-CTA stamps
+  unsigned long long* trace_buf = nullptr;  // vox_trace_*: [count, cap, records...]
+  int64_t trace_cap = 0;
   bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;  // debug: eager decode steps
   int gemm_l2_prefetch = getenv("VOX_GEMM_L2PF") ? atoi(getenv("VOX_GEMM_L2PF")) : 0;  // measured slower (profiles/gemm_l2_prefetch_ab_r01.txt)
   int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
@@ -261,7 +266,7 @@ struct TimedLaunch {  // RAII event pair around a launch (eager + timing only)
 static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* base, int K,
                           int rows) {
   // box rows: the 1-CTA tiles (16..256) and the multicast slices (bn / cs)
-  for (int bn : {8, 16, 24, 28, 32, 48, 56, 64, 96, 112, 128, 192, 224, 256}) {
+  for (int bn : {8, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128, 160, 192, 224, 256}) {
     CUtensorMap t;
     if (!make_tmap_bf16(&t, base, K, rows, static_cast<uint64_t>(K) * 2, bn)) return false;
     m[bn] = t;
@@ -1542,6 +1547,52 @@ int vox_timing_read(VoxCtx* c, const char* name, double* total_ms, int64_t* laun
   if (total_ms) *total_ms = ms;
   if (launches) *launches = cnt;
   if (bytes) *bytes = by;
+  return VOX_OK;
+}
+
+}  // extern "C" (trace setters below are C++ symbols of the kernel TUs)
+namespace vox {
+void trace_set_attn(unsigned long long*);
+void trace_set_detok_fused(unsigned long long*);
+void trace_set_detok(unsigned long long*);
+void trace_set_gemm(unsigned long long*);
+void trace_set_lm(unsigned long long*);
+void trace_set_sampler(unsigned long long*);
+}  // namespace vox
+static void trace_set_all(unsigned long long* b) {
+  vox::trace_set_attn(b);
+  vox::trace_set_detok_fused(b);
+  vox::trace_set_detok(b);
+  vox::trace_set_gemm(b);
+  vox::trace_set_lm(b);
+  vox::trace_set_sampler(b);
+}
+extern "C" {
+
+int vox_trace_arm(VoxCtx* c, int64_t capacity) {
+  if (!c || capacity < 1) return fail(c, VOX_ERR_INVALID, "bad trace arguments");
+  CK(cudaDeviceSynchronize());
+  if (c->trace_buf) cudaFree(c->trace_buf);
+  c->trace_cap = capacity;
+  CK(cudaMalloc(&c->trace_buf, (2 + 3 * capacity) * 8));
+  unsigned long long hdr[2] = {0ull, static_cast<unsigned long long>(capacity)};
+  CK(cudaMemcpy(c->trace_buf, hdr, 16, cudaMemcpyHostToDevice));
+  trace_set_all(c->trace_buf);
+  return VOX_OK;
+}
+
+int vox_trace_read(VoxCtx* c, void* records, int64_t max_records, int64_t* n_records) {
+  if (!c || !records || !n_records) return fail(c, VOX_ERR_INVALID, "null argument");
+  if (!c->trace_buf) return fail(c, VOX_ERR_INVALID, "trace not armed");
+  CK(cudaDeviceSynchronize());
+  trace_set_all(nullptr);
+  unsigned long long n = 0;
+  CK(cudaMemcpy(&n, c->trace_buf, 8, cudaMemcpyDeviceToHost));
+  n = std::min<unsigned long long>(n, static_cast<unsigned long long>(std::min(max_records, c->trace_cap)));
+  CK(cudaMemcpy(records, c->trace_buf + 2, n * 24, cudaMemcpyDeviceToHost));
+  *n_records = static_cast<int64_t>(n);
+  cudaFree(c->trace_buf);
+  c->trace_buf = nullptr;
   return VOX_OK;
 }
 

@@ -220,6 +220,18 @@ class VoxDevice:
         self._check(self.lib.vox_timing_read(self.ctx, cls.encode(), C.byref(ms), C.byref(n), C.byref(by)))
         return ms.value, n.value, by.value
 
+    def trace_arm(self, capacity: int = 1 << 20) -> None:
+        """Arm the in-graph kernel tracer (one record per CTA of every instrumented kernel)."""
+        self._check(self.lib.vox_trace_arm(self.ctx, capacity))
+
+    def trace_read(self, max_records: int = 1 << 20) -> np.ndarray:
+        """Records {tag (kernel | grid CTAs << 8), smid, t0_ns, t1_ns}; disarms the tracer."""
+        dt = np.dtype([("tag", np.uint32), ("smid", np.uint32), ("t0", np.uint64), ("t1", np.uint64)])
+        out = np.zeros(max_records, dt)
+        n = C.c_int64()
+        self._check(self.lib.vox_trace_read(self.ctx, out.ctypes.data_as(C.c_void_p), max_records, C.byref(n)))
+        return out[: n.value]
+
     def launch_count(self) -> int:
         n = C.c_int64()
         self._check(self.lib.vox_launch_count(self.ctx, C.byref(n)))
