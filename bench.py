@@ -199,18 +199,41 @@ def steady_state_steps(dev, B: int, steps: int, warmup: int, prompt: int, seed: 
     dec0, chunks0, pcm0 = st0.decode_rows, len(eng.trace.chunks), st0.pcm_samples
     rows0, dcalls0, wait0 = st0.lm_rows, st0.detok_calls, st0.wait_s
     launches0 = dev.launch_count()
+    import gc
+
+    gc.collect()  # before the first event: a full collection takes tens of ms
+    gc.freeze()
+    gc.disable()  # as StreamingEngine.run: no cyclic-GC stalls of the host loop while timed
     ev0.record(s_lm)
     s_dt.wait_event(ev0)
     t0 = time.perf_counter()
-    for _ in range(steps):
+    trace_from = 0 if (os.environ.get("VOX_BENCH_TRACE") and steps >= 8) else steps + 1
+    it_ms = []
+    for i_step in range(steps):
+        if i_step == trace_from:
+            dev.trace_arm(1 << 23)
+        t_it = time.perf_counter()
         one_iter()
+        it_ms.append((time.perf_counter() - t_it) * 1e3)
+        if i_step == 0:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(s_lm)
     ev_lm.record(s_lm)
     ev_dt.record(s_dt)
     torch.cuda.synchronize()
+    if os.environ.get("VOX_BENCH_TRACE"):
+        a = np.array(it_ms)
+        print(f"ev0->ev1 (first iteration) {ev0.elapsed_time(ev1):.2f} ms; host iteration ms: first {a[0]:.2f} "
+              f"median {np.median(a):.2f} max {a.max():.2f} top5 {np.sort(a)[-5:].round(2).tolist()} "
+              f"sum {a.sum():.1f}", file=sys.stderr)
     while eng._tickets:
         eng._poll(block=True)
     t_wall = time.perf_counter() - t0
+    gc.unfreeze()
+    gc.enable()
     dev_ms = max(ev0.elapsed_time(ev_lm), ev0.elapsed_time(ev_dt))
+    if trace_from < steps:
+        _trace_summary(dev.trace_read(1 << 23))
     st = eng.stats
     decoded = st.decode_rows - dec0
     chunks = len(eng.trace.chunks) - chunks0
@@ -236,6 +259,51 @@ def steady_state_steps(dev, B: int, steps: int, warmup: int, prompt: int, seed: 
     out["lm_graph_rows"] = len(live)
     eng.shutdown()
     return out
+
+
+def _trace_summary(rec):
+    """Diagnostics (VOX_BENCH_TRACE=1): LM vs detok kernel activity over the traced steps."""
+    rec = np.sort(rec, order="t0")
+    t0 = int(rec["t0"].min())
+    det = rec[(rec["tag"] & 255) == 10]
+    lm = rec[(rec["tag"] & 255) != 10]
+    span = (int(rec["t1"].max()) - t0) / 1e3
+
+    def busy(r):  # union of CTA intervals
+        iv = sorted(zip(r["t0"].astype(np.int64), r["t1"].astype(np.int64)))
+        tot, cs, ce = 0, None, None
+        for a, b in iv:
+            if cs is None or a > ce:
+                if cs is not None:
+                    tot += ce - cs
+                cs, ce = a, b
+            else:
+                ce = max(ce, b)
+        return (tot + (ce - cs if cs is not None else 0)) / 1e3
+
+    print(f"trace: span {span:.1f} us; LM busy {busy(lm):.1f} us; detok busy {busy(det):.1f} us; "
+          f"detok CTAs {len(det)}, first {(int(det['t0'].min()) - t0) / 1e3 if len(det) else -1:.1f} us, "
+          f"last end {(int(det['t1'].max()) - t0) / 1e3 if len(det) else -1:.1f} us; "
+          f"LM last end {(int(lm['t1'].max()) - t0) / 1e3:.1f} us", file=sys.stderr)
+    # per-step detok windows relative to the LM step boundaries (sampler CTAs end a step)
+    # LM-stream idle gaps (no LM CTA running): host not keeping up
+    iv = sorted(zip(lm["t0"].astype(np.int64), lm["t1"].astype(np.int64)))
+    gaps, ce = [], iv[0][1]
+    for a, b in iv[1:]:
+        if a > ce:
+            gaps.append(a - ce)
+        ce = max(ce, b)
+    gaps = np.array(gaps) / 1e3
+    print(f"trace: LM idle gaps: n={len(gaps)} total {gaps.sum():.1f} us, >50us: {int((gaps > 50).sum())}, "
+          f"largest {np.sort(gaps)[-5:].round(1).tolist() if len(gaps) else []}", file=sys.stderr)
+    samp = np.sort(lm[(lm["tag"] & 255) == 9]["t1"].astype(np.int64))
+    print("trace: sampler ends (us):", [round((int(x) - t0) / 1e3, 1) for x in samp[:: max(1, len(samp) // 8)]],
+          file=sys.stderr)
+    if len(det):
+        dd = np.sort(det["t0"].astype(np.int64))
+        gaps = np.where(np.diff(dd) > 100000)[0]
+        starts = [dd[0]] + [dd[g + 1] for g in gaps]
+        print("trace: detok burst starts (us):", [round((int(x) - t0) / 1e3, 1) for x in starts], file=sys.stderr)
 
 
 def args_batch_decode(B: int) -> int:
