@@ -290,6 +290,22 @@ VOX_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// Distributed shared memory: address of the same smem offset in CTA `rank`
+// of this cluster, and a 16-byte load from it.
+VOX_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+VOX_DEV float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
 // Programmatic dependent launch: wait for the preceding grid's completion
 // (and memory flush) / allow the next grid to start its prologue.
 VOX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

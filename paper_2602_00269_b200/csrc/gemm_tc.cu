@@ -560,7 +560,49 @@ __global__ void __launch_bounds__(256, 1)
   mbar_wait(done, 0);
   const long long t_done = clock64();
   tc_fence_after();
-  mc_epilogue<BN>(p, smem, tmem, warp, lane, m0, n0, split);
+  if (p.red) {
+    // Split-K reduced inside the cluster (cluster = the S splits of this tile):
+    // each CTA parks its fp32 partial tile in its own smem ([n][128 m], the
+    // ring is idle), then CTA r sums columns n = r, r + S, ... over all S
+    // partials through distributed shared memory in fixed order s = 0..S-1
+    // (deterministic) and writes ONE output plane -- the S fp32 planes never
+    // touch L2/HBM and the consumer kernel reads one plane instead of S.
+    constexpr int kChunks = (BN + 31) / 32;
+    float* part = reinterpret_cast<float*>(smem);
+    {
+      const int q = warp & 3, h = warp >> 2;
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+      for (int ch = h; ch < kChunks; ch += 2) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + ch * 32, r);
+        tmem_ld_wait();
+        float* d = part + ch * 32 * 128 + q * 32 + lane;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) d[j * 128] = __uint_as_float(r[j]);
+      }
+    }
+    cluster_sync();  // every partial tile complete and visible cluster-wide
+    const int S = static_cast<int>(gridDim.z);
+    const int nv = min(BN, p.N - n0);
+    const int mq = (threadIdx.x & 31) * 4;
+    const bool mok = m0 + mq + 3 < p.m_valid;
+    const uint32_t base = smem_u32(part);
+    float* outp = p.out + static_cast<int64_t>(n0) * p.ldo + m0 + mq;
+#pragma unroll 1
+    for (int n = split + S * (threadIdx.x >> 5); n < nv; n += S * 8) {
+      const uint32_t off = base + static_cast<uint32_t>((n * 128 + mq) * 4);
+      float4 acc = ld_dsmem_f4(mapa_shared(off, 0));
+      for (int s2 = 1; s2 < S; ++s2) {
+        const float4 v = ld_dsmem_f4(mapa_shared(off, static_cast<uint32_t>(s2)));
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      if (mok) *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo) = acc;
+    }
+    cluster_sync();  // peers are done reading this CTA's partial tile
+  } else {
+    mc_epilogue<BN>(p, smem, tmem, warp, lane, m0, n0, split);
+  }
   if (p.dbg != nullptr) {
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     unsigned long long* d = p.dbg + cta * 8;
@@ -828,9 +870,9 @@ static cudaError_t launch_mc(const CUtensorMap& txs, const GemmArgs& a, int spli
   at[1].id = cudaLaunchAttributeClusterDimension;
   at[1].val.clusterDim.x = 1;
   at[1].val.clusterDim.y = CS;
-  at[1].val.clusterDim.z = 1;
+  at[1].val.clusterDim.z = a2.red ? splits : 1;
   cfg.attrs = at;
-  cfg.numAttrs = CS > 1 ? 2 : 1;
+  cfg.numAttrs = (CS > 1 || a2.red) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, gemm_mc_kernel<BN, CS>, txs, a2);
 }
 
@@ -854,21 +896,22 @@ static cudaError_t launch_mc_cs(const CUtensorMap& txs, const GemmArgs& a, int s
 // a cluster's CTAs must share one GPC, so clusters of 8 one-CTA-per-SM blocks
 // leave some SMs of each GPC idle).  Queried once per instantiation.
 template <int BN, int CS>
-static int mc_capacity_t() {
-  static int cap = 0;
+static int mc_capacity_t(int cz = 1) {
+  static int caps[9] = {0};
+  int& cap = caps[cz < 1 ? 1 : (cz > 8 ? 8 : cz)];
   if (cap == 0) {
     using C = McCfg<BN>;
     cudaFuncSetAttribute(gemm_mc_kernel<BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          C::kSmemMax);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1, CS * 64, 1);
+    cfg.gridDim = dim3(1, CS * 64, cz);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = C::smem_bytes(C::stages(gemm_mc_budget_kb()), 0);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 1;
     at[0].val.clusterDim.y = CS;
-    at[0].val.clusterDim.z = 1;
+    at[0].val.clusterDim.z = cz;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
@@ -876,29 +919,29 @@ static int mc_capacity_t() {
       cudaGetLastError();
       n = kNumSMs / CS;
     }
-    cap = n * CS;
+    cap = n * CS * cz;
   }
   return cap;
 }
 template <int BN>
-static int mc_capacity_bn(int cs) {
+static int mc_capacity_bn(int cs, int cz) {
   constexpr bool k8 = (BN / 8) % 8 == 0, k4 = (BN / 4) % 8 == 0, k2 = (BN / 2) % 8 == 0;
   if constexpr (k8) if (cs == 8) return mc_capacity_t<BN, 8>();
   if constexpr (k4) if (cs == 4) return mc_capacity_t<BN, 4>();
   if constexpr (k2) if (cs == 2) return mc_capacity_t<BN, 2>();
-  return mc_capacity_t<BN, 1>();
+  return mc_capacity_t<BN, 1>(cz);
 }
-int gemm_mc_capacity(int bn, int cs) {
+int gemm_mc_capacity(int bn, int cs, int cz) {
   switch (bn) {
-    case 16: return mc_capacity_bn<16>(cs);
-    case 32: return mc_capacity_bn<32>(cs);
-    case 64: return mc_capacity_bn<64>(cs);
-    case 128: return mc_capacity_bn<128>(cs);
-    case 96: return mc_capacity_bn<96>(cs);
-    case 160: return mc_capacity_bn<160>(cs);
-    case 192: return mc_capacity_bn<192>(cs);
-    case 224: return mc_capacity_bn<224>(cs);
-    default: return mc_capacity_bn<256>(cs);
+    case 16: return mc_capacity_bn<16>(cs, cz);
+    case 32: return mc_capacity_bn<32>(cs, cz);
+    case 64: return mc_capacity_bn<64>(cs, cz);
+    case 96: return mc_capacity_bn<96>(cs, cz);
+    case 128: return mc_capacity_bn<128>(cs, cz);
+    case 160: return mc_capacity_bn<160>(cs, cz);
+    case 192: return mc_capacity_bn<192>(cs, cz);
+    case 224: return mc_capacity_bn<224>(cs, cz);
+    default: return mc_capacity_bn<256>(cs, cz);
   }
 }
 
@@ -1005,6 +1048,7 @@ int gemm_bn_for_rows(int rows) {
 GemmPlan gemm_plan_1cta(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
+  g.red = 0;
   g.pair = 0;
   g.mc = 0;
   g.cs = 1;
@@ -1071,7 +1115,7 @@ GemmPlan gemm_plan(int M, int rows, int K) {
       const int f = atoi(e);
       if ((f == 1 || f == 2 || f == 4 || f == 8) && mtiles % f == 0 && (bn / f) % 8 == 0) cs = f;
     }
-    const int cap = gemm_mc_capacity(bn, cs);
+    const int cap = gemm_mc_capacity(bn, cs, 1);
     int best = 1;
     for (int s2 = 1; s2 <= kGemmMaxSplits; ++s2) {
       const int per = (n_kb + s2 - 1) / s2;
@@ -1086,6 +1130,18 @@ GemmPlan gemm_plan(int M, int rows, int K) {
     g.mt = 1;
     g.splits = best;
     if (const char* e = getenv("VOX_GEMM_SPLITS_TEST")) g.splits = atoi(e) < 1 ? 1 : atoi(e);
+    // split-K reduced in a (1, 1, splits) cluster through DSMEM: needs <= 8
+    // splits, the fp32 tile in the ring, and whole clusters co-resident
+    // Opt-in (VOX_GEMM_RED=1): measured slower on the serving step than fp32
+    // partial planes through L2 (profiles/gemm_mc_ab_r01.txt) -- the cluster
+    // co-scheduling and the DSMEM round trip cost more than the L2 traffic.
+    const char* re = getenv("VOX_GEMM_RED");
+    g.red = 0;
+    if (g.splits > 1 && g.splits <= 8 && cs == 1 && re && atoi(re) == 1 &&
+        bn * 128 * 4 <= 144 * 1024) {
+      const int capz = gemm_mc_capacity(bn, 1, g.splits);
+      if (mtiles * g.splits <= capz) g.red = 1;
+    }
     return g;
   }
   return gemm_plan_1cta(M, rows, K);

@@ -52,6 +52,7 @@ struct GemmArgs {
   int64_t ld_act;
   const bf16* x_packed;   // non-null: activations in the packed tile layout (bulk copies)
   int stages;             // mc kernel: smem ring depth (set by the launcher)
+  int red;                // mc kernel: splits reduced in a (1,1,splits) cluster -> one plane
   unsigned long long* dbg; // gemm_test only: per-CTA clock64 stamps (VOX_GEMM_DBG=1)
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
@@ -68,7 +69,10 @@ struct GemmPlan {
   int splits;  // split-K factor (fp32 partial planes)
   int mc;      // 1: cluster-multicast kernel (one n-tile of bn >= rows, packed weights)
   int cs;      // mc: CTAs per cluster along M sharing each activation k-block
+  int red;     // mc: split-K reduced through DSMEM inside the cluster (one output plane)
 };
+// fp32 output planes a GEMM with this plan leaves for its consumer
+inline int gemm_out_planes(const GemmPlan& g) { return g.red ? 1 : g.splits; }
 GemmPlan gemm_plan(int M, int rows, int K);
 GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA / pair kernels only
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
@@ -80,7 +84,7 @@ bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K);
 // cluster-multicast kernel: txs = activation map with box rows bn / cs
 cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
                            cudaStream_t st);
-int gemm_mc_capacity(int bn, int cs);
+int gemm_mc_capacity(int bn, int cs, int cz);
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).

@@ -282,7 +282,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm", const bf16* wp = nullptr,
                     const CUtensorMap* twp = nullptr, bf16* act_out = nullptr,
-                    int64_t ld_act = 0) {
+                    int64_t ld_act = 0, int* planes_out = nullptr) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
   if (plan.mc && wp == nullptr) plan = gemm_plan_1cta(M, rows, K);  // mc streams packed tiles only
   if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
@@ -308,6 +308,9 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.probe = c->gemm_probe;
   a.l2_prefetch = c->gemm_l2_prefetch;
   a.epi = act_out != nullptr ? 1 : 0;
+  a.red = (plan.mc && plan.red && splits == plan.splits && a.epi == 0 && bias == nullptr &&
+           resid == nullptr) ? 1 : 0;
+  if (planes_out) *planes_out = a.red ? 1 : splits;
   a.act = act_out;
   a.ld_act = ld_act;
   if (a.epi == 1 && (splits != 1 || plan.pair || plan.mt != 1))
@@ -668,11 +671,15 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     launch_embed_norm(c->d_rows, nrows, c->token_store, g.max_ctx, c->emb, c->norm_attn, dm, c->h,
                       c->x, st);
   }
-  const int sp_qkv = gemm_plan(c->nqkv, nrows, d).splits;
-  const int sp_o = gemm_plan(d, nrows, Hhd).splits;
+  const GemmPlan qkv_plan = gemm_plan(c->nqkv, nrows, d), o_plan = gemm_plan(d, nrows, Hhd);
+  const GemmPlan dn_plan = gemm_plan(d, nrows, dff);
+  const int sp_qkv = qkv_plan.splits, sp_o = o_plan.splits;
+  // fp32 planes the consumers reduce (1 when the GEMM reduced its splits in-cluster)
+  const int pl_qkv = gemm_out_planes(qkv_plan), pl_o = gemm_out_planes(o_plan);
+  const int pl_dn = gemm_out_planes(dn_plan);
   const GemmPlan gu_plan = gemm_plan(2 * dff, nrows, d);
   const int sp_gu = gu_plan.splits;
-  const int sp_dn = gemm_plan(d, nrows, dff).splits;
+  const int sp_dn = dn_plan.splits;
   const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
   const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
   const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
@@ -681,8 +688,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
                  nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv, &c->tp_qkv[l]));
     {
-      TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * sp_qkv);
-      launch_qkv_rope_append(c->d_rows, nrows, c->ws, sp_qkv,
+      TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * pl_qkv);
+      launch_qkv_rope_append(c->d_rows, nrows, c->ws, pl_qkv,
                              static_cast<int64_t>(nrows) * c->nqkv, dm, c->rope_tab,
                              c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
     }
@@ -695,8 +702,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st, "gemm", c->w_o + l * n_o, &c->tp_o[l]));
     {
-      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_o + 10));
-      launch_resid_norm(c->d_rows, nrows, c->ws, sp_o, static_cast<int64_t>(nrows) * d, dm, c->h,
+      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_o + 10));
+      launch_resid_norm(c->d_rows, nrows, c->ws, pl_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
     if (sp_gu == 1 && !gu_plan.pair && !c->silu_unfused) {  // SiLU(gate) * up in the epilogue
@@ -705,16 +712,17 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
     } else {
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
                    nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
-      TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
-      launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
+      const int pl_gu = gemm_out_planes(gu_plan);
+      TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * pl_gu + 2));
+      launch_silu_mul(c->d_rows, nrows, c->ws, pl_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
                  d, st, "gemm", c->w_down + l * n_dn, &c->tp_down[l]));
     {
       const bool last = (l == L - 1);
-      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * sp_dn + 10));
-      launch_resid_norm(c->d_rows, nrows, c->ws, sp_dn, static_cast<int64_t>(nrows) * d, dm, c->h,
+      TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_dn + 10));
+      launch_resid_norm(c->d_rows, nrows, c->ws, pl_dn, static_cast<int64_t>(nrows) * d, dm, c->h,
                         last ? c->norm_final : c->norm_attn + static_cast<int64_t>(l + 1) * d,
                         last ? c->xf : c->x, last ? c->d_out_index : nullptr, st);
     }
@@ -1669,12 +1677,13 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   int rc = VOX_OK;
+  int planes = splits;
   double total_ms = 0.0;
   for (int it = 0; it < iters && rc == VOX_OK; ++it) {
     launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
     CK(cudaEventRecord(a, c->s_lm));
     rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm, "gemm", wpk, wpk ? &tpk : nullptr);
+                  c->s_lm, "gemm", wpk, wpk ? &tpk : nullptr, nullptr, 0, &planes);
     CK(cudaEventRecord(b, c->s_lm));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;
@@ -1718,7 +1727,7 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     CK(cudaMemcpy(tmp.data(), dout, tmp.size() * 4, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < static_cast<size_t>(N) * M; ++i) {
       float s = 0.f;
-      for (int k = 0; k < splits; ++k) s += tmp[k * static_cast<size_t>(N) * M + i];
+      for (int k = 0; k < planes; ++k) s += tmp[k * static_cast<size_t>(N) * M + i];
       out[i] = s;
     }
   }

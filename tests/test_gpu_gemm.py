@@ -50,3 +50,18 @@ def test_gemm_cluster_multicast(tiny_dev, monkeypatch, M, N, K, splits, cs):
     ref = x.astype(np.float64) @ w.astype(np.float64).T
     err = np.abs(out - ref).max()
     assert err < 1e-3 * np.sqrt(K), err
+
+
+@pytest.mark.parametrize("M,N,K", [(3072, 224, 3072), (1024, 256, 2048), (5120, 64, 1024), (640, 100, 512)])
+@pytest.mark.parametrize("splits", [2, 3, 5, 8])
+def test_gemm_split_k_cluster_reduction(tiny_dev, monkeypatch, M, N, K, splits):
+    """Split-K reduced inside a (1,1,splits) cluster through DSMEM (one output plane)."""
+    monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
+    monkeypatch.setenv("VOX_GEMM_SPLITS_TEST", str(splits))
+    rng = np.random.default_rng(M + N + splits)
+    w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
+    x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
+    out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), None, splits)
+    ref = x.astype(np.float64) @ w.astype(np.float64).T
+    err = np.abs(out - ref).max()
+    assert err < 1e-3 * np.sqrt(K), err
