@@ -76,6 +76,8 @@ typedef struct VoxModelCfg {
   int32_t latent_dim, decoder_dim, n_rates;
   int32_t rates[4];
   int32_t max_detok_frames; /* max latent frames per detok call (all requests) */
+  /* Qwen2-style bias on the fused q|k|v projection (CosyVoice2's LM); 0 = Llama */
+  int32_t qkv_bias;
 } VoxModelCfg;
 
 /* Per-request sampling parameters (SamplingParams, model_api.py:105-121). */

@@ -3,11 +3,13 @@
 The reference's LM forward is a hash stub (profiles.py:318-331), so this
 backbone follows the public Llama architecture ([3P] transformers 5.5.0
 models/llama/modeling_llama.py: LlamaRMSNorm :53, rotate_half RoPE :73,
-LlamaMLP :171, LlamaAttention :225 with GQA) and mirrors the GPU rounding
-points exactly: bf16 weights, fp32 residual stream, bf16 GEMM inputs
-(normalised x, attention output, SiLU*up), fp32 accumulation, fp32 logits.
-Parity status: UNPINNED by the reference (no LM arithmetic there); pinned
-by tests/golden/tiny_greedy.npz generated from this module.
+LlamaMLP :171, LlamaAttention :225 with GQA) -- and, with cfg.qkv_bias, its
+Qwen2 variant (q/k/v projections with bias: [3P] models/qwen2/modeling_qwen2.py
+Qwen2Attention) -- and mirrors the GPU rounding points exactly: bf16 weights,
+fp32 residual stream, bf16 GEMM inputs (normalised x, attention output,
+SiLU*up), fp32 accumulation, fp32 logits.
+Parity status: UNPINNED by the reference (no LM arithmetic there); checked
+against the device path by tests/test_gpu_lm.py and tests/test_gpu_cosy.py.
 """
 
 from __future__ import annotations
@@ -69,6 +71,8 @@ class LlamaOracle:
         scale = f32(1.0) / np.sqrt(f32(hd))
         for l, L in enumerate(w.layers):
             qkv = x @ L["qkv"].T
+            if "qkv_bias" in L:  # Qwen2 q|k|v bias, added after the projection (lm_kernels.cu)
+                qkv = qkv + L["qkv_bias"]
             q = qkv[:, : H * hd].reshape(n, H, hd)
             k = qkv[:, H * hd: (H + KV) * hd].reshape(n, KV, hd)
             v = qkv[:, (H + KV) * hd:].reshape(n, KV, hd)

@@ -14,7 +14,7 @@ GOLDEN = 0x9E3779B97F4A7C15
 
 # tensor ids (csrc/vox_api.cu: TensorId)
 T_EMB, T_NORM_ATTN, T_NORM_MLP, T_NORM_FINAL = 1, 2, 3, 4
-T_QKV, T_O, T_GU, T_DOWN = 5, 6, 7, 8
+T_QKV, T_O, T_GU, T_DOWN, T_QKV_BIAS = 5, 6, 7, 8, 9
 T_VQ_TAB, T_IN_DW_W, T_IN_DW_B, T_IN_PW_W, T_IN_PW_B = 20, 21, 22, 23, 24
 T_UP_ALPHA, T_UP_W, T_UP_B = 30, 34, 38
 T_RU_A1, T_RU_DW_W, T_RU_DW_B, T_RU_A2, T_RU_PW_W, T_RU_PW_B = 50, 70, 90, 110, 130, 150
@@ -95,6 +95,8 @@ class BackboneWeights:
             L["o"] = init_bf16(d * H * hd, k(T_O, l), np.sqrt(f32(3.0) / f32(H * hd))).reshape(d, H * hd)
             L["gu"] = init_bf16(2 * dff * d, k(T_GU, l), np.sqrt(f32(3.0) / f32(d))).reshape(2 * dff, d)
             L["down"] = init_bf16(d * dff, k(T_DOWN, l), np.sqrt(f32(3.0) / f32(dff))).reshape(d, dff)
+            if getattr(cfg, "qkv_bias", False):  # Qwen2-style (vox_api.cu: T_QKV_BIAS)
+                L["qkv_bias"] = init_f32(nqkv, k(T_QKV_BIAS, l), 0.5, 0.0)
             self.layers.append(L)
         self.norm_final = init_f32(d, k(T_NORM_FINAL), 0.25, 1.0)
         self.inv_freq = np.array(

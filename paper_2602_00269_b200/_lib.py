@@ -36,6 +36,7 @@ class VoxModelCfg(C.Structure):
         ("latent_dim", C.c_int32), ("decoder_dim", C.c_int32), ("n_rates", C.c_int32),
         ("rates", C.c_int32 * 4),
         ("max_detok_frames", C.c_int32),
+        ("qkv_bias", C.c_int32),
     ]
 
 

@@ -48,6 +48,7 @@ class ModelConfig:
     rates: tuple = (8, 8, 4, 2)
     max_detok_frames: int = 256
     embed_scale: float = 0.0  # 0 -> logit std ~2.5 (see embed_half_width)
+    qkv_bias: bool = False    # Qwen2-style q|k|v bias (CosyVoice2's LM)
 
     @property
     def embed_half_width(self) -> float:
@@ -112,4 +113,31 @@ def orpheus3b(**kw) -> ModelConfig:
     return replace(base, **kw)
 
 
-CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b}
+# CosyVoice2's LM is Qwen2.5-0.5B ([3P] Qwen2.5-0.5B config: hidden 896, 24 layers,
+# 14 q / 2 kv heads of 64, FFN 4864, rope theta 1e6, rms eps 1e-6, tied embeddings,
+# q|k|v bias).  Token layout: 151,936 Qwen ids, then the 6,561 + 3 speech tokens
+# (FSQ codes + sos/eos/task, CosyVoice2 llm_decoder width); speech positions may
+# only emit speech ids (the same range mask as Orpheus's frame slots, one slot).
+COSY_TEXT_VOCAB = 151643
+COSY_SPEECH_BASE = 151936
+COSY_SPEECH_TOKENS = 6564
+
+
+def cosyvoice2(**kw) -> ModelConfig:
+    """Config 4 (LM): CosyVoice2-style Qwen2.5-0.5B backbone over speech tokens."""
+    base = ModelConfig(
+        name="cosyvoice2-0.5b", n_layers=24, d_model=896, n_heads=14, n_kv_heads=2, head_dim=64,
+        d_ff=4864, vocab=COSY_SPEECH_BASE + COSY_SPEECH_TOKENS, rope_theta=1e6, rms_eps=1e-6,
+        text_vocab=COSY_TEXT_VOCAB, audio_base=COSY_SPEECH_BASE, codebook_size=COSY_SPEECH_TOKENS,
+        frame_tokens=1, qkv_bias=True, detok_enabled=False, max_slots=256, max_ctx=1024, max_rows=1024,
+    )
+    return replace(base, **kw)
+
+
+def tiny_cosy(**kw) -> ModelConfig:
+    """CPU-oracle-sized CosyVoice2-style LM: 2 layers, same head geometry (G = 7, hd 64) + bias."""
+    return cosyvoice2(**{"name": "tiny-cosyvoice2", "n_layers": 2, "d_model": 448, "d_ff": 1024,
+                         "max_slots": 16, "max_ctx": 512, "max_rows": 512, **kw})
+
+
+CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy}

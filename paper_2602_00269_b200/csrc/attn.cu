@@ -438,7 +438,17 @@ static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16
     case 2: attn_launch<HD, 2>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
     case 3: attn_launch<HD, 3>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
     case 4: attn_launch<HD, 4>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
-    default: break;  // rejected at vox_create
+    default:
+      if constexpr (HD == 64) {  // wider GQA groups (Qwen2.5-0.5B: 14 q / 2 kv heads)
+        switch (dm.n_heads / dm.n_kv) {
+          case 5: attn_launch<HD, 5>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 6: attn_launch<HD, 6>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 7: attn_launch<HD, 7>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 8: attn_launch<HD, 8>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          default: break;  // rejected at vox_create
+        }
+      }
+      break;
   }
 }
 

@@ -118,7 +118,7 @@ struct LmDims {
 
 void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x, cudaStream_t st);
-void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int splits,
+void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const float* bias, int splits,
                             int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st);

@@ -120,7 +120,7 @@ void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx,
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256)
     qkv_rope_append_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws,
-                           int splits, int64_t split_stride, LmDims dm,
+                           const float* __restrict__ bias, int splits, int64_t split_stride, LmDims dm,
                            const float2* __restrict__ rope, const int* __restrict__ page_table,
                            bf16* __restrict__ kc, bf16* __restrict__ vc, bf16* __restrict__ q_out) {
   VOX_TRACE(kTrQkvRope);
@@ -145,8 +145,12 @@ __global__ void __launch_bounds__(256)
   for (int it = threadIdx.x + 256 * blockIdx.y; it < n_items; it += cta_stride) {
     const int head = it / q4, i = (it % q4) * 4;
     const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
-    const float4 a = sum_splits4(w4, splits, ss4, c1);
-    const float4 b = sum_splits4(w4, splits, ss4, c2);
+    float4 a = sum_splits4(w4, splits, ss4, c1);
+    float4 b = sum_splits4(w4, splits, ss4, c2);
+    if (bias != nullptr) {  // Qwen2-style q|k|v bias, added after the split-K sum
+      a = add4(a, reinterpret_cast<const float4*>(bias)[c1]);
+      b = add4(b, reinterpret_cast<const float4*>(bias)[c2]);
+    }
     const float x1[4] = {a.x, a.y, a.z, a.w}, x2[4] = {b.x, b.y, b.z, b.w};
     float o1[4], o2[4];
 #pragma unroll
@@ -170,7 +174,8 @@ __global__ void __launch_bounds__(256)
   // V head-pages are stored TRANSPOSED ([hd][page_size]) so the attention PV
   // mma reads 4 consecutive tokens of one dim as a single 8-byte load
   for (int e = threadIdx.x + 256 * blockIdx.y; e < dm.n_kv * hd4; e += cta_stride) {
-    const float4 v = sum_splits4(w4, splits, ss4, vbase4 + e);
+    float4 v = sum_splits4(w4, splits, ss4, vbase4 + e);
+    if (bias != nullptr) v = add4(v, reinterpret_cast<const float4*>(bias)[vbase4 + e]);
     const int kvh = e / hd4, dd = (e % hd4) * 4;
     bf16* vt = vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * hd + dd) * dm.page_size + off;
     vt[0] = __float2bfloat16_rn(v.x);
@@ -180,11 +185,11 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, int splits,
+void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const float* bias, int splits,
                             int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
-  launch_k(qkv_rope_append_kernel, dim3(n, 2), dim3(256), 0, st, rows, ws, splits, split_stride, dm,
+  launch_k(qkv_rope_append_kernel, dim3(n, 2), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
            rope, page_table, kc, vc, q_out);
 }
 

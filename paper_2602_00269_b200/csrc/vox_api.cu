@@ -31,6 +31,7 @@ enum TensorId : uint64_t {
   T_O = 6,
   T_GU = 7,
   T_DOWN = 8,
+  T_QKV_BIAS = 9,
   // detokenizer
   T_VQ_TAB = 20,
   T_IN_DW_W = 21,
@@ -122,6 +123,7 @@ struct VoxCtx {
   // ---- backbone weights
   bf16* emb = nullptr;
   float *norm_attn = nullptr, *norm_mlp = nullptr, *norm_final = nullptr;
+  float* b_qkv = nullptr;  // [L][nqkv] fp32 when cfg.qkv_bias (Qwen2-style)
   bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
   float* inv_freq = nullptr;
   float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
@@ -384,6 +386,11 @@ static int create_backbone(VoxCtx* c) {
     RET(packed(c->w_head_audio, rows, d, g.audio_base, T_EMB, 0, g.embed_scale));
   }
   RET(init_f32(c, c->norm_final, d, T_NORM_FINAL, 0, 0.25f, 1.0f));
+  if (g.qkv_bias) {
+    CK(dalloc(&c->b_qkv, static_cast<size_t>(L) * c->nqkv));
+    for (int l = 0; l < L; ++l)
+      RET(init_f32(c, c->b_qkv + static_cast<int64_t>(l) * c->nqkv, c->nqkv, T_QKV_BIAS, l, 0.5f, 0.0f));
+  }
   // RoPE inverse frequencies, fp64 -> fp32 (oracle: identical table)
   std::vector<float> inv(hd / 2);
   for (int i = 0; i < hd / 2; ++i)
@@ -689,7 +696,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
                  nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv, &c->tp_qkv[l]));
     {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * pl_qkv);
-      launch_qkv_rope_append(c->d_rows, nrows, c->ws, pl_qkv,
+      launch_qkv_rope_append(c->d_rows, nrows, c->ws,
+                             c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr, pl_qkv,
                              static_cast<int64_t>(nrows) * c->nqkv, dm, c->rope_tab,
                              c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
     }
@@ -785,7 +793,8 @@ static int validate_cfg(const VoxModelCfg* g) {
   if (!(g->head_dim == 64 || g->head_dim == 128)) return 0;
   if (g->n_heads % g->n_kv_heads) return 0;
   const int grp = g->n_heads / g->n_kv_heads;
-  if (grp < 1 || grp > 4) return 0;
+  // GQA group: the q slot of the attention ring holds G * hd bf16 <= 1 KB
+  if (grp < 1 || grp > 8 || grp * g->head_dim > 512) return 0;
   if ((g->n_heads * g->head_dim) % 64) return 0;
   // 8-token chunks; the attention smem ring holds 6 x 2 head-pages (<= 192 KB)
   // the attention kernel's mma tiling is built for 16-token pages
@@ -874,7 +883,8 @@ void vox_destroy(VoxCtx* c) {
                       c->slot_prompt, c->slot_seed, c->slot_params, c->d_rows, c->attn_sched, c->d_sample_rows,
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
-                      c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w};
+                      c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
+                      c->trace_buf};
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (c->cfg.detok_enabled && c->dw.tabs) {
@@ -1767,6 +1777,9 @@ int vox_read_weight(VoxCtx* c, const char* name, int32_t layer, void* out, size_
       o[i] = pk[static_cast<size_t>(t * 8192 + r * 64 + ch * 8 + k % 8)];
     }
     return VOX_OK;
+  } else if (n == "qkv_bias" && c->b_qkv) {
+    src = c->b_qkv + static_cast<int64_t>(layer) * c->nqkv;
+    avail = static_cast<size_t>(c->nqkv) * 4;
   } else if (n == "norm_attn") {
     src = c->norm_attn + static_cast<int64_t>(layer) * d;
     avail = d * 4;

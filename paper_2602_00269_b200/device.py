@@ -57,6 +57,7 @@ class VoxDevice:
         for i, r in enumerate(cfg.rates):
             c.rates[i] = r
         c.max_detok_frames = cfg.max_detok_frames
+        c.qkv_bias = int(cfg.qkv_bias)
         self._c = c
         h = C.c_void_p()
         _lib.check(self.lib.vox_create(device, C.byref(c), C.c_uint64(weight_seed & (2**64 - 1)), C.byref(h)))
