@@ -418,6 +418,63 @@ def run_slo(dev, rates, seconds: float, seed: int, prompt: int, ws: int = 1, ran
     return (max(ok) if ok else 0.0), out
 
 
+def cosy_lm_steps(batch: int, ctx: int, steps: int, seed: int, hbm: float, device: int):
+    """BASELINE config 4's LM (CosyVoice2-style Qwen2.5-0.5B backbone) alone: graph-captured
+    decode steps with sampling (cosy_like params: T .8, top-k 50, top-p .95, rp 1.1) over
+    `batch` streams at context `ctx`; speech tokens/s, ms/step, HBM roofline of the step
+    (weights + KV read), and the LM floor of time-to-first-chunk per chunk size
+    (prefill + chunk decode steps; the token-to-mel/vocoder detokenizer is not built)."""
+    import torch
+
+    from paper_2602_00269_b200.config import cosyvoice2
+    from paper_2602_00269_b200.device import Sampling, VoxDevice
+
+    cfg = cosyvoice2(max_slots=batch + 8, max_ctx=ctx + steps + 64)
+    dev = VoxDevice(cfg, weight_seed=seed, device=device)
+    prm = Sampling(temperature=0.8, top_p=0.95, top_k=50, repetition_penalty=1.1)
+    slots = [dev.admit(seed * 7919 + i, 50, ctx + steps, prm) for i in range(batch)]
+    # KV fill: prompt prefill, then (ctx - 50) sampled decode steps so contexts are real
+    for a in range(0, batch, 16):  # <= max_rows per forward
+        dev.forward(np.array([[s, p, -1, 0] for s in slots[a:a + 16] for p in range(49)], np.int32),
+                    sample=False)
+    t0 = time.perf_counter()
+    dev.forward(np.array([[slots[0], 0, -1, 0]], np.int32), sample=False, sync=True)
+    for k in range(ctx - 50):
+        dev.forward(np.array([[s, 49 + k, -1, 1] for s in slots], np.int32))
+    dev.synchronize()
+    lm_s, _ = dev.streams()
+    st = torch.cuda.ExternalStream(lm_s)
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    pos0 = ctx - 1
+    for k in range(3):  # warm
+        dev.forward(np.array([[s, pos0 + k, -1, 1] for s in slots], np.int32))
+    dev.synchronize()
+    ea.record(st)
+    for k in range(steps):
+        dev.forward(np.array([[s, pos0 + 3 + k, -1, 1] for s in slots], np.int32))
+    eb.record(st)
+    torch.cuda.synchronize()
+    ms = ea.elapsed_time(eb) / steps
+    mean_ctx = pos0 + 3 + steps / 2
+    by = cfg.weight_bytes - 2 * cfg.vocab * cfg.d_model + 2 * cfg.codebook_size * cfg.d_model  # serving head
+    by += batch * mean_ctx * cfg.kv_bytes_per_token
+    # prefill time of one 50-token prompt (graph-less, as the engine runs prefill)
+    s_new = dev.admit(seed + 99991, 50, 16, prm)
+    t1 = time.perf_counter()
+    dev.forward(np.array([[s_new, p, -1, 0] for p in range(49)], np.int32), sample=False, sync=True)
+    pre_ms = (time.perf_counter() - t1) * 1e3
+    dev.close()
+    return {"model": "cosyvoice2-style LM (Qwen2.5-0.5B geometry, q|k|v bias, GQA 14:2, hd 64) random-init",
+            "batch": batch, "ctx": ctx, "ms_per_step": round(ms, 4),
+            "speech_tokens_per_s": round(batch / (ms / 1e3), 1),
+            "audio_s_per_s_lm_only": round(batch / (ms / 1e3) / 25.0, 1),
+            "roofline": {"bound": "hbm", "achieved": round(by / (ms / 1e3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(by / (ms / 1e3) / 1e9 / hbm, 4), "bytes_per_step": int(by)},
+            "lm_first_chunk_floor_ms": {str(c): round(pre_ms + c * ms, 2) for c in (5, 10, 15, 25, 50)},
+            "prefill_ms_50_tokens": round(pre_ms, 3), "kv_fill_s": round(time.perf_counter() - t0, 2),
+            "detokenizer": "not built (token-to-mel flow matching + HiFT are SURVEY §8f next rows)"}
+
+
 def cpu_port_sample(seconds_budget: float = 20.0):
     """Oracle port of the same step on host cores (bounded sample); returns audio-s/s."""
     from oracle.cpu_step import time_cpu_step
@@ -441,6 +498,7 @@ def main():
     ap.add_argument("--slo-startup-limit", type=int, default=16, help="scheduler startup concurrency")
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cosy", action="store_true", help="skip the config-4 (CosyVoice2-style LM) line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -511,6 +569,13 @@ def main():
                "duration_s": args.slo_seconds, "routing": "reference route_dp (seeded uniform), replicas",
                "sweep": sweep}
 
+    cosy = None
+    if not args.no_cosy and rank == 0:
+        try:
+            cosy = cosy_lm_steps(128, 512, 32, args.seed + 5, hbm, local)
+        except Exception as e:  # report, never mask the headline
+            cosy = {"error": repr(e)[:200]}
+
     cpu = None
     if not args.no_cpu and rank == 0:
         from oracle.cpu_step import time_cpu_step
@@ -536,6 +601,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "slo": slo,
+            "config4_cosyvoice2_lm": cosy,
             "detail": {"tokens_decoded": decoded, "chunks": chunks, "pcm_samples": pcm,
                        "device_ms": round(dev_ms, 3), "wall_s": round(wall_s, 4),
                        "host_blocked_ms_per_step": round(res["wait_s"] * 1000 / steps, 3),
