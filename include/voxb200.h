@@ -78,6 +78,14 @@ typedef struct VoxModelCfg {
   int32_t max_detok_frames; /* max latent frames per detok call (all requests) */
   /* Qwen2-style bias on the fused q|k|v projection (CosyVoice2's LM); 0 = Llama */
   int32_t qkv_bias;
+  /* CSM-style multi-codebook frames: n_codebooks > 1 adds a frame store of the
+   * codebook-1..n-1 ids of every position; the input embedding of a position is
+   * the sum of the embedding rows of all its ids (codebook 0 in the token store) */
+  int32_t n_codebooks;
+  /* ext_dim > 0: rows with token == -2 take their input from an external hidden
+   * state of width ext_dim projected by this ctx's input projector (CSM depth
+   * decoder position 0 = projected backbone state), see vox_project_ext */
+  int32_t ext_dim;
 } VoxModelCfg;
 
 /* Per-request sampling parameters (SamplingParams, model_api.py:105-121). */
@@ -197,6 +205,24 @@ int vox_gemm_test(VoxCtx* ctx, const uint16_t* w, const uint16_t* x, const float
  * pipeline stages (<= 0: run to completion). */
 int vox_debug_detok(VoxCtx* ctx, int32_t stop_after, float* out, size_t n_floats,
                     uint16_t* bf_out, size_t n_bf);
+
+/* multi-codebook frames (n_codebooks > 1): ids of codebooks 1..n-1 at positions
+ * [pos, pos + n_pos) of a slot, [n_pos][n_codebooks - 1], -1 = none */
+int vox_write_frame(VoxCtx* ctx, int32_t slot, int32_t pos, int32_t n_pos, const int32_t* ids);
+int vox_read_frame(VoxCtx* ctx, int32_t slot, int32_t pos, int32_t n_pos, int32_t* out);
+/* ext rows (ext_dim > 0): ext[0..n) = src.final_hidden[0..n) * P^T on the device,
+ * where src.final_hidden are the sampled rows of src's last vox_forward (in row
+ * order) and P [d_model, ext_dim] is this ctx's input projector.  Ordered after
+ * src's LM stream; the next vox_forward of ctx reads ext row r for its row r
+ * when that row has token == -2. */
+int vox_project_ext(VoxCtx* ctx, VoxCtx* src, int32_t n);
+/* device-side token hand-over between two ctxs on one device (no host sync):
+ * links[i] = {dst_slot, dst_pos, src_slot, src_pos}.
+ * mode 0: dst.tokens[dst_slot][dst_pos] = src.tokens[src_slot][src_pos] + offset
+ * mode 1: dst.frame[dst_slot][dst_pos][k] = src.tokens[src_slot][src_pos + k] + offset,
+ *         k = 0 .. dst.n_codebooks - 2 */
+int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, int32_t offset,
+                    int32_t mode);
 
 /* weights / state introspection for parity tests (host copies) */
 int vox_read_weight(VoxCtx* ctx, const char* name, int32_t layer, void* out, size_t bytes);

@@ -55,8 +55,33 @@ class LlamaOracle:
             self.v[rid] = np.zeros_like(self.k[rid])
         return self.k[rid], self.v[rid]
 
-    def forward(self, rid, tokens: np.ndarray, positions: np.ndarray, want_logits: bool = True):
-        """Run tokens [n] at positions [n] (contiguous, ascending) of request rid.
+    def embed(self, tokens: np.ndarray, ext: np.ndarray | None = None) -> np.ndarray:
+        """lm_kernels.cu:embed_norm_kernel input rows, fp32.
+
+        tokens [n] or [n, C] (CSM-style frame: the sum of the embedding rows of all
+        ids, codebook order, -1 = absent); an id of -2 in column 0 takes ext[i]."""
+        t = np.asarray(tokens)
+        if t.ndim == 1:
+            t = t[:, None]
+        h = np.zeros((t.shape[0], self.cfg.d_model), np.float32)
+        for i in range(t.shape[0]):
+            if t[i, 0] == -2:
+                h[i] = ext[i]
+                continue
+            acc = self.w.emb[t[i, 0]].astype(np.float32)
+            for cb in range(1, t.shape[1]):
+                if t[i, cb] >= 0:
+                    acc = acc + self.w.emb[t[i, cb]]
+            h[i] = acc
+        return h
+
+    def project(self, xf: np.ndarray) -> np.ndarray:
+        """vox_project_ext: bf16 source hidden rows x the bf16 input projector, fp32."""
+        return (xf.astype(np.float32) @ self.w.proj.T).astype(np.float32)
+
+    def forward(self, rid, tokens: np.ndarray, positions: np.ndarray, want_logits: bool = True,
+                ext: np.ndarray | None = None):
+        """Run tokens [n] (or CSM frames [n, C]) at positions [n] (ascending) of request rid.
 
         Returns logits [n, vocab] fp32 of every row (or None) and the final
         normalised hidden rows xf [n, d] (bf16 values).
@@ -66,7 +91,7 @@ class LlamaOracle:
         G = H // KV
         n = len(tokens)
         K, V = self._layer_kv(rid)
-        h = w.emb[tokens].astype(np.float32)  # fp32 residual
+        h = self.embed(tokens, ext)  # fp32 residual
         x = rmsnorm_bf16(h, w.layers[0]["norm_attn"], c.rms_eps)
         scale = f32(1.0) / np.sqrt(f32(hd))
         for l, L in enumerate(w.layers):

@@ -14,7 +14,7 @@ GOLDEN = 0x9E3779B97F4A7C15
 
 # tensor ids (csrc/vox_api.cu: TensorId)
 T_EMB, T_NORM_ATTN, T_NORM_MLP, T_NORM_FINAL = 1, 2, 3, 4
-T_QKV, T_O, T_GU, T_DOWN, T_QKV_BIAS = 5, 6, 7, 8, 9
+T_QKV, T_O, T_GU, T_DOWN, T_QKV_BIAS, T_PROJ = 5, 6, 7, 8, 9, 10
 T_VQ_TAB, T_IN_DW_W, T_IN_DW_B, T_IN_PW_W, T_IN_PW_B = 20, 21, 22, 23, 24
 T_UP_ALPHA, T_UP_W, T_UP_B = 30, 34, 38
 T_RU_A1, T_RU_DW_W, T_RU_DW_B, T_RU_A2, T_RU_PW_W, T_RU_PW_B = 50, 70, 90, 110, 130, 150
@@ -99,6 +99,9 @@ class BackboneWeights:
                 L["qkv_bias"] = init_f32(nqkv, k(T_QKV_BIAS, l), 0.5, 0.0)
             self.layers.append(L)
         self.norm_final = init_f32(d, k(T_NORM_FINAL), 0.25, 1.0)
+        ext = getattr(cfg, "ext_dim", 0)
+        if ext:  # input projector of external hidden rows (vox_api.cu: T_PROJ)
+            self.proj = init_bf16(d * ext, k(T_PROJ), np.sqrt(f32(3.0) / f32(ext))).reshape(d, ext)
         self.inv_freq = np.array(
             [np.float32(1.0 / (float(cfg.rope_theta) ** ((2.0 * i) / hd))) for i in range(hd // 2)],
             dtype=np.float32,

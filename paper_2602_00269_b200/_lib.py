@@ -37,6 +37,8 @@ class VoxModelCfg(C.Structure):
         ("rates", C.c_int32 * 4),
         ("max_detok_frames", C.c_int32),
         ("qkv_bias", C.c_int32),
+        ("n_codebooks", C.c_int32),
+        ("ext_dim", C.c_int32),
     ]
 
 
@@ -114,6 +116,10 @@ _SIGS = {
                                 C.c_int32, C.c_int32, C.c_int32, _f32p, C.POINTER(C.c_double)]),
     "vox_read_weight": (C.c_int, [_P, C.c_char_p, C.c_int32, _P, C.c_size_t]),
     "vox_read_kv": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _f32p, _f32p]),
+    "vox_write_frame": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _i32p]),
+    "vox_read_frame": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _i32p]),
+    "vox_project_ext": (C.c_int, [_P, _P, C.c_int32]),
+    "vox_link_tokens": (C.c_int, [_P, _P, _i32p, C.c_int32, C.c_int32, C.c_int32]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -49,6 +49,8 @@ class ModelConfig:
     max_detok_frames: int = 256
     embed_scale: float = 0.0  # 0 -> logit std ~2.5 (see embed_half_width)
     qkv_bias: bool = False    # Qwen2-style q|k|v bias (CosyVoice2's LM)
+    n_codebooks: int = 1      # CSM-style frames: embedding = sum over the frame's codebook ids
+    ext_dim: int = 0          # > 0: token -2 rows take a projected external hidden (CSM depth pos 0)
 
     @property
     def embed_half_width(self) -> float:
@@ -140,4 +142,54 @@ def tiny_cosy(**kw) -> ModelConfig:
                          "max_slots": 16, "max_ctx": 512, "max_rows": 512, **kw})
 
 
-CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy}
+# CSM-1B ([3P] transformers CsmConfig defaults, configuration_csm.py:55-157): Llama-1B
+# backbone (16 layers, d 2048, 32 q / 8 kv heads of 64, FFN 8192) over frames of 32
+# codebooks, and a depth decoder (4 layers, d 1024, 8 q / 2 kv heads of 128, FFN 8192)
+# that fills codebooks 1..31 of each frame from the backbone's last hidden state.
+# Codebooks are 2048 codes here (CSM's 2051 carries 3 specials; 2048 keeps every
+# codebook slice a whole number of 128-row weight tiles).  Backbone rows: 128,256 text
+# ids, then codebook c at [base + c*2048, base + (c+1)*2048); the codebook-0 head is
+# tied to its embedding rows.  Depth rows: codebook c at [c*2048, (c+1)*2048), tied
+# input/output table (HF CSM unties the depth head; one table keeps the id of a
+# sampled codebook-k code equal to its input row at the next depth position).
+CSM_TEXT_VOCAB = 128256
+CSM_CODES = 2048
+
+
+def csm_backbone(**kw) -> ModelConfig:
+    """Config 3 backbone: CSM-1B-style Llama-1B over 32-codebook frames (codebook-0 head)."""
+    nc = kw.pop("n_codebooks", 32)
+    base = ModelConfig(
+        name="csm-1b-backbone", n_layers=16, d_model=2048, n_heads=32, n_kv_heads=8, head_dim=64,
+        d_ff=8192, vocab=CSM_TEXT_VOCAB + nc * CSM_CODES, text_vocab=CSM_TEXT_VOCAB,
+        audio_base=CSM_TEXT_VOCAB, codebook_size=CSM_CODES, frame_tokens=1, n_codebooks=nc,
+        detok_enabled=False, max_slots=256, max_ctx=512, max_rows=512,
+    )
+    return replace(base, **kw)
+
+
+def csm_depth(**kw) -> ModelConfig:
+    """Config 3 depth decoder: position 0 = projected backbone state, position k >= 1 =
+    the frame's codebook k-1 code; position k samples codebook k (frame slot k-1)."""
+    nc = kw.pop("n_codebooks", 32)
+    ext = kw.pop("ext_dim", 2048)
+    base = ModelConfig(
+        name="csm-1b-depth", n_layers=4, d_model=1024, n_heads=8, n_kv_heads=2, head_dim=128,
+        d_ff=8192, vocab=nc * CSM_CODES, text_vocab=CSM_CODES, audio_base=CSM_CODES,
+        codebook_size=CSM_CODES, frame_tokens=nc - 1, ext_dim=ext, detok_enabled=False,
+        max_slots=256, max_ctx=48, max_rows=512,
+    )
+    return replace(base, **kw)
+
+
+def tiny_csm(n_codebooks: int = 8):
+    """CPU-oracle-sized CSM-style pair (same head geometries, 8 codebooks)."""
+    bb = csm_backbone(name="tiny-csm-backbone", n_layers=2, d_model=256, n_codebooks=n_codebooks,
+                      max_slots=8, max_ctx=256, max_rows=256)
+    dp = csm_depth(name="tiny-csm-depth", n_layers=2, d_model=256, n_heads=4, n_kv_heads=1,
+                   d_ff=1024, n_codebooks=n_codebooks, ext_dim=256, max_slots=8, max_rows=256)
+    return bb, dp
+
+
+CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy,
+           "csm_backbone": csm_backbone, "csm_depth": csm_depth}

@@ -116,7 +116,12 @@ struct LmDims {
   int page_size, max_pages_per_slot, n_pages, max_ctx;
 };
 
-void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
+// frame (nullable): [slot][max_ctx][nfc] extra codebook ids summed into the
+// embedding; ext (nullable): fp32 [rows][d] inputs of token == -2 rows
+void launch_link_tokens(const int* links, int n, const int* src_ts, int src_max_ctx, int* dst,
+                        int dst_max_ctx, int nfc, int offset, int mode, cudaStream_t st);
+void launch_embed_norm(const RowDev* rows, int n, int* token_store, const int* frame, int nfc,
+                       const float* ext, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x, cudaStream_t st);
 void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const float* bias, int splits,
                             int64_t split_stride, const LmDims& dm, const float2* rope,

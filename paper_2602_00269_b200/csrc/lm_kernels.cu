@@ -67,6 +67,8 @@ VOX_DEV void norm_store4(bf16* x, float4 h, float inv, float4 w) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restrict__ rows,
                                                          int* __restrict__ token_store,
+                                                         const int* __restrict__ frame, int nfc,
+                                                         const float* __restrict__ ext,
                                                          int max_ctx, const bf16* __restrict__ emb,
                                                          const float* __restrict__ nw, int d,
                                                          float eps, float* __restrict__ h,
@@ -79,21 +81,44 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restric
   const RowDev rw = rows[r];
   if (rw.slot < 0) return;
   int* ts = token_store + static_cast<int64_t>(rw.slot) * max_ctx + rw.pos;
+  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
+  const int d4 = d / 4;
+  float ss = 0.f;
+  if (rw.token == -2) {  // external input row (projected hidden state, vox_project_ext)
+    const float4* x4 = reinterpret_cast<const float4*>(ext + static_cast<int64_t>(r) * d);
+    for (int i = threadIdx.x; i < d4; i += 256) {
+      const float4 v = x4[i];
+      h4[i] = v;
+      ss = fmaf(v.x, v.x, ss);
+      ss = fmaf(v.y, v.y, ss);
+      ss = fmaf(v.z, v.z, ss);
+      ss = fmaf(v.w, v.w, ss);
+    }
+  }
   int tok = rw.token;
   if (tok >= 0) {
     if (threadIdx.x == 0) *ts = tok;
   } else {
     tok = *ts;
   }
+  // multi-codebook frame: ids of codebooks 1..nfc summed in codebook order
+  const int* fr = frame != nullptr ? frame + (static_cast<int64_t>(rw.slot) * max_ctx + rw.pos) * nfc : nullptr;
   const bf16* e = emb + static_cast<int64_t>(tok) * d;
-  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
-  const int d4 = d / 4;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d4; i += 256) {
+  for (int i = threadIdx.x; i < d4 && rw.token != -2; i += 256) {
     const uint2 u = *reinterpret_cast<const uint2*>(e + 4 * i);
     const bf16* b = reinterpret_cast<const bf16*>(&u);
-    const float4 v = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]),
-                                 __bfloat162float(b[2]), __bfloat162float(b[3]));
+    float4 v = make_float4(__bfloat162float(b[0]), __bfloat162float(b[1]),
+                           __bfloat162float(b[2]), __bfloat162float(b[3]));
+    for (int cb = 0; cb < nfc && fr != nullptr; ++cb) {
+      const int id = fr[cb];
+      if (id < 0) continue;
+      const uint2 u2 = *reinterpret_cast<const uint2*>(emb + static_cast<int64_t>(id) * d + 4 * i);
+      const bf16* b2 = reinterpret_cast<const bf16*>(&u2);
+      v.x = __fadd_rn(v.x, __bfloat162float(b2[0]));
+      v.y = __fadd_rn(v.y, __bfloat162float(b2[1]));
+      v.z = __fadd_rn(v.z, __bfloat162float(b2[2]));
+      v.w = __fadd_rn(v.w, __bfloat162float(b2[3]));
+    }
     h4[i] = v;
     ss = fmaf(v.x, v.x, ss);
     ss = fmaf(v.y, v.y, ss);
@@ -107,11 +132,37 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const RowDev* __restric
   for (int i = threadIdx.x; i < d4; i += 256) norm_store4(xr + 4 * i, h4[i], inv, w4[i]);
 }
 
-void launch_embed_norm(const RowDev* rows, int n, int* token_store, int max_ctx, const bf16* emb,
+void launch_embed_norm(const RowDev* rows, int n, int* token_store, const int* frame, int nfc,
+                       const float* ext, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x,
                        cudaStream_t st) {
-  launch_k(embed_norm_kernel, dim3(n), dim3(256), 0, st, rows, token_store, max_ctx, emb, norm_w,
-           dm.d, dm.eps, h, x);
+  launch_k(embed_norm_kernel, dim3(n), dim3(256), 0, st, rows, token_store, frame, nfc, ext, max_ctx,
+           emb, norm_w, dm.d, dm.eps, h, x);
+}
+
+// token hand-over between two contexts (CSM backbone <-> depth decoder)
+__global__ void link_tokens_kernel(const int* __restrict__ links, int n, const int* __restrict__ src_ts,
+                                   int src_max_ctx, int* __restrict__ dst, int dst_max_ctx, int nfc,
+                                   int offset, int mode) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mode == 0) {
+    if (i >= n) return;
+    const int* l = links + 4 * i;
+    dst[static_cast<int64_t>(l[0]) * dst_max_ctx + l[1]] = src_ts[static_cast<int64_t>(l[2]) * src_max_ctx + l[3]] + offset;
+  } else {
+    if (i >= n * nfc) return;
+    const int j = i / nfc, k = i % nfc;
+    const int* l = links + 4 * j;
+    dst[(static_cast<int64_t>(l[0]) * dst_max_ctx + l[1]) * nfc + k] =
+        src_ts[static_cast<int64_t>(l[2]) * src_max_ctx + l[3] + k] + offset;
+  }
+}
+
+void launch_link_tokens(const int* links, int n, const int* src_ts, int src_max_ctx, int* dst,
+                        int dst_max_ctx, int nfc, int offset, int mode, cudaStream_t st) {
+  const int total = mode == 0 ? n : n * nfc;
+  link_tokens_kernel<<<(total + 127) / 128, 128, 0, st>>>(links, n, src_ts, src_max_ctx, dst, dst_max_ctx,
+                                                          nfc, offset, mode);
 }
 
 // ---------------------------------------------------------------------------

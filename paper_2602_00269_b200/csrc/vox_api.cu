@@ -32,6 +32,7 @@ enum TensorId : uint64_t {
   T_GU = 7,
   T_DOWN = 8,
   T_QKV_BIAS = 9,
+  T_PROJ = 10,  // ext input projector [d_model, ext_dim] (CSM depth decoder)
   // detokenizer
   T_VQ_TAB = 20,
   T_IN_DW_W = 21,
@@ -124,6 +125,13 @@ struct VoxCtx {
   bf16* emb = nullptr;
   float *norm_attn = nullptr, *norm_mlp = nullptr, *norm_final = nullptr;
   float* b_qkv = nullptr;  // [L][nqkv] fp32 when cfg.qkv_bias (Qwen2-style)
+  int* frame_store = nullptr;  // [slot][max_ctx][n_codebooks - 1] when n_codebooks > 1
+  int nfc = 0;                 // n_codebooks - 1
+  float* ext = nullptr;        // [max_rows][d] projected external inputs (ext_dim > 0)
+  bf16* w_proj = nullptr;      // packed [d, ext_dim]
+  std::map<const void*, std::map<int, CUtensorMap>> ext_maps;  // src final-hidden maps
+  int* d_links = nullptr;      // [max_rows * 4] vox_link_tokens staging
+  cudaEvent_t ev_xfer = nullptr;
   bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
   float* inv_freq = nullptr;
   float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
@@ -479,6 +487,22 @@ static int create_buffers(VoxCtx* c) {
   CK(cudaMemset(c->vc, 0, kv_elems * 2));
   CK(dalloc(&c->token_store, static_cast<size_t>(g.max_slots) * g.max_ctx));
   CK(cudaMemset(c->token_store, 0, static_cast<size_t>(g.max_slots) * g.max_ctx * 4));
+  c->nfc = g.n_codebooks > 1 ? g.n_codebooks - 1 : 0;
+  if (c->nfc > 0) {
+    const size_t nf = static_cast<size_t>(g.max_slots) * g.max_ctx * c->nfc;
+    CK(dalloc(&c->frame_store, nf));
+    CK(cudaMemset(c->frame_store, 0xFF, nf * 4));  // -1: no id
+  }
+  if (g.ext_dim > 0) {
+    CK(dalloc(&c->ext, static_cast<size_t>(g.max_rows) * g.d_model));
+    CK(cudaMemset(c->ext, 0, static_cast<size_t>(g.max_rows) * g.d_model * 4));
+    CK(dalloc(&c->w_proj, static_cast<size_t>(packed_elems(g.d_model, g.ext_dim))));
+    launch_init_bf16_packed(c->w_proj, g.d_model, g.ext_dim, 0, tensor_key(c->seed, T_PROJ, 0),
+                            std::sqrt(3.0f / g.ext_dim), c->s_lm);
+    CK(cudaGetLastError());
+  }
+  CK(dalloc(&c->d_links, static_cast<size_t>(g.max_rows) * 4));
+  CK(cudaEventCreateWithFlags(&c->ev_xfer, cudaEventDisableTiming));
   CK(dalloc(&c->page_table, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot));
   CK(cudaMemset(c->page_table, 0, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot * 4));
   CK(dalloc(&c->slot_prompt, static_cast<size_t>(g.max_slots)));
@@ -675,8 +699,8 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
   const int L = g.n_layers, d = g.d_model, dff = g.d_ff, Hhd = g.n_heads * g.head_dim;
   {
     TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * 8);
-    launch_embed_norm(c->d_rows, nrows, c->token_store, g.max_ctx, c->emb, c->norm_attn, dm, c->h,
-                      c->x, st);
+    launch_embed_norm(c->d_rows, nrows, c->token_store, c->frame_store, c->nfc, c->ext, g.max_ctx,
+                      c->emb, c->norm_attn, dm, c->h, c->x, st);
   }
   const GemmPlan qkv_plan = gemm_plan(c->nqkv, nrows, d), o_plan = gemm_plan(d, nrows, Hhd);
   const GemmPlan dn_plan = gemm_plan(d, nrows, dff);
@@ -799,6 +823,7 @@ static int validate_cfg(const VoxModelCfg* g) {
   // 8-token chunks; the attention smem ring holds 6 x 2 head-pages (<= 192 KB)
   // the attention kernel's mma tiling is built for 16-token pages
   if (g->page_size != 16 || g->max_rows < 1 || g->max_rows > 2048) return 0;
+  if (g->n_codebooks < 0 || g->n_codebooks > 64 || g->ext_dim < 0 || g->ext_dim % 64) return 0;
   if (g->max_slots < 1 || g->n_pages < 1 || g->max_ctx < 2) return 0;
   if (g->detok_enabled) {
     if (g->audio_base < 0 || g->n_rates != 4 || g->latent_dim % 64 || g->decoder_dim % 1024)
@@ -884,7 +909,8 @@ void vox_destroy(VoxCtx* c) {
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
-                      c->trace_buf};
+                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links};
+  if (c->ev_xfer) cudaEventDestroy(c->ev_xfer);
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (c->cfg.detok_enabled && c->dw.tabs) {
@@ -982,6 +1008,9 @@ int vox_admit(VoxCtx* c, uint64_t req_seed, int32_t prompt_len, int32_t target_l
   if (g.detok_enabled)
     CK(cudaMemsetAsync(c->dstate + static_cast<int64_t>(slot) * 2 * c->dd.state_floats, 0,
                        sizeof(float) * 2 * c->dd.state_floats, st));
+  if (c->nfc > 0)
+    CK(cudaMemsetAsync(c->frame_store + static_cast<int64_t>(slot) * g.max_ctx * c->nfc, 0xFF,
+                       static_cast<size_t>(g.max_ctx) * c->nfc * 4, st));
   CK(cudaEventRecord(as.ev, st));
   as.in_flight = true;
   c->slot_used[slot] = 1;
@@ -1043,6 +1072,70 @@ int vox_write_tokens(VoxCtx* c, int32_t slot, int32_t pos, int32_t n, const int3
   return VOX_OK;
 }
 
+int vox_write_frame(VoxCtx* c, int32_t slot, int32_t pos, int32_t n_pos, const int32_t* ids) {
+  if (!c || !ids || c->nfc == 0 || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot] ||
+      pos < 0 || n_pos < 0 || pos + n_pos > c->cfg.max_ctx)
+    return fail(c, VOX_ERR_INVALID, "bad frame range");
+  for (int i = 0; i < n_pos * c->nfc; ++i)
+    if (ids[i] < -1 || ids[i] >= c->cfg.vocab) return fail(c, VOX_ERR_INVALID, "frame id outside vocab");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(c->frame_store + (static_cast<int64_t>(slot) * c->cfg.max_ctx + pos) * c->nfc, ids,
+                static_cast<size_t>(n_pos) * c->nfc * 4, cudaMemcpyHostToDevice));
+  return VOX_OK;
+}
+
+int vox_read_frame(VoxCtx* c, int32_t slot, int32_t pos, int32_t n_pos, int32_t* out) {
+  if (!c || !out || c->nfc == 0 || slot < 0 || slot >= c->cfg.max_slots || pos < 0 || n_pos < 0 ||
+      pos + n_pos > c->cfg.max_ctx)
+    return fail(c, VOX_ERR_INVALID, "bad frame range");
+  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaMemcpy(out, c->frame_store + (static_cast<int64_t>(slot) * c->cfg.max_ctx + pos) * c->nfc,
+                static_cast<size_t>(n_pos) * c->nfc * 4, cudaMemcpyDeviceToHost));
+  return VOX_OK;
+}
+
+int vox_project_ext(VoxCtx* c, VoxCtx* src, int32_t n) {
+  if (!c || !src || c->cfg.ext_dim <= 0 || src->cfg.d_model != c->cfg.ext_dim || n < 1 ||
+      n > c->cfg.max_rows || n > src->cfg.max_rows || c->device != src->device)
+    return fail(c, VOX_ERR_INVALID, "bad ext projection");
+  auto& xm = c->ext_maps[src->xf];
+  if (xm.empty() && !make_act_maps(c, xm, src->xf, src->cfg.d_model, src->cfg.max_rows))
+    return fail(c, VOX_ERR_CUDA, "tensor map (ext source)");
+  CK(cudaEventRecord(src->ev_xfer, src->s_lm));
+  CK(cudaStreamWaitEvent(c->s_lm, src->ev_xfer, 0));
+  const CUtensorMap& tw_unused = c->tm_head_full;
+  const int M = c->cfg.d_model, K = c->cfg.ext_dim;
+  GemmPlan pl = gemm_plan(M, n, K);
+  const int splits = 1;  // one plane straight into ext[n][d]
+  (void)pl;
+  return run_gemm(c, tw_unused, xm, M, n, K, c->ext, M, splits, nullptr, nullptr, 0, M, c->s_lm, "gemm",
+                  c->w_proj, nullptr);
+}
+
+int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, int32_t offset,
+                    int32_t mode) {
+  VoxCtx* c = dst;  // error context of CK()
+  if (!dst || !src || !links || n < 1 || n > dst->cfg.max_rows || (mode != 0 && mode != 1) ||
+      (mode == 1 && dst->nfc == 0) || dst->device != src->device)
+    return fail(dst, VOX_ERR_INVALID, "bad token links");
+  for (int i = 0; i < n; ++i) {
+    const int32_t* l = links + 4 * i;
+    const int span = mode == 1 ? dst->nfc : 1;
+    if (l[0] < 0 || l[0] >= dst->cfg.max_slots || l[1] < 0 || l[1] >= dst->cfg.max_ctx || l[2] < 0 ||
+        l[2] >= src->cfg.max_slots || l[3] < 0 || l[3] + span > src->cfg.max_ctx)
+      return fail(dst, VOX_ERR_INVALID, "token link out of range");
+  }
+  CK(cudaEventRecord(src->ev_xfer, src->s_lm));
+  CK(cudaStreamWaitEvent(dst->s_lm, src->ev_xfer, 0));
+  CK(cudaMemcpyAsync(dst->d_links, links, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, dst->s_lm));
+  launch_link_tokens(dst->d_links, n, src->token_store, src->cfg.max_ctx,
+                     mode == 0 ? dst->token_store : dst->frame_store, dst->cfg.max_ctx, dst->nfc, offset, mode,
+                     dst->s_lm);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(dst->s_lm));  // `links` is a pageable host buffer of the caller
+  return VOX_OK;
+}
+
 int vox_slot_info(VoxCtx* c, int32_t slot, int32_t* prompt_len, int32_t* target_len) {
   if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
     return fail(c, VOX_ERR_CACHE_MISSING, "unknown slot");
@@ -1070,6 +1163,9 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
     if (r.pos < 0 || r.pos + 1 >= g.max_ctx || r.pos >= cap)
       return fail(c, VOX_ERR_INVALID, "row position outside the reserved KV range");
     if (r.token >= g.vocab) return fail(c, VOX_ERR_INVALID, "token id outside the vocabulary");
+    if (r.token == -2 && g.ext_dim <= 0)
+      return fail(c, VOX_ERR_INVALID, "external input row on a ctx without an input projector");
+    if (r.token < -2) return fail(c, VOX_ERR_INVALID, "bad token id");
     if (r.sample) {
       if (r.pos + 1 < c->h_prompt[r.slot])
         return fail(c, VOX_ERR_INVALID, "sampling row inside the prompt");

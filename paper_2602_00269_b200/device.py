@@ -58,6 +58,8 @@ class VoxDevice:
             c.rates[i] = r
         c.max_detok_frames = cfg.max_detok_frames
         c.qkv_bias = int(cfg.qkv_bias)
+        c.n_codebooks = int(cfg.n_codebooks)
+        c.ext_dim = int(cfg.ext_dim)
         self._c = c
         h = C.c_void_p()
         _lib.check(self.lib.vox_create(device, C.byref(c), C.c_uint64(weight_seed & (2**64 - 1)), C.byref(h)))
@@ -220,6 +222,26 @@ class VoxDevice:
         ms, n, by = C.c_double(), C.c_int64(), C.c_double()
         self._check(self.lib.vox_timing_read(self.ctx, cls.encode(), C.byref(ms), C.byref(n), C.byref(by)))
         return ms.value, n.value, by.value
+
+    # ------------------------------------------------------------------ CSM-style frames
+    def write_frame(self, slot: int, pos: int, ids: np.ndarray) -> None:
+        """ids [n_pos, n_codebooks - 1] of codebooks 1.. at positions pos.. (-1 = none)."""
+        a = np.ascontiguousarray(ids, dtype=np.int32)
+        self._check(self.lib.vox_write_frame(self.ctx, slot, pos, a.shape[0], _ptr(a, C.c_int32)))
+
+    def read_frame(self, slot: int, pos: int, n_pos: int) -> np.ndarray:
+        out = np.empty((n_pos, self.cfg.n_codebooks - 1), np.int32)
+        self._check(self.lib.vox_read_frame(self.ctx, slot, pos, n_pos, _ptr(out, C.c_int32)))
+        return out
+
+    def project_ext(self, src: "VoxDevice", n: int) -> None:
+        """ext rows 0..n-1 = src's last sampled final-hidden rows x this ctx's input projector."""
+        self._check(self.lib.vox_project_ext(self.ctx, src.ctx, n))
+
+    def link_tokens(self, src: "VoxDevice", links: np.ndarray, offset: int, mode: int) -> None:
+        """Device-side token hand-over; links [n, 4] = (dst_slot, dst_pos, src_slot, src_pos)."""
+        a = np.ascontiguousarray(links, dtype=np.int32)
+        self._check(self.lib.vox_link_tokens(self.ctx, src.ctx, _ptr(a, C.c_int32), a.shape[0], offset, mode))
 
     def trace_arm(self, capacity: int = 1 << 20) -> None:
         """Arm the in-graph kernel tracer (one record per CTA of every instrumented kernel)."""

@@ -12,7 +12,7 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-from paper_2602_00269_b200.config import orpheus3b  # noqa: E402
+from paper_2602_00269_b200.config import CONFIGS  # noqa: E402
 from paper_2602_00269_b200.device import Sampling, VoxDevice  # noqa: E402
 
 NAMES = {1: "gemm1cta", 2: "gemm_mc", 3: "attn", 4: "attn_comb", 5: "qkv_rope", 6: "resid_norm",
@@ -42,9 +42,11 @@ def main():
     ap.add_argument("--batch", type=int, default=224)
     ap.add_argument("--ctx", type=int, default=394)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--config", default="orpheus3b")
     a = ap.parse_args()
-    dev = VoxDevice(orpheus3b(max_slots=max(a.batch, 8)), 0)
-    prm = Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3)
+    dev = VoxDevice(CONFIGS[a.config](max_slots=max(a.batch, 8)), 0)
+    prm = (Sampling(temperature=0.8, top_p=0.95, top_k=50, repetition_penalty=1.1) if "cosy" in a.config
+           else Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3))
     P = 50
     slots = [dev.admit(1000 + i, P, 688, prm) for i in range(a.batch)]
     per = max(1, 1000 // (a.ctx - 1))
