@@ -475,6 +475,60 @@ def cosy_lm_steps(batch: int, ctx: int, steps: int, seed: int, hbm: float, devic
             "detokenizer": "not built (token-to-mel flow matching + HiFT are SURVEY §8f next rows)"}
 
 
+def csm_frames(batch: int, frames: int, seed: int, hbm: float, device: int):
+    """BASELINE config 3 (CSM-1B-style): frames/s of the multi-codebook path -- one backbone
+    forward (codebook 0) + 31 depth-decoder forwards (codebooks 1..31) per frame for
+    `batch` streams (greedy), hand-overs on the device.  Roofline bytes per frame =
+    backbone weights + 31 x depth weights (one codebook head slice each) + KV reads."""
+    import torch
+
+    from paper_2602_00269_b200.config import csm_backbone, csm_depth
+    from paper_2602_00269_b200.csm import CsmFrames
+    from paper_2602_00269_b200.device import Sampling, VoxDevice
+
+    bcfg = csm_backbone(max_slots=batch + 4, max_ctx=128, max_rows=max(512, batch * 2))
+    dcfg = csm_depth(max_slots=batch + 4, max_rows=max(512, batch * 2))
+    bb, dp = VoxDevice(bcfg, seed, device), VoxDevice(dcfg, seed + 1, device)
+    pipe = CsmFrames(bb, dp)
+    g = Sampling(temperature=0.0, repetition_penalty=1.0)
+    P = 50
+    streams = [pipe.admit(seed * 131 + i, P, frames + 8, g, g) for i in range(batch)]
+    for a in range(0, batch, 8):
+        pipe.prefill(streams[a:a + 8])
+    for _ in range(2):  # warm: graphs for every depth position
+        pipe.step(streams)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(frames):
+        pipe.step(streams)
+    bb.synchronize()
+    dp.synchronize()
+    dt = (time.perf_counter() - t0) / frames
+    dcodes = (bcfg.n_codebooks - 1)
+
+    def layer_bytes(c):
+        return 2 * ((c.n_heads + 2 * c.n_kv_heads) * c.head_dim * c.d_model + c.d_model * c.n_heads * c.head_dim
+                    + 3 * c.d_model * c.d_ff) * c.n_layers
+    ctx = P + 2 + frames / 2
+    by = (layer_bytes(bcfg) + 2 * bcfg.codebook_size * bcfg.d_model + batch * ctx * bcfg.kv_bytes_per_token
+          + dcodes * (layer_bytes(dcfg) + 2 * dcfg.codebook_size * dcfg.d_model)
+          + batch * sum(range(2, 33)) * dcfg.kv_bytes_per_token)
+    out = {"model": "csm-1b-style random-init: Llama-1B backbone (16 x 2048, 32q/8kv hd 64) + depth decoder "
+                    "(4 x 1024, 8q/2kv hd 128) over 32 codebooks x 2048 codes",
+           "batch": batch, "frames_timed": frames, "ms_per_frame": round(dt * 1e3, 3),
+           "frames_per_s": round(batch / dt, 1), "audio_s_per_s_lm_only": round(batch / dt * 0.08, 1),
+           "forwards_per_frame": 1 + dcodes,
+           "roofline": {"bound": "hbm", "achieved": round(by / dt / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(by / dt / 1e9 / hbm, 4), "bytes_per_frame": int(by)},
+           "timing": "host wall clock around the frames (the pipeline syncs the host at each hand-over)",
+           "detokenizer": "not built (Mimi decoder is SURVEY §8f row 1 remainder)"}
+    for s_ in streams:
+        pipe.release(s_)
+    bb.close()
+    dp.close()
+    return out
+
+
 def cpu_port_sample(seconds_budget: float = 20.0):
     """Oracle port of the same step on host cores (bounded sample); returns audio-s/s."""
     from oracle.cpu_step import time_cpu_step
@@ -499,6 +553,7 @@ def main():
     ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cosy", action="store_true", help="skip the config-4 (CosyVoice2-style LM) line")
+    ap.add_argument("--no-csm", action="store_true", help="skip the config-3 (CSM-1B-style frames) line")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -576,6 +631,13 @@ def main():
         except Exception as e:  # report, never mask the headline
             cosy = {"error": repr(e)[:200]}
 
+    csm = None
+    if not args.no_csm and rank == 0:
+        try:
+            csm = csm_frames(64, 8, args.seed + 9, hbm, local)
+        except Exception as e:  # report, never mask the headline
+            csm = {"error": repr(e)[:200]}
+
     cpu = None
     if not args.no_cpu and rank == 0:
         from oracle.cpu_step import time_cpu_step
@@ -601,6 +663,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
             "slo": slo,
+            "config3_csm_frames": csm,
             "config4_cosyvoice2_lm": cosy,
             "detail": {"tokens_decoded": decoded, "chunks": chunks, "pcm_samples": pcm,
                        "device_ms": round(dev_ms, 3), "wall_s": round(wall_s, 4),

@@ -181,8 +181,9 @@ struct VoxCtx {
   double step_attn_bytes = 0;    // per layer, for timing/roofline
 
   // ---- graphs keyed by (row bucket, sample bucket)
-  std::map<std::pair<int, int>, cudaGraphExec_t> graphs;
-  std::map<std::pair<int, int>, int64_t> graph_launches;
+  // key = (row bucket, sample bucket, head frame slot or -1)
+  std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int, int>, int64_t> graph_launches;
   int64_t fwd_seq = 0;
   std::vector<cudaEvent_t> fwd_events;  // ring
   std::vector<int64_t> fwd_event_seq;
@@ -692,7 +693,9 @@ static int create_detok(VoxCtx* c) {
 // ---------------------------------------------------------------------------
 // the decode step (eager or captured)
 // ---------------------------------------------------------------------------
-static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
+// hslot >= 0: every sampled row is at the same frame slot, so the LM head runs
+// over that slot's codebook rows only (CSM depth decoder: 1 of 31 codebook heads)
+static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1) {
   const VoxModelCfg& g = c->cfg;
   const LmDims& dm = c->dm;
   cudaStream_t st = c->s_lm;
@@ -761,16 +764,20 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits) {
   }
   if (nsamp > 0) {
     const bool audio = (g.audio_base >= 0) && !full_logits;
-    const int M = audio ? c->head_audio_rows : g.vocab;
+    const bool one_slot = audio && hslot >= 0;
+    const int M = one_slot ? g.codebook_size : (audio ? c->head_audio_rows : g.vocab);
+    const bf16* wh = audio ? c->w_head_audio : nullptr;
+    if (one_slot)  // packed 128-row tiles: slot k starts at tile k * codebook_size / 128
+      wh += static_cast<int64_t>(hslot) * (g.codebook_size / 128) * (d / 64) * 8192;
     RET(run_gemm(c, c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits, M, 1, nullptr, nullptr, 0,
-                 M, st, "lm_head", audio ? c->w_head_audio : nullptr, audio ? &c->tp_head : nullptr));
+                 M, st, "lm_head", wh, (audio && !one_slot) ? &c->tp_head : nullptr));
     SampFusedArgs a{};
     a.rows = c->d_rows;
     a.sample_rows = c->d_sample_rows;
     a.n_sample = nsamp;
     a.logits = c->logits;
     a.ld = M;
-    a.col_base = audio ? g.audio_base : 0;
+    a.col_base = audio ? g.audio_base + (one_slot ? hslot * g.codebook_size : 0) : 0;
     a.token_store = c->token_store;
     a.max_ctx = g.max_ctx;
     a.slot_prompt_len = c->slot_prompt;
@@ -1232,20 +1239,32 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
     CK(cudaMemcpyAsync(c->d_sample_rows, sg.sample_rows, sizeof(int) * ns,
                        cudaMemcpyHostToDevice, st));
   const bool use_graph = !(flags & VOX_FWD_NO_GRAPH) && !full && !c->timing && !c->no_graphs;
+  // one frame slot for every sampled row -> that slot's head rows only
+  int hslot = -1;
+  if (!full && ns > 0 && g.audio_base >= 0 && g.frame_tokens > 1 && g.codebook_size % 128 == 0) {
+    for (int i = 0; i < n; ++i) {
+      if (!rows[i].sample) continue;
+      const int step = rows[i].pos + 1 - c->h_prompt[rows[i].slot];
+      const int k = ((step % g.frame_tokens) + g.frame_tokens) % g.frame_tokens;
+      if (hslot == -1) hslot = k;
+      else if (hslot != k) { hslot = -2; break; }
+    }
+    if (hslot < 0) hslot = -1;
+  }
   int rc = VOX_OK;
   if (use_graph) {
-    auto key = std::make_pair(nrows, ns);
+    auto key = std::make_tuple(nrows, ns, hslot);
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       // eager pass (executes this step and sets kernel attributes), then capture
-      rc = enqueue_forward(c, nrows, ns, false);
+      rc = enqueue_forward(c, nrows, ns, false, hslot);
       if (rc != VOX_OK) return rc;
       CK(cudaStreamSynchronize(st));
       const int64_t before = c->launches;
       cudaGraph_t graph;
       c->capturing = true;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_forward(c, nrows, ns, false);
+      rc = enqueue_forward(c, nrows, ns, false, hslot);
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       c->capturing = false;
       if (rc != VOX_OK) return rc;
@@ -1261,7 +1280,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       c->launches += c->graph_launches[key];
     }
   } else {
-    rc = enqueue_forward(c, nrows, ns, full);
+    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot);
     if (rc != VOX_OK) return rc;
   }
   if (nsamp > 0)
