@@ -130,7 +130,10 @@ struct VoxCtx {
   float* ext = nullptr;        // [max_rows][d] projected external inputs (ext_dim > 0)
   bf16* w_proj = nullptr;      // packed [d, ext_dim]
   std::map<const void*, std::map<int, CUtensorMap>> ext_maps;  // src final-hidden maps
-  int* d_links = nullptr;      // [max_rows * 4] vox_link_tokens staging
+  int* d_links = nullptr;      // [8][max_rows * 4] vox_link_tokens device staging
+  int* h_links = nullptr;      // pinned twin (ring of 8, reused once its event completed)
+  cudaEvent_t ev_links[8] = {};
+  int64_t link_seq = 0;
   cudaEvent_t ev_xfer = nullptr;
   bf16 *w_qkv = nullptr, *w_o = nullptr, *w_gu = nullptr, *w_down = nullptr;
   float* inv_freq = nullptr;
@@ -502,7 +505,9 @@ static int create_buffers(VoxCtx* c) {
                             std::sqrt(3.0f / g.ext_dim), c->s_lm);
     CK(cudaGetLastError());
   }
-  CK(dalloc(&c->d_links, static_cast<size_t>(g.max_rows) * 4));
+  CK(dalloc(&c->d_links, static_cast<size_t>(g.max_rows) * 4 * 8));
+  CK(cudaHostAlloc(&c->h_links, static_cast<size_t>(g.max_rows) * 4 * 8 * 4, cudaHostAllocDefault));
+  for (auto& e : c->ev_links) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->ev_xfer, cudaEventDisableTiming));
   CK(dalloc(&c->page_table, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot));
   CK(cudaMemset(c->page_table, 0, static_cast<size_t>(g.max_slots) * c->max_pages_per_slot * 4));
@@ -918,6 +923,9 @@ void vox_destroy(VoxCtx* c) {
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
                       c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links};
   if (c->ev_xfer) cudaEventDestroy(c->ev_xfer);
+  for (auto& e : c->ev_links)
+    if (e) cudaEventDestroy(e);
+  if (c->h_links) cudaFreeHost(c->h_links);
   for (void* p : dev_ptrs)
     if (p) cudaFree(p);
   if (c->cfg.detok_enabled && c->dw.tabs) {
@@ -1132,14 +1140,20 @@ int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, i
         l[2] >= src->cfg.max_slots || l[3] < 0 || l[3] + span > src->cfg.max_ctx)
       return fail(dst, VOX_ERR_INVALID, "token link out of range");
   }
+  // pinned staging ring: no host sync (the entry is reused once its copy completed)
+  const int e = static_cast<int>(dst->link_seq++ % 8);
+  CK(cudaEventSynchronize(dst->ev_links[e]));
+  int* hl = dst->h_links + static_cast<size_t>(e) * dst->cfg.max_rows * 4;
+  int* dl = dst->d_links + static_cast<size_t>(e) * dst->cfg.max_rows * 4;
+  std::memcpy(hl, links, static_cast<size_t>(n) * 16);
   CK(cudaEventRecord(src->ev_xfer, src->s_lm));
   CK(cudaStreamWaitEvent(dst->s_lm, src->ev_xfer, 0));
-  CK(cudaMemcpyAsync(dst->d_links, links, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, dst->s_lm));
-  launch_link_tokens(dst->d_links, n, src->token_store, src->cfg.max_ctx,
+  CK(cudaMemcpyAsync(dl, hl, static_cast<size_t>(n) * 16, cudaMemcpyHostToDevice, dst->s_lm));
+  launch_link_tokens(dl, n, src->token_store, src->cfg.max_ctx,
                      mode == 0 ? dst->token_store : dst->frame_store, dst->cfg.max_ctx, dst->nfc, offset, mode,
                      dst->s_lm);
   CK(cudaGetLastError());
-  CK(cudaStreamSynchronize(dst->s_lm));  // `links` is a pageable host buffer of the caller
+  CK(cudaEventRecord(dst->ev_links[e], dst->s_lm));
   return VOX_OK;
 }
 
