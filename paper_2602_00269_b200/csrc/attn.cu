@@ -454,8 +454,11 @@ static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16
 
 int attn_pick_splits(int n_rows, int n_kv) {
   if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) return atoi(e) < 1 ? 1 : atoi(e);  // debug
+  // split only when the items would leave at least half of the 2-per-SM CTA
+  // slots idle: the combine launch costs more than a partly filled wave
+  // (CosyVoice2-style LM at 128 rows x 2 kv heads: 1.38 -> 1.19 ms/step unsplit)
   const int ctas = n_rows * n_kv;
-  int s = (2 * kNumSMs + ctas - 1) / ctas;
+  int s = (2 * kNumSMs) / ctas;
   if (s > kAttnMaxSplits) s = kAttnMaxSplits;
   if (n_rows > kAttnSplitRows) s = 1;
   return s < 1 ? 1 : s;
