@@ -338,10 +338,46 @@ def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: flo
         ms, cnt, by = dev.timing_read(cls)
         classes[cls] = dict(ms=ms / n, launches=cnt // n, bytes=by / n)
     dev.timing(False)
+    sweep = batch_sweep(dev, slots, ctx, hbm, tflops)
     for s in slots:
         dev.release(s)
     step_ms = sum(v["ms"] for v in classes.values())
-    return classes, step_ms, ctx
+    return classes, step_ms, ctx, sweep
+
+
+def batch_sweep(dev, slots, ctx: int, hbm: float, tflops: float):
+    """Config 2 batch sweep: graph-captured decode step (head + sampler
+    included) over the first b of the filled slots at context ctx, CUDA events on the LM
+    stream; HBM roofline bytes = serving weights + b * ctx * KV bytes per token."""
+    import torch
+
+    cfg = dev.cfg
+    d, hd = cfg.d_model, cfg.head_dim
+    proj = 2 * cfg.n_layers * ((cfg.n_heads + 2 * cfg.n_kv_heads) * hd * d + d * cfg.n_heads * hd + 3 * d * cfg.d_ff)
+    head = 2 * cfg.frame_tokens * cfg.codebook_size * d
+    flops_tok = proj + head  # 2 FLOP per bf16 weight (2 bytes) per row
+    lm_s, _ = dev.streams()
+    st = torch.cuda.ExternalStream(lm_s)
+    out = []
+    for b in [1, 2, 4, 8, 16, 32, 64, 128, 192, 224, 256]:
+        if b > len(slots):
+            break
+        rows = np.array([[s, ctx - 1, -1, 1] for s in slots[:b]], np.int32)
+        for _ in range(2):
+            dev.forward(rows)
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(st)
+        for _ in range(10):
+            dev.forward(rows)
+        eb.record(st)
+        torch.cuda.synchronize()
+        ms = ea.elapsed_time(eb) / 10
+        by = proj + head + b * ctx * cfg.kv_bytes_per_token
+        out.append({"batch": b, "ms_per_step": round(ms, 4), "tokens_per_s": round(b / ms * 1e3, 1),
+                    "audio_s_per_s": round(b / ms * 1e3 / 86.0, 1), "hbm_gbs": round(by / ms / 1e6, 1),
+                    "hbm_frac": round(by / ms / 1e6 / hbm, 4),
+                    "tflops": round(flops_tok * b / ms / 1e9, 1)})
+    return out
 
 
 def roofline_summary(cfg, classes, B: int, ctx: int, hbm: float, tfl: float, peak_kind: str):
@@ -610,9 +646,10 @@ def main():
 
     roof = None
     if not args.no_roofline and rank == 0:
-        classes, step_ms, ctx = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77, hbm, tfl)
+        classes, step_ms, ctx, sweep = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77, hbm, tfl)
         roof = roofline_summary(cfg, classes, args.batch, ctx, hbm, tfl, peak_kind)
         roof["eager_step_ms"] = round(step_ms, 3)
+        roof["batch_sweep"] = {"ctx": ctx, "points": sweep}
 
     slo = None
     if not args.no_slo:

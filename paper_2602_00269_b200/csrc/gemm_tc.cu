@@ -350,8 +350,11 @@ __device__ __forceinline__ void mc_epilogue(const GemmArgs& p, uint8_t* smem, ui
   const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
   const int nv = min(BN, p.N - n0);  // valid columns of this tile
   if (p.epi == 1) {
-    float* sg = reinterpret_cast<float*>(smem);  // [BN][64] gate, then [BN][64] up
-    float* dst = sg + (q >= 2 ? BN * 64 : 0) + (q & 1) * 32 + lane;
+    // [kChunks*32][64] gate, then the same for up: whole 32-column chunks are
+    // parked (BN = 16 still loads 32 TMEM columns)
+    constexpr int kRowsP = kChunks * 32;
+    float* sg = reinterpret_cast<float*>(smem);
+    float* dst = sg + (q >= 2 ? kRowsP * 64 : 0) + (q & 1) * 32 + lane;
 #pragma unroll 1
     for (int ch = h; ch < kChunks; ch += 2) {
       uint32_t r[32];
@@ -362,7 +365,7 @@ __device__ __forceinline__ void mc_epilogue(const GemmArgs& p, uint8_t* smem, ui
       for (int j = 0; j < 32; ++j) d[j * 64] = __uint_as_float(r[j]);
     }
     __syncthreads();
-    const float* su = sg + BN * 64;
+    const float* su = sg + kRowsP * 64;
     const int fp = lane * 2;
     __nv_bfloat162* out = reinterpret_cast<__nv_bfloat162*>(p.act + static_cast<int64_t>(n0) * p.ld_act +
                                                             (m0 / 128) * 64 + fp);
@@ -444,7 +447,7 @@ struct McCfg {
   }
   // the fused-SiLU epilogue parks gate and up ([BN][64] fp32 each) in the ring
   __host__ __device__ static int ring_bytes(int st, int epi) {
-    const int r = st * kStageBytes, e = epi == 1 ? 2 * BN * 64 * 4 : 0;
+    const int r = st * kStageBytes, e = epi == 1 ? 2 * ((BN + 31) / 32 * 32) * 64 * 4 : 0;
     return r > e ? r : e;
   }
   static int smem_bytes(int st, int epi) { return ring_bytes(st, epi) + 1024 + 256; }
@@ -1100,7 +1103,8 @@ GemmPlan gemm_plan(int M, int rows, int K) {
   // the co-resident CTA slots).  Callers fall back to the plan below when the
   // weights are not in the packed layout.
   const char* mce = getenv("VOX_GEMM_MC");
-  if (rows >= 64 && rows <= 256 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
+  static const int mc_min_rows = getenv("VOX_GEMM_MC_MIN_ROWS") ? atoi(getenv("VOX_GEMM_MC_MIN_ROWS")) : 1;  // B=1 step 2.29 -> 2.03 ms
+  if (rows >= mc_min_rows && rows <= 256 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
     int bn = 256;
     for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
       if (rows <= b) { bn = b; break; }
