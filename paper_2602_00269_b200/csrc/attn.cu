@@ -95,7 +95,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     attn_decode_kernel(const RowDev* __restrict__ rows, const bf16* __restrict__ q,
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
-                       float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched) {
+                       float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched,
+                       int fuse_combine) {
   VOX_TRACE(kTrAttn);
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
@@ -108,6 +109,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __shared__ float s_m[4][G], s_l[4][G];
   __shared__ __align__(16) float s_acc[4][G][HD];
   __shared__ int s_pt[2][kAttnItemPages];
+  __shared__ int s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ps = dm.page_size;
@@ -367,6 +369,35 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             }
           }
         }
+        if (n_split > 1 && fuse_combine) {
+          // the last split of (row, kv head) to finish merges all n_split partials in
+          // fixed z order (deterministic whichever CTA is last): no combine launch
+          __threadfence();
+          named_bar_consumers();
+          int* cnt = sched + 2 + m.row * dm.n_kv + m.kvh;
+          if (tid == 0) s_last = (atomicAdd(cnt, 1) == n_split - 1);
+          named_bar_consumers();
+          if (s_last) {
+            __threadfence();
+            const float* base = ws + (static_cast<int64_t>(m.row) * dm.n_kv + m.kvh) * n_split * G * (HD + 2);
+            for (int idx = tid; idx < G * HD; idx += 128) {
+              const int g = idx / HD, dd = idx % HD;
+              float M = -INFINITY;
+              for (int zz = 0; zz < n_split; ++zz)
+                M = fmaxf(M, __ldcg(base + zz * G * (HD + 2) + g * (HD + 2) + HD));
+              float Ls = 0.f, A = 0.f;
+              for (int zz = 0; zz < n_split; ++zz) {
+                const float* pz = base + zz * G * (HD + 2) + g * (HD + 2);
+                const float mz = __ldcg(pz + HD);
+                const float f = (mz == -INFINITY) ? 0.f : exp2f(mz - M);
+                Ls += __ldcg(pz + HD + 1) * f;
+                A += __ldcg(pz + dd) * f;
+              }
+              out[(static_cast<int64_t>(m.row) * dm.n_heads + m.kvh * G + g) * HD + dd] = __float2bfloat16_rn(A / Ls);
+            }
+            if (tid == 0) *cnt = 0;
+          }
+        }
         named_bar_consumers();  // s_acc / s_m / s_l are reused by the next item
       }
     }
@@ -422,9 +453,15 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
   }
   const int n_items = n * dm.n_kv * n_split;
   const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
+  // VOX_ATTN_FUSED_COMBINE=1: the last split CTA of each (row, kv head) merges the
+  // partials (no combine launch).  Measured slower than the separate combine kernel
+  // (B=1 decode 2.06 -> 2.29 ms, CSM frame 8.58 -> 9.30 ms): every split item pays a
+  // fence + two consumer barriers + an atomic, and the merge lengthens the last
+  // CTA's critical path.  Kept opt-in.
+  static const int fuse = getenv("VOX_ATTN_FUSED_COMBINE") ? 1 : 0;
   launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), smem, st, rows, q, kc, vc, pt, dm,
-           out, ws, n_split, n_items, sched);
-  if (n_split > 1)
+           out, ws, n_split, n_items, sched, fuse);
+  if (n_split > 1 && !fuse)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
              out);
 }

@@ -526,8 +526,13 @@ static int create_buffers(VoxCtx* c) {
   c->h_seed.assign(g.max_slots, 0);
 
   CK(dalloc(&c->d_rows, static_cast<size_t>(R)));
-  CK(dalloc(&c->attn_sched, 2));
-  CK(cudaMemset(c->attn_sched, 0, 2 * sizeof(int)));
+  // [0..1] persistent work counters, [2 + row * n_kv + kvh] split arrival counters
+  // (the last split of a (row, kv head) combines the partials; all self-resetting)
+  {
+    const size_t ns = 2 + static_cast<size_t>(R) * g.n_kv_heads;
+    CK(dalloc(&c->attn_sched, ns));
+    CK(cudaMemset(c->attn_sched, 0, ns * sizeof(int)));
+  }
   CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
   CK(dalloc(&c->d_out_index, static_cast<size_t>(R)));
   CK(dalloc(&c->d_tokens, static_cast<size_t>(R)));

@@ -53,20 +53,20 @@ def main():
     for i in range(0, a.batch, per):
         rows = np.array([[s, p, -1, 0] for s in slots[i:i + per] for p in range(a.ctx - 1)], np.int32)
         dev.forward(rows, sample=False)
-    for w in range(3):
-        rows = np.array([[s, a.ctx - 1 + w, -1, 1] for s in slots], np.int32)
+    for w in range(8):  # >= 7: one graph per head frame slot when every row shares it
+        rows = np.array([[s, a.ctx - 8 + w, -1, 1] for s in slots], np.int32)
         dev.forward(rows)
     dev.synchronize()
     import time
     t = time.perf_counter()
     for step in range(a.steps):
-        rows = np.array([[s, a.ctx - 1 + 3 + step, -1, 1] for s in slots], np.int32)
+        rows = np.array([[s, a.ctx + step, -1, 1] for s in slots], np.int32)
         dev.forward(rows)
     dev.synchronize()
     print(f"untraced wall {(time.perf_counter() - t) * 1e3 / a.steps:.3f} ms/step")
     dev.trace_arm()
     for step in range(a.steps):
-        rows = np.array([[s, a.ctx + 2 + a.steps + step, -1, 1] for s in slots], np.int32)
+        rows = np.array([[s, a.ctx + a.steps + step, -1, 1] for s in slots], np.int32)
         dev.forward(rows)
     dev.synchronize()
     rec = dev.trace_read()
