@@ -1104,11 +1104,15 @@ GemmPlan gemm_plan(int M, int rows, int K) {
   // weights are not in the packed layout.
   const char* mce = getenv("VOX_GEMM_MC");
   static const int mc_min_rows = getenv("VOX_GEMM_MC_MIN_ROWS") ? atoi(getenv("VOX_GEMM_MC_MIN_ROWS")) : 1;  // B=1 step 2.29 -> 2.03 ms
-  if (rows >= mc_min_rows && rows <= 256 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
+  if (rows >= mc_min_rows && rows <= 512 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
+    // <= 256 rows: one n-tile (each weight byte read once); 257..512 rows (decode
+    // plus a burst of prefill rows): two n-tiles of half the rows each
+    const int ntiles = rows > 256 ? 2 : 1;
+    const int per_tile = (rows + ntiles - 1) / ntiles;
     int bn = 256;
     for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
-      if (rows <= b) { bn = b; break; }
-    const int mtiles = (M + 127) / 128;
+      if (per_tile <= b) { bn = b; break; }
+    const int mtiles = (M + 127) / 128 * ntiles;  // CTAs per split
     // Multicast is measured SLOWER than cs = 1 on every decode shape
     // (profiles/gemm_mc_sweep_r01.txt): with one n-tile the activation L2
     // reads are not the bound -- the k-loop already streams weights at HBM
@@ -1117,7 +1121,7 @@ GemmPlan gemm_plan(int M, int rows, int K) {
     int cs = 1;
     if (const char* e = getenv("VOX_GEMM_CS_TEST")) {
       const int f = atoi(e);
-      if ((f == 1 || f == 2 || f == 4 || f == 8) && mtiles % f == 0 && (bn / f) % 8 == 0) cs = f;
+      if ((f == 1 || f == 2 || f == 4 || f == 8) && ((M + 127) / 128) % f == 0 && (bn / f) % 8 == 0) cs = f;
     }
     const int cap = gemm_mc_capacity(bn, cs, 1);
     int best = 1;

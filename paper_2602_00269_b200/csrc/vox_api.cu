@@ -56,7 +56,7 @@ enum TensorId : uint64_t {
 // decode-step row buckets (one CUDA graph each): steps of 32 rows between 64
 // and 256 so a step pays at most 31 padding rows of tensor work -- at ~224 rows
 // the projections are at the tensor/HBM ridge
-constexpr int kBuckets[] = {16, 32, 64, 96, 128, 160, 192, 224, 256, 512, 1024, 2048};
+constexpr int kBuckets[] = {16, 32, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512, 1024, 2048};
 constexpr int kTicketRing = 32;  // in-flight detok calls (VOX_TICKET_RING in voxb200.h)
 
 struct TimingRec {

@@ -65,3 +65,15 @@ def test_gemm_split_k_cluster_reduction(tiny_dev, monkeypatch, M, N, K, splits):
     ref = x.astype(np.float64) @ w.astype(np.float64).T
     err = np.abs(out - ref).max()
     assert err < 1e-3 * np.sqrt(K), err
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 300, 512), (2048, 512, 1024), (640, 448, 768)])
+def test_gemm_two_row_tiles(tiny_dev, monkeypatch, M, N, K):
+    """257..512 rows: the decode GEMM splits the rows over two n-tiles."""
+    monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
+    rng = np.random.default_rng(M + N)
+    w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
+    x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
+    out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), None, 1)
+    ref = x.astype(np.float64) @ w.astype(np.float64).T
+    assert np.abs(out - ref).max() < 1e-3 * np.sqrt(K)
