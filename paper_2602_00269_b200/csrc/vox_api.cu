@@ -1125,10 +1125,8 @@ int vox_project_ext(VoxCtx* c, VoxCtx* src, int32_t n) {
   CK(cudaStreamWaitEvent(c->s_lm, src->ev_xfer, 0));
   const CUtensorMap& tw_unused = c->tm_head_full;
   const int M = c->cfg.d_model, K = c->cfg.ext_dim;
-  GemmPlan pl = gemm_plan(M, n, K);
-  const int splits = 1;  // one plane straight into ext[n][d]
-  (void)pl;
-  return run_gemm(c, tw_unused, xm, M, n, K, c->ext, M, splits, nullptr, nullptr, 0, M, c->s_lm, "gemm",
+  // one split: the result lands as a single fp32 plane straight in ext[n][d]
+  return run_gemm(c, tw_unused, xm, M, n, K, c->ext, M, 1, nullptr, nullptr, 0, M, c->s_lm, "gemm",
                   c->w_proj, nullptr);
 }
 
