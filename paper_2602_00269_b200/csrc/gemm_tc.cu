@@ -1124,8 +1124,9 @@ GemmPlan gemm_plan(int M, int rows, int K) {
       if ((f == 1 || f == 2 || f == 4 || f == 8) && ((M + 127) / 128) % f == 0 && (bn / f) % 8 == 0) cs = f;
     }
     const int cap = gemm_mc_capacity(bn, cs, 1);
+    static const int max_splits = getenv("VOX_GEMM_MAX_SPLITS") ? atoi(getenv("VOX_GEMM_MAX_SPLITS")) : kGemmMaxSplits;
     int best = 1;
-    for (int s2 = 1; s2 <= kGemmMaxSplits; ++s2) {
+    for (int s2 = 1; s2 <= max_splits; ++s2) {
       const int per = (n_kb + s2 - 1) / s2;
       if (per < 2) break;
       if ((n_kb + per - 1) / per != s2) continue;  // every split non-empty
