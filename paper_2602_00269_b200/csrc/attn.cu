@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
                        float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched,
-                       int fuse_combine) {
+                       int fuse_combine, int l2pf) {
   VOX_TRACE(kTrAttn);
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
@@ -200,6 +200,17 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                             : page_table[static_cast<int64_t>(cur.slot) * dm.max_pages_per_slot + pa + jp];
         const int64_t base = (static_cast<int64_t>(pid) * dm.n_kv + cur.kvh) * page_elems;
         bulk_load(stage_ptr(s, jp, kv), (kv ? vc : kc) + base, page_elems * 2, &full[s], pol);
+        // l2pf > 0: also pull this item's pages l2pf stages ahead into L2 -- the
+        // smem ring (96 KB per CTA) caps the bytes in flight per SM; L2
+        // prefetches add memory-level parallelism without smem
+        const int off2 = off + l2pf * kP;
+        if (l2pf > 0 && cur.begin + off2 < cur.end) {
+          const int pid2 = off2 < kAttnItemPages
+                               ? s_pt[buf][off2]
+                               : page_table[static_cast<int64_t>(cur.slot) * dm.max_pages_per_slot + cur.begin + off2];
+          prefetch_l2_bulk((kv ? vc : kc) + (static_cast<int64_t>(pid2) * dm.n_kv + cur.kvh) * page_elems,
+                           page_elems * 2);
+        }
       } else if (lane == 2 * kP && cur.rr == 0 && with_q) {
         bulk_load(q_slot(s), q + (static_cast<int64_t>(cur.row) * dm.n_heads + cur.kvh * G) * HD,
                   kQBytes, &full[s], pol);
@@ -459,8 +470,9 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
   // fence + two consumer barriers + an atomic, and the merge lengthens the last
   // CTA's critical path.  Kept opt-in.
   static const int fuse = getenv("VOX_ATTN_FUSED_COMBINE") ? 1 : 0;
+  static const int l2pf = getenv("VOX_ATTN_L2PF") ? atoi(getenv("VOX_ATTN_L2PF")) : 0;
   launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), smem, st, rows, q, kc, vc, pt, dm,
-           out, ws, n_split, n_items, sched, fuse);
+           out, ws, n_split, n_items, sched, fuse, l2pf);
   if (n_split > 1 && !fuse)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
              out);
