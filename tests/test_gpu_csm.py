@@ -97,3 +97,23 @@ def test_greedy_frames_vs_oracle(csm):
     assert checked >= 0.75 * R * F * C, (checked, ties)
     for s in streams:
         pipe.release(s)
+
+
+def test_stochastic_frames_deterministic_and_in_range(csm):
+    """Sampled (T 0.9, top-k 50) frames: every code lies in its codebook's range, and the
+    same seeds reproduce the same frames (counter-based RNG keyed by request seed/step)."""
+    bcfg, dcfg, bb, dp, _, _ = csm
+    pipe = CsmFrames(bb, dp)
+    prm = Sampling(temperature=0.9, top_k=50, repetition_penalty=1.0)
+    runs = []
+    for _ in range(2):
+        streams = [pipe.admit(request_seed(8, r), 10, 4, prm, prm) for r in range(2)]
+        pipe.prefill(streams)
+        for _ in range(2):
+            pipe.step(streams)
+        runs.append(np.array([[pipe.frame(s, 10 + f) for f in range(2)] for s in streams]))
+        for s in streams:
+            pipe.release(s)
+    assert ((runs[0] >= 0) & (runs[0] < bcfg.codebook_size)).all()
+    assert np.array_equal(runs[0], runs[1])
+    assert len(np.unique(runs[0])) > 4  # not collapsed onto one code

@@ -166,3 +166,29 @@ def test_greedy_tokens_bit_exact_config1(tiny_dev, tiny_cfg):
     for r, sl in enumerate(slots):
         tiny_dev.release(sl)
         orc.release(r)
+
+
+@pytest.mark.parametrize("n_req,P", [(3, 33), (6, 50), (11, 30)])
+def test_mixed_batch_row_buckets(tiny_cfg, n_req, P):
+    """Prefill + decode rows of many requests in ONE forward: 96..330 rows exercise the
+    32-row graph buckets, the decode GEMM's tile widths and its two-n-tile path
+    (257..512 rows); every request's next-token logits match the oracle."""
+    from paper_2602_00269_b200.device import VoxDevice
+
+    c = tiny_cfg.with_capacity(max_slots=16)
+    dev = VoxDevice(c, weight_seed=1234)
+    orc = LlamaOracle(c, 1234)
+    slots, prompts = [], []
+    for r in range(n_req):
+        seed = request_seed(11, 100 * n_req + r)
+        slots.append(dev.admit(seed, P, 8, Sampling(temperature=0.0)))
+        prompts.append(np.array(prompt_ids(seed, P, c.text_vocab)))
+    # all prompts in one forward; only the last position of each request is sampled
+    rows = np.array([[s, p, -1, int(p == P - 1)] for s in slots for p in range(P)], np.int32)
+    assert rows.shape[0] >= 96
+    _, lg = dev.forward(rows, sample=False, full_logits=True, sync=True, graph=False)
+    for r in range(n_req):
+        ol, _ = orc.forward(r, prompts[r], np.arange(P))
+        err = np.abs(lg[r] - ol[-1]).max()
+        assert err < 2e-2 * max(1.0, np.abs(ol[-1]).max()), (r, err)
+    dev.close()
