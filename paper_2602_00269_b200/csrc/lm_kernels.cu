@@ -18,6 +18,7 @@
 // Rows with slot < 0 are padding and are skipped.
 #include "common.cuh"
 #include "kernels.h"
+#include <cstdlib>
 
 namespace vox {
 VOX_TRACE_TU(trace_set_lm)
@@ -35,6 +36,21 @@ VOX_DEV float block_sum256(float v, float* red) {
   }
   __syncthreads();
   return red[8];
+}
+
+// block-wide sum for blockDim.x <= 1024 (multiple of 32); red holds >= 33 floats
+VOX_DEV float block_sum_any(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float t = (l < nw) ? red[l] : 0.f;
+    t = warp_sum(t);
+    if (l == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
 }
 
 VOX_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
@@ -240,14 +256,15 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const fl
                             int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
-  launch_k(qkv_rope_append_kernel, dim3(n, 2), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
+  static const int gy = getenv("VOX_ROPE_Y") ? atoi(getenv("VOX_ROPE_Y")) : 2;
+  launch_k(qkv_rope_append_kernel, dim3(n, gy), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
            rope, page_table, kc, vc, q_out);
 }
 
 // ---------------------------------------------------------------------------
 // split-K reduce + residual add + RMSNorm (optionally compacting output rows)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
     resid_norm_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, int splits,
                       int64_t split_stride, int d, float eps, float* __restrict__ h,
                       const float* __restrict__ nw, bf16* __restrict__ x_out,
@@ -255,16 +272,17 @@ __global__ void __launch_bounds__(256)
   VOX_TRACE(kTrResidNorm);
   griddep_wait();
   griddep_launch();
-  __shared__ float red[9];
+  __shared__ float red[33];
   const int r = blockIdx.x;
   if (rows[r].slot < 0) return;
   float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
   const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * d);
   const int64_t ss4 = split_stride / 4;
   const int d4 = d / 4;
+  const int nt = blockDim.x;
   float ss = 0.f;
 #pragma unroll 4
-  for (int i = threadIdx.x; i < d4; i += 256) {
+  for (int i = threadIdx.x; i < d4; i += nt) {
     const float4 v = add4(h4[i], sum_splits4(w4, splits, ss4, i));
     h4[i] = v;
     ss = fmaf(v.x, v.x, ss);
@@ -272,19 +290,20 @@ __global__ void __launch_bounds__(256)
     ss = fmaf(v.z, v.z, ss);
     ss = fmaf(v.w, v.w, ss);
   }
-  ss = block_sum256(ss, red);
+  ss = block_sum_any(ss, red);
   const int orow = out_index ? out_index[r] : r;
   if (orow < 0) return;
   const float inv = 1.0f / sqrtf(ss / static_cast<float>(d) + eps);
   const float4* n4 = reinterpret_cast<const float4*>(nw);
   bf16* xr = x_out + static_cast<int64_t>(orow) * d;
-  for (int i = threadIdx.x; i < d4; i += 256) norm_store4(xr + 4 * i, h4[i], inv, n4[i]);
+  for (int i = threadIdx.x; i < d4; i += nt) norm_store4(xr + 4 * i, h4[i], inv, n4[i]);
 }
 
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st) {
-  launch_k(resid_norm_kernel, dim3(n), dim3(256), 0, st, rows, ws, splits, split_stride, dm.d,
+  static const int nt = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 256;
+  launch_k(resid_norm_kernel, dim3(n), dim3(nt), 0, st, rows, ws, splits, split_stride, dm.d,
            dm.eps, h, norm_w, x_out, out_index);
 }
 
