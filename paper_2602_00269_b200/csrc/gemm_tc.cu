@@ -14,6 +14,7 @@
 // warps run the epilogue (tcgen05.ld 32x32b -> registers -> coalesced stores).
 #include "common.cuh"
 #include "kernels.h"
+#include "rownorm.cuh"
 #include <cstdlib>
 
 namespace vox {
@@ -451,7 +452,8 @@ struct McCfg {
     return r > e ? r : e;
   }
   static int smem_bytes(int st, int epi) { return ring_bytes(st, epi) + 1024 + 256; }
-  static constexpr int kSmemMax = 8 * kStageBytes + 1024 + 256 > 227 * 1024 ? 227 * 1024 : 8 * kStageBytes + 1024 + 256;
+  // dynamic smem cap: 227 KB minus the static smem of the fused-norm prologue
+  static constexpr int kSmemMax = 8 * kStageBytes + 1024 + 256 > 226 * 1024 ? 226 * 1024 : 8 * kStageBytes + 1024 + 256;
 };
 
 template <int BN, int CS>
@@ -505,16 +507,48 @@ __global__ void __launch_bounds__(256, 1)
   long long t_first = 0, t_lastmma = 0;
 
   griddep_launch();
+  const uint64_t pol_w = policy_evict_first();
+  const int pre = nkb < nst ? nkb : nst;
   if (warp == 0 && lane == 0) {
-    // ---------------- producer: own weight tile + this CTA's activation slice ----------------
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
-    const int pre = nkb < nst ? nkb : nst;
     for (int i = 0; i < pre; ++i) {  // weights do not depend on the preceding kernel
       mbar_arrive_expect_tx(&full[i], C::kStageBytes);
       bulk_load(smem + i * C::kStageBytes, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[i],
                 pol_w);
     }
+  }
+  if (p.nrm_rows != nullptr) {
+    // fused residual + RMSNorm of the rows this GEMM consumes (replaces a
+    // resid_norm launch and its kernel boundary); the weight stages stream in
+    __shared__ float red[33];
+    griddep_wait();
+    const int nct = static_cast<int>(gridDim.x * gridDim.y * gridDim.z);
+    const int cta = static_cast<int>((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
+    for (int r = cta; r < p.nrm_n; r += nct)
+      if (p.nrm_rows[r].slot >= 0)
+        resid_norm_row(r, p.nrm_ws, p.nrm_splits, p.nrm_ss, p.nrm_d, p.nrm_eps, p.nrm_h, p.nrm_w, p.nrm_x,
+                       r, red);
+    // grid barrier (generation-counted, self-resetting): every normalised row is
+    // written before any CTA's TMA reads the activation buffer
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      volatile int* gen = p.nrm_bar + 1;
+      const int g0 = *gen;
+      __threadfence();
+      if (atomicAdd(p.nrm_bar, 1) == nct - 1) {
+        p.nrm_bar[0] = 0;
+        __threadfence();
+        atomicAdd(p.nrm_bar + 1, 1);
+      } else {
+        while (*gen == g0) __nanosleep(64);
+      }
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+    }
+    __syncthreads();
+  }
+  if (warp == 0 && lane == 0) {
+    // ---------------- producer: activation slices (and the remaining weights) ----------------
+    const uint64_t pol_x = policy_evict_last();
     griddep_wait();
     const int xoff = C::kABytes + rank * kSlice * 128;
     for (int i = 0; i < pre; ++i) {

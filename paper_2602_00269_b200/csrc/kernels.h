@@ -54,6 +54,19 @@ struct GemmArgs {
   int stages;             // mc kernel: smem ring depth (set by the launcher)
   int red;                // mc kernel: splits reduced in a (1,1,splits) cluster -> one plane
   unsigned long long* dbg; // gemm_test only: per-CTA clock64 stamps (VOX_GEMM_DBG=1)
+  // fused RMSNorm prologue (mc kernel; nrm_rows != null): the CTAs first run
+  // resid_norm_row over rows (cta, cta + n_ctas, ...) -- the preceding GEMM's
+  // split planes + residual -> h, bf16 normalised rows -> the activation
+  // buffer this GEMM reads -- then meet at a grid barrier (all CTAs resident)
+  const struct RowDev* nrm_rows;
+  int nrm_n, nrm_splits, nrm_d;
+  int64_t nrm_ss;
+  const float* nrm_ws;
+  float* nrm_h;
+  const float* nrm_w;
+  bf16* nrm_x;
+  float nrm_eps;
+  int* nrm_bar;           // {arrivals, generation}, self-resetting
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };

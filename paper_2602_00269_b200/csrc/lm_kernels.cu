@@ -18,65 +18,12 @@
 // Rows with slot < 0 are padding and are skipped.
 #include "common.cuh"
 #include "kernels.h"
+#include "rownorm.cuh"
 #include <cstdlib>
 
 namespace vox {
 VOX_TRACE_TU(trace_set_lm)
 
-
-VOX_DEV float block_sum256(float v, float* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = (l < 8) ? red[l] : 0.f;
-    t = warp_sum(t);
-    if (l == 0) red[8] = t;
-  }
-  __syncthreads();
-  return red[8];
-}
-
-// block-wide sum for blockDim.x <= 1024 (multiple of 32); red holds >= 33 floats
-VOX_DEV float block_sum_any(float v, float* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float t = (l < nw) ? red[l] : 0.f;
-    t = warp_sum(t);
-    if (l == 0) red[32] = t;
-  }
-  __syncthreads();
-  return red[32];
-}
-
-VOX_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-
-// sum of the split-K partial planes at float4 index i (fixed split order)
-VOX_DEV float4 sum_splits4(const float4* __restrict__ w, int splits, int64_t split_stride4,
-                           int64_t i) {
-  float4 a = w[i];
-  for (int s = 1; s < splits; ++s) a = add4(a, w[s * split_stride4 + i]);
-  return a;
-}
-
-VOX_DEV void store_bf16x4(bf16* dst, float a, float b, float c, float d) {
-  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b);
-  __nv_bfloat162 hi = __floats2bfloat162_rn(c, d);
-  uint2 u;
-  u.x = *reinterpret_cast<uint32_t*>(&lo);
-  u.y = *reinterpret_cast<uint32_t*>(&hi);
-  *reinterpret_cast<uint2*>(dst) = u;
-}
-
-// x = bf16(h * inv * w) in the oracle's rounding order (two fp32 products)
-VOX_DEV void norm_store4(bf16* x, float4 h, float inv, float4 w) {
-  store_bf16x4(x, __fmul_rn(__fmul_rn(h.x, inv), w.x), __fmul_rn(__fmul_rn(h.y, inv), w.y),
-               __fmul_rn(__fmul_rn(h.z, inv), w.z), __fmul_rn(__fmul_rn(h.w, inv), w.w));
-}
 
 // ---------------------------------------------------------------------------
 // embedding gather + first RMSNorm
@@ -275,28 +222,7 @@ __global__ void __launch_bounds__(1024)
   __shared__ float red[33];
   const int r = blockIdx.x;
   if (rows[r].slot < 0) return;
-  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
-  const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * d);
-  const int64_t ss4 = split_stride / 4;
-  const int d4 = d / 4;
-  const int nt = blockDim.x;
-  float ss = 0.f;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < d4; i += nt) {
-    const float4 v = add4(h4[i], sum_splits4(w4, splits, ss4, i));
-    h4[i] = v;
-    ss = fmaf(v.x, v.x, ss);
-    ss = fmaf(v.y, v.y, ss);
-    ss = fmaf(v.z, v.z, ss);
-    ss = fmaf(v.w, v.w, ss);
-  }
-  ss = block_sum_any(ss, red);
-  const int orow = out_index ? out_index[r] : r;
-  if (orow < 0) return;
-  const float inv = 1.0f / sqrtf(ss / static_cast<float>(d) + eps);
-  const float4* n4 = reinterpret_cast<const float4*>(nw);
-  bf16* xr = x_out + static_cast<int64_t>(orow) * d;
-  for (int i = threadIdx.x; i < d4; i += nt) norm_store4(xr + 4 * i, h4[i], inv, n4[i]);
+  resid_norm_row(r, ws, splits, split_stride, d, eps, h, nw, x_out, out_index ? out_index[r] : r, red);
 }
 
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,

@@ -171,6 +171,11 @@ struct VoxCtx {
   // ---- per-step staging
   RowDev* d_rows = nullptr;
   int* attn_sched = nullptr;  // persistent attention work counters (self-resetting)
+  int* nrm_bar = nullptr;     // grid barrier of the GEMMs' fused norm prologue
+  // opt-in (VOX_FUSE_NORM=1): measured slower (750 -> 727 audio-s/s): 128 CTAs
+  // normalising ~2 rows each serially + a grid barrier take longer than the
+  // 224-CTA resid_norm launch whose boundary PDL already overlaps
+  bool fuse_norm = getenv("VOX_FUSE_NORM") && atoi(getenv("VOX_FUSE_NORM")) == 1;
   int* d_sample_rows = nullptr;
   int* d_out_index = nullptr;
   int* d_tokens = nullptr;
@@ -296,7 +301,8 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm", const bf16* wp = nullptr,
                     const CUtensorMap* twp = nullptr, bf16* act_out = nullptr,
-                    int64_t ld_act = 0, int* planes_out = nullptr) {
+                    int64_t ld_act = 0, int* planes_out = nullptr,
+                    const GemmArgs* nrm = nullptr) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
   if (plan.mc && wp == nullptr) plan = gemm_plan_1cta(M, rows, K);  // mc streams packed tiles only
   if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
@@ -322,6 +328,20 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.probe = c->gemm_probe;
   a.l2_prefetch = c->gemm_l2_prefetch;
   a.epi = act_out != nullptr ? 1 : 0;
+  if (nrm != nullptr) {  // fused residual + RMSNorm prologue (mc kernel only)
+    if (!plan.mc) return fail(c, VOX_ERR_INVALID, "fused norm prologue needs the mc GEMM");
+    a.nrm_rows = nrm->nrm_rows;
+    a.nrm_n = nrm->nrm_n;
+    a.nrm_splits = nrm->nrm_splits;
+    a.nrm_d = nrm->nrm_d;
+    a.nrm_ss = nrm->nrm_ss;
+    a.nrm_ws = nrm->nrm_ws;
+    a.nrm_h = nrm->nrm_h;
+    a.nrm_w = nrm->nrm_w;
+    a.nrm_x = nrm->nrm_x;
+    a.nrm_eps = nrm->nrm_eps;
+    a.nrm_bar = nrm->nrm_bar;
+  }
   a.red = (plan.mc && plan.red && splits == plan.splits && a.epi == 0 && bias == nullptr &&
            resid == nullptr) ? 1 : 0;
   if (planes_out) *planes_out = a.red ? 1 : splits;
@@ -533,6 +553,8 @@ static int create_buffers(VoxCtx* c) {
     CK(dalloc(&c->attn_sched, ns));
     CK(cudaMemset(c->attn_sched, 0, ns * sizeof(int)));
   }
+  CK(dalloc(&c->nrm_bar, 2));
+  CK(cudaMemset(c->nrm_bar, 0, 2 * sizeof(int)));
   CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
   CK(dalloc(&c->d_out_index, static_cast<size_t>(R)));
   CK(dalloc(&c->d_tokens, static_cast<size_t>(R)));
@@ -724,6 +746,10 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   const GemmPlan gu_plan = gemm_plan(2 * dff, nrows, d);
   const int sp_gu = gu_plan.splits;
   const int sp_dn = dn_plan.splits;
+  // gate|up CTAs (1 split, mc kernel) all co-resident -> norm fusable
+  const bool gu_norm_fusable = c->fuse_norm && gu_plan.mc && gu_plan.splits == 1 &&
+                               ((2 * dff + 127) / 128) * ((nrows + gu_plan.bn - 1) / gu_plan.bn) <=
+                                   gemm_mc_capacity(gu_plan.bn, 1, 1);
   const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
   const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
   const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
@@ -746,14 +772,33 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st, "gemm", c->w_o + l * n_o, &c->tp_o[l]));
-    {
+    // the O projection's residual + RMSNorm folds into the gate|up GEMM's
+    // prologue when every gate|up CTA is co-resident (its grid barrier needs it)
+    const bool gu_fused = sp_gu == 1 && !gu_plan.pair && !c->silu_unfused;
+    const bool norm_in_gu = gu_fused && gu_norm_fusable;
+    if (!norm_in_gu) {
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_o + 10));
       launch_resid_norm(c->d_rows, nrows, c->ws, pl_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
-    if (sp_gu == 1 && !gu_plan.pair && !c->silu_unfused) {  // SiLU(gate) * up in the epilogue
+    if (gu_fused) {  // SiLU(gate) * up in the epilogue
+      GemmArgs nrm{};
+      if (norm_in_gu) {
+        nrm.nrm_rows = c->d_rows;
+        nrm.nrm_n = nrows;
+        nrm.nrm_splits = pl_o;
+        nrm.nrm_d = d;
+        nrm.nrm_ss = static_cast<int64_t>(nrows) * d;
+        nrm.nrm_ws = c->ws;
+        nrm.nrm_h = c->h;
+        nrm.nrm_w = c->norm_mlp + static_cast<int64_t>(l) * d;
+        nrm.nrm_x = c->x;
+        nrm.nrm_eps = g.rms_eps;
+        nrm.nrm_bar = c->nrm_bar;
+      }
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, 1, nullptr, nullptr,
-                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l], c->act, dff));
+                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l], c->act, dff, nullptr,
+                   norm_in_gu ? &nrm : nullptr));
     } else {
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
                    nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
@@ -926,7 +971,7 @@ void vox_destroy(VoxCtx* c) {
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
-                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links};
+                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links, c->nrm_bar};
   if (c->ev_xfer) cudaEventDestroy(c->ev_xfer);
   for (auto& e : c->ev_links)
     if (e) cudaEventDestroy(e);
