@@ -145,9 +145,20 @@ constexpr int kAttnSplitRows = 128;  // split-KV only for batches up to this man
 int attn_pick_splits(int n_rows, int n_kv);
 // ws: split-KV partials [rows][kv][n_split][G][hd + 2] (unused when n_split == 1)
 // sched: 2 zeroed ints (work counter, done counter), self-resetting per launch
+// Fused q|k|v split-K reduce + bias + RoPE + KV append inside the attention
+// kernel (decode steps whose rows are distinct slots): ws != nullptr enables it
+struct RopeIn {
+  const float* ws;     // QKV GEMM output planes [splits][rows][nqkv]
+  int splits;
+  int64_t ss;          // elements between planes
+  const float2* rope;  // (cos, sin) table [pos][hd / 2]
+  const float* bias;   // [nqkv] or null
+  bf16* kc;            // this layer's K / V pools (append target)
+  bf16* vc;
+};
 void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* page_table, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        int* sched, cudaStream_t st);
+                        int* sched, cudaStream_t st, const RopeIn* rope_in = nullptr);
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st);

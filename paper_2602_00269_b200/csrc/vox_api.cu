@@ -727,7 +727,10 @@ static int create_detok(VoxCtx* c) {
 // ---------------------------------------------------------------------------
 // hslot >= 0: every sampled row is at the same frame slot, so the LM head runs
 // over that slot's codebook rows only (CSM depth decoder: 1 of 31 codebook heads)
-static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1) {
+// fused_rope: every row is a distinct slot (a pure decode step), so the q|k|v
+// reduce + RoPE + KV append runs inside the attention kernel (no rope launch)
+static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1,
+                           bool fused_rope = false) {
   const VoxModelCfg& g = c->cfg;
   const LmDims& dm = c->dm;
   cudaStream_t st = c->s_lm;
@@ -757,7 +760,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   for (int l = 0; l < L; ++l) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
                  nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv, &c->tp_qkv[l]));
-    {
+    if (!fused_rope) {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * pl_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws,
                              c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr, pl_qkv,
@@ -767,8 +770,11 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
     {
       const int asp = attn_pick_splits(nrows, g.n_kv_heads);
       TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
+      const RopeIn ri{c->ws, pl_qkv, static_cast<int64_t>(nrows) * c->nqkv, c->rope_tab,
+                      c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr,
+                      c->kc + l * kv_layer, c->vc + l * kv_layer};
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
-                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st);
+                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st, fused_rope ? &ri : nullptr);
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st, "gemm", c->w_o + l * n_o, &c->tp_o[l]));
@@ -1313,20 +1319,33 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
     }
     if (hslot < 0) hslot = -1;
   }
+  // pure decode step (each slot once): RoPE + KV append fused into attention.
+  // Opt-in (VOX_FUSED_ROPE=1): measured slower (742 -> 691 audio-s/s) -- every
+  // (row, kv head) item pays its q|k|v reduction + RoPE on the consumers'
+  // critical path, and the early-started K/V stream contends with the QKV GEMM
+  bool unique = getenv("VOX_FUSED_ROPE") && atoi(getenv("VOX_FUSED_ROPE")) == 1;
+  {
+    std::vector<int> seen;
+    seen.reserve(n);
+    for (int i = 0; i < n && unique; ++i) seen.push_back(rows[i].slot);
+    std::sort(seen.begin(), seen.end());
+    for (size_t i = 1; i < seen.size() && unique; ++i)
+      if (seen[i] == seen[i - 1]) unique = false;
+  }
   int rc = VOX_OK;
   if (use_graph) {
-    auto key = std::make_tuple(nrows, ns, hslot);
+    auto key = std::make_tuple(nrows, ns, hslot * 2 + (unique ? 1 : 0));
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       // eager pass (executes this step and sets kernel attributes), then capture
-      rc = enqueue_forward(c, nrows, ns, false, hslot);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, unique);
       if (rc != VOX_OK) return rc;
       CK(cudaStreamSynchronize(st));
       const int64_t before = c->launches;
       cudaGraph_t graph;
       c->capturing = true;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_forward(c, nrows, ns, false, hslot);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, unique);
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       c->capturing = false;
       if (rc != VOX_OK) return rc;
@@ -1342,7 +1361,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       c->launches += c->graph_launches[key];
     }
   } else {
-    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot);
+    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot, unique);
     if (rc != VOX_OK) return rc;
   }
   if (nsamp > 0)
