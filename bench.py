@@ -338,11 +338,38 @@ def kernel_roofline(dev, B: int, prompt: int, seed: int, hbm: float, tflops: flo
         ms, cnt, by = dev.timing_read(cls)
         classes[cls] = dict(ms=ms / n, launches=cnt // n, bytes=by / n)
     dev.timing(False)
+    in_graph = traced_classes(dev, rows, classes)
     sweep = batch_sweep(dev, slots, ctx, hbm, tflops)
     for s in slots:
         dev.release(s)
     step_ms = sum(v["ms"] for v in classes.values())
-    return classes, step_ms, ctx, sweep
+    return classes, step_ms, ctx, sweep, in_graph
+
+
+def traced_classes(dev, rows, classes, steps: int = 4):
+    """Per-class time on the LM critical path INSIDE the graph-captured step (PDL
+    overlap included): vox_trace per-CTA spans -> exposed ms per step; achieved =
+    the class's algorithmic bytes per step (as in the eager classes) / exposed time."""
+    from paper_2602_00269_b200 import trace
+
+    for _ in range(8):  # graphs for every head frame slot (rows share one position)
+        dev.forward(rows)
+    dev.synchronize()
+    dev.trace_arm()
+    for _ in range(steps):
+        dev.forward(rows)
+    dev.synchronize()
+    rec = dev.trace_read()
+    ls = trace.launches(rec)
+    ex = trace.exposed(ls, key=lambda tag: trace.CLASS.get(trace.name_of(tag), "?"))
+    span = (max(l["t1max"] for l in ls) - min(l["t0"] for l in ls)) / 1e6 / steps
+    out = {"step_ms": round(span, 4), "classes": {}}
+    for cls, ns in sorted(ex.items(), key=lambda kv: -kv[1]):
+        ms = ns / 1e6 / steps
+        by = sum(classes[c]["bytes"] for c in ([cls, "lm_head"] if cls == "gemm" else [cls]) if c in classes)
+        out["classes"][cls] = {"exposed_ms_per_step": round(ms, 4),
+                               "hbm_gbs": round(by / (ms / 1e3) / 1e9, 1) if ms > 0 else None}
+    return out
 
 
 def batch_sweep(dev, slots, ctx: int, hbm: float, tflops: float):
@@ -646,9 +673,14 @@ def main():
 
     roof = None
     if not args.no_roofline and rank == 0:
-        classes, step_ms, ctx, sweep = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77, hbm, tfl)
+        classes, step_ms, ctx, sweep, in_graph = kernel_roofline(dev, args.batch, args.prompt, args.seed + 77,
+                                                                 hbm, tfl)
         roof = roofline_summary(cfg, classes, args.batch, ctx, hbm, tfl, peak_kind)
         roof["eager_step_ms"] = round(step_ms, 3)
+        for v in in_graph["classes"].values():
+            if v["hbm_gbs"] is not None:
+                v["hbm_frac"] = round(v["hbm_gbs"] / hbm, 4)
+        roof["in_graph"] = in_graph
         roof["batch_sweep"] = {"ctx": ctx, "points": sweep}
 
     slo = None

@@ -15,26 +15,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2602_00269_b200.config import CONFIGS  # noqa: E402
 from paper_2602_00269_b200.device import Sampling, VoxDevice  # noqa: E402
 
-NAMES = {1: "gemm1cta", 2: "gemm_mc", 3: "attn", 4: "attn_comb", 5: "qkv_rope", 6: "resid_norm",
-         7: "embed_norm", 8: "silu", 9: "sampler", 10: "detok", 11: "gemm_pair"}
-
-
-def launches(rec):
-    """Group per-CTA records into launches: a launch = maximal run (by start time) of one tag."""
-    rec = np.sort(rec, order="t0")
-    out = []
-    open_ = {}
-    for r in rec:
-        tag = int(r["tag"])
-        cur = open_.get(tag)
-        if cur is not None and r["t0"] <= cur["t1max"] + 500 and cur["n"] < (tag >> 8):
-            cur["n"] += 1
-            cur["t1max"] = max(cur["t1max"], int(r["t1"]))
-            continue
-        cur = {"tag": tag, "t0": int(r["t0"]), "t1max": int(r["t1"]), "n": 1}
-        open_[tag] = cur
-        out.append(cur)
-    return out
+from paper_2602_00269_b200.trace import NAMES, launches  # noqa: E402
 
 
 def main():
