@@ -609,7 +609,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=50)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--slo-seconds", type=float, default=12.0)
-    ap.add_argument("--slo-rates", default="72,80,88,92,96,104")
+    ap.add_argument("--slo-rates", default="72,80,88,92,94,96,104")
     ap.add_argument("--no-slo", action="store_true")
     ap.add_argument("--slo-max-batch", type=int, default=256, help="LM batch cap of the load test")
     ap.add_argument("--slo-startup-limit", type=int, default=16, help="scheduler startup concurrency")
