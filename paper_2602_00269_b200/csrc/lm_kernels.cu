@@ -203,6 +203,7 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const fl
                             int64_t split_stride, const LmDims& dm, const float2* rope,
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
+  // CTAs per row (8 for <= 32 rows measured no different from 2)
   static const int gy = getenv("VOX_ROPE_Y") ? atoi(getenv("VOX_ROPE_Y")) : 2;
   launch_k(qkv_rope_append_kernel, dim3(n, gy), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
            rope, page_table, kc, vc, q_out);
@@ -228,7 +229,11 @@ __global__ void __launch_bounds__(1024)
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st) {
-  static const int nt = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 256;
+  // few rows: more threads per row shorten each row's dependent-load chain; many
+  // rows: 256-thread CTAs co-reside with the PDL-launched GEMM CTAs (768 threads
+  // measured slower at 224 rows, profiles/gemm_mc_ab_r01.txt)
+  static const int nt_env = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 0;
+  const int nt = nt_env > 0 ? nt_env : (n <= 32 ? 1024 : 256);
   launch_k(resid_norm_kernel, dim3(n), dim3(nt), 0, st, rows, ws, splits, split_stride, dm.d,
            dm.eps, h, norm_w, x_out, out_index);
 }
