@@ -233,7 +233,13 @@ void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
   // rows: 256-thread CTAs co-reside with the PDL-launched GEMM CTAs (768 threads
   // measured slower at 224 rows, profiles/gemm_mc_ab_r01.txt)
   static const int nt_env = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 0;
-  const int nt = nt_env > 0 ? nt_env : (n <= 32 ? 1024 : 256);
+  int nt = 256;
+  if (nt_env > 0) {
+    nt = nt_env;
+  } else if (n <= 32) {  // one float4 per thread (d = 3072: 768 threads)
+    nt = (dm.d / 4 + 31) / 32 * 32;
+    nt = nt < 256 ? 256 : (nt > 1024 ? 1024 : nt);
+  }
   launch_k(resid_norm_kernel, dim3(n), dim3(nt), 0, st, rows, ws, splits, split_stride, dm.d,
            dm.eps, h, norm_w, x_out, out_index);
 }
