@@ -578,11 +578,14 @@ static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16
   }
 }
 
-int attn_pick_splits(int n_rows, int n_kv) {
+// Split-KV (+ a combine launch) only pays for long contexts: at the contexts of
+// these serving configs (<= 768 tokens) one item per (row, kv head) is faster at
+// every batch size (traced decode step: B=1 2.01 -> 1.92 ms, B=16 2.13 -> 1.99 ms
+// unsplit; CosyVoice2 LM at 128 rows 1.38 -> 1.19 ms), so split only when
+// contexts can exceed 1024 tokens and the items leave half the CTA slots idle.
+int attn_pick_splits(int n_rows, int n_kv, int max_ctx) {
   if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) return atoi(e) < 1 ? 1 : atoi(e);  // debug
-  // split only when the items would leave at least half of the 2-per-SM CTA
-  // slots idle: the combine launch costs more than a partly filled wave
-  // (CosyVoice2-style LM at 128 rows x 2 kv heads: 1.38 -> 1.19 ms/step unsplit)
+  if (max_ctx < 1024) return 1;
   const int ctas = n_rows * n_kv;
   int s = (2 * kNumSMs) / ctas;
   if (s > kAttnMaxSplits) s = kAttnMaxSplits;

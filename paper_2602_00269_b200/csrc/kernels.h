@@ -142,7 +142,7 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const fl
                             cudaStream_t st);
 constexpr int kAttnMaxSplits = 8;    // split-KV factor cap
 constexpr int kAttnSplitRows = 128;  // split-KV only for batches up to this many rows
-int attn_pick_splits(int n_rows, int n_kv);
+int attn_pick_splits(int n_rows, int n_kv, int max_ctx);
 // ws: split-KV partials [rows][kv][n_split][G][hd + 2] (unused when n_split == 1)
 // sched: 2 zeroed ints (work counter, done counter), self-resetting per launch
 // Fused q|k|v split-K reduce + bias + RoPE + KV append inside the attention

@@ -768,7 +768,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
                              c->page_table, c->kc + l * kv_layer, c->vc + l * kv_layer, c->q, st);
     }
     {
-      const int asp = attn_pick_splits(nrows, g.n_kv_heads);
+      const int asp = attn_pick_splits(nrows, g.n_kv_heads, g.max_ctx);
       TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
       const RopeIn ri{c->ws, pl_qkv, static_cast<int64_t>(nrows) * c->nqkv, c->rope_tab,
                       c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr,
