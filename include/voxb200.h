@@ -151,6 +151,12 @@ int vox_slot_info(VoxCtx* ctx, int32_t slot, int32_t* prompt_len, int32_t* targe
 int vox_forward(VoxCtx* ctx, const VoxRow* rows, int32_t n, uint32_t flags,
                 float* logits_out, int32_t* tokens_out);
 
+/* `steps` consecutive decode steps over the same rows in one call (no host round
+ * trip between them): step k runs `rows` with every pos advanced by k, each
+ * sampled row feeding the next step from the token store (CSM depth loop).
+ * No host outputs; flags as vox_forward (VOX_FWD_SAMPLE required). */
+int vox_forward_steps(VoxCtx* ctx, const VoxRow* rows, int32_t n, int32_t steps, uint32_t flags);
+
 /* sequence number of the last issued vox_forward (1-based), and a host wait
  * for forward `seq` to complete on the device (bounds host run-ahead) */
 int vox_forward_seq(VoxCtx* ctx, int64_t* seq);

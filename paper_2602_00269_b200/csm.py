@@ -59,8 +59,8 @@ class CsmFrames:
                             -self.base, 0)
         rows = [[s.dslot, 0, -2, 0] for s in streams] + [[s.dslot, 1, -1, 1] for s in streams]
         self.dp.forward(np.array(rows, np.int32))
-        for p in range(2, self.C):
-            self.dp.forward(np.array([[s.dslot, p, -1, 1] for s in streams], np.int32))
+        if self.C > 2:  # positions 2 .. C-1 in one call
+            self.dp.forward_steps(np.array([[s.dslot, 2, -1, 1] for s in streams], np.int32), self.C - 2)
         self.bb.link_tokens(self.dp, np.array([[s.bslot, s.pos + 1, s.dslot, 2] for s in streams], np.int32),
                             self.base, 1)
         for s in streams:

@@ -1220,6 +1220,26 @@ int vox_slot_info(VoxCtx* c, int32_t slot, int32_t* prompt_len, int32_t* target_
 }
 
 int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float* logits_out,
+                int32_t* tokens_out);
+
+int vox_forward_steps(VoxCtx* c, const VoxRow* rows, int32_t n, int32_t steps, uint32_t flags) {
+  if (!c || !rows || n <= 0 || steps < 1 || !(flags & VOX_FWD_SAMPLE) ||
+      (flags & (VOX_FWD_FULL_LOGITS | VOX_FWD_SYNC)))
+    return fail(c, VOX_ERR_INVALID, "bad multi-step forward");
+  std::vector<VoxRow> r(rows, rows + n);
+  for (int k = 0; k < steps; ++k) {
+    if (k > 0)
+      for (auto& x : r) {
+        ++x.pos;
+        x.token = -1;  // the previous step's sample, from the token store
+      }
+    const int rc = vox_forward(c, r.data(), n, flags, nullptr, nullptr);
+    if (rc != VOX_OK) return rc;
+  }
+  return VOX_OK;
+}
+
+int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float* logits_out,
                 int32_t* tokens_out) {
   if (!c || (!rows && n > 0)) return fail(c, VOX_ERR_INVALID, "null argument");
   const VoxModelCfg& g = c->cfg;

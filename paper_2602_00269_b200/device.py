@@ -137,6 +137,13 @@ class VoxDevice:
         self._check(self.lib.vox_forward(self.ctx, rp, n, flags, lp, tp))
         return toks, logits
 
+    def forward_steps(self, rows: np.ndarray, steps: int) -> None:
+        """`steps` sampled decode steps over the same rows, pos advancing by one per step,
+        issued in one call (no host round trip between steps)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        rp = rows.ctypes.data_as(C.POINTER(_lib.VoxRow))
+        self._check(self.lib.vox_forward_steps(self.ctx, rp, rows.shape[0], steps, _lib.VOX_FWD_SAMPLE))
+
     def forward_seq(self) -> int:
         s = C.c_int64()
         self._check(self.lib.vox_forward_seq(self.ctx, C.byref(s)))
