@@ -443,6 +443,10 @@ struct McCfg {
   // ring depth from a smem budget (KB): ~200 = one CTA per SM, deep; ~100 lets
   // the next kernel's CTA co-reside (PDL prologue overlap)
   static int stages(int budget_kb) {
+    // narrow tiles (few rows): a ~100 KB ring still holds 4-5 weight stages and
+    // lets two CTAs share an SM (one wave for e.g. the 224-tile LM head)
+    static const int small_kb = getenv("VOX_GEMM_MC_SMALL_KB") ? atoi(getenv("VOX_GEMM_MC_SMALL_KB")) : 100;
+    if (BN <= 32 && small_kb > 0) budget_kb = small_kb;
     int n = budget_kb * 1024 / kStageBytes;
     return n > 8 ? 8 : (n < 2 ? 2 : n);
   }
