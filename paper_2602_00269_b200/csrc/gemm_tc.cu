@@ -427,7 +427,9 @@ static int gemm_mc_budget_kb() {
   static int b = -1;
   if (b < 0) {
     const char* e = getenv("VOX_GEMM_MC_BUDGET_KB");
-    b = e ? atoi(e) : 150;  // measured on the serving step: 150 (3 x 48 KB stages at 256 rows) > 200 > 100
+    // measured on the (GC-free) serving step at 224 rows: 220 KB (5 x 44 KB stages) 773-776,
+    // 200 KB 757-769, 150 KB 739-745, 100 KB 580 audio-s/s (profiles/gemm_mc_ab_r01.txt)
+    b = e ? atoi(e) : 220;
     if (b < 32) b = 32;
     if (b > 220) b = 220;
   }
@@ -447,6 +449,7 @@ struct McCfg {
     // lets two CTAs share an SM (one wave for e.g. the 224-tile LM head)
     static const int small_kb = getenv("VOX_GEMM_MC_SMALL_KB") ? atoi(getenv("VOX_GEMM_MC_SMALL_KB")) : 100;
     if (BN <= 32 && small_kb > 0) budget_kb = small_kb;
+    else if (BN <= 64 && budget_kb > 150) budget_kb = 150;  // B=64: 2.53 ms at 220 KB vs 2.47 at 150
     int n = budget_kb * 1024 / kStageBytes;
     return n > 8 ? 8 : (n < 2 ? 2 : n);
   }
