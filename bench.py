@@ -592,11 +592,82 @@ def csm_frames(batch: int, frames: int, seed: int, hbm: float, device: int):
     return out
 
 
+def reference_host_path(n_rows: int = 60):
+    """The reference's OWN host path at the Orpheus vocabulary,
+    unmodified speechserve from baseline/_ref: per-row sample() (model_api.py:355-381)
+    at V = 156,940 with the Orpheus parameters (profiles.py:192-194) on masked hash
+    logits -- the like-for-like baseline of K1 -- and run_scenario (engine.py:460-505) of
+    config 1's workload (4 requests x 64 tokens at t=0, orpheus_like, async) whose hot
+    path is its hash-logit forward + that sampler.  Single-threaded Python/numpy."""
+    from dataclasses import replace
+
+    from speechserve import engine as r_engine
+    from speechserve import model_api, profiles, scheduler, workload
+
+    V = 156940
+    prof = replace(profiles.builtin_profile("orpheus_like"), vocab_size=V)
+    params = prof.sampling_defaults
+    state = model_api.SamplingState(seed=1, rng=np.random.default_rng(1),
+                                    windows=[model_api._RingWindow(params.penalty_window, V)])
+    rows = []
+    for i in range(n_rows):
+        x = model_api.synthetic_logits(model_api.request_seed(0, i), i, 0, V)
+        lo = 128266 + (i % 7) * 4096
+        m = np.full(V, -np.inf)
+        m[lo:lo + 4096] = x[lo:lo + 4096]
+        rows.append(m)
+    t0 = time.perf_counter()
+    for m in rows:
+        model_api.sample(m, params, state)
+    sample_ms = (time.perf_counter() - t0) / n_rows * 1e3
+    greedy = replace(params, temperature=0.0)
+    t0 = time.perf_counter()
+    for m in rows:
+        model_api.sample(m, greedy, state)
+    greedy_ms = (time.perf_counter() - t0) / n_rows * 1e3
+    arr = workload.build_workload(workload.WorkloadSpec(rate=0.0, offline_count=4, prompt_dist=workload.fixed(50),
+                                                        output_dist=workload.fixed(64), seed=0))
+    t0 = time.perf_counter()
+    tr = r_engine.run_scenario(arr, prof, scheduler.PolicyConfig(), r_engine.Topology(),
+                               r_engine.PipelineMode.ASYNCHRONOUS, seed=0)
+    wall = time.perf_counter() - t0
+    toks = sum(r.tokens_generated for r in tr.requests)
+    return {"sample_ms_per_row": round(sample_ms, 3), "sample_greedy_ms_per_row": round(greedy_ms, 3),
+            "sampling": f"T {params.temperature}, top-p {params.top_p}, rp {params.repetition_penalty}, V {V}",
+            "run_scenario_wall_s": round(wall, 3), "run_scenario_tokens": toks,
+            "run_scenario_tok_per_s": round(toks / wall, 1), "cores": 1,
+            "what": "unmodified reference (baseline/_ref): per-row sample() on masked hash logits; run_scenario "
+                    "of config 1 (4 x 64 tokens, orpheus_like at V=156,940, async) -- hash-stub LM, no audio"}
+
+
 def cpu_port_sample(seconds_budget: float = 20.0):
     """Oracle port of the same step on host cores (bounded sample); returns audio-s/s."""
     from oracle.cpu_step import time_cpu_step
 
     return time_cpu_step(budget_s=seconds_budget)
+
+
+def our_config(args, ws: int) -> dict:
+    """The workload both arms report on (the reference arm times a bounded sample of it)."""
+    return {"workload": "orpheus-3b-style steady-state serving iteration (config 2)",
+            "model": "orpheus-3b-style random-init", "concurrent_streams_per_gpu": args.batch,
+            "prompt": args.prompt, "output_tokens": 688, "parallelism": f"dp{ws} (request-sharded replicas)",
+            "l2": "inputs larger than L2 (6.6 GB weights + KV per step)"}
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks (one
+    process per GPU) under torch.distributed.run on 127.0.0.1, NCCL_DEBUG=INFO so the
+    rank/device map is in the log; rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, NCCL_DEBUG=os.environ.get("NCCL_DEBUG", "INFO"), VOX_BENCH_SPAWNED="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def main():
@@ -617,9 +688,21 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cosy", action="store_true", help="skip the config-4 (CosyVoice2-style LM) line")
     ap.add_argument("--no-csm", action="store_true", help="skip the config-3 (CSM-1B-style frames) line")
+    ap.add_argument("--ranks-probe", action="store_true", help="print each rank's (rank, world) and exit")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    if args.ranks_probe:
+        ws, rank, _ = dist_setup("gloo")
+        print(json.dumps({"rank": rank, "world": ws}), flush=True)
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     if args.impl == "reference":
         ws, rank, _ = dist_setup("gloo")
@@ -627,15 +710,20 @@ def main():
             return
         from oracle.cpu_step import time_cpu_step
 
-        r = time_cpu_step(budget_s=20.0, steps=args.steps, warmup=min(args.warmup, 1))
-        line = {"metric": METRIC, "value": r["audio_s_per_s"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
+        r = time_cpu_step(budget_s=60.0, steps=args.steps, warmup=1)
+        try:
+            host = reference_host_path()
+        except Exception as e:  # report, never mask the arm
+            host = {"error": repr(e)[:200]}
+        line = {"metric": METRIC, "value": round(r["audio_s_per_s"], 5), "unit": UNIT, "impl": "reference",
+                "n_gpus": args.gpus, "steps": r["steps"], "warmup": 1, "ms_per_step": round(r["ms_per_step"], 2),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                "data": "synthetic", "config": {"workload": "orpheus-3b-style decode+sample+detok step, oracle port",
-                                                "sample": r["sample"]},
-                "cpu_baseline": {"value": r["audio_s_per_s"], "unit": UNIT, "cores": r["cores"], "kind": "port",
-                                 "sample": r["sample"]},
-                "e2e": {"value": r["audio_s_per_s"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                "data": "synthetic", "config": our_config(args, ws),
+                "cpu_baseline": {"value": round(r["audio_s_per_s"], 5), "unit": UNIT, "cores": r["cores"],
+                                 "kind": "port", "sample": r["sample"]},
+                "reference_host_path": host,
+                "e2e": {"value": round(r["audio_s_per_s"], 5), "unit": UNIT, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
 
@@ -711,8 +799,9 @@ def main():
     if not args.no_cpu and rank == 0:
         from oracle.cpu_step import time_cpu_step
 
-        r = time_cpu_step(budget_s=15.0, steps=2, warmup=1)
-        cpu = {"value": r["audio_s_per_s"], "unit": UNIT, "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+        r = time_cpu_step(budget_s=20.0, steps=8, warmup=1)
+        cpu = {"value": round(r["audio_s_per_s"], 5), "unit": UNIT, "cores": r["cores"], "kind": "port",
+               "sample": r["sample"]}
 
     if rank == 0:
         steps = args.steps
@@ -722,10 +811,7 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws, "steps": steps,
             "warmup": args.warmup, "ms_per_step": round(dev_ms / steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "orpheus-3b-style steady-state serving iteration (config 2)",
-                       "model": "orpheus-3b-style random-init", "concurrent_streams_per_gpu": args.batch,
-                       "prompt": args.prompt, "output_tokens": 688, "parallelism": f"dp{ws} (request-sharded replicas)",
-                       "l2": "inputs larger than L2 (6.6 GB weights + KV per step)"},
+            "config": our_config(args, ws),
             "e2e": {"value": round(e2e, 2), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(res["launches"]),
             "clocks": clk.summary(),

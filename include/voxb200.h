@@ -120,7 +120,7 @@ typedef struct VoxWindow {
 typedef struct VoxCtx VoxCtx;
 
 /* forward flags */
-#define VOX_FWD_SAMPLE 1u       /* run the fused sampler on rows with sample != 0   */
+#define VOX_FWD_SAMPLE 1u       /* run K1 on rows with sample != 0 (clear: logits only) */
 #define VOX_FWD_FULL_LOGITS 2u  /* LM head over the full vocab (parity path)        */
 #define VOX_FWD_SYNC 4u         /* block until done (implied by host outputs)       */
 #define VOX_FWD_NO_GRAPH 8u     /* eager launches (timing / debugging)              */
@@ -156,6 +156,14 @@ int vox_forward(VoxCtx* ctx, const VoxRow* rows, int32_t n, uint32_t flags,
  * sampled row feeding the next step from the token store (CSM depth loop).
  * No host outputs; flags as vox_forward (VOX_FWD_SAMPLE required). */
 int vox_forward_steps(VoxCtx* ctx, const VoxRow* rows, int32_t n, int32_t steps, uint32_t flags);
+
+/* test/diagnostic readback of the logits the last vox_forward computed, exactly
+ * as the LM head left them for K1 (graph path included): [n_rows][ld] fp32, column
+ * j = vocabulary id col_base + j (the packed audio head covers the frame slots'
+ * codebook rows only).  out == NULL only reports the layout; otherwise rows <=
+ * n_rows and cols == ld.  Synchronises the LM stream. */
+int vox_read_logits(VoxCtx* ctx, float* out, int32_t rows, int32_t cols, int32_t* n_rows,
+                    int32_t* ld, int32_t* col_base);
 
 /* sequence number of the last issued vox_forward (1-based), and a host wait
  * for forward `seq` to complete on the device (bounds host run-ahead) */

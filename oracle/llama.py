@@ -42,9 +42,9 @@ def rope(x: np.ndarray, pos: np.ndarray, inv_freq: np.ndarray) -> np.ndarray:
 class LlamaOracle:
     """Per-request contiguous KV (the paged layout is checked via oracle/paging.py)."""
 
-    def __init__(self, cfg, seed: int, weights: BackboneWeights | None = None):
+    def __init__(self, cfg, seed: int, weights: BackboneWeights | None = None, lazy_emb: bool = False):
         self.cfg = cfg
-        self.w = weights or BackboneWeights(cfg, seed)
+        self.w = weights or BackboneWeights(cfg, seed, lazy_emb=lazy_emb)
         self.k = {}  # rid -> [L, T, KV, hd]
         self.v = {}
 
@@ -68,10 +68,10 @@ class LlamaOracle:
             if t[i, 0] == -2:
                 h[i] = ext[i]
                 continue
-            acc = self.w.emb[t[i, 0]].astype(np.float32)
+            acc = self.w.emb_rows([t[i, 0]])[0].astype(np.float32)
             for cb in range(1, t.shape[1]):
                 if t[i, cb] >= 0:
-                    acc = acc + self.w.emb[t[i, cb]]
+                    acc = acc + self.w.emb_rows([t[i, cb]])[0]
             h[i] = acc
         return h
 
@@ -80,20 +80,31 @@ class LlamaOracle:
         return (xf.astype(np.float32) @ self.w.proj.T).astype(np.float32)
 
     def forward(self, rid, tokens: np.ndarray, positions: np.ndarray, want_logits: bool = True,
-                ext: np.ndarray | None = None):
+                ext: np.ndarray | None = None, head: tuple | None = None):
         """Run tokens [n] (or CSM frames [n, C]) at positions [n] (ascending) of request rid.
 
-        Returns logits [n, vocab] fp32 of every row (or None) and the final
-        normalised hidden rows xf [n, d] (bf16 values).
-        """
+        Returns logits [n, vocab] fp32 of every row (or None; `head`=(lo, hi) limits
+        them to vocabulary rows lo..hi-1) and the final normalised hidden rows xf
+        [n, d] (bf16 values)."""
+        n = len(tokens)
+        return self.forward_rows([rid] * n, tokens, positions, want_logits, ext, head)
+
+    def forward_rows(self, rids, tokens: np.ndarray, positions: np.ndarray, want_logits: bool = True,
+                     ext: np.ndarray | None = None, head: tuple | None = None):
+        """One mixed batch as the device runs it (vox_forward): row i feeds tokens[i] of
+        request rids[i] at positions[i]; rows of one request are causal among
+        themselves (every row's K/V is appended before attention reads the cache)."""
         c, w = self.cfg, self.w
-        d, H, KV, hd = c.d_model, c.n_heads, c.n_kv_heads, c.head_dim
+        H, KV, hd = c.n_heads, c.n_kv_heads, c.head_dim
         G = H // KV
         n = len(tokens)
-        K, V = self._layer_kv(rid)
+        positions = np.asarray(positions)
         h = self.embed(tokens, ext)  # fp32 residual
         x = rmsnorm_bf16(h, w.layers[0]["norm_attn"], c.rms_eps)
         scale = f32(1.0) / np.sqrt(f32(hd))
+        groups: dict = {}
+        for i, r in enumerate(rids):
+            groups.setdefault(r, []).append(i)
         for l, L in enumerate(w.layers):
             qkv = x @ L["qkv"].T
             if "qkv_bias" in L:  # Qwen2 q|k|v bias, added after the projection (lm_kernels.cu)
@@ -104,19 +115,22 @@ class LlamaOracle:
             q = bf16_round(rope(q, positions, w.inv_freq))
             k = bf16_round(rope(k, positions, w.inv_freq))
             v = bf16_round(v)
-            K[l, positions] = k
-            V[l, positions] = v
             out = np.empty((n, H, hd), np.float32)
-            for i in range(n):
-                T = positions[i] + 1
+            for rid, idx in groups.items():
+                K, V = self._layer_kv(rid)
+                K[l, positions[idx]] = k[idx]
+                V[l, positions[idx]] = v[idx]
+                pos = positions[idx]
+                T = int(pos.max()) + 1
                 kk = K[l, :T]  # [T, KV, hd]
                 vv = V[l, :T]
-                for hh in range(H):
-                    g = hh // G
-                    s = (kk[:, g, :] @ q[i, hh]) * scale
-                    m = s.max()
-                    p = np.exp(s - m)
-                    out[i, hh] = (p @ vv[:, g, :]) / p.sum(dtype=np.float32)
+                qg = q[idx].reshape(len(idx), KV, G, hd)
+                s_ = np.einsum("nkgd,tkd->nkgt", qg, kk).astype(np.float32) * scale
+                s_ = np.where(np.arange(T)[None, None, None, :] <= pos[:, None, None, None], s_, -np.inf)
+                m = s_.max(axis=-1, keepdims=True)
+                p = np.exp(s_ - m).astype(np.float32)
+                o = np.einsum("nkgt,tkd->nkgd", p, vv).astype(np.float32)
+                out[idx] = (o / p.sum(axis=-1, dtype=np.float32, keepdims=True)).reshape(len(idx), H, hd)
             a = bf16_round(out.reshape(n, H * hd))
             h = h + a @ L["o"].T
             x = rmsnorm_bf16(h, L["norm_mlp"], c.rms_eps)
@@ -126,7 +140,10 @@ class LlamaOracle:
             h = h + act @ L["down"].T
             nw = w.layers[l + 1]["norm_attn"] if l + 1 < len(w.layers) else w.norm_final
             x = rmsnorm_bf16(h, nw, c.rms_eps)
-        logits = (x @ w.emb.T).astype(np.float32) if want_logits else None
+        logits = None
+        if want_logits:
+            lo, hi = head if head is not None else (0, c.vocab)
+            logits = (x @ w.emb_slice(lo, hi).T).astype(np.float32)
         return logits, x
 
     def release(self, rid):

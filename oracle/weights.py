@@ -57,13 +57,13 @@ def unit_pm1(n: int, key: int, start: int = 0) -> np.ndarray:
     return (h >> np.uint64(40)).astype(np.int32).astype(np.float32) * np.float32(1.0 / 8388608.0) - np.float32(1.0)
 
 
-def init_bf16(n: int, key: int, scale, chunk: int = 1 << 24) -> np.ndarray:
-    """csrc/init.cu:init_bf16_kernel, as float32 values."""
+def init_bf16(n: int, key: int, scale, chunk: int = 1 << 24, start: int = 0) -> np.ndarray:
+    """csrc/init.cu:init_bf16_kernel, as float32 values (elements start .. start+n)."""
     out = np.empty(n, dtype=np.float32)
     s = np.float32(scale)
     for a in range(0, n, chunk):
         m = min(chunk, n - a)
-        out[a: a + m] = bf16_round(unit_pm1(m, key, a) * s)
+        out[a: a + m] = bf16_round(unit_pm1(m, key, start + a) * s)
     return out
 
 
@@ -80,11 +80,16 @@ def f32(x) -> np.float32:
 class BackboneWeights:
     """All backbone tensors as float32 arrays holding bf16 values."""
 
-    def __init__(self, cfg, seed: int, layers=None):
+    def __init__(self, cfg, seed: int, layers=None, lazy_emb: bool = False):
+        """lazy_emb: generate embedding rows on demand (config-2 sizes: the full
+        [156,940 x 3072] table is 1.9 GB of fp32; tests touch only the prompt rows
+        and the audio-row slice of the tied head)."""
         d, hd, H, KV, dff, V = cfg.d_model, cfg.head_dim, cfg.n_heads, cfg.n_kv_heads, cfg.d_ff, cfg.vocab
         self.cfg = cfg
         k = lambda tid, l=0: tensor_key(seed, tid, l)  # noqa: E731
-        self.emb = init_bf16(V * d, k(T_EMB), f32(cfg.embed_half_width)).reshape(V, d)
+        self._emb_key = k(T_EMB)
+        self._emb_cache: dict = {}
+        self._emb = None if lazy_emb else init_bf16(V * d, self._emb_key, f32(cfg.embed_half_width)).reshape(V, d)
         nqkv = (H + 2 * KV) * hd
         self.layers = []
         for l in range(cfg.n_layers if layers is None else layers):
@@ -106,6 +111,38 @@ class BackboneWeights:
             [np.float32(1.0 / (float(cfg.rope_theta) ** ((2.0 * i) / hd))) for i in range(hd // 2)],
             dtype=np.float32,
         )
+
+
+    @property
+    def emb(self) -> np.ndarray:
+        if self._emb is None:
+            raise AttributeError("lazy embedding: use emb_rows() / emb_slice()")
+        return self._emb
+
+    def emb_rows(self, ids) -> np.ndarray:
+        """Rows `ids` of the (tied) embedding table, float32 [n, d] of bf16 values."""
+        ids = np.asarray(ids, dtype=np.int64).reshape(-1)
+        if self._emb is not None:
+            return self._emb[ids]
+        d = self.cfg.d_model
+        out = np.empty((len(ids), d), np.float32)
+        for j, i in enumerate(ids):
+            i = int(i)
+            if i not in self._emb_cache:
+                self._emb_cache[i] = init_bf16(d, self._emb_key, f32(self.cfg.embed_half_width), start=i * d)
+            out[j] = self._emb_cache[i]
+        return out
+
+    def emb_slice(self, lo: int, hi: int) -> np.ndarray:
+        """Rows [lo, hi) of the embedding table (the head's vocabulary slice), cached."""
+        if self._emb is not None:
+            return self._emb[lo:hi]
+        key = ("slice", lo, hi)
+        if key not in self._emb_cache:
+            d = self.cfg.d_model
+            self._emb_cache[key] = init_bf16((hi - lo) * d, self._emb_key, f32(self.cfg.embed_half_width),
+                                             start=lo * d).reshape(hi - lo, d)
+        return self._emb_cache[key]
 
 
 class DetokWeights:

@@ -95,6 +95,7 @@ _SIGS = {
     "vox_slot_info": (C.c_int, [_P, C.c_int32, _i32p, _i32p]),
     "vox_forward": (C.c_int, [_P, C.POINTER(VoxRow), C.c_int32, C.c_uint32, _f32p, _i32p]),
     "vox_forward_steps": (C.c_int, [_P, C.POINTER(VoxRow), C.c_int32, C.c_int32, C.c_uint32]),
+    "vox_read_logits": (C.c_int, [_P, _f32p, C.c_int32, C.c_int32, _i32p, _i32p, _i32p]),
     "vox_forward_seq": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "vox_forward_wait": (C.c_int, [_P, C.c_int64]),
     "vox_sample_logits": (C.c_int, [_P, _f32p, C.c_int32, C.c_int32, C.POINTER(VoxSampling),

@@ -106,6 +106,28 @@ def tiny(**kw) -> ModelConfig:
     return replace(base, **kw)
 
 
+# Greedy-parity init (config 1, SURVEY.md section 7 "Hard parts"): the same tiny
+# backbone with the tied embedding's half-width x400.  RMSNorm makes every GEMM
+# input scale-free, so the attention/MLP contributions keep their size while the
+# token embedding carries more of the residual stream; device/oracle differences
+# (tensor-core vs CPU fp32 summation order -> 1-ulp bf16 flips) then rarely reach
+# the final hidden state (median |dlogit| ~1e-3 at logit std ~1000, measured on
+# B200) while the decisions still depend on the layers: with weight seed 2024,
+# zeroing the attention output changes 81 of config 1's 256 greedy tokens and
+# zeroing attention + MLP 157 (tests/test_oracle_greedy.py).
+# tests/test_gpu_lm.py asserts, at every decision, that the oracle's penalised
+# top-2 margin exceeds 10x that step's measured device/oracle logit error before
+# demanding bit-exact token streams.
+PLANTED_EMBED_MULT = 400.0
+PLANTED_WEIGHT_SEED = 2024
+
+
+def tiny_planted(**kw) -> ModelConfig:
+    """Config 1 with the planted-margin init (greedy token streams bit-exact)."""
+    base = tiny(**kw)
+    return replace(base, name="tiny-orpheus-planted", embed_scale=PLANTED_EMBED_MULT * base.embed_half_width)
+
+
 def orpheus3b(**kw) -> ModelConfig:
     """Config 2: Orpheus-3B-style (Llama-3.2-3B backbone + SNAC-24k-style decoder)."""
     base = ModelConfig(
@@ -191,5 +213,5 @@ def tiny_csm(n_codebooks: int = 8):
     return bb, dp
 
 
-CONFIGS = {"tiny": tiny, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy,
+CONFIGS = {"tiny": tiny, "tiny_planted": tiny_planted, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy,
            "csm_backbone": csm_backbone, "csm_depth": csm_depth}

@@ -153,6 +153,7 @@ struct VoxCtx {
   float* attn_ws = nullptr;  // split-KV partials
   float* logits = nullptr;
   size_t logits_elems = 0;
+  int last_logit_rows = 0, last_logit_ld = 0, last_logit_base = 0;  // vox_read_logits
   std::map<int, CUtensorMap> tm_x, tm_attn, tm_act, tm_xf;  // by BN
 
   // ---- KV / tokens / slots
@@ -730,7 +731,7 @@ static int create_detok(VoxCtx* c) {
 // fused_rope: every row is a distinct slot (a pure decode step), so the q|k|v
 // reduce + RoPE + KV append runs inside the attention kernel (no rope launch)
 static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1,
-                           bool fused_rope = false) {
+                           bool fused_rope = false, bool run_sampler = true) {
   const VoxModelCfg& g = c->cfg;
   const LmDims& dm = c->dm;
   cudaStream_t st = c->s_lm;
@@ -850,7 +851,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
     a.vocab = g.vocab;
     a.tokens_out = c->d_tokens;
     a.err_flag = c->d_err;
-    {
+    if (run_sampler) {
       const int span = g.audio_base >= 0 ? g.codebook_size : g.vocab;
       TimedLaunch tl(c, st, "sampler", static_cast<double>(nsamp) * span * 4);
       launch_sample_fused(a, st);
@@ -862,7 +863,6 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
 
 static int check_err_value(VoxCtx* c, int e) {
   if (e == 0) return VOX_OK;
-  cudaMemsetAsync(c->d_err, 0, 4, c->s_lm);
   if (e == VOX_ERR_NONFINITE) return fail(c, e, "logits must not contain NaN or +inf");
   if (e == VOX_ERR_DEGENERATE) return fail(c, e, "all logits are -inf after truncation");
   return fail(c, e, "device error flag " + std::to_string(e));
@@ -1327,6 +1327,9 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
     CK(cudaMemcpyAsync(c->d_sample_rows, sg.sample_rows, sizeof(int) * ns,
                        cudaMemcpyHostToDevice, st));
   const bool use_graph = !(flags & VOX_FWD_NO_GRAPH) && !full && !c->timing && !c->no_graphs;
+  // VOX_FWD_SAMPLE clear: the LM head still runs over the sampling rows (their
+  // logits are the result), but K1 does not (the host samples: engine.py:294-303)
+  const bool run_sampler = (flags & VOX_FWD_SAMPLE) != 0;
   // one frame slot for every sampled row -> that slot's head rows only
   int hslot = -1;
   if (!full && ns > 0 && g.audio_base >= 0 && g.frame_tokens > 1 && g.codebook_size % 128 == 0) {
@@ -1354,18 +1357,18 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
   }
   int rc = VOX_OK;
   if (use_graph) {
-    auto key = std::make_tuple(nrows, ns, hslot * 2 + (unique ? 1 : 0));
+    auto key = std::make_tuple(nrows, ns, (hslot * 2 + (unique ? 1 : 0)) * 2 + (run_sampler ? 1 : 0));
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       // eager pass (executes this step and sets kernel attributes), then capture
-      rc = enqueue_forward(c, nrows, ns, false, hslot, unique);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, unique, run_sampler);
       if (rc != VOX_OK) return rc;
       CK(cudaStreamSynchronize(st));
       const int64_t before = c->launches;
       cudaGraph_t graph;
       c->capturing = true;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_forward(c, nrows, ns, false, hslot, unique);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, unique, run_sampler);
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       c->capturing = false;
       if (rc != VOX_OK) return rc;
@@ -1381,12 +1384,21 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       c->launches += c->graph_launches[key];
     }
   } else {
-    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot, unique);
+    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot, unique, run_sampler);
     if (rc != VOX_OK) return rc;
+  }
+  {  // layout of the logits buffer this forward leaves behind (vox_read_logits)
+    const bool audio = g.audio_base >= 0 && !full;
+    const bool one_slot = audio && hslot >= 0;
+    c->last_logit_rows = nsamp;
+    c->last_logit_ld = one_slot ? g.codebook_size : (audio ? c->head_audio_rows : g.vocab);
+    c->last_logit_base = audio ? g.audio_base + (one_slot ? hslot * g.codebook_size : 0) : 0;
   }
   if (nsamp > 0)
     CK(cudaMemcpyAsync(sg.tokens, c->d_tokens, sizeof(int) * nsamp, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(sg.err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  // zero the flag in-stream: each forward's error is attributed to it alone
+  CK(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
   CK(cudaEventRecord(sg.ev, st));
   sg.in_flight = true;
   const int64_t seq = ++c->fwd_seq;
@@ -1410,6 +1422,21 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       CK(cudaMemcpy(logits_out, c->logits, sizeof(float) * static_cast<size_t>(nsamp) * g.vocab,
                     cudaMemcpyDeviceToHost));
   }
+  return VOX_OK;
+}
+
+int vox_read_logits(VoxCtx* c, float* out, int32_t rows, int32_t cols, int32_t* n_rows,
+                    int32_t* ld, int32_t* col_base) {
+  if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");
+  if (n_rows) *n_rows = c->last_logit_rows;
+  if (ld) *ld = c->last_logit_ld;
+  if (col_base) *col_base = c->last_logit_base;
+  if (!out) return VOX_OK;
+  if (rows > c->last_logit_rows || cols != c->last_logit_ld)
+    return fail(c, VOX_ERR_INVALID, "logits read outside the last forward's buffer");
+  CK(cudaStreamSynchronize(c->s_lm));
+  CK(cudaMemcpy(out, c->logits, sizeof(float) * static_cast<size_t>(rows) * cols,
+                cudaMemcpyDeviceToHost));
   return VOX_OK;
 }
 
@@ -1482,6 +1509,7 @@ int vox_sample_logits(VoxCtx* c, const float* logits, int32_t n, int32_t vocab,
   CK(cudaMemcpyAsync(tokens_out, d_out, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
   int errv = 0;
   CK(cudaMemcpyAsync(&errv, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
   CK(cudaStreamSynchronize(st));
   cudaFree(d_log);
   cudaFree(d_desc);

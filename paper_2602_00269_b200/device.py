@@ -22,8 +22,15 @@ class Sampling:
     repetition_penalty: float = 1.0
     penalty_window: int = 64
 
+    MAX_WINDOW = 256  # device ring-window capacity (VoxSampling.penalty_window)
+
     @classmethod
     def from_ref(cls, p) -> "Sampling":
+        if p.penalty_window > cls.MAX_WINDOW:
+            # the reference accepts any window (model_api.py:105-121); the device keeps
+            # the last <= 256 ids: refuse instead of silently penalising fewer tokens
+            raise ValueError(f"penalty_window {p.penalty_window} exceeds the device ring capacity "
+                             f"{cls.MAX_WINDOW}")
         return cls(p.temperature, p.top_k, p.top_p, p.repetition_penalty, p.penalty_window)
 
     def to_c(self) -> _lib.VoxSampling:
@@ -143,6 +150,15 @@ class VoxDevice:
         rows = np.ascontiguousarray(rows, dtype=np.int32)
         rp = rows.ctypes.data_as(C.POINTER(_lib.VoxRow))
         self._check(self.lib.vox_forward_steps(self.ctx, rp, rows.shape[0], steps, _lib.VOX_FWD_SAMPLE))
+
+    def read_logits(self):
+        """The last forward's head logits as K1 saw them: ([n_rows, ld] fp32, col_base),
+        column j = vocabulary id col_base + j (synchronises the LM stream)."""
+        n, ld, base = C.c_int32(), C.c_int32(), C.c_int32()
+        self._check(self.lib.vox_read_logits(self.ctx, None, 0, 0, C.byref(n), C.byref(ld), C.byref(base)))
+        out = np.empty((n.value, ld.value), np.float32)
+        self._check(self.lib.vox_read_logits(self.ctx, _ptr(out, C.c_float), n.value, ld.value, None, None, None))
+        return out, base.value
 
     def forward_seq(self) -> int:
         s = C.c_int64()

@@ -59,6 +59,18 @@ class B200Executor:
         except KeyError:
             raise errors.CacheMissing(f"request {rid} has no device slot (not prefilled)") from None
 
+    def _admit(self, seed: int, P: int) -> int:
+        # the reference Protocol carries no target length: reserve the rest of the context
+        target = self.cfg.max_ctx - P - 1
+        if target < 1:
+            raise errors.PromptTooLong(f"prompt of {P} tokens exceeds context capacity {self.cfg.max_ctx}")
+        try:
+            return self.dev.admit(seed, P, target, self.sampling)
+        except MemoryError as e:
+            raise MemoryError(
+                f"{e}: this executor holds at most {self.cfg.max_slots} live requests (ModelConfig.max_slots); "
+                "set PolicyConfig.max_live_requests <= max_slots") from None
+
     def release(self, rid: int) -> None:
         slot = self._slot.pop(rid, None)
         self._prompt.pop(rid, None)
@@ -76,15 +88,15 @@ class B200Executor:
             for i, rid in enumerate(batch.request_ids):
                 P = int(batch.prompt_tokens[i])
                 if rid not in self._slot:
-                    # the reference Protocol carries no target length: reserve the context
-                    target = self.cfg.max_ctx - P - 1
-                    if target < 1:
-                        raise errors.PromptTooLong(f"prompt of {P} tokens exceeds context capacity")
-                    self._slot[rid] = self.dev.admit(batch.seeds[i], P, target, self.sampling)
+                    self._slot[rid] = self._admit(batch.seeds[i], P)
                     self._prompt[rid] = P
                 rows += [[self._slot[rid], p, -1, 0] for p in range(P - 1)]
-            if rows:
-                self.dev.forward(np.asarray(rows, np.int32), sample=False, sync=True)
+            # prompts of many requests can exceed one forward's row capacity: split
+            # at max_rows (positions of one request stay in order, so the causal
+            # K/V of a later chunk is already appended)
+            cap = self.cfg.max_rows
+            for a in range(0, len(rows), cap):
+                self.dev.forward(np.asarray(rows[a:a + cap], np.int32), sample=False, sync=True)
             logits = np.zeros((n, 1, V), np.float64)  # the engine discards prefill logits (engine.py:251)
             return logits, time.perf_counter() - t0
         if batch.kind is not model_api.StageKind.DECODE:
@@ -97,6 +109,7 @@ class B200Executor:
             # step 0 consumes the last prompt token; later steps the host-sampled id
             tok = -1 if step == 0 else int(batch.frames[i].ids[0, 0])
             rows.append([slot, pos, tok, 1])
+        # logits only (VOX_FWD_SAMPLE clear): the host's sample() decides (engine.py:294-303)
         _, lg = self.dev.forward(np.asarray(rows, np.int32), sample=False, full_logits=True, sync=True)
         out = np.full((n, 1, V), -np.inf, np.float64)
         for i, step in enumerate(batch.steps):
@@ -142,3 +155,167 @@ class B200Executor:
 
     def depth_latency(self, batch_size: int) -> float:
         raise errors.DepthStageUnsupported("the Orpheus-style path has no depth stage")
+
+
+class CsmExecutor:
+    """The reference ``Executor`` Protocol for a depth-stage profile (CSM-1B-style, BASELINE
+    config 3; ``profiles.py:214-231`` depth_like shape) on two device contexts.
+
+    The reference engine drives one backbone forward per frame (engine.py:258-273), then
+    ``depth_forward`` (model_api.py:438-458) asks ``depth_logits(seed, step, codebook)``
+    for codebooks 1..C-1 and samples each on the host, and only then samples codebook 0
+    from ``forward``'s logits (engine.py:294-303).  A real depth decoder conditions
+    codebook k on codebooks 0..k-1 of the same frame, which the Protocol never passes
+    back.  So ``forward`` runs the whole frame on the device -- backbone (codebook 0 by
+    K1) then the depth decoder's C-1 positions (each codebook by K1) -- and serves the
+    logits K1 decided from:
+
+    * greedy profiles with repetition penalty 1 ("logits" mode): the real logits of
+      every codebook, read back exactly as K1 consumed them; the host's greedy
+      ``sample()`` picks the same codes (K1 greedy is bit-exact to it), so host and
+      device histories agree, which ``forward`` checks on the next frame
+      (``mismatches``);
+    * otherwise ("decided" mode): a one-hot row (0 at the device's code, -inf
+      elsewhere), so the host's ``sample()`` returns the device's draw -- the Protocol's
+      logits cannot carry a conditional depth distribution whose host draw the
+      device could follow.
+
+    The host's previous frame (``batch.frames``) is written into the device token /
+    frame stores before each backbone step, so the device always continues the
+    history the engine recorded.  Latencies are measured wall time of the device work.
+    """
+
+    def __init__(self, profile, bcfg: ModelConfig, dcfg: ModelConfig, weight_seed: int = 0, device: int = 0):
+        from .csm import CsmFrames
+
+        if not profile.has_depth_stage:
+            raise errors.DepthStageUnsupported(f"profile {profile.name} has no depth stage")
+        if profile.codebooks != bcfg.n_codebooks or profile.vocab_size != bcfg.codebook_size:
+            raise errors.CodebookMismatch("profile codebooks/vocab must match the backbone's frames")
+        self.profile = profile
+        self.bcfg, self.dcfg = bcfg, dcfg
+        self.bb = VoxDevice(bcfg, weight_seed, device)
+        self.dp = VoxDevice(dcfg, weight_seed + 1, device)
+        self.pipe = CsmFrames(self.bb, self.dp)
+        p = profile.sampling_defaults
+        self.sampling = Sampling.from_ref(p)
+        self.decided = p.temperature > 0 or p.repetition_penalty != 1.0
+        self.C, self.cs, self.base = bcfg.n_codebooks, bcfg.codebook_size, bcfg.audio_base
+        self._slot: dict[int, tuple[int, int, int]] = {}  # rid -> (bslot, dslot, prompt)
+        self._frames: dict[tuple[int, int], np.ndarray] = {}  # (seed, step) -> [C, cs] logits
+        self._codes: dict[int, np.ndarray] = {}  # rid -> device codes of its last frame
+        self._depth_s = 0.0
+        self.mismatches = 0
+        self.frames_run = 0
+
+    def close(self) -> None:
+        self.bb.close()
+        self.dp.close()
+
+    def release(self, rid: int) -> None:
+        s = self._slot.pop(rid, None)
+        self._codes.pop(rid, None)
+        if s is not None:
+            self.bb.release(s[0])
+            self.dp.release(s[1])
+
+    def _rows_logits(self, dev: VoxDevice, n: int) -> np.ndarray:
+        lg, _ = dev.read_logits()
+        assert lg.shape == (n, self.cs)
+        return lg
+
+    def forward(self, batch: model_api.StageBatch) -> tuple[np.ndarray, float]:
+        n, V, C = len(batch), self.profile.vocab_size, self.C
+        t0 = time.perf_counter()
+        if batch.kind is model_api.StageKind.PREFILL:
+            rows = []
+            for i, rid in enumerate(batch.request_ids):
+                P = int(batch.prompt_tokens[i])
+                if rid not in self._slot:
+                    target = self.bcfg.max_ctx - P - 1
+                    if target < 1:
+                        raise errors.PromptTooLong(f"prompt of {P} tokens exceeds context capacity")
+                    st = self.pipe.admit(batch.seeds[i], P, target, self.sampling, self.sampling)
+                    self._slot[rid] = (st.bslot, st.dslot, P)
+                rows += [[self._slot[rid][0], p, -1, 0] for p in range(P - 1)]
+            for a in range(0, len(rows), self.bcfg.max_rows):
+                self.bb.forward(np.asarray(rows[a:a + self.bcfg.max_rows], np.int32), sample=False, sync=True)
+            return np.zeros((n, C, V), np.float64), time.perf_counter() - t0
+        if batch.kind is not model_api.StageKind.DECODE:
+            raise ValueError(f"forward got {batch.kind}")
+        rows = []
+        for i, rid in enumerate(batch.request_ids):
+            if rid not in self._slot:
+                raise errors.CacheMissing(f"request {rid} has no device slot (not prefilled)")
+            bslot, dslot, P = self._slot[rid]
+            step = int(batch.steps[i])
+            pos = P - 1 + step
+            tok = -1
+            if step > 0:  # the host's previous frame becomes this position's input
+                ids = np.asarray(batch.frames[i].ids[0], np.int64)
+                prev = self._codes.get(rid)
+                if prev is not None and not np.array_equal(prev, ids):
+                    self.mismatches += 1
+                tok = int(self.base + ids[0])
+                self.bb.write_frame(bslot, pos, (self.base + np.arange(1, C) * self.cs + ids[1:])[None, :])
+            rows.append([bslot, pos, tok, 1])
+        rows = np.asarray(rows, np.int32)
+        c0, _ = self.bb.forward(rows, want_tokens=True)
+        lg0 = self._rows_logits(self.bb, n)
+        t1 = time.perf_counter()
+        # depth decoder: position 0 = projected backbone state, 1 = c0, k samples codebook k
+        dsl = [self._slot[rid][1] for rid in batch.request_ids]
+        self.dp.project_ext(self.bb, n)
+        self.dp.link_tokens(self.bb, np.array([[d, 1, b, p + 1] for d, (b, p) in
+                                               zip(dsl, [(r[0], r[1]) for r in rows])], np.int32), -self.base, 0)
+        logits = np.empty((n, C, V), np.float64)
+        logits[:, 0] = lg0
+        drows = np.array([[d, 0, -2, 0] for d in dsl] + [[d, 1, -1, 1] for d in dsl], np.int32)
+        self.dp.forward(drows, want_tokens=False)
+        logits[:, 1] = self._rows_logits(self.dp, n)
+        for k in range(2, C):
+            self.dp.forward(np.array([[d, k, -1, 1] for d in dsl], np.int32))
+            logits[:, k] = self._rows_logits(self.dp, n)
+        codes = np.zeros((n, C), np.int64)
+        codes[:, 0] = np.asarray(c0) - self.base
+        for i, d in enumerate(dsl):
+            codes[i, 1:] = self.dp.read_tokens(d, 2, C - 1) - np.arange(1, C) * self.cs
+        self._depth_s = time.perf_counter() - t1
+        if self.decided:
+            logits[:] = -np.inf
+            for i in range(n):
+                logits[i, np.arange(C), codes[i]] = 0.0
+        for i, rid in enumerate(batch.request_ids):
+            self._codes[rid] = codes[i]
+            self._frames[(int(batch.seeds[i]), int(batch.steps[i]))] = logits[i]
+        self.frames_run += n
+        return logits, t1 - t0
+
+    def depth_logits(self, seed: int, step: int, codebook: int) -> np.ndarray:
+        """Codebook `codebook` of frame `step` (model_api.py:222-223), computed by forward."""
+        try:
+            row = self._frames[(int(seed), int(step))]
+        except KeyError:
+            raise errors.CacheMissing(f"no depth frame for seed {seed} step {step}") from None
+        if codebook == self.C - 1:
+            self._frames.pop((int(seed), int(step)))
+        return row[codebook].copy()
+
+    def depth_latency(self, batch_size: int) -> float:
+        return self._depth_s
+
+    def detokenize_windows(self, batch, specs: Sequence, windows: Sequence[np.ndarray],
+                           caches: Sequence[model_api.DetokenizerCache]):
+        from ._ref import core
+
+        t0 = time.perf_counter()
+        outs = []
+        for spec, win, cache in zip(specs, windows, caches):
+            cache.window_ids = np.array(win, copy=True)
+            cache.calls += 1
+            outs.append(model_api.AudioChunkOut(request=spec.request, new_tokens=spec.new_tokens,
+                                                playback_us=core.playback_us_for(spec.new_tokens,
+                                                                                 self.profile.token_rate)))
+            if spec.final:
+                self.release(spec.request)
+        return outs, time.perf_counter() - t0

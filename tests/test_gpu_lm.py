@@ -82,90 +82,85 @@ def test_page_tables_bit_exact(tiny_cfg):
             alloc.release(s)
 
 
-def _oracle_greedy(cfg, orc, run_seed, rid, P, T, penalty):
-    seed = request_seed(run_seed, rid)
-    prompt = np.array(prompt_ids(seed, P, cfg.text_vocab))
-    orc.forward(rid, prompt[:-1], np.arange(P - 1), want_logits=False)
-    win = osamp.RingWindow(64, cfg.vocab)
-    out, margins = [], []
-    tok = int(prompt[-1])
-    for s in range(T):
-        lg, _ = orc.forward(rid, np.array([tok]), np.array([P - 1 + s]))
-        lo, hi = audio_range(cfg, s)
-        row = osamp.apply_repetition_penalty(masked(lg[0], lo, hi), penalty, win)
-        srt = np.sort(row[lo:hi])[::-1]
-        margins.append(srt[0] - srt[1])
-        tok = osamp.sample(masked(lg[0], lo, hi), 0.0, None, 1.0, penalty, win, None)
-        out.append(tok)
-    orc.release(rid)
-    return np.array(out), np.array(margins)
+def test_greedy_tokens_bit_exact_config1():
+    """Config 1: 4 concurrent greedy requests x 64 audio tokens, rp 1.3, free-running.
 
-
-def test_greedy_tokens_bit_exact_config1(tiny_dev, tiny_cfg):
-    """Config 1: 4 concurrent greedy requests x 64 audio tokens, rp 1.3.
-
-    1. The fused device path (graph-captured step + K1) generates free-running.
-    2. The same token histories are replayed through the full-logit parity
-       path (teacher forcing) and through the CPU oracle.
-    3. Every device token equals the argmax of the device's own penalised
-       logits (K1 in situ, bit-exact), and equals the ORACLE's greedy choice
-       at every step whose oracle top-2 margin exceeds twice the measured
-       |device - oracle| logit error of that step, i.e. wherever the decision
-       is numerically determined.  Near-ties (margin <= 2*err) are counted
-       and must be rare.
+    The device generates every token on its serving path (graph-captured step,
+    packed audio head, K1 greedy writing the token store).  After each step the
+    head logits K1 consumed are read back (vox_read_logits) and the oracle runs
+    the same step on the same history.  Precondition (planted-margin init,
+    config.tiny_planted): at EVERY decision the oracle's penalised top-2 margin
+    exceeds 10x that step's measured max |device - oracle| penalised-logit
+    error, so every decision is numerically determined.  Then:
+      * K1 in situ: each device token is the argmax of the device's own
+        penalised logits (bit-exact);
+      * each device token equals the oracle's greedy choice on that history, so
+        by induction the device stream IS the oracle's free-running stream --
+        and it equals the golden streams the reference's sample() produced
+        (tests/golden/greedy_config1.npz).
     """
-    c = tiny_cfg
-    orc = LlamaOracle(c, 1234)
-    P, T, R = 50, 64, 4
-    pen = 1.3
+    from pathlib import Path
+
+    from paper_2602_00269_b200.config import PLANTED_WEIGHT_SEED, tiny_planted
+    from paper_2602_00269_b200.device import VoxDevice
+
+    g = np.load(Path(__file__).resolve().parent / "golden" / "greedy_config1.npz")
+    ws, run_seed, R, P, T = (int(x) for x in g["meta"])
+    pen = float(g["penalty"])
+    c = tiny_planted(max_slots=8)
+    assert ws == PLANTED_WEIGHT_SEED
+    dev = VoxDevice(c, weight_seed=ws)
+    orc = LlamaOracle(c, ws)
     greedy = Sampling(temperature=0.0, repetition_penalty=pen)
-    slots = [tiny_dev.admit(request_seed(0, r), P, T, greedy) for r in range(R)]
-    tiny_dev.forward(np.concatenate([_prefill_rows(s, P) for s in slots]), sample=False)
+    slots = [dev.admit(request_seed(run_seed, r), P, T, greedy) for r in range(R)]
+    dev.forward(np.concatenate([_prefill_rows(s, P) for s in slots]), sample=False)
+    prompts = [np.array(prompt_ids(request_seed(run_seed, r), P, c.text_vocab)) for r in range(R)]
+    for r in range(R):
+        orc.forward(r, prompts[r][:-1], np.arange(P - 1), want_logits=False)
+    wins = [osamp.RingWindow(64, c.vocab) for _ in range(R)]
     got = np.zeros((R, T), np.int64)
+    choice = np.zeros((R, T), np.int64)
+    err = np.zeros((R, T))
+    margin = np.zeros((R, T))
     for s in range(T):
         rows = np.array([[sl, P - 1 + s, -1, 1] for sl in slots], np.int32)
-        toks, _ = tiny_dev.forward(rows, want_tokens=True)
+        toks, _ = dev.forward(rows, want_tokens=True)
         got[:, s] = toks
-    for r, sl in enumerate(slots):
-        assert np.array_equal(tiny_dev.read_tokens(sl, P, T), got[r])
-        tiny_dev.release(sl)
-
-    # teacher-forced replay: device full logits + oracle logits on the same history
-    slots = [tiny_dev.admit(request_seed(0, r), P, T, greedy) for r in range(R)]
-    tiny_dev.forward(np.concatenate([_prefill_rows(s, P) for s in slots]), sample=False)
-    for r in range(R):
-        prompt = np.array(prompt_ids(request_seed(0, r), P, c.text_vocab))
-        orc.forward(r, prompt[:-1], np.arange(P - 1), want_logits=False)
-    wins = [osamp.RingWindow(64, c.vocab) for _ in range(R)]
-    near_ties, checked = 0, 0
-    for s in range(T):
-        rows = np.array([[sl, P - 1 + s, (-1 if s == 0 else int(got[r, s - 1])), 1] for r, sl in enumerate(slots)],
-                        np.int32)
-        _, dlog = tiny_dev.forward(rows, sample=False, full_logits=True, sync=True)
+        dlog, base = dev.read_logits()
         lo, hi = audio_range(c, s)
+        assert base == lo and dlog.shape == (R, hi - lo)  # one frame slot -> that slot's head rows
         for r in range(R):
-            tok_in = (int(prompt_ids(request_seed(0, r), P, c.text_vocab)[-1]) if s == 0 else int(got[r, s - 1]))
-            ol, _ = orc.forward(r, np.array([tok_in]), np.array([P - 1 + s]))
-            dpen = osamp.apply_repetition_penalty(masked(dlog[r], lo, hi), pen, wins[r])
-            open_ = osamp.apply_repetition_penalty(masked(ol[0], lo, hi), pen, wins[r])
-            # K1 in situ: device token == argmax of the device's own penalised logits
-            assert int(np.argmax(dpen)) == got[r, s], (r, s)
-            err = np.abs(dlog[r, lo:hi].astype(np.float64) - ol[0, lo:hi]).max()
-            assert err < 0.15, (r, s, err)  # bf16 rounding noise is ~0.03-0.06; bugs are O(1)
-            srt = np.sort(open_[lo:hi])[::-1]
-            margin = srt[0] - srt[1]
-            if margin > 2 * err:
-                checked += 1
-                assert int(np.argmax(open_)) == got[r, s], (r, s, margin, err)
-            else:
-                near_ties += 1
+            tok_in = int(prompts[r][-1]) if s == 0 else int(got[r, s - 1])
+            ol, _ = orc.forward(r, np.array([tok_in]), np.array([P - 1 + s]), head=(lo, hi))
+            dpen = osamp.apply_repetition_penalty(dlog[r].astype(np.float64), pen, _Shift(wins[r], lo, hi))
+            open_ = osamp.apply_repetition_penalty(ol[0].astype(np.float64), pen, _Shift(wins[r], lo, hi))
+            assert int(np.argmax(dpen)) + lo == got[r, s], (r, s)  # K1 in situ
+            err[r, s] = np.abs(dpen - open_).max()
+            srt = np.sort(open_)[::-1]
+            margin[r, s] = srt[0] - srt[1]
+            choice[r, s] = int(np.argmax(open_)) + lo
             wins[r].append(int(got[r, s]))
-    # bf16 GEMM operands make device/oracle logits differ by O(1e-2) (rounding
-    # cascades); only decisions closer than that may legitimately differ.
-    assert checked >= 0.85 * R * T, (checked, near_ties)
+    ratio = margin / np.maximum(err, 1e-30)
+    print(f"config-1 greedy parity: min margin {margin.min():.4f}, max |dlogit| {err.max():.3e}, "
+          f"median |dlogit| {np.median(err):.3e}, min per-step margin/err {ratio.min():.1f}")
+    assert ratio.min() >= 10, (ratio.min(), np.argwhere(ratio < 10)[:4].tolist())  # planted-margin precondition
+    assert np.array_equal(got, choice)
+    assert np.array_equal(got, g["tokens"])
     for r, sl in enumerate(slots):
-        tiny_dev.release(sl)
-        orc.release(r)
+        assert np.array_equal(dev.read_tokens(sl, P, T), got[r])
+        dev.release(sl)
+    dev.close()
+
+
+class _Shift:
+    """A RingWindow seen through a column offset (logits slice [lo, hi) -> ids lo..)."""
+
+    def __init__(self, win, lo, hi):
+        self.counts = win.counts[lo:hi]
+        self._n = len(win)
+
+    def __len__(self):
+        return self._n
 
 
 @pytest.mark.parametrize("n_req,P", [(3, 33), (6, 50), (11, 30)])
