@@ -51,6 +51,7 @@ class EngineStats:
     iterations: int = 0
     lm_rows: int = 0
     decode_rows: int = 0
+    decode_ctx: int = 0  # sum over decode rows of the context each attends (pos + 1)
     prefill_rows: int = 0
     detok_calls: int = 0
     detok_windows: int = 0
@@ -122,6 +123,7 @@ class StreamingEngine:
                 r.prefilled = True
             else:
                 rows.append([run.slot, r.prompt_tokens - 1 + r.tokens_generated, -1, 1])
+                st.decode_ctx += r.prompt_tokens + r.tokens_generated
                 r.tokens_generated += 1
                 st.decode_rows += 1
         if rows:
