@@ -187,3 +187,109 @@ class DetokWeights:
         self.out_w = init_f32(7 * C4, k(T_OUT_W), f32(0.15) * np.sqrt(f32(3.0) / (f32(7.0) * f32(C4))),
                               0.0).reshape(C4, 7)
         self.out_b = init_f32(1, k(T_OUT_B), 0.05, 0.0)[0]
+
+
+# Mimi-style decoder (csrc/mimi.cu: mimi_create) -- tensor ids 300.., layer = codebook /
+# transformer layer / SEANet block.  GEMM weights are generated directly in the device's
+# GEMM layout ([out, taps * in] with tap-major K); MimiWeights.torch_layout() turns them
+# into the PyTorch Conv1d / ConvTranspose1d / Linear layouts transformers uses.
+T_MI_EMB, T_MI_PSEM, T_MI_PAC, T_MI_UP = 300, 301, 302, 303
+T_MI_LN1W, T_MI_LN1B, T_MI_LN2W, T_MI_LN2B = 310, 311, 312, 313
+T_MI_QKV, T_MI_O, T_MI_FC1, T_MI_FC2, T_MI_LS1, T_MI_LS2 = 314, 315, 316, 317, 318, 319
+T_MI_C0W, T_MI_C0B, T_MI_UPW, T_MI_UPB = 330, 331, 332, 333
+T_MI_R1W, T_MI_R1B, T_MI_R2W, T_MI_R2B, T_MI_OUTW, T_MI_OUTB = 334, 335, 336, 337, 338, 339
+
+
+class MimiWeights:
+    """All Mimi tensors as float32 arrays holding bf16-representable values."""
+
+    def __init__(self, cfg, seed: int):
+        k = lambda tid, l=0: tensor_key(seed, tid, l)  # noqa: E731
+        D, cd, cb, F = cfg.hidden, cfg.cb_dim, cfg.cb_size, cfg.ffn
+        self.cfg = cfg
+        self.emb = [init_f32(cb * cd, k(T_MI_EMB, q), np.sqrt(f32(3.0) / f32(cfg.n_q)), 0.0).reshape(cb, cd)
+                    for q in range(cfg.n_q)]
+        self.psem = init_bf16(D * cd, k(T_MI_PSEM), np.sqrt(f32(3.0) / f32(cd))).reshape(D, cd)
+        self.pac = init_bf16(D * cd, k(T_MI_PAC), np.sqrt(f32(3.0) / f32(cd))).reshape(D, cd)
+        self.up = init_f32(D * 4, k(T_MI_UP), 0.5, 0.0).reshape(D, 4)
+        self.layers = []
+        for l in range(cfg.n_layers):
+            self.layers.append(dict(
+                ln1w=init_f32(D, k(T_MI_LN1W, l), 0.25, 1.0), ln1b=init_f32(D, k(T_MI_LN1B, l), 0.05, 0.0),
+                ln2w=init_f32(D, k(T_MI_LN2W, l), 0.25, 1.0), ln2b=init_f32(D, k(T_MI_LN2B, l), 0.05, 0.0),
+                qkv=init_bf16(3 * D * D, k(T_MI_QKV, l), np.sqrt(f32(3.0) / f32(D))).reshape(3 * D, D),
+                o=init_bf16(D * D, k(T_MI_O, l), np.sqrt(f32(3.0) / f32(D))).reshape(D, D),
+                fc1=init_bf16(F * D, k(T_MI_FC1, l), np.sqrt(f32(3.0) / f32(D))).reshape(F, D),
+                fc2=init_bf16(D * F, k(T_MI_FC2, l), np.sqrt(f32(3.0) / f32(F))).reshape(D, F),
+                ls1=init_f32(D, k(T_MI_LS1, l), 0.05, 0.1), ls2=init_f32(D, k(T_MI_LS2, l), 0.05, 0.1),
+            ))
+        ch = cfg.channels
+        kk = cfg.kernel
+        self.c0w = init_bf16(ch[0] * kk * D, k(T_MI_C0W), np.sqrt(f32(3.0) / f32(kk * D))).reshape(ch[0], kk * D)
+        self.c0b = init_f32(ch[0], k(T_MI_C0B), 0.05, 0.0)
+        self.blocks = []
+        rk = cfg.res_kernel
+        for b, s in enumerate(cfg.ratios):
+            Ci, Co = ch[b], ch[b + 1]
+            h = Co // cfg.compress
+            self.blocks.append(dict(
+                upw=init_bf16(s * Co * 2 * Ci, k(T_MI_UPW, b), np.sqrt(f32(3.0) / (f32(2.0) * f32(Ci)))).reshape(s * Co, 2 * Ci),
+                upb=init_f32(Co, k(T_MI_UPB, b), 0.05, 0.0),
+                r1w=init_bf16(h * rk * Co, k(T_MI_R1W, b), np.sqrt(f32(3.0) / f32(rk * Co))).reshape(h, rk * Co),
+                r1b=init_f32(h, k(T_MI_R1B, b), 0.05, 0.0),
+                r2w=init_bf16(Co * h, k(T_MI_R2W, b), f32(0.5) * np.sqrt(f32(3.0) / f32(h))).reshape(Co, h),
+                r2b=init_f32(Co, k(T_MI_R2B, b), 0.05, 0.0),
+            ))
+        lk, C4 = cfg.last_kernel, ch[-1]
+        self.outw = init_f32(lk * C4, k(T_MI_OUTW), np.sqrt(f32(3.0) / f32(lk * C4)), 0.0).reshape(lk * C4)
+        self.outb = init_f32(1, k(T_MI_OUTB), 0.05, 0.0)[0]
+
+    def torch_layout(self) -> dict:
+        """name -> np.ndarray in transformers MimiModel parameter layout (modeling_mimi.py)."""
+        cfg, D = self.cfg, self.cfg.hidden
+        out = {}
+        for q in range(cfg.n_q):
+            if q < cfg.n_semantic:
+                pre = f"quantizer.semantic_residual_vector_quantizer.layers.{q}.codebook"
+            else:
+                pre = f"quantizer.acoustic_residual_vector_quantizer.layers.{q - cfg.n_semantic}.codebook"
+            out[pre + ".embed_sum"] = self.emb[q]
+            out[pre + ".cluster_usage"] = np.ones(cfg.cb_size, np.float32)
+        out["quantizer.semantic_residual_vector_quantizer.output_proj.weight"] = self.psem[:, :, None]
+        out["quantizer.acoustic_residual_vector_quantizer.output_proj.weight"] = self.pac[:, :, None]
+        out["upsample.conv.weight"] = self.up[:, None, :]
+        for l, L in enumerate(self.layers):
+            p = f"decoder_transformer.layers.{l}."
+            out[p + "input_layernorm.weight"], out[p + "input_layernorm.bias"] = L["ln1w"], L["ln1b"]
+            out[p + "post_attention_layernorm.weight"], out[p + "post_attention_layernorm.bias"] = L["ln2w"], L["ln2b"]
+            out[p + "self_attn.q_proj.weight"] = L["qkv"][:D]
+            out[p + "self_attn.k_proj.weight"] = L["qkv"][D:2 * D]
+            out[p + "self_attn.v_proj.weight"] = L["qkv"][2 * D:]
+            out[p + "self_attn.o_proj.weight"] = L["o"]
+            out[p + "mlp.fc1.weight"], out[p + "mlp.fc2.weight"] = L["fc1"], L["fc2"]
+            out[p + "self_attn_layer_scale.scale"], out[p + "mlp_layer_scale.scale"] = L["ls1"], L["ls2"]
+        ch, kk, rk = cfg.channels, cfg.kernel, cfg.res_kernel
+        # GEMM layout W[o, j*Cin + c] (tap j reads x[t-(k-1)+j]) -> Conv1d weight[o, c, j]
+        conv = lambda w, k, ci: w.reshape(w.shape[0], k, ci).transpose(0, 2, 1)  # noqa: E731
+        out["decoder.layers.0.conv.weight"] = conv(self.c0w, kk, D)
+        out["decoder.layers.0.conv.bias"] = self.c0b
+        for b, s in enumerate(cfg.ratios):
+            B = self.blocks[b]
+            Ci, Co = ch[b], ch[b + 1]
+            h = Co // cfg.compress
+            # GEMM row j*Co + o, cols [x_{t-1} | x_t]: out[t*s + j] = x_t w[:, :, j] + x_{t-1} w[:, :, j + s]
+            w4 = B["upw"].reshape(s, Co, 2, Ci)
+            wt = np.empty((Ci, Co, 2 * s), np.float32)
+            wt[:, :, :s] = w4[:, :, 1, :].transpose(2, 1, 0)
+            wt[:, :, s:] = w4[:, :, 0, :].transpose(2, 1, 0)
+            i = 1 + 3 * b
+            out[f"decoder.layers.{i + 1}.conv.weight"] = wt
+            out[f"decoder.layers.{i + 1}.conv.bias"] = B["upb"]
+            out[f"decoder.layers.{i + 2}.block.1.conv.weight"] = conv(B["r1w"], rk, Co)
+            out[f"decoder.layers.{i + 2}.block.1.conv.bias"] = B["r1b"]
+            out[f"decoder.layers.{i + 2}.block.3.conv.weight"] = conv(B["r2w"], 1, h)
+            out[f"decoder.layers.{i + 2}.block.3.conv.bias"] = B["r2b"]
+        n = 2 + 3 * len(cfg.ratios)
+        out[f"decoder.layers.{n}.conv.weight"] = conv(self.outw[None, :], cfg.last_kernel, ch[-1])
+        out[f"decoder.layers.{n}.conv.bias"] = np.array([self.outb], np.float32)
+        return out

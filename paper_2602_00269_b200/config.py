@@ -213,5 +213,74 @@ def tiny_csm(n_codebooks: int = 8):
     return bb, dp
 
 
+@dataclass(frozen=True)
+class MimiConfig:
+    """Config 3 detokenizer: Mimi-style 12.5 Hz streaming decoder ([3P] transformers 5.5.0
+    ``MimiConfig`` defaults, configuration_mimi.py:86-123; ``MimiModel.decode``
+    modeling_mimi.py:1613-1680): split RVQ (1 semantic + n_q-1 acoustic codebooks of
+    2048 x 256, each group summed then projected 256 -> 512), depthwise ConvT x2 to 25 Hz,
+    an 8-layer sliding-window (250) transformer (LayerNorm, GELU MLP, layer scale, RoPE),
+    and the causal SEANet decoder (k7 conv 512 -> 1024; per ratio 8/6/5/4: ELU,
+    ConvT(k = 2r, stride r) halving channels, one residual block ELU-k3-ELU-k1; ELU, k3
+    conv -> 1 channel).  1920 samples per 12.5 Hz frame at 24 kHz."""
+
+    name: str = "mimi-12.5hz"
+    n_q: int = 32
+    n_semantic: int = 1
+    cb_size: int = 2048
+    cb_dim: int = 256
+    hidden: int = 512
+    n_layers: int = 8
+    n_heads: int = 8
+    ffn: int = 2048
+    window: int = 250
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+    filters: int = 64
+    ratios: tuple = (8, 6, 5, 4)
+    kernel: int = 7
+    last_kernel: int = 3
+    res_kernel: int = 3
+    compress: int = 2
+    max_slots: int = 64
+    max_frames: int = 256     # 12.5 Hz frames per decode call (all requests)
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.n_heads
+
+    @property
+    def hop(self) -> int:
+        """samples per 25 Hz transformer position"""
+        h = 1
+        for r in self.ratios:
+            h *= r
+        return h
+
+    @property
+    def frame_samples(self) -> int:
+        return 2 * self.hop
+
+    @property
+    def channels(self) -> list:
+        """SEANet channels: 2^len(ratios) * filters halving per ratio (1024 .. 64)"""
+        c = [self.filters * (1 << len(self.ratios))]
+        for _ in self.ratios:
+            c.append(c[-1] // 2)
+        return c
+
+    def with_capacity(self, **kw) -> "MimiConfig":
+        return replace(self, **kw)
+
+
+def mimi(**kw) -> MimiConfig:
+    return MimiConfig(**kw)
+
+
+def tiny_mimi(**kw) -> MimiConfig:
+    """CPU-test-sized Mimi: production conv/transformer dims, 2 transformer layers, 4 codebooks."""
+    return MimiConfig(**{"name": "tiny-mimi", "n_q": 4, "n_layers": 2, "max_slots": 8, "max_frames": 64, **kw})
+
+
 CONFIGS = {"tiny": tiny, "tiny_planted": tiny_planted, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy,
            "csm_backbone": csm_backbone, "csm_depth": csm_depth}
