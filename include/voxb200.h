@@ -243,6 +243,43 @@ int vox_read_weight(VoxCtx* ctx, const char* name, int32_t layer, void* out, siz
 int vox_read_kv(VoxCtx* ctx, int32_t layer, int32_t slot, int32_t pos, float* k_out,
                 float* v_out);
 
+/* ------------------------------------------------------------------------
+ * K7: Mimi-style 12.5 Hz streaming detokenizer (BASELINE config 3, CSM-1B-style;
+ * [3P] transformers MimiModel.decode, modeling_mimi.py:1613-1680).  Replaces
+ * Executor.detokenize_windows (model_api.py:213-220) for a depth-stage profile
+ * (profiles.py:214-231: token_rate 12.5, stateful_detok) -- the reference's own
+ * detokenizer is a stub (profiles.py:333-356).  A stream (vox_mimi_open) keeps its
+ * conv padding caches and a sliding-window K/V ring on the device, so consecutive
+ * vox_mimi_decode calls over its frames reproduce the full-sequence decode.
+ * ------------------------------------------------------------------------ */
+typedef struct VoxMimiCfg {
+  int32_t n_q, n_semantic, cb_size, cb_dim;   /* split RVQ: codebooks x codes x dim  */
+  int32_t hidden, n_layers, n_heads, ffn, window;
+  float rope_theta, eps;
+  int32_t filters, n_ratios, ratios[4];       /* SEANet: channels filters << n_ratios */
+  int32_t kernel, last_kernel, res_kernel, compress;
+  int32_t max_slots;                          /* concurrent streams                   */
+  int32_t max_frames;                         /* 12.5 Hz frames per decode call       */
+} VoxMimiCfg;
+
+typedef struct VoxMimiReq {
+  int32_t slot;     /* stream from vox_mimi_open                                  */
+  int32_t n_frames; /* new frames, in order; 1 <= n_frames <= min(64, max_frames) */
+} VoxMimiReq;
+
+typedef struct VoxMimi VoxMimi;
+
+int vox_mimi_create(int device, const VoxMimiCfg* cfg, uint64_t weight_seed, VoxMimi** out);
+void vox_mimi_destroy(VoxMimi* m);
+const char* vox_mimi_last_error(const VoxMimi* m); /* m may be NULL */
+int vox_mimi_open(VoxMimi* m, int32_t* slot);      /* new stream, zero history     */
+int vox_mimi_close(VoxMimi* m, int32_t slot);
+/* codes: host [sum n_frames][n_q] int32 (request order); pcm_out: host
+ * [sum n_frames * frame_samples] float (request order), blocking. */
+int vox_mimi_decode(VoxMimi* m, const VoxMimiReq* reqs, int32_t n, const int32_t* codes,
+                    float* pcm_out, int64_t* n_samples);
+int vox_mimi_launch_count(VoxMimi* m, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

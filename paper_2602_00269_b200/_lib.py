@@ -60,6 +60,21 @@ class VoxWindow(C.Structure):
     ]
 
 
+class VoxMimiCfg(C.Structure):
+    _fields_ = [
+        ("n_q", C.c_int32), ("n_semantic", C.c_int32), ("cb_size", C.c_int32), ("cb_dim", C.c_int32),
+        ("hidden", C.c_int32), ("n_layers", C.c_int32), ("n_heads", C.c_int32), ("ffn", C.c_int32),
+        ("window", C.c_int32), ("rope_theta", C.c_float), ("eps", C.c_float),
+        ("filters", C.c_int32), ("n_ratios", C.c_int32), ("ratios", C.c_int32 * 4),
+        ("kernel", C.c_int32), ("last_kernel", C.c_int32), ("res_kernel", C.c_int32), ("compress", C.c_int32),
+        ("max_slots", C.c_int32), ("max_frames", C.c_int32),
+    ]
+
+
+class VoxMimiReq(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("n_frames", C.c_int32)]
+
+
 # status -> exception (VoxStatus in include/voxb200.h)
 _STATUS_TO_EXC = {
     1: ValueError,
@@ -122,6 +137,13 @@ _SIGS = {
     "vox_read_frame": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _i32p]),
     "vox_project_ext": (C.c_int, [_P, _P, C.c_int32]),
     "vox_link_tokens": (C.c_int, [_P, _P, _i32p, C.c_int32, C.c_int32, C.c_int32]),
+    "vox_mimi_create": (C.c_int, [C.c_int, C.POINTER(VoxMimiCfg), C.c_uint64, C.POINTER(_P)]),
+    "vox_mimi_destroy": (None, [_P]),
+    "vox_mimi_last_error": (C.c_char_p, [_P]),
+    "vox_mimi_open": (C.c_int, [_P, _i32p]),
+    "vox_mimi_close": (C.c_int, [_P, C.c_int32]),
+    "vox_mimi_decode": (C.c_int, [_P, C.POINTER(VoxMimiReq), C.c_int32, _i32p, _f32p, C.POINTER(C.c_int64)]),
+    "vox_mimi_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -151,9 +173,9 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
     return lib
 
 
-def check(rc: int, ctx=None) -> None:
+def check(rc: int, ctx=None, mimi=None) -> None:
     if rc == 0:
         return
-    msg = load().vox_last_error(ctx)
+    msg = load().vox_mimi_last_error(mimi) if mimi is not None else load().vox_last_error(ctx)
     text = msg.decode() if msg else f"status {rc}"
     raise _STATUS_TO_EXC.get(rc, RuntimeError)(text)
