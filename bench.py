@@ -709,12 +709,49 @@ def csm_frames(batch: int, frames: int, seed: int, hbm: float, device: int):
            "forwards_per_frame": 1 + dcodes,
            "roofline": {"bound": "hbm", "achieved": round(by / dt / 1e9, 1), "peak": hbm, "unit": "GB/s",
                         "frac": round(by / dt / 1e9 / hbm, 4), "bytes_per_frame": int(by)},
-           "timing": "host wall clock around the frames (the pipeline syncs the host at each hand-over)",
-           "detokenizer": "not built (Mimi decoder is SURVEY §8f row 1 remainder)"}
+           "timing": "host wall clock around the frames (the pipeline syncs the host at each hand-over)"}
     for s_ in streams:
         pipe.release(s_)
     bb.close()
     dp.close()
+    out["detokenizer"] = mimi_chunks(batch, 10, seed, device)
+    out["audio_s_per_s_lm_plus_detok"] = round(1.0 / (1.0 / out["audio_s_per_s_lm_only"] +
+                                                       1.0 / out["detokenizer"]["audio_s_per_s"]), 1)
+    return out
+
+
+def mimi_chunks(batch: int, chunk: int, seed: int, device: int, calls: int = 6):
+    """K7 Mimi-style detokenizer at config-3 dims: `batch` streams each decoding one
+    `chunk`-frame window per call (depth_like profile: chunk_size 10, profiles.py:214-231),
+    steady state (streams already hold history).  Device time by CUDA events around the
+    kernels; tensor roofline on the algorithmic FLOPs of the decode (MimiDecoder.flops_per_frame)."""
+    from paper_2602_00269_b200.config import MimiConfig
+    from paper_2602_00269_b200.mimi import MimiDecoder
+
+    _, tflops, _ = _peaks()
+    cfg = MimiConfig(max_slots=batch, max_frames=batch * chunk)
+    dec = MimiDecoder(cfg, seed, device)
+    rng = np.random.default_rng(seed)
+    slots = [dec.open() for _ in range(batch)]
+    ms = []
+    t0 = time.perf_counter()
+    for i in range(calls + 2):
+        codes = [rng.integers(0, cfg.cb_size, size=(chunk, cfg.n_q)) for _ in range(batch)]
+        dec.decode(slots, codes)
+        if i >= 2:
+            ms.append(dec.last_ms())
+    wall = (time.perf_counter() - t0) / (calls + 2)
+    m = float(np.median(ms))
+    fl = dec.flops_per_frame() * batch * chunk
+    audio = batch * chunk / 12.5
+    out = {"kernel": "K7 csrc/mimi.cu (sliding-window transformer + SEANet convs as tcgen05 im2col GEMMs)",
+           "streams": batch, "frames_per_call": chunk, "ms_per_call": round(m, 3),
+           "wall_ms_per_call_incl_copies": round(wall * 1e3, 3), "audio_s_per_s": round(audio / (m / 1e3), 1),
+           "launches_per_call": dec.launch_count() // (calls + 2),
+           "roofline": {"bound": "tensor", "achieved": round(fl / (m / 1e3) / 1e12, 2), "peak": tflops,
+                        "unit": "TFLOP/s", "frac": round(fl / (m / 1e3) / 1e12 / tflops, 4),
+                        "gflop_per_call": round(fl / 1e9, 2)}}
+    dec.close()
     return out
 
 

@@ -279,6 +279,8 @@ int vox_mimi_close(VoxMimi* m, int32_t slot);
 int vox_mimi_decode(VoxMimi* m, const VoxMimiReq* reqs, int32_t n, const int32_t* codes,
                     float* pcm_out, int64_t* n_samples);
 int vox_mimi_launch_count(VoxMimi* m, int64_t* launches);
+/* CUDA-event time of the last decode's kernels (H2D of codes / D2H of PCM excluded) */
+int vox_mimi_last_ms(VoxMimi* m, double* ms);
 
 #ifdef __cplusplus
 }

@@ -144,6 +144,7 @@ _SIGS = {
     "vox_mimi_close": (C.c_int, [_P, C.c_int32]),
     "vox_mimi_decode": (C.c_int, [_P, C.POINTER(VoxMimiReq), C.c_int32, _i32p, _f32p, C.POINTER(C.c_int64)]),
     "vox_mimi_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "vox_mimi_last_ms": (C.c_int, [_P, C.POINTER(C.c_double)]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -356,6 +356,8 @@ struct VoxMimi {
   size_t stage_ints = 0;
   int64_t launches = 0;
   std::vector<int> chans;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // device time of the last decode's kernels
+  double last_ms = 0.0;
 };
 
 namespace {
@@ -694,6 +696,8 @@ int vox_mimi_create(int device, const VoxMimiCfg* cfg, uint64_t seed, VoxMimi** 
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   int rc = cudaStreamCreateWithPriority(&m->st, cudaStreamNonBlocking, lo) == cudaSuccess ? VOX_OK : VOX_ERR_CUDA;
+  if (rc == VOX_OK && (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess))
+    rc = mfail(m, VOX_ERR_CUDA, "event create");
   if (rc == VOX_OK) rc = create_weights(m, seed);
   if (rc == VOX_OK) rc = create_state(m);
   if (rc == VOX_OK && cudaStreamSynchronize(m->st) != cudaSuccess) rc = mfail(m, VOX_ERR_CUDA, "init sync");
@@ -729,6 +733,8 @@ void vox_mimi_destroy(VoxMimi* m) {
     cudaFree(p);
   if (m->h_stage) cudaFreeHost(m->h_stage);
   if (m->h_pcm) cudaFreeHost(m->h_pcm);
+  if (m->ev0) cudaEventDestroy(m->ev0);
+  if (m->ev1) cudaEventDestroy(m->ev1);
   if (m->st) cudaStreamDestroy(m->st);
   delete m;
 }
@@ -789,18 +795,31 @@ int vox_mimi_decode(VoxMimi* m, const VoxMimiReq* reqs, int32_t n, const int32_t
     hcodes[e] = codes[e];
   }
   MCK(cudaMemcpyAsync(m->d_stage, m->h_stage, m->stage_ints * 4, cudaMemcpyHostToDevice, m->st));
+  MCK(cudaEventRecord(m->ev0, m->st));
   MRET(enqueue(m, n, F));
+  MCK(cudaEventRecord(m->ev1, m->st));
   int64_t hop = 2;
   for (int b = 0; b < g.n_ratios; ++b) hop *= g.ratios[b];
   const int64_t total = F * hop;
   MCK(cudaMemcpyAsync(m->h_pcm, m->pcm, total * 4, cudaMemcpyDeviceToHost, m->st));
   MCK(cudaStreamSynchronize(m->st));
+  {
+    float ms = 0.f;
+    MCK(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    m->last_ms = ms;
+  }
   if (pcm_out) std::copy(m->h_pcm, m->h_pcm + total, pcm_out);
   if (n_samples) *n_samples = total;
   for (int i = 0; i < n; ++i) {
     m->parity[reqs[i].slot] ^= 1;
     m->pos[reqs[i].slot] += 2 * reqs[i].n_frames;
   }
+  return VOX_OK;
+}
+
+int vox_mimi_last_ms(VoxMimi* m, double* ms) {
+  if (!m || !ms) return mfail(m, VOX_ERR_INVALID, "null argument");
+  *ms = m->last_ms;
   return VOX_OK;
 }
 

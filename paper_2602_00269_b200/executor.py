@@ -185,8 +185,11 @@ class CsmExecutor:
     history the engine recorded.  Latencies are measured wall time of the device work.
     """
 
-    def __init__(self, profile, bcfg: ModelConfig, dcfg: ModelConfig, weight_seed: int = 0, device: int = 0):
+    def __init__(self, profile, bcfg: ModelConfig, dcfg: ModelConfig, weight_seed: int = 0, device: int = 0,
+                 mimi_cfg=None):
+        from .config import MimiConfig
         from .csm import CsmFrames
+        from .mimi import MimiDecoder
 
         if not profile.has_depth_stage:
             raise errors.DepthStageUnsupported(f"profile {profile.name} has no depth stage")
@@ -207,17 +210,32 @@ class CsmExecutor:
         self._depth_s = 0.0
         self.mismatches = 0
         self.frames_run = 0
+        # K7: the Mimi-style streaming detokenizer over this profile's codebooks
+        mc = mimi_cfg or MimiConfig(max_slots=bcfg.max_slots, max_frames=max(64, profile.max_detok_batch *
+                                                                            profile.chunk_size))
+        if mc.n_q != self.C or mc.cb_size != self.cs:
+            from dataclasses import replace as _replace
+
+            mc = _replace(mc, n_q=self.C, cb_size=self.cs)
+        self.mimi = MimiDecoder(mc, weight_seed + 2, device)
+        self._mslot: dict[int, int] = {}
+        self._covered: dict[int, int] = {}
 
     def close(self) -> None:
         self.bb.close()
         self.dp.close()
+        self.mimi.close()
 
     def release(self, rid: int) -> None:
         s = self._slot.pop(rid, None)
         self._codes.pop(rid, None)
+        self._covered.pop(rid, None)
         if s is not None:
             self.bb.release(s[0])
             self.dp.release(s[1])
+        ms = self._mslot.pop(rid, None)
+        if ms is not None:
+            self.mimi.release(ms)
 
     def _rows_logits(self, dev: VoxDevice, n: int) -> np.ndarray:
         lg, _ = dev.read_logits()
@@ -237,6 +255,8 @@ class CsmExecutor:
                         raise errors.PromptTooLong(f"prompt of {P} tokens exceeds context capacity")
                     st = self.pipe.admit(batch.seeds[i], P, target, self.sampling, self.sampling)
                     self._slot[rid] = (st.bslot, st.dslot, P)
+                    self._mslot[rid] = self.mimi.open()
+                    self._covered[rid] = 0
                 rows += [[self._slot[rid][0], p, -1, 0] for p in range(P - 1)]
             for a in range(0, len(rows), self.bcfg.max_rows):
                 self.bb.forward(np.asarray(rows[a:a + self.bcfg.max_rows], np.int32), sample=False, sync=True)
@@ -306,16 +326,33 @@ class CsmExecutor:
 
     def detokenize_windows(self, batch, specs: Sequence, windows: Sequence[np.ndarray],
                            caches: Sequence[model_api.DetokenizerCache]):
+        """Stateful Mimi decode of each window's new frames (model_api.py:213-220;
+        profiles.py:333-356 is the stub it replaces): the request's stream on the K7
+        context continues from its cached history, so the chunks concatenate to the
+        full-sequence decode."""
         from ._ref import core
 
         t0 = time.perf_counter()
+        slots, codes = [], []
+        for spec, win in zip(specs, windows):
+            if spec.request not in self._mslot:
+                raise errors.CacheMissing(f"request {spec.request} has no detokenizer stream")
+            w = np.asarray(win)
+            g0 = spec.start + spec.length - spec.new_tokens
+            if g0 != self._covered[spec.request]:
+                raise errors.WindowRuleViolation("the stateful Mimi decoder needs in-order windows")
+            slots.append(self._mslot[spec.request])
+            codes.append(w[w.shape[0] - spec.new_tokens:])
+        pcms = self.mimi.decode(slots, codes) if slots else []
         outs = []
-        for spec, win, cache in zip(specs, windows, caches):
+        for spec, win, cache, pcm in zip(specs, windows, caches, pcms):
             cache.window_ids = np.array(win, copy=True)
             cache.calls += 1
-            outs.append(model_api.AudioChunkOut(request=spec.request, new_tokens=spec.new_tokens,
-                                                playback_us=core.playback_us_for(spec.new_tokens,
-                                                                                 self.profile.token_rate)))
+            cache.bytes_held = 4 * pcm.size
+            self._covered[spec.request] += spec.new_tokens
+            outs.append(PcmChunkOut(request=spec.request, new_tokens=spec.new_tokens,
+                                    playback_us=core.playback_us_for(spec.new_tokens, self.profile.token_rate),
+                                    pcm=pcm))
             if spec.final:
                 self.release(spec.request)
         return outs, time.perf_counter() - t0

@@ -93,6 +93,32 @@ class MimiDecoder:
             a = b
         return out
 
+    def last_ms(self) -> float:
+        """CUDA-event time of the last decode's kernels."""
+        v = C.c_double()
+        self._check(self.lib.vox_mimi_last_ms(self.h, C.byref(v)))
+        return v.value
+
+    def flops_per_frame(self, ctx: int | None = None) -> float:
+        """Algorithmic FLOPs per 12.5 Hz frame (2 per MAC): transformer projections +
+        attention over a window of `ctx` keys (default: full window), SEANet convs."""
+        c = self.cfg
+        D, F, L = c.hidden, c.ffn, c.n_layers
+        ctx = c.window if ctx is None else ctx
+        pos = 2
+        fl = pos * L * 2 * (4 * D * D + 2 * D * F + 2 * ctx * D)
+        ch = c.channels
+        fl += pos * 2 * c.kernel * D * ch[0]
+        rows = pos
+        for b, s in enumerate(c.ratios):
+            Ci, Co = ch[b], ch[b + 1]
+            hh = Co // c.compress
+            fl += rows * 2 * (2 * Ci) * (s * Co)
+            rows *= s
+            fl += rows * 2 * (c.res_kernel * Co * hh + hh * Co)
+        fl += rows * 2 * c.last_kernel * ch[-1]
+        return float(fl)
+
     def launch_count(self) -> int:
         v = C.c_int64()
         self._check(self.lib.vox_mimi_launch_count(self.h, C.byref(v)))

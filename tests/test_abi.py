@@ -57,13 +57,16 @@ def test_struct_layouts_match_header(tmp_path):
         '#include <stdio.h>\n#include <stddef.h>\n#include "voxb200.h"\n'
         "int main(void){printf(\"%zu %zu %zu %zu %zu %zu %zu\\n\", sizeof(VoxModelCfg), sizeof(VoxSampling),"
         " sizeof(VoxRow), sizeof(VoxWindow), offsetof(VoxModelCfg, rates), offsetof(VoxModelCfg, max_detok_frames),"
-        " offsetof(VoxSampling, top_k));return 0;}\n")
+        " offsetof(VoxSampling, top_k));"
+        "printf(\"%zu %zu %zu %zu\\n\", sizeof(VoxMimiCfg), offsetof(VoxMimiCfg, ratios), offsetof(VoxMimiCfg, max_frames),"
+        " sizeof(VoxMimiReq));return 0;}\n")
     exe = tmp_path / "p"
     subprocess.run([gcc, "-I", str(ROOT / "include"), "-o", str(exe), str(src)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     exp = [ctypes.sizeof(_lib.VoxModelCfg), ctypes.sizeof(_lib.VoxSampling), ctypes.sizeof(_lib.VoxRow),
            ctypes.sizeof(_lib.VoxWindow), _lib.VoxModelCfg.rates.offset, _lib.VoxModelCfg.max_detok_frames.offset,
-           _lib.VoxSampling.top_k.offset]
+           _lib.VoxSampling.top_k.offset, ctypes.sizeof(_lib.VoxMimiCfg), _lib.VoxMimiCfg.ratios.offset,
+           _lib.VoxMimiCfg.max_frames.offset, ctypes.sizeof(_lib.VoxMimiReq)]
     assert got == exp
 
 
@@ -76,6 +79,11 @@ def test_create_without_gpu_fails_loudly(lib):
 
     with pytest.raises(RuntimeError):
         VoxDevice(tiny())
+    from paper_2602_00269_b200.config import tiny_mimi
+    from paper_2602_00269_b200.mimi import MimiDecoder
+
+    with pytest.raises(RuntimeError):
+        MimiDecoder(tiny_mimi())
 
 
 def test_sm100a_cubin_contains_tcgen05_and_tma():

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 def test_reference_engine_drives_depth_stage(temperature):
     from paper_2602_00269_b200._ref import ref_engine as r_engine
     from paper_2602_00269_b200._ref import model_api, profiles, scheduler, workload
-    from paper_2602_00269_b200.config import tiny_csm
+    from oracle.mimi import MimiOracle
+    from paper_2602_00269_b200.config import tiny_csm, tiny_mimi
     from paper_2602_00269_b200.csm import CsmFrames
     from paper_2602_00269_b200.device import Sampling
     from paper_2602_00269_b200.executor import CsmExecutor
@@ -32,15 +33,21 @@ def test_reference_engine_drives_depth_stage(temperature):
                                       repetition_penalty=1.0)
     prof = replace(profiles.builtin_profile("depth_like"), codebooks=bcfg.n_codebooks,
                    vocab_size=bcfg.codebook_size, sampling_defaults=params)
-    ex = CsmExecutor(prof, bcfg, dcfg, weight_seed=31)
+    mcfg = tiny_mimi(n_q=bcfg.n_codebooks, max_slots=8, max_frames=64)
+    ex = CsmExecutor(prof, bcfg, dcfg, weight_seed=31, mimi_cfg=mcfg)
     assert ex.decided == (temperature > 0)
     seen: dict = {}
+    pcm: dict = {}
     orig = ex.detokenize_windows
 
     def spy(batch, specs, windows, caches):
         for sp, w in zip(specs, windows):
             seen.setdefault(sp.request, {})[sp.start] = np.asarray(w)
-        return orig(batch, specs, windows, caches)
+        outs, lat = orig(batch, specs, windows, caches)
+        for sp, o in zip(specs, outs):
+            assert o.pcm.shape == (sp.new_tokens * mcfg.frame_samples,)
+            pcm.setdefault(sp.request, []).append(o.pcm)
+        return outs, lat
 
     ex.detokenize_windows = spy
     eng = r_engine.SimEngine(prof, scheduler.PolicyConfig(), r_engine.PipelineMode.ASYNCHRONOUS, seed=5)
@@ -57,6 +64,13 @@ def test_reference_engine_drives_depth_stage(temperature):
         for start, w in wins.items():
             toks[start:start + len(w)] = w
         host[rid] = toks
+    # K7: every request's streamed audio == the Mimi oracle's full decode of its frames
+    orc = MimiOracle(mcfg, 31 + 2)
+    for rid, toks in host.items():
+        got = np.concatenate(pcm[rid])
+        ref = orc.decode(toks, exact=True)
+        snr = 10 * np.log10((ref ** 2).sum() / ((got - ref) ** 2).sum())
+        assert got.shape == ref.shape and np.abs(got - ref).max() < 2e-2 and snr >= 35, (rid, snr)
     if temperature > 0:
         ex.close()
         return
