@@ -282,6 +282,47 @@ int vox_mimi_launch_count(VoxMimi* m, int64_t* launches);
 /* CUDA-event time of the last decode's kernels (H2D of codes / D2H of PCM excluded) */
 int vox_mimi_last_ms(VoxMimi* m, double* ms);
 
+/* ------------------------------------------------------------------------
+ * K8: CosyVoice2-style chunked detokenizer (BASELINE config 4): token-to-mel flow
+ * matching (transformer encoder, CFG Euler ODE over a transformer estimator) + a
+ * causal HiFT-style vocoder with an iSTFT head.  Replaces
+ * Executor.detokenize_windows (model_api.py:213-220) for cosy_like
+ * (profiles.py:163-179; its stub is profiles.py:333-356).  Every call consumes
+ * the request's ref_tokens reference tokens plus the chunk's new tokens
+ * (profiles.py:135 ref_window_tokens); the vocoder keeps per-request
+ * conv histories + the iSTFT overlap tail across calls.
+ * ------------------------------------------------------------------------ */
+typedef struct VoxCosyCfg {
+  int32_t vocab, ref_tokens;
+  int32_t d_enc, enc_layers, enc_heads, enc_ffn, mel;
+  int32_t d_est, est_layers, est_heads, est_ffn, n_steps;
+  float cfg_rate, rope_theta, eps;
+  int32_t voc_ch, n_ratios, ratios[4], voc_kernel, res_kernel, post_kernel, n_fft, hop;
+  float slope;
+  int32_t max_slots, max_tokens, max_chunk;
+} VoxCosyCfg;
+
+typedef struct VoxCosyReq {
+  int32_t slot;     /* stream from vox_cosy_open                         */
+  int32_t n_tokens; /* new speech tokens of this chunk (<= max_chunk)    */
+} VoxCosyReq;
+
+typedef struct VoxCosy VoxCosy;
+
+int vox_cosy_create(int device, const VoxCosyCfg* cfg, uint64_t weight_seed, VoxCosy** out);
+void vox_cosy_destroy(VoxCosy* m);
+const char* vox_cosy_last_error(const VoxCosy* m); /* m may be NULL */
+/* new request: reference tokens / speaker embedding / reference mel derived from
+ * req_seed, zero vocoder history */
+int vox_cosy_open(VoxCosy* m, uint64_t req_seed, int32_t* slot);
+int vox_cosy_close(VoxCosy* m, int32_t slot);
+/* tokens: host [sum n_tokens] int32 (request order); pcm_out: host
+ * [sum n_tokens * samples_per_token] float, blocking */
+int vox_cosy_decode(VoxCosy* m, const VoxCosyReq* reqs, int32_t n, const int32_t* tokens, float* pcm_out,
+                    int64_t* n_samples);
+int vox_cosy_last_ms(VoxCosy* m, double* ms);
+int vox_cosy_launch_count(VoxCosy* m, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

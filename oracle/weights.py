@@ -293,3 +293,94 @@ class MimiWeights:
         out[f"decoder.layers.{n}.conv.weight"] = conv(self.outw[None, :], cfg.last_kernel, ch[-1])
         out[f"decoder.layers.{n}.conv.bias"] = np.array([self.outb], np.float32)
         return out
+
+
+# CosyVoice2-style detokenizer (csrc/cosy_detok.cu: cd_create) -- tensor ids 400..;
+# per-request tensors (reference tokens / speaker embedding / reference mel / ODE noise)
+# are keyed by the REQUEST seed instead of the weight seed.
+T_CD_EMB = 400
+T_CD_ENC = 401          # + 0..7: ln1w ln1b ln2w ln2b qkv o fc1 fc2 (layer = encoder layer)
+T_CD_ELNFW, T_CD_ELNFB, T_CD_MU, T_CD_MUB = 409, 410, 411, 412
+T_CD_SPK, T_CD_REFTOK, T_CD_REFMEL, T_CD_NOISE = 413, 414, 415, 416
+T_CD_IN, T_CD_INB, T_CD_T1, T_CD_T1B, T_CD_T2, T_CD_T2B = 420, 421, 422, 423, 424, 425
+T_CD_EST = 430          # + 0..7 as T_CD_ENC (layer = estimator layer)
+T_CD_OLNW, T_CD_OLNB, T_CD_OUT, T_CD_OUTB = 438, 439, 440, 441
+T_CD_VPRE, T_CD_VPREB, T_CD_UPW, T_CD_UPB = 450, 451, 452, 453
+T_CD_R1W, T_CD_R1B, T_CD_R2W, T_CD_R2B, T_CD_VPOST, T_CD_VPOSTB = 454, 455, 456, 457, 458, 459
+
+
+def _xf_layer(k, base, l, d, ffn):
+    return dict(
+        ln1w=init_f32(d, k(base + 0, l), 0.25, 1.0), ln1b=init_f32(d, k(base + 1, l), 0.05, 0.0),
+        ln2w=init_f32(d, k(base + 2, l), 0.25, 1.0), ln2b=init_f32(d, k(base + 3, l), 0.05, 0.0),
+        qkv=init_bf16(3 * d * d, k(base + 4, l), np.sqrt(f32(3.0) / f32(d))).reshape(3 * d, d),
+        o=init_bf16(d * d, k(base + 5, l), f32(0.5) * np.sqrt(f32(3.0) / f32(d))).reshape(d, d),
+        fc1=init_bf16(ffn * d, k(base + 6, l), np.sqrt(f32(3.0) / f32(d))).reshape(ffn, d),
+        fc2=init_bf16(d * ffn, k(base + 7, l), f32(0.5) * np.sqrt(f32(3.0) / f32(ffn))).reshape(d, ffn),
+    )
+
+
+def _pad_k(w: np.ndarray) -> np.ndarray:
+    K = w.shape[1]
+    Kp = (K + 63) // 64 * 64
+    return w if Kp == K else np.concatenate([w, np.zeros((w.shape[0], Kp - K), np.float32)], axis=1)
+
+
+class CosyDetokWeights:
+    """All CosyVoice2-style detokenizer tensors (float32 arrays of bf16-representable values)."""
+
+    def __init__(self, cfg, seed: int):
+        k = lambda tid, l=0: tensor_key(seed, tid, l)  # noqa: E731
+        de, ds, M = cfg.d_enc, cfg.d_est, cfg.mel
+        self.cfg = cfg
+        self.emb = init_f32(cfg.vocab * de, k(T_CD_EMB), 1.0, 0.0).reshape(cfg.vocab, de)
+        self.enc = [_xf_layer(k, T_CD_ENC, l, de, cfg.enc_ffn) for l in range(cfg.enc_layers)]
+        self.elnf_w, self.elnf_b = init_f32(de, k(T_CD_ELNFW), 0.25, 1.0), init_f32(de, k(T_CD_ELNFB), 0.05, 0.0)
+        self.mu = init_bf16(M * de, k(T_CD_MU), np.sqrt(f32(3.0) / f32(de))).reshape(M, de)
+        self.mu_b = init_f32(M, k(T_CD_MUB), 0.05, 0.0)
+        self.w_in = init_bf16(ds * 4 * M, k(T_CD_IN), np.sqrt(f32(3.0) / f32(4 * M))).reshape(ds, 4 * M)
+        self.b_in = init_f32(ds, k(T_CD_INB), 0.05, 0.0)
+        self.t1 = init_f32(ds * ds, k(T_CD_T1), np.sqrt(f32(3.0) / f32(ds)), 0.0).reshape(ds, ds)
+        self.t1b = init_f32(ds, k(T_CD_T1B), 0.05, 0.0)
+        self.t2 = init_f32(ds * ds, k(T_CD_T2), np.sqrt(f32(3.0) / f32(ds)), 0.0).reshape(ds, ds)
+        self.t2b = init_f32(ds, k(T_CD_T2B), 0.05, 0.0)
+        self.est = [_xf_layer(k, T_CD_EST, l, ds, cfg.est_ffn) for l in range(cfg.est_layers)]
+        self.oln_w, self.oln_b = init_f32(ds, k(T_CD_OLNW), 0.25, 1.0), init_f32(ds, k(T_CD_OLNB), 0.05, 0.0)
+        self.w_out = init_bf16(M * ds, k(T_CD_OUT), np.sqrt(f32(3.0) / f32(ds))).reshape(M, ds)
+        self.b_out = init_f32(M, k(T_CD_OUTB), 0.05, 0.0)
+        ch, vk, rk = cfg.voc_channels, cfg.voc_kernel, cfg.res_kernel
+        self.vpre = _pad_k(init_bf16(ch[0] * vk * M, k(T_CD_VPRE), np.sqrt(f32(3.0) / f32(vk * M))).reshape(ch[0], vk * M))
+        self.vpre_b = init_f32(ch[0], k(T_CD_VPREB), 0.05, 0.0)
+        self.blocks = []
+        for b, s in enumerate(cfg.ratios):
+            Ci, Co = ch[b], ch[b + 1]
+            self.blocks.append(dict(
+                upw=init_bf16(s * Co * 2 * Ci, k(T_CD_UPW, b), np.sqrt(f32(3.0) / (f32(2.0) * f32(Ci)))).reshape(s * Co, 2 * Ci),
+                upb=init_f32(Co, k(T_CD_UPB, b), 0.05, 0.0),
+                r1w=init_bf16(Co * rk * Co, k(T_CD_R1W, b), np.sqrt(f32(3.0) / f32(rk * Co))).reshape(Co, rk * Co),
+                r1b=init_f32(Co, k(T_CD_R1B, b), 0.05, 0.0),
+                r2w=init_bf16(Co * rk * Co, k(T_CD_R2W, b), f32(0.5) * np.sqrt(f32(3.0) / f32(rk * Co))).reshape(Co, rk * Co),
+                r2b=init_f32(Co, k(T_CD_R2B, b), 0.05, 0.0),
+            ))
+        nb = cfg.n_fft // 2 + 1
+        pk = cfg.post_kernel
+        self.vpost = _pad_k(init_bf16(2 * nb * pk * ch[-1], k(T_CD_VPOST), np.sqrt(f32(3.0) / f32(pk * ch[-1]))).reshape(2 * nb, pk * ch[-1]))
+        self.vpost_b = init_f32(2 * nb, k(T_CD_VPOSTB), 0.05, 0.0)
+
+
+def cosy_request_tensors(cfg, req_seed: int):
+    """Per-request reference tokens [ref_tokens], speaker embedding [mel], reference mel
+    [2 * ref_tokens, mel] (csrc/cosy_detok.cu: vox_cosy_open)."""
+    k = lambda tid, l=0: tensor_key(req_seed, tid, l)  # noqa: E731
+    i = np.arange(cfg.ref_tokens, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = mix64_arr(np.uint64(k(T_CD_REFTOK)) + i)
+    ref = (h % np.uint64(cfg.vocab)).astype(np.int64)
+    spk = init_f32(cfg.mel, k(T_CD_SPK), 1.0, 0.0)
+    rmel = init_f32(2 * cfg.ref_tokens * cfg.mel, k(T_CD_REFMEL), 1.0, 0.0).reshape(2 * cfg.ref_tokens, cfg.mel)
+    return ref, spk, rmel
+
+
+def cosy_noise(cfg, req_seed: int, chunk: int, rows: int) -> np.ndarray:
+    """x0 of the flow ODE for call `chunk` of a request: unit-variance uniform noise."""
+    return init_f32(rows * cfg.mel, tensor_key(req_seed, T_CD_NOISE, chunk), np.sqrt(f32(3.0)), 0.0).reshape(rows, cfg.mel)

@@ -75,6 +75,25 @@ class VoxMimiReq(C.Structure):
     _fields_ = [("slot", C.c_int32), ("n_frames", C.c_int32)]
 
 
+class VoxCosyCfg(C.Structure):
+    _fields_ = [
+        ("vocab", C.c_int32), ("ref_tokens", C.c_int32),
+        ("d_enc", C.c_int32), ("enc_layers", C.c_int32), ("enc_heads", C.c_int32), ("enc_ffn", C.c_int32),
+        ("mel", C.c_int32),
+        ("d_est", C.c_int32), ("est_layers", C.c_int32), ("est_heads", C.c_int32), ("est_ffn", C.c_int32),
+        ("n_steps", C.c_int32),
+        ("cfg_rate", C.c_float), ("rope_theta", C.c_float), ("eps", C.c_float),
+        ("voc_ch", C.c_int32), ("n_ratios", C.c_int32), ("ratios", C.c_int32 * 4), ("voc_kernel", C.c_int32),
+        ("res_kernel", C.c_int32), ("post_kernel", C.c_int32), ("n_fft", C.c_int32), ("hop", C.c_int32),
+        ("slope", C.c_float),
+        ("max_slots", C.c_int32), ("max_tokens", C.c_int32), ("max_chunk", C.c_int32),
+    ]
+
+
+class VoxCosyReq(C.Structure):
+    _fields_ = [("slot", C.c_int32), ("n_tokens", C.c_int32)]
+
+
 # status -> exception (VoxStatus in include/voxb200.h)
 _STATUS_TO_EXC = {
     1: ValueError,
@@ -145,6 +164,14 @@ _SIGS = {
     "vox_mimi_decode": (C.c_int, [_P, C.POINTER(VoxMimiReq), C.c_int32, _i32p, _f32p, C.POINTER(C.c_int64)]),
     "vox_mimi_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
     "vox_mimi_last_ms": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "vox_cosy_create": (C.c_int, [C.c_int, C.POINTER(VoxCosyCfg), C.c_uint64, C.POINTER(_P)]),
+    "vox_cosy_destroy": (None, [_P]),
+    "vox_cosy_last_error": (C.c_char_p, [_P]),
+    "vox_cosy_open": (C.c_int, [_P, C.c_uint64, _i32p]),
+    "vox_cosy_close": (C.c_int, [_P, C.c_int32]),
+    "vox_cosy_decode": (C.c_int, [_P, C.POINTER(VoxCosyReq), C.c_int32, _i32p, _f32p, C.POINTER(C.c_int64)]),
+    "vox_cosy_last_ms": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "vox_cosy_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -174,9 +201,14 @@ def load(path: Path | str = LIB_PATH) -> C.CDLL:
     return lib
 
 
-def check(rc: int, ctx=None, mimi=None) -> None:
+def check(rc: int, ctx=None, mimi=None, cosy=None) -> None:
     if rc == 0:
         return
-    msg = load().vox_mimi_last_error(mimi) if mimi is not None else load().vox_last_error(ctx)
+    if cosy is not None:
+        msg = load().vox_cosy_last_error(cosy)
+    elif mimi is not None:
+        msg = load().vox_mimi_last_error(mimi)
+    else:
+        msg = load().vox_last_error(ctx)
     text = msg.decode() if msg else f"status {rc}"
     raise _STATUS_TO_EXC.get(rc, RuntimeError)(text)

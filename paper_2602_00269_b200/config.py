@@ -282,5 +282,85 @@ def tiny_mimi(**kw) -> MimiConfig:
     return MimiConfig(**{"name": "tiny-mimi", "n_q": 4, "n_layers": 2, "max_slots": 8, "max_frames": 64, **kw})
 
 
+@dataclass(frozen=True)
+class CosyDetokConfig:
+    """Config 4 detokenizer: CosyVoice2-style chunked token-to-mel flow matching + HiFT-style
+    vocoder (public CosyVoice2 architecture [3P] FunAudioLLM/CosyVoice, not installed here;
+    PAPER.md:102 'flow-matching module built on Transformer layers and a HiFi-GAN vocoder'),
+    as VoxServe runs it: each call consumes the request's reference tokens
+    (ref_tokens = 50, profiles.py:135 ref_window_tokens) plus the chunk's new tokens.
+
+    flow:    speech-token embedding -> enc_layers pre-LN transformer (full attention over
+             the call's tokens, RoPE) -> LN -> x2 upsample to 50 Hz mel frames -> linear to
+             80 = mu;  n_steps Euler steps of the conditional flow ODE (cosine t schedule)
+             with classifier-free guidance (cfg_rate): the estimator is in-proj of
+             [x | mu | spk | prompt-mel] + timestep embedding -> est_layers transformer ->
+             LN -> linear to 80;
+    vocoder: causal HiFT-style: k7 conv 80 -> voc_ch, per ratio LeakyReLU + ConvT(k 2r,
+             stride r) halving channels + residual block (LReLU-k3-LReLU-k3), LReLU, k7 conv
+             to n_fft/2+1 log-magnitudes + phases, causal iSTFT (Hann, n_fft 16, hop 4):
+             480 samples per mel frame, 960 per token at 24 kHz.  Stateful per request
+             (conv histories + iSTFT overlap tail) across chunks."""
+
+    name: str = "cosyvoice2-detok"
+    vocab: int = 6561
+    ref_tokens: int = 50
+    d_enc: int = 512
+    enc_layers: int = 6
+    enc_heads: int = 8
+    enc_ffn: int = 2048
+    mel: int = 80
+    d_est: int = 256
+    est_layers: int = 8
+    est_heads: int = 4
+    est_ffn: int = 1024
+    n_steps: int = 10
+    cfg_rate: float = 0.7
+    rope_theta: float = 10000.0
+    eps: float = 1e-5
+    voc_ch: int = 512
+    ratios: tuple = (8, 5, 3)
+    voc_kernel: int = 7
+    res_kernel: int = 3
+    post_kernel: int = 7
+    n_fft: int = 16
+    hop: int = 4
+    slope: float = 0.1
+    max_slots: int = 128
+    max_tokens: int = 2048    # new tokens per call over all requests
+    max_chunk: int = 64       # new tokens per request per call
+
+    @property
+    def mel_per_token(self) -> int:
+        return 2
+
+    @property
+    def samples_per_mel(self) -> int:
+        h = self.hop
+        for r in self.ratios:
+            h *= r
+        return h
+
+    @property
+    def samples_per_token(self) -> int:
+        return self.mel_per_token * self.samples_per_mel
+
+    @property
+    def voc_channels(self) -> list:
+        c = [self.voc_ch]
+        for _ in self.ratios:
+            c.append(c[-1] // 2)
+        return c
+
+    def with_capacity(self, **kw) -> "CosyDetokConfig":
+        return replace(self, **kw)
+
+
+def tiny_cosy_detok(**kw) -> CosyDetokConfig:
+    """CPU-test-sized: 2 encoder / 2 estimator layers, 4 ODE steps, production vocoder."""
+    return CosyDetokConfig(**{"name": "tiny-cosy-detok", "enc_layers": 2, "est_layers": 2, "n_steps": 4,
+                              "max_slots": 8, "max_tokens": 256, **kw})
+
+
 CONFIGS = {"tiny": tiny, "tiny_planted": tiny_planted, "orpheus3b": orpheus3b, "cosyvoice2": cosyvoice2, "tiny_cosy": tiny_cosy,
            "csm_backbone": csm_backbone, "csm_depth": csm_depth}

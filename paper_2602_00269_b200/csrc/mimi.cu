@@ -30,15 +30,10 @@
 #include <string>
 #include <vector>
 
-#include "common.cuh"
-#include "kernels.h"
+#include "codec_common.cuh"
 
 namespace vox {
 namespace {
-
-struct MimiReqDev {
-  int32_t slot, f_off, nf, parity, pos0, pad_[3];
-};
 
 // tensor ids (oracle/weights.py: T_MI_*)
 enum : uint64_t {
@@ -51,41 +46,14 @@ enum : uint64_t {
 
 constexpr int kMaxWin = 256;
 
-struct StateView {  // one slot's state, parity half `p` read, `1 - p` written
-  float* base;
-  int64_t slot_floats, half;
-  VOX_DEV const float* in(const MimiReqDev& q, int64_t off) const {
-    return base + q.slot * slot_floats + q.parity * half + off;
-  }
-  VOX_DEV float* out(const MimiReqDev& q, int64_t off) const {
-    return base + q.slot * slot_floats + (1 - q.parity) * half + off;
-  }
-};
-
-VOX_DEV float elu(float x) { return x > 0.f ? x : expm1f(x); }
-
-template <int NT>
-VOX_DEV float block_sum(float v, float* red) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < NT / 32; ++i) s += red[i];
-  return s;
-}
-
 // codes [F][n_q] -> h rows 2f, 2f+1 (25 Hz): x_f = sum_q T_q[code], depthwise ConvT
 // (k 4, stride 2, right-trimmed): y[2t + j] = x_t * w[j] + x_{t-1} * w[j + 2]
 __global__ void __launch_bounds__(128) mimi_embed_up_kernel(
     const int32_t* __restrict__ codes, const int32_t* __restrict__ frame_req,
-    const MimiReqDev* __restrict__ reqs, int n_q, int cb, int D, const float* __restrict__ tabs,
+    const SegDev* __restrict__ reqs, int n_q, int cb, int D, const float* __restrict__ tabs,
     const float4* __restrict__ up, StateView sv, int64_t off_up, float* __restrict__ h) {
   const int f = blockIdx.x;
-  const MimiReqDev q = reqs[frame_req[f]];
+  const SegDev q = reqs[frame_req[f]];
   const int t = f - q.f_off;
   for (int c = threadIdx.x; c < D; c += blockDim.x) {
     float x = 0.f, xp = 0.f;
@@ -103,55 +71,14 @@ __global__ void __launch_bounds__(128) mimi_embed_up_kernel(
   }
 }
 
-// h (+= ls * tmp) ; x = bf16(LayerNorm(h) * w + b).  One 128-thread CTA per row, D <= 1024.
-__global__ void __launch_bounds__(128) mimi_ln_kernel(float* __restrict__ h, const float* __restrict__ tmp,
-                                                      const float* __restrict__ ls, const float* __restrict__ w,
-                                                      const float* __restrict__ b, bf16* __restrict__ x, int D,
-                                                      float eps) {
-  __shared__ float red[4];
-  const int64_t r = blockIdx.x;
-  float v[8];
-  const int n = D / 128;
-  float s = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < n) {
-      const int c = threadIdx.x + 128 * i;
-      float a = h[r * D + c];
-      if (tmp != nullptr) {
-        a = a + ls[c] * tmp[r * D + c];
-        h[r * D + c] = a;
-      }
-      v[i] = a;
-      s += a;
-    }
-  }
-  const float mean = block_sum<128>(s, red) / static_cast<float>(D);
-  float ss = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (i < n) {
-      v[i] -= mean;
-      ss += v[i] * v[i];
-    }
-  const float var = block_sum<128>(ss, red) / static_cast<float>(D);
-  const float sd = sqrtf(var + eps);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (i < n) {
-      const int c = threadIdx.x + 128 * i;
-      x[r * D + c] = f32_to_bf16(v[i] / sd * w[c] + b[c]);
-    }
-}
-
 // RoPE (rotate-half) on q and k of every row, append k, v to the stream's K/V ring
 // kv[slot][layer][W][2][D] at pos % W; q -> qo (fp32).
 __global__ void __launch_bounds__(128) mimi_rope_kv_kernel(
-    const float* __restrict__ qkv, const int32_t* __restrict__ frame_req, const MimiReqDev* __restrict__ reqs,
+    const float* __restrict__ qkv, const int32_t* __restrict__ frame_req, const SegDev* __restrict__ reqs,
     int D, int hd, int W, int L, int layer, const float* __restrict__ inv_freq, float* __restrict__ kv,
     float* __restrict__ qo) {  // W = ring size
   const int64_t r = blockIdx.x;
-  const MimiReqDev q = reqs[frame_req[r >> 1]];
+  const SegDev q = reqs[frame_req[r >> 1]];
   const int pos = q.pos0 + static_cast<int>(r - 2LL * q.f_off);
   float* kvr = kv + ((static_cast<int64_t>(q.slot) * L + layer) * W + pos % W) * 2 * D;
   const float* src = qkv + r * 3 * D;
@@ -174,12 +101,12 @@ __global__ void __launch_bounds__(128) mimi_rope_kv_kernel(
 // holds Wr = W + 2 * max_chunk positions: a chunk of n new positions reads the
 // W + n - 1 positions [P0 - W + 1, P0 + n - 1], none of which its own appends evict.
 __global__ void __launch_bounds__(128) mimi_attn_kernel(const float* __restrict__ qi,
-                                                        const MimiReqDev* __restrict__ reqs,
+                                                        const SegDev* __restrict__ reqs,
                                                         const float* __restrict__ kv, int D, int hd, int W,
                                                         int Wr, int L, int layer, bf16* __restrict__ out) {
   __shared__ float p[4][kMaxWin];
   __shared__ float sq[4][128];
-  const MimiReqDev q = reqs[blockIdx.x];
+  const SegDev q = reqs[blockIdx.x];
   const int hh = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float scale = rsqrtf(static_cast<float>(hd));
@@ -223,66 +150,14 @@ __global__ void __launch_bounds__(128) mimi_attn_kernel(const float* __restrict_
   }
 }
 
-__global__ void mimi_gelu_kernel(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const float v = x[i];
-    y[i] = f32_to_bf16(0.5f * v * (1.f + erff(v * 0.70710678118654752f)));
-  }
-}
-
-// Causal-conv operand: out[r][j*C + c] = act(x[t - (k-1) + j][c]) (history rows of
-// the previous chunk for negative indices), zero for cols >= k*C (K padding).
-__global__ void mimi_im2col_kernel(const float* __restrict__ x, int C, int k, int elu_on, int Kp, int u,
-                                   const int32_t* __restrict__ frame_req, const MimiReqDev* __restrict__ reqs,
-                                   StateView sv, int64_t off, int64_t rows, bf16* __restrict__ out) {
-  const int chunks = Kp / 8;
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= rows * chunks) return;
-  const int64_t r = idx / chunks;
-  const int col0 = static_cast<int>(idx % chunks) * 8;
-  uint4 pk = make_uint4(0, 0, 0, 0);
-  if (col0 < k * C) {
-    const MimiReqDev q = reqs[frame_req[r / u]];
-    const int64_t t = r - static_cast<int64_t>(q.f_off) * u;
-    const int j = col0 / C, c0 = col0 % C;
-    const int64_t src = t - (k - 1) + j;
-    const float* p = src >= 0 ? x + (r - t + src) * C + c0 : sv.in(q, off) + ((k - 1) + src) * C + c0;
-    const float4 a = *reinterpret_cast<const float4*>(p);
-    const float4 b = *reinterpret_cast<const float4*>(p + 4);
-    float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    __nv_bfloat162 h2[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float v0 = elu_on ? elu(v[2 * i]) : v[2 * i];
-      const float v1 = elu_on ? elu(v[2 * i + 1]) : v[2 * i + 1];
-      h2[i] = __floats2bfloat162_rn(v0, v1);
-    }
-    pk = *reinterpret_cast<uint4*>(h2);
-  }
-  *reinterpret_cast<uint4*>(out + r * Kp + col0) = pk;
-}
-
-// next chunk's history: the last k-1 rows of (old history ++ this chunk's rows)
-__global__ void mimi_hist_kernel(const float* __restrict__ x, int C, int k, int u,
-                                 const MimiReqDev* __restrict__ reqs, StateView sv, int64_t off) {
-  const MimiReqDev q = reqs[blockIdx.x];
-  const int64_t n = static_cast<int64_t>(q.nf) * u, ro = static_cast<int64_t>(q.f_off) * u;
-  for (int e = threadIdx.x; e < (k - 1) * C; e += blockDim.x) {
-    const int m = e / C, c = e % C;
-    const int64_t src = n - (k - 1) + m;
-    sv.out(q, off)[e] = src >= 0 ? x[(ro + src) * C + c] : sv.in(q, off)[((k - 1) + src) * C + c];
-  }
-}
-
 // last conv (C -> 1, k taps, ELU on the input), one thread per output sample
 __global__ void mimi_out_kernel(const float* __restrict__ x, int C, int k, int u,
-                                const int32_t* __restrict__ frame_req, const MimiReqDev* __restrict__ reqs,
+                                const int32_t* __restrict__ frame_req, const SegDev* __restrict__ reqs,
                                 StateView sv, int64_t off, const float* __restrict__ w, float b, int64_t rows,
                                 float* __restrict__ pcm) {
   const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (r >= rows) return;
-  const MimiReqDev q = reqs[frame_req[r / u]];
+  const SegDev q = reqs[frame_req[r / u]];
   const int64_t t = r - static_cast<int64_t>(q.f_off) * u;
   float acc = 0.f;
   for (int j = 0; j < k; ++j) {
@@ -391,30 +266,13 @@ uint64_t key(const VoxMimi* m, uint64_t seed, uint64_t tid, uint64_t l) { return
 
 int gemm(VoxMimi* m, const CUtensorMap& tw, int M, const bf16* x, int K, int64_t rows, float* out, int64_t ldo,
          const float* bias, const float* resid, int64_t ldr) {
-  if (rows <= 0) return VOX_OK;
-  const int bn = gemm_bn_for_rows(static_cast<int>(std::min<int64_t>(rows, 256)));
-  CUtensorMap tx;
-  if (!make_tmap_bf16(&tx, x, K, rows, static_cast<uint64_t>(K) * 2, bn))
-    return mfail(m, VOX_ERR_CUDA, "mimi: activation tensor map");
-  GemmArgs a{};
-  a.M = M;
-  a.N = static_cast<int>(rows);
-  a.K = K;
-  a.out = out;
-  a.ldo = ldo;
-  a.split_stride = rows * ldo;
-  a.bias = bias;
-  a.resid = resid;
-  a.ldr = ldr;
-  a.m_valid = M;
-  m->launches++;
-  const cudaError_t e = gemm_launch(tw, tx, a, 1, bn, 1, m->st);
+  const cudaError_t e = codec_gemm(tw, M, x, K, rows, out, ldo, bias, resid, ldr, m->st, &m->launches);
   if (e != cudaSuccess) return mfail(m, VOX_ERR_CUDA, std::string("mimi gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
 }
 
 int wmap(VoxMimi* m, CUtensorMap* t, const bf16* w, int M, int K) {
-  if (!make_tmap_bf16(t, w, K, M, static_cast<uint64_t>(K) * 2, 128)) return mfail(m, VOX_ERR_CUDA, "mimi: weight map");
+  if (!codec_wmap(t, w, M, K)) return mfail(m, VOX_ERR_CUDA, "mimi: weight map");
   return VOX_OK;
 }
 
@@ -585,7 +443,7 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
   const int D = g.hidden, hd = g.hidden / g.n_heads;
   const std::vector<int>& ch = m->chans;
   cudaStream_t st = m->st;
-  const MimiReqDev* reqs = reinterpret_cast<const MimiReqDev*>(m->d_stage);
+  const SegDev* reqs = reinterpret_cast<const SegDev*>(m->d_stage);
   const int32_t* frame_req = m->d_stage + 8 * g.max_slots;
   const int32_t* codes = frame_req + g.max_frames;
   StateView sv{m->state, 2 * m->half, m->half};
@@ -597,7 +455,7 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
     const MimiLayerW& w = m->layers[l];
     const bool first = l == 0;
     const MimiLayerW* prev = first ? nullptr : &m->layers[l - 1];
-    LK(mimi_ln_kernel<<<R0, 128, 0, st>>>(m->h, first ? nullptr : m->tmp, first ? nullptr : prev->ls2, w.ln1w,
+    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, first ? nullptr : m->tmp, first ? nullptr : prev->ls2, w.ln1w,
                                           w.ln1b, m->xbf, D, g.eps));
     MRET(gemm(m, w.tm_qkv, 3 * D, m->xbf, D, R0, m->qkv, 3 * D, nullptr, nullptr, 0));
     LK(mimi_rope_kv_kernel<<<R0, 128, 0, st>>>(m->qkv, frame_req, reqs, D, hd, m->ring, g.n_layers, l,
@@ -605,23 +463,23 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
     LK(mimi_attn_kernel<<<dim3(n, g.n_heads), 128, 0, st>>>(m->q, reqs, m->kv, D, hd, g.window, m->ring, g.n_layers, l,
                                                             m->xbf));
     MRET(gemm(m, w.tm_o, D, m->xbf, D, R0, m->tmp, D, nullptr, nullptr, 0));
-    LK(mimi_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls1, w.ln2w, w.ln2b, m->xbf, D, g.eps));
+    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls1, w.ln2w, w.ln2b, m->xbf, D, g.eps));
     MRET(gemm(m, w.tm_fc1, g.ffn, m->xbf, D, R0, m->tmp, g.ffn, nullptr, nullptr, 0));
     const int64_t ne = R0 * g.ffn;
-    LK(mimi_gelu_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->tmp, m->xbf, ne));
+    LK(codec_gelu_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->tmp, m->xbf, ne));
     MRET(gemm(m, w.tm_fc2, D, m->xbf, g.ffn, R0, m->tmp, D, nullptr, nullptr, 0));
   }
   // h += ls2 * fc2 of the last layer (residual into the conv stack's input rows)
   {
     // reuse mimi_ln's residual update: LN output discarded into xbf (cheap, R0 rows)
     const MimiLayerW& w = m->layers[g.n_layers - 1];
-    LK(mimi_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls2, w.ln1w, w.ln1b, m->xbf, D, g.eps));
+    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls2, w.ln1w, w.ln1b, m->xbf, D, g.eps));
   }
   auto im2col = [&](const float* x, int C, int k, int elu_on, int Kp, int u, int64_t off, int64_t rows) -> int {
     const int64_t tot = rows * (Kp / 8);
-    LK(mimi_im2col_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(x, C, k, elu_on, Kp, u, frame_req,
+    LK(codec_im2col_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, st>>>(x, C, k, elu_on ? kActElu : kActNone, 0.f, Kp, u, frame_req,
                                                                                     reqs, sv, off, rows, m->col));
-    if (k > 1) LK(mimi_hist_kernel<<<n, 256, 0, st>>>(x, C, k, u, reqs, sv, off));
+    if (k > 1) LK(codec_hist_kernel<<<n, 256, 0, st>>>(x, C, k, u, reqs, sv, off));
     return VOX_OK;
   };
   // SEANet: k7 conv 512 -> ch0 (no activation before it)
@@ -651,7 +509,7 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
     const int64_t rows = static_cast<int64_t>(Ftot) * u;
     LK(mimi_out_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(
         x, C4, g.last_kernel, u, frame_req, reqs, sv, m->off_out, m->outw, m->outb, rows, m->pcm));
-    LK(mimi_hist_kernel<<<n, 256, 0, st>>>(x, C4, g.last_kernel, u, reqs, sv, m->off_out));
+    LK(codec_hist_kernel<<<n, 256, 0, st>>>(x, C4, g.last_kernel, u, reqs, sv, m->off_out));
   }
   return VOX_OK;
 }
@@ -769,7 +627,7 @@ int vox_mimi_decode(VoxMimi* m, const VoxMimiReq* reqs, int32_t n, const int32_t
   if (n <= 0) return mfail(m, VOX_ERR_EMPTY_BATCH, "empty Mimi batch");
   const VoxMimiCfg& g = m->cfg;
   cudaSetDevice(m->device);
-  MimiReqDev* hr = reinterpret_cast<MimiReqDev*>(m->h_stage);
+  SegDev* hr = reinterpret_cast<SegDev*>(m->h_stage);
   int32_t* frame_req = m->h_stage + 8 * g.max_slots;
   int32_t* hcodes = frame_req + g.max_frames;
   if (n > g.max_slots) return mfail(m, VOX_ERR_BATCH_TOO_LARGE, "more streams than Mimi slots");
@@ -786,7 +644,7 @@ int vox_mimi_decode(VoxMimi* m, const VoxMimiReq* reqs, int32_t n, const int32_t
     if (r.n_frames > m->max_chunk)
       return mfail(m, VOX_ERR_BATCH_TOO_LARGE, "Mimi request exceeds 64 frames (or max_frames) per call");
     if (F + r.n_frames > g.max_frames) return mfail(m, VOX_ERR_BATCH_TOO_LARGE, "Mimi batch exceeds max_frames");
-    hr[i] = MimiReqDev{r.slot, F, r.n_frames, m->parity[r.slot], m->pos[r.slot], {0, 0, 0}};
+    hr[i] = SegDev{r.slot, F, r.n_frames, m->parity[r.slot], m->pos[r.slot], 0, {0, 0}};
     for (int f = 0; f < r.n_frames; ++f) frame_req[F + f] = i;
     F += r.n_frames;
   }
