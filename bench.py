@@ -661,7 +661,53 @@ def cosy_lm_steps(batch: int, ctx: int, steps: int, seed: int, hbm: float, devic
                          "frac": round(by / (ms / 1e3) / 1e9 / hbm, 4), "bytes_per_step": int(by)},
             "lm_first_chunk_floor_ms": {str(c): round(pre_ms + c * ms, 2) for c in (5, 10, 15, 25, 50)},
             "prefill_ms_50_tokens": round(pre_ms, 3), "kv_fill_s": round(time.perf_counter() - t0, 2),
-            "detokenizer": "not built (token-to-mel flow matching + HiFT are SURVEY §8f next rows)"}
+            "detokenizer": cosy_detok_sweep(batch, seed, device, pre_ms, ms)}
+
+
+def cosy_detok_sweep(batch: int, seed: int, device: int, lm_prefill_ms: float, lm_step_ms: float,
+                     chunks=(5, 10, 15, 25, 50), calls: int = 3):
+    """K8 CosyVoice2-style detokenizer (flow matching + HiFT-style vocoder) at config-4 dims:
+    chunk-size sweep for TTFA vs throughput (cosy_like chunk 15,
+    profiles.py:163-179).  Per chunk size: device ms of one call over `batch` streams (steady
+    state, every stream with vocoder history) -> detok audio-s/s and tensor roofline on the
+    algorithmic FLOPs; device ms of a single request's FIRST call -> the TTFA floor = LM
+    prefill + chunk x LM step (measured by cosy_lm_steps at `batch` streams) + that call."""
+    from paper_2602_00269_b200.config import CosyDetokConfig
+    from paper_2602_00269_b200.cosy_detok import CosyDetokenizer
+
+    _, tflops, _ = _peaks()
+    cfg = CosyDetokConfig(max_slots=batch + 1, max_tokens=batch * max(chunks), max_chunk=max(chunks))
+    dec = CosyDetokenizer(cfg, seed, device)
+    rng = np.random.default_rng(seed)
+    out = {"kernel": "K8 csrc/cosy_detok.cu: flow (6-layer encoder, 10 CFG Euler steps x 8-layer estimator) + "
+                     "HiFT-style vocoder, every call re-consumes 50 reference tokens",
+           "streams": batch, "sweep": []}
+    for c in chunks:
+        slots = [dec.open(seed * 31 + i) for i in range(batch)]
+        ms = []
+        for k in range(calls + 1):
+            dec.decode(slots, [rng.integers(0, cfg.vocab, c) for _ in slots])
+            if k >= 1:
+                ms.append(dec.last_ms())
+        for s_ in slots:
+            dec.release(s_)
+        one = dec.open(seed + c)
+        dec.decode([one], [rng.integers(0, cfg.vocab, c)])
+        first_ms = dec.last_ms()
+        dec.release(one)
+        m = float(np.median(ms))
+        fl = dec.flops_per_call(c) * batch
+        audio = batch * c / 25.0
+        out["sweep"].append({
+            "chunk": c, "ms_per_call": round(m, 3), "audio_s_per_s": round(audio / (m / 1e3), 1),
+            "first_call_ms_b1": round(first_ms, 3),
+            "ttfa_floor_ms": round(lm_prefill_ms + c * lm_step_ms + first_ms, 2),
+            "roofline": {"bound": "tensor", "achieved": round(fl / (m / 1e3) / 1e12, 2), "peak": tflops,
+                         "unit": "TFLOP/s", "frac": round(fl / (m / 1e3) / 1e12 / tflops, 4),
+                         "gflop_per_call": round(fl / 1e9, 1)}})
+    out["launches_per_call"] = dec.launch_count() // (len(chunks) * (calls + 2))
+    dec.close()
+    return out
 
 
 def csm_frames(batch: int, frames: int, seed: int, hbm: float, device: int):

@@ -40,7 +40,9 @@ class B200Executor:
     """Implements speechserve.model_api.Executor on one B200 (one VoxDevice)."""
 
     def __init__(self, profile, model_cfg: ModelConfig, weight_seed: int = 0, device: int = 0,
-                 dev: Optional[VoxDevice] = None):
+                 dev: Optional[VoxDevice] = None, detokenizer=None):
+        """detokenizer: None -> the ctx's SNAC-style decoder (Orpheus, config 2); a
+        ``cosy_detok.CosyDetokenizer`` -> the CosyVoice2-style flow + vocoder (config 4)."""
         if profile.codebooks != 1:
             raise errors.CodebookMismatch("the Orpheus-style path is single-codebook")
         if profile.vocab_size != model_cfg.vocab:
@@ -51,6 +53,8 @@ class B200Executor:
         self.sampling = Sampling.from_ref(profile.sampling_defaults)
         self._slot: dict[int, int] = {}
         self._prompt: dict[int, int] = {}
+        self.detokenizer = detokenizer
+        self._dslot: dict[int, int] = {}
 
     # ------------------------------------------------------------------ helpers
     def _slot_for(self, rid: int) -> int:
@@ -76,6 +80,9 @@ class B200Executor:
         self._prompt.pop(rid, None)
         if slot is not None:
             self.dev.release(slot)
+        ds = self._dslot.pop(rid, None)
+        if ds is not None:
+            self.detokenizer.release(ds)
 
     # ------------------------------------------------------------------ Protocol
     def forward(self, batch: model_api.StageBatch) -> tuple[np.ndarray, float]:
@@ -90,6 +97,8 @@ class B200Executor:
                 if rid not in self._slot:
                     self._slot[rid] = self._admit(batch.seeds[i], P)
                     self._prompt[rid] = P
+                    if self.detokenizer is not None:
+                        self._dslot[rid] = self.detokenizer.open(int(batch.seeds[i]))
                 rows += [[self._slot[rid], p, -1, 0] for p in range(P - 1)]
             # prompts of many requests can exceed one forward's row capacity: split
             # at max_rows (positions of one request stay in order, so the causal
@@ -127,6 +136,8 @@ class B200Executor:
     def detokenize_windows(self, batch, specs: Sequence, windows: Sequence[np.ndarray],
                            caches: Sequence[model_api.DetokenizerCache]):
         """Chunk-wise streaming detokenization (model_api.py:213-220, profiles.py:333-356)."""
+        if self.detokenizer is not None:
+            return self._detok_cosy(specs, windows, caches)
         t0 = time.perf_counter()
         rows = []
         for spec, win, cache in zip(specs, windows, caches):
@@ -143,6 +154,35 @@ class B200Executor:
             cache.bytes_held = 4 * pcm.size
             from ._ref import core
 
+            outs.append(PcmChunkOut(request=spec.request, new_tokens=spec.new_tokens,
+                                    playback_us=core.playback_us_for(spec.new_tokens, self.profile.token_rate),
+                                    pcm=pcm))
+            if spec.final:
+                self.release(spec.request)
+        return outs, time.perf_counter() - t0
+
+    def _detok_cosy(self, specs, windows, caches):
+        """CosyVoice2-style: each window's new speech tokens (ids - audio_base; the LM's
+        3 special ids past the 6,561 codes clamp to the last code) through the flow +
+        stateful vocoder of the request's stream."""
+        from ._ref import core
+
+        t0 = time.perf_counter()
+        c = self.cfg
+        slots, toks = [], []
+        for spec, win in zip(specs, windows):
+            if spec.request not in self._dslot:
+                raise errors.CacheMissing(f"request {spec.request} has no detokenizer stream")
+            w = np.asarray(win)[:, 0]
+            ids = w[w.shape[0] - spec.new_tokens:] - max(c.audio_base, 0)
+            slots.append(self._dslot[spec.request])
+            toks.append(np.clip(ids, 0, self.detokenizer.cfg.vocab - 1).astype(np.int32))
+        pcms = self.detokenizer.decode(slots, toks) if slots else []
+        outs = []
+        for spec, win, cache, pcm in zip(specs, windows, caches, pcms):
+            cache.window_ids = np.array(win, copy=True)
+            cache.calls += 1
+            cache.bytes_held = 4 * pcm.size
             outs.append(PcmChunkOut(request=spec.request, new_tokens=spec.new_tokens,
                                     playback_us=core.playback_us_for(spec.new_tokens, self.profile.token_rate),
                                     pcm=pcm))

@@ -85,3 +85,50 @@ def test_errors():
     with pytest.raises(MemoryError):
         dec.open(3)
     dec.close()
+
+
+def test_reference_simengine_drives_cosy_lm_and_detok():
+    """The UNMODIFIED reference SimEngine on a cosy_like profile (profiles.py:163-179, chunk
+    15, greedy here) drives B200Executor: the CosyVoice2-style LM (config 4 geometry, tiny)
+    decodes on the device, the host samples with the reference sample(), and
+    detokenize_windows runs K8 per chunk; every request's streamed PCM equals the
+    oracle's flow + vocoder over the tokens the engine sampled."""
+    from dataclasses import replace
+
+    from paper_2602_00269_b200._ref import profiles, ref_engine, scheduler, workload
+    from paper_2602_00269_b200.config import tiny_cosy
+    from paper_2602_00269_b200.cosy_detok import CosyDetokenizer
+    from paper_2602_00269_b200.executor import B200Executor
+
+    lm = tiny_cosy(max_slots=8)
+    dcfg = tiny_cosy_detok()
+    base = profiles.builtin_profile("cosy_like")
+    prof = replace(base, vocab_size=lm.vocab, sampling_defaults=replace(base.sampling_defaults, temperature=0.0))
+    ex = B200Executor(prof, lm, weight_seed=9, detokenizer=CosyDetokenizer(dcfg, weight_seed=10))
+    seen: dict = {}
+    orig = ex.detokenize_windows
+
+    def spy(batch, specs, windows, caches):
+        outs, lat = orig(batch, specs, windows, caches)
+        for sp, w, o in zip(specs, windows, outs):
+            ids = np.asarray(w)[:, 0]
+            seen.setdefault(sp.request, []).append((ids[len(ids) - sp.new_tokens:] - lm.audio_base, o.pcm))
+        return outs, lat
+
+    ex.detokenize_windows = spy
+    eng = ref_engine.SimEngine(prof, scheduler.PolicyConfig(max_lm_batch=16, max_detok_batch=16),
+                               ref_engine.PipelineMode.ASYNCHRONOUS, seed=4)
+    eng.executor = ex
+    arr = [(i, workload.ArrivalSpec(arrival_us=i * 500, prompt_tokens=12, target_output_tokens=40)) for i in range(3)]
+    tr = eng.run(arr)
+    assert len(tr.requests) == 3 and all(r.tokens_generated == 40 for r in tr.requests)
+    from paper_2602_00269_b200._ref import model_api
+
+    orc = CosyDetokOracle(dcfg, 10)
+    for rid, chunks in seen.items():
+        toks = [np.clip(t, 0, dcfg.vocab - 1) for t, _ in chunks]
+        got = np.concatenate([p for _, p in chunks])
+        ref = orc.decode(model_api.request_seed(4, rid), toks, exact=True)
+        assert got.shape == ref.shape and np.abs(got - ref).max() < 2e-2 and _snr(ref, got) >= 35, rid
+    assert not ex._dslot
+    ex.detokenizer.close()
