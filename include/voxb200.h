@@ -238,6 +238,12 @@ int vox_project_ext(VoxCtx* ctx, VoxCtx* src, int32_t n);
 int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, int32_t offset,
                     int32_t mode);
 
+/* Disaggregated LM -> detok (reference engine.py:119-123,150-156): copy
+ * token-store spans spans[n][5] = {dst_slot, dst_pos, src_slot, src_pos, len} from the LM
+ * context `src` into the detokenizer context `dst` (same GPU or an NVLink peer), ordered
+ * after src's enqueued forwards and before dst's next detok work. */
+int vox_copy_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* spans, int32_t n);
+
 /* weights / state introspection for parity tests (host copies) */
 int vox_read_weight(VoxCtx* ctx, const char* name, int32_t layer, void* out, size_t bytes);
 int vox_read_kv(VoxCtx* ctx, int32_t layer, int32_t slot, int32_t pos, float* k_out,

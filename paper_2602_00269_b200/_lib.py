@@ -156,6 +156,7 @@ _SIGS = {
     "vox_read_frame": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, _i32p]),
     "vox_project_ext": (C.c_int, [_P, _P, C.c_int32]),
     "vox_link_tokens": (C.c_int, [_P, _P, _i32p, C.c_int32, C.c_int32, C.c_int32]),
+    "vox_copy_tokens": (C.c_int, [_P, _P, _i32p, C.c_int32]),
     "vox_mimi_create": (C.c_int, [C.c_int, C.POINTER(VoxMimiCfg), C.c_uint64, C.POINTER(_P)]),
     "vox_mimi_destroy": (None, [_P]),
     "vox_mimi_last_error": (C.c_char_p, [_P]),

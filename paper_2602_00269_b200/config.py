@@ -97,6 +97,15 @@ class ModelConfig:
         return d
 
 
+def detok_role(lm: ModelConfig, **kw) -> ModelConfig:
+    """The detokenizer-side context of a disaggregated deployment: the
+    same token layout and detokenizer as `lm`, with a 1-layer d=64 placeholder backbone
+    that is never run (the context only needs the token store, slots and the SNAC-style
+    decoder; a few MB instead of the LM's weights and KV pool)."""
+    return replace(lm, name=lm.name + "-detok", n_layers=1, d_model=64, n_heads=1, n_kv_heads=1, head_dim=64,
+                   d_ff=64, detok_enabled=True, **kw)
+
+
 def tiny(**kw) -> ModelConfig:
     """Config 1: 2-layer Llama backbone, d=256 (runs on the CPU oracle)."""
     base = ModelConfig(

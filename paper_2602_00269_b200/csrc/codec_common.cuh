@@ -52,45 +52,58 @@ VOX_DEV float act_fn(float x, int act, float slope) {
   return act == kActElu ? elu(x) : act == kActLeaky ? (x > 0.f ? x : slope * x) : x;
 }
 
-// h (+= ls * tmp) ; x = bf16(LayerNorm(h) * w + b).  One 128-thread CTA per row, D <= 1024.
+// h (+= ls * tmp) ; x = bf16(LayerNorm(h) * w + b).  One warp per row, NV = D / 32 values
+// per lane held in registers (D in {256, 512, 1024}).
+template <int NV>
 __global__ void __launch_bounds__(128) codec_ln_kernel(float* __restrict__ h, const float* __restrict__ tmp,
                                                       const float* __restrict__ ls, const float* __restrict__ w,
-                                                      const float* __restrict__ b, bf16* __restrict__ x, int D,
-                                                      float eps) {
-  __shared__ float red[4];
-  const int64_t r = blockIdx.x;
-  float v[8];
-  const int n = D / 128;
+                                                      const float* __restrict__ b, bf16* __restrict__ x, float eps,
+                                                      int64_t rows) {
+  constexpr int D = NV * 32;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  float v[NV];
   float s = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    if (i < n) {
-      const int c = threadIdx.x + 128 * i;
-      float a = h[r * D + c];
-      if (tmp != nullptr) {
-        a = a + ls[c] * tmp[r * D + c];
-        h[r * D + c] = a;
-      }
-      v[i] = a;
-      s += a;
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    float a = h[r * D + c];
+    if (tmp != nullptr) {
+      a = a + ls[c] * tmp[r * D + c];
+      h[r * D + c] = a;
     }
+    v[i] = a;
+    s += a;
   }
-  const float mean = block_sum<128>(s, red) / static_cast<float>(D);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / static_cast<float>(D);
   float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (i < n) {
-      v[i] -= mean;
-      ss += v[i] * v[i];
-    }
-  const float var = block_sum<128>(ss, red) / static_cast<float>(D);
-  const float sd = sqrtf(var + eps);
+  for (int i = 0; i < NV; ++i) {
+    v[i] -= mean;
+    ss += v[i] * v[i];
+  }
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (i < n) {
-      const int c = threadIdx.x + 128 * i;
-      x[r * D + c] = f32_to_bf16(v[i] / sd * w[c] + b[c]);
-    }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float sd = sqrtf(ss / static_cast<float>(D) + eps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = lane + 32 * i;
+    x[r * D + c] = f32_to_bf16(v[i] / sd * w[c] + b[c]);
+  }
+}
+
+inline void launch_codec_ln(float* h, const float* tmp, const float* ls, const float* w, const float* b, bf16* x,
+                            int D, float eps, int64_t rows, cudaStream_t st) {
+  const unsigned grid = static_cast<unsigned>((rows + 3) / 4);
+  switch (D) {
+    case 256: codec_ln_kernel<8><<<grid, 128, 0, st>>>(h, tmp, ls, w, b, x, eps, rows); break;
+    case 512: codec_ln_kernel<16><<<grid, 128, 0, st>>>(h, tmp, ls, w, b, x, eps, rows); break;
+    case 768: codec_ln_kernel<24><<<grid, 128, 0, st>>>(h, tmp, ls, w, b, x, eps, rows); break;
+    default: codec_ln_kernel<32><<<grid, 128, 0, st>>>(h, tmp, ls, w, b, x, eps, rows); break;
+  }
 }
 
 __global__ void codec_gelu_kernel(const float* __restrict__ x, bf16* __restrict__ y, int64_t n) {

@@ -60,75 +60,110 @@ __global__ void __launch_bounds__(128) cd_embed_kernel(const int32_t* __restrict
   for (int c = threadIdx.x; c < D; c += blockDim.x) h[r * D + c] = emb[static_cast<int64_t>(tok) * D + c];
 }
 
-// RoPE (rotate-half) in place on q and k of qkv rows; position = row index within its
-// segment (rows of segment g: [f_off, f_off + nf), u = 1)
-__global__ void __launch_bounds__(128) cd_rope_kernel(float* __restrict__ qkv, const int32_t* __restrict__ row_seg,
-                                                      const SegDev* __restrict__ seg, int D, int hd,
-                                                      const float* __restrict__ inv_freq) {
-  const int64_t r = blockIdx.x;
-  const SegDev q = seg[row_seg[r]];
-  const int pos = static_cast<int>(r - q.f_off);
-  float* src = qkv + r * 3 * D;
-  const int half = hd / 2;
-  // each thread owns a (lo, hi) pair of one head so the in-place update is race free
-  for (int e = threadIdx.x; e < D / 2; e += blockDim.x) {
-    const int head = e / half, i = e % half;
-    const int lo = head * hd + i, hi = lo + half;
+// Full (bidirectional) attention inside each segment with RoPE (rotate-half, position =
+// row index in the segment) applied while staging: one CTA (8 warps) per (segment, head);
+// the head's K (row stride hd + 1: conflict-free column reads) and V live in shared
+// memory, each warp takes 4 queries at a time (every K/V element read from smem feeds 4
+// query FMAs).  hd <= 64, segment rows <= kCdMaxRows.
+constexpr int kAttnQ = 4;
+__global__ void __launch_bounds__(256) cd_attn_kernel(const float* __restrict__ qkv, const SegDev* __restrict__ seg,
+                                                      int D, int hd, const float* __restrict__ inv_freq,
+                                                      bf16* __restrict__ out) {
+  extern __shared__ float sm[];
+  const SegDev q = seg[blockIdx.x];
+  const int hh = blockIdx.y;
+  const int n = q.nf, half = hd / 2, ks = hd + 1;
+  float* Ks = sm;                       // [n][hd + 1]
+  float* Vs = Ks + n * ks;              // [n][hd]
+  float* Ps = Vs + n * hd;              // [8][kAttnQ][n]
+  float* Qs = Ps + 8 * kAttnQ * n;      // [8][kAttnQ][hd]
+  const float* base = qkv + static_cast<int64_t>(q.f_off) * 3 * D + hh * hd;
+  for (int e = threadIdx.x; e < n * half; e += blockDim.x) {
+    const int j = e / half, i = e % half;
     float sn, cs;
-    sincosf(static_cast<float>(pos) * inv_freq[i], &sn, &cs);
-    const float q0 = src[lo], q1 = src[hi];
-    src[lo] = q0 * cs - q1 * sn;
-    src[hi] = q1 * cs + q0 * sn;
-    const float k0 = src[D + lo], k1 = src[D + hi];
-    src[D + lo] = k0 * cs - k1 * sn;
-    src[D + hi] = k1 * cs + k0 * sn;
+    sincosf(static_cast<float>(j) * inv_freq[i], &sn, &cs);
+    const float* kr = base + static_cast<int64_t>(j) * 3 * D + D;
+    const float k0 = kr[i], k1 = kr[i + half];
+    Ks[j * ks + i] = k0 * cs - k1 * sn;
+    Ks[j * ks + i + half] = k1 * cs + k0 * sn;
+  }
+  for (int e = threadIdx.x; e < n * hd; e += blockDim.x) {
+    const int j = e / hd, d = e % hd;
+    Vs[e] = base[static_cast<int64_t>(j) * 3 * D + 2 * D + d];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float scale = rsqrtf(static_cast<float>(hd));
+  float* P = Ps + warp * kAttnQ * n;
+  float* Q = Qs + warp * kAttnQ * hd;
+  for (int t0 = warp * kAttnQ; t0 < n; t0 += 8 * kAttnQ) {
+    for (int e = lane; e < kAttnQ * half; e += 32) {
+      const int qi = e / half, i = e % half, t = t0 + qi;
+      float q0 = 0.f, q1 = 0.f, sn = 0.f, cs = 1.f;
+      if (t < n) {
+        const float* qr = base + static_cast<int64_t>(t) * 3 * D;
+        q0 = qr[i];
+        q1 = qr[i + half];
+        sincosf(static_cast<float>(t) * inv_freq[i], &sn, &cs);
+      }
+      Q[qi * hd + i] = q0 * cs - q1 * sn;
+      Q[qi * hd + i + half] = q1 * cs + q0 * sn;
+    }
+    __syncwarp();
+    float mx[kAttnQ];
+#pragma unroll
+    for (int qi = 0; qi < kAttnQ; ++qi) mx[qi] = -INFINITY;
+    for (int j = lane; j < n; j += 32) {
+      float s[kAttnQ] = {};
+      const float* kr = Ks + j * ks;
+      for (int d = 0; d < hd; ++d) {
+        const float kv = kr[d];
+#pragma unroll
+        for (int qi = 0; qi < kAttnQ; ++qi) s[qi] += Q[qi * hd + d] * kv;
+      }
+#pragma unroll
+      for (int qi = 0; qi < kAttnQ; ++qi) {
+        P[qi * n + j] = s[qi] * scale;
+        mx[qi] = fmaxf(mx[qi], s[qi] * scale);
+      }
+    }
+    float sum[kAttnQ];
+#pragma unroll
+    for (int qi = 0; qi < kAttnQ; ++qi) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx[qi] = fmaxf(mx[qi], __shfl_xor_sync(0xffffffffu, mx[qi], o));
+      sum[qi] = 0.f;
+    }
+    for (int j = lane; j < n; j += 32)
+#pragma unroll
+      for (int qi = 0; qi < kAttnQ; ++qi) {
+        const float e = __expf(P[qi * n + j] - mx[qi]);
+        P[qi * n + j] = e;
+        sum[qi] += e;
+      }
+#pragma unroll
+    for (int qi = 0; qi < kAttnQ; ++qi)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum[qi] += __shfl_xor_sync(0xffffffffu, sum[qi], o);
+    __syncwarp();
+    for (int d = lane; d < hd; d += 32) {
+      float o[kAttnQ] = {};
+      for (int j = 0; j < n; ++j) {
+        const float vv = Vs[j * hd + d];
+#pragma unroll
+        for (int qi = 0; qi < kAttnQ; ++qi) o[qi] += P[qi * n + j] * vv;
+      }
+#pragma unroll
+      for (int qi = 0; qi < kAttnQ; ++qi)
+        if (t0 + qi < n) out[(static_cast<int64_t>(q.f_off) + t0 + qi) * D + hh * hd + d] = f32_to_bf16(o[qi] / sum[qi]);
+    }
+    __syncwarp();
   }
 }
 
-// full (bidirectional) attention inside each segment; one CTA per (segment, head)
-__global__ void __launch_bounds__(128) cd_attn_kernel(const float* __restrict__ qkv, const SegDev* __restrict__ seg,
-                                                      int D, int hd, bf16* __restrict__ out) {
-  __shared__ float p[4][kCdMaxRows];
-  __shared__ float sq[4][128];
-  const SegDev q = seg[blockIdx.x];
-  const int hh = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float scale = rsqrtf(static_cast<float>(hd));
-  const int n = q.nf;
-  const float* base = qkv + static_cast<int64_t>(q.f_off) * 3 * D;
-  for (int t = warp; t < n; t += 4) {
-    for (int d = lane; d < hd; d += 32) sq[warp][d] = base[static_cast<int64_t>(t) * 3 * D + hh * hd + d];
-    __syncwarp();
-    float mx = -INFINITY;
-    for (int j = lane; j < n; j += 32) {
-      const float* kr = base + static_cast<int64_t>(j) * 3 * D + D + hh * hd;
-      float s = 0.f;
-      for (int d = 0; d < hd; d += 4) {
-        const float4 k4 = *reinterpret_cast<const float4*>(kr + d);
-        s += sq[warp][d] * k4.x + sq[warp][d + 1] * k4.y + sq[warp][d + 2] * k4.z + sq[warp][d + 3] * k4.w;
-      }
-      s *= scale;
-      p[warp][j] = s;
-      mx = fmaxf(mx, s);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float e = __expf(p[warp][j] - mx);
-      p[warp][j] = e;
-      sum += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    __syncwarp();
-    for (int d = lane; d < hd; d += 32) {
-      float o = 0.f;
-      for (int j = 0; j < n; ++j) o += p[warp][j] * base[static_cast<int64_t>(j) * 3 * D + 2 * D + hh * hd + d];
-      out[(static_cast<int64_t>(q.f_off) + t) * D + hh * hd + d] = f32_to_bf16(o / sum);
-    }
-    __syncwarp();
-  }
+inline size_t cd_attn_smem(int n, int hd) {
+  return sizeof(float) * (static_cast<size_t>(n) * (hd + 1) + static_cast<size_t>(n) * hd + 8 * kAttnQ * n +
+                          8 * kAttnQ * hd);
 }
 
 // x0: unit-variance uniform noise, bit-identical to oracle/weights.py:cosy_noise
@@ -319,6 +354,7 @@ struct VoxCosy {
   std::vector<uint64_t> seeds;
   // workspaces
   int64_t max_erows = 0, max_vrows = 0;
+  int max_seg = 0;  // token rows of the longest request in the current call
   float *h = nullptr, *qkv = nullptr, *tmp = nullptr, *mu_t = nullptr, *x = nullptr, *v = nullptr, *z = nullptr;
   float *mel = nullptr, *va = nullptr, *vb = nullptr, *vt = nullptr, *spec = nullptr, *wf = nullptr, *pcm = nullptr;
   bf16 *xbf = nullptr, *col = nullptr;
@@ -575,17 +611,17 @@ int create(VoxCosy* m, uint64_t seed) {
 }
 
 int xf_layers(VoxCosy* m, std::vector<CdXf>& layers, float* h, int64_t rows, int d, int heads, int ffn, int nseg,
-              const int32_t* row_seg, const SegDev* seg, const float* inv) {
+              const int32_t* row_seg, const SegDev* seg, const float* inv, int max_rows) {
+  (void)row_seg;
   const VoxCosyCfg& g = m->cfg;
   cudaStream_t st = m->st;
   const int hd = d / heads;
   for (auto& w : layers) {
-    CLK(codec_ln_kernel<<<static_cast<unsigned>(rows), 128, 0, st>>>(h, nullptr, nullptr, w.ln1w, w.ln1b, m->xbf, d, g.eps));
+    CLK(launch_codec_ln(h, nullptr, nullptr, w.ln1w, w.ln1b, m->xbf, d, g.eps, rows, st));
     CRET(gemm(m, w.tm_qkv, 3 * d, m->xbf, d, rows, m->qkv, 3 * d, nullptr, nullptr, 0));
-    CLK(cd_rope_kernel<<<static_cast<unsigned>(rows), 128, 0, st>>>(m->qkv, row_seg, seg, d, hd, inv));
-    CLK(cd_attn_kernel<<<dim3(nseg, heads), 128, 0, st>>>(m->qkv, seg, d, hd, m->xbf));
+    CLK(cd_attn_kernel<<<dim3(nseg, heads), 256, cd_attn_smem(max_rows, hd), st>>>(m->qkv, seg, d, hd, inv, m->xbf));
     CRET(gemm(m, w.tm_o, d, m->xbf, d, rows, h, d, nullptr, h, d));
-    CLK(codec_ln_kernel<<<static_cast<unsigned>(rows), 128, 0, st>>>(h, nullptr, nullptr, w.ln2w, w.ln2b, m->xbf, d, g.eps));
+    CLK(launch_codec_ln(h, nullptr, nullptr, w.ln2w, w.ln2b, m->xbf, d, g.eps, rows, st));
     CRET(gemm(m, w.tm_fc1, ffn, m->xbf, d, rows, m->tmp, ffn, nullptr, nullptr, 0));
     const int64_t ne = rows * ffn;
     CLK(codec_gelu_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->tmp, m->xbf, ne));
@@ -609,8 +645,8 @@ int enqueue(VoxCosy* m, int n, int64_t E, int64_t V) {
   StateView sv{m->state, 2 * m->half, m->half};
   // ---------------- flow: encoder over [ref | new] tokens
   CLK(cd_embed_kernel<<<static_cast<unsigned>(E), 128, 0, st>>>(row_seg, fseg, m->reftok, ref, toks, m->emb, de, m->h));
-  CRET(xf_layers(m, m->enc, m->h, E, de, g.enc_heads, g.enc_ffn, n, row_seg, fseg, m->inv_enc));
-  CLK(codec_ln_kernel<<<static_cast<unsigned>(E), 128, 0, st>>>(m->h, nullptr, nullptr, m->elnfw, m->elnfb, m->xbf, de, g.eps));
+  CRET(xf_layers(m, m->enc, m->h, E, de, g.enc_heads, g.enc_ffn, n, row_seg, fseg, m->inv_enc, m->max_seg));
+  CLK(launch_codec_ln(m->h, nullptr, nullptr, m->elnfw, m->elnfb, m->xbf, de, g.eps, E, st));
   CRET(gemm(m, m->tm_mu, M, m->xbf, de, E, m->mu_t, M, m->mub, nullptr, 0));
   // ---------------- flow matching ODE (CFG: rows [0, R) cond, [R, 2R) uncond)
   const int64_t R = 2 * E;
@@ -622,8 +658,9 @@ int enqueue(VoxCosy* m, int n, int64_t E, int64_t V) {
     CLK(cd_est_in_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->x, m->mu_t, row_seg, fseg, m->spk,
                                                                                  m->refmel, ref, M, R, m->xbf));
     CRET(gemm(m, m->tm_in, ds, m->xbf, 4 * M, 2 * R, m->z, ds, m->step_bias + static_cast<int64_t>(i) * ds, nullptr, 0));
-    CRET(xf_layers(m, m->est, m->z, 2 * R, ds, g.est_heads, g.est_ffn, 2 * n, mrow_seg, gseg, m->inv_est));
-    CLK(codec_ln_kernel<<<static_cast<unsigned>(2 * R), 128, 0, st>>>(m->z, nullptr, nullptr, m->olnw, m->olnb, m->xbf, ds, g.eps));
+    CRET(xf_layers(m, m->est, m->z, 2 * R, ds, g.est_heads, g.est_ffn, 2 * n, mrow_seg, gseg, m->inv_est,
+                   2 * m->max_seg));
+    CLK(launch_codec_ln(m->z, nullptr, nullptr, m->olnw, m->olnb, m->xbf, ds, g.eps, 2 * R, st));
     CRET(gemm(m, m->tm_out, M, m->xbf, ds, 2 * R, m->v, M, m->outb, nullptr, 0));
     CLK(cd_euler_kernel<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, st>>>(m->x, m->v, nx, m->ts[i + 1] - m->ts[i], lam));
   }
@@ -720,7 +757,7 @@ int vox_cosy_create(int device, const VoxCosyCfg* cfg, uint64_t seed, VoxCosy** 
   *out = nullptr;
   const VoxCosyCfg& g = *cfg;
   auto bad_xf = [](int d, int heads, int ffn) {
-    return d % 128 || d > 1024 || heads < 1 || d % heads || (d / heads) % 4 || d / heads > 128 || ffn % 64;
+    return (d != 256 && d != 512 && d != 768 && d != 1024) || heads < 1 || d % heads || (d / heads) % 2 || d / heads > 64 || ffn % 64;
   };
   if (bad_xf(g.d_enc, g.enc_heads, g.enc_ffn) || bad_xf(g.d_est, g.est_heads, g.est_ffn) || g.mel % 16 ||
       g.enc_layers < 0 || g.est_layers < 0 || g.n_steps < 1 || g.vocab < 1 || g.ref_tokens < 0 ||
@@ -745,6 +782,9 @@ int vox_cosy_create(int device, const VoxCosyCfg* cfg, uint64_t seed, VoxCosy** 
   int rc = cudaStreamCreateWithPriority(&m->st, cudaStreamNonBlocking, lo) == cudaSuccess ? VOX_OK : VOX_ERR_CUDA;
   if (rc == VOX_OK && (cudaEventCreate(&m->ev0) != cudaSuccess || cudaEventCreate(&m->ev1) != cudaSuccess))
     rc = cfail(m, VOX_ERR_CUDA, "event create");
+  if (rc == VOX_OK && cudaFuncSetAttribute(cd_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(cd_attn_smem(kCdMaxRows, 64))) != cudaSuccess)
+    rc = cfail(m, VOX_ERR_CUDA, "attention smem attribute");
   if (rc == VOX_OK) rc = create(m, seed);
   if (rc == VOX_OK && cudaStreamSynchronize(m->st) != cudaSuccess) rc = cfail(m, VOX_ERR_CUDA, "init sync");
   if (rc != VOX_OK) {
@@ -799,6 +839,7 @@ int vox_cosy_decode(VoxCosy* m, const VoxCosyReq* reqs, int32_t n, const int32_t
   cudaSetDevice(m->device);
   const Stage L = stage_layout(g, m->max_erows, m->max_vrows);
   int32_t* hs = m->h_stage;
+  m->max_seg = 0;
   SegDev* fseg = reinterpret_cast<SegDev*>(hs + L.fseg);
   SegDev* vseg = reinterpret_cast<SegDev*>(hs + L.vseg);
   SegDev* gseg = reinterpret_cast<SegDev*>(hs + L.gseg);
@@ -815,6 +856,7 @@ int vox_cosy_decode(VoxCosy* m, const VoxCosyReq* reqs, int32_t n, const int32_t
     if (r.n_tokens > g.max_chunk) return cfail(m, VOX_ERR_BATCH_TOO_LARGE, "chunk exceeds max_chunk tokens");
     if (C + r.n_tokens > g.max_tokens) return cfail(m, VOX_ERR_BATCH_TOO_LARGE, "batch exceeds max_tokens");
     const int T = g.ref_tokens + r.n_tokens;
+    m->max_seg = std::max(m->max_seg, T);
     const uint64_t key = tensor_key(m->seeds[r.slot], T_CD_NOISE, static_cast<uint64_t>(m->calls[r.slot]));
     fseg[i] = SegDev{r.slot, static_cast<int32_t>(E), T, m->parity[r.slot], 0, static_cast<int32_t>(C),
                      {static_cast<int32_t>(key & 0xffffffffu), static_cast<int32_t>(key >> 32)}};

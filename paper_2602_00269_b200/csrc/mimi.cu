@@ -455,15 +455,15 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
     const MimiLayerW& w = m->layers[l];
     const bool first = l == 0;
     const MimiLayerW* prev = first ? nullptr : &m->layers[l - 1];
-    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, first ? nullptr : m->tmp, first ? nullptr : prev->ls2, w.ln1w,
-                                          w.ln1b, m->xbf, D, g.eps));
+    LK(launch_codec_ln(m->h, first ? nullptr : m->tmp, first ? nullptr : prev->ls2, w.ln1w,
+                                          w.ln1b, m->xbf, D, g.eps, R0, st));
     MRET(gemm(m, w.tm_qkv, 3 * D, m->xbf, D, R0, m->qkv, 3 * D, nullptr, nullptr, 0));
     LK(mimi_rope_kv_kernel<<<R0, 128, 0, st>>>(m->qkv, frame_req, reqs, D, hd, m->ring, g.n_layers, l,
                                                m->inv_freq, m->kv, m->q));
     LK(mimi_attn_kernel<<<dim3(n, g.n_heads), 128, 0, st>>>(m->q, reqs, m->kv, D, hd, g.window, m->ring, g.n_layers, l,
                                                             m->xbf));
     MRET(gemm(m, w.tm_o, D, m->xbf, D, R0, m->tmp, D, nullptr, nullptr, 0));
-    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls1, w.ln2w, w.ln2b, m->xbf, D, g.eps));
+    LK(launch_codec_ln(m->h, m->tmp, w.ls1, w.ln2w, w.ln2b, m->xbf, D, g.eps, R0, st));
     MRET(gemm(m, w.tm_fc1, g.ffn, m->xbf, D, R0, m->tmp, g.ffn, nullptr, nullptr, 0));
     const int64_t ne = R0 * g.ffn;
     LK(codec_gelu_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->tmp, m->xbf, ne));
@@ -473,7 +473,7 @@ int enqueue(VoxMimi* m, int n, int Ftot) {
   {
     // reuse mimi_ln's residual update: LN output discarded into xbf (cheap, R0 rows)
     const MimiLayerW& w = m->layers[g.n_layers - 1];
-    LK(codec_ln_kernel<<<R0, 128, 0, st>>>(m->h, m->tmp, w.ls2, w.ln1w, w.ln1b, m->xbf, D, g.eps));
+    LK(launch_codec_ln(m->h, m->tmp, w.ls2, w.ln1w, w.ln1b, m->xbf, D, g.eps, R0, st));
   }
   auto im2col = [&](const float* x, int C, int k, int elu_on, int Kp, int u, int64_t off, int64_t rows) -> int {
     const int64_t tot = rows * (Kp / 8);
@@ -528,7 +528,7 @@ int vox_mimi_create(int device, const VoxMimiCfg* cfg, uint64_t seed, VoxMimi** 
   if (!cfg || !out) return mfail(m, VOX_ERR_INVALID, "null argument");
   *out = nullptr;
   const VoxMimiCfg& g = *cfg;
-  if (g.hidden % 128 || g.hidden > 1024 || g.n_heads < 1 || g.hidden % g.n_heads || (g.hidden / g.n_heads) % 4 ||
+  if ((g.hidden != 256 && g.hidden != 512 && g.hidden != 768 && g.hidden != 1024) || g.n_heads < 1 || g.hidden % g.n_heads || (g.hidden / g.n_heads) % 4 ||
       g.hidden / g.n_heads > 128 || g.window < 1 || g.window > kMaxWin || g.n_ratios < 1 || g.n_ratios > 4 ||
       g.n_q < 2 || g.n_semantic < 1 || g.n_semantic >= g.n_q || g.cb_dim < 1 || g.ffn % 64 || g.kernel < 1 ||
       g.last_kernel < 1 || g.res_kernel < 1 || g.compress < 1 || g.max_slots < 1 || g.max_frames < 1 ||

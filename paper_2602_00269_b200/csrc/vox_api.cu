@@ -1211,6 +1211,71 @@ int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, i
   return VOX_OK;
 }
 
+// Disaggregated LM -> detok (reference engine.py:119-123,150-156): copy
+// token-store spans of an LM context into a detokenizer context, possibly on another GPU,
+// ordered after every forward already enqueued on the LM context and before the next
+// work on the detok stream of `dst`.  Peer-accessible contexts (same device, or NVLink
+// peers with access enabled here) use one gather kernel on the destination reading the
+// source store through its device pointer; otherwise one cudaMemcpyPeerAsync per span.
+int vox_copy_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* spans, int32_t n) {
+  VoxCtx* c = dst;
+  if (!dst || !src || !spans || n < 1 || n > dst->cfg.max_rows) return fail(dst, VOX_ERR_INVALID, "bad token spans");
+  for (int i = 0; i < n; ++i) {
+    const int32_t* l = spans + 5 * i;
+    if (l[0] < 0 || l[0] >= dst->cfg.max_slots || l[2] < 0 || l[2] >= src->cfg.max_slots || l[4] < 1 ||
+        l[1] < 0 || l[1] + l[4] > dst->cfg.max_ctx || l[3] < 0 || l[3] + l[4] > src->cfg.max_ctx)
+      return fail(dst, VOX_ERR_INVALID, "token span out of range");
+  }
+  bool peer = dst->device == src->device;
+  if (!peer) {
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dst->device, src->device);
+    if (can) {
+      CK(cudaSetDevice(dst->device));
+      const cudaError_t pe = cudaDeviceEnablePeerAccess(src->device, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      peer = pe == cudaSuccess || pe == cudaErrorPeerAccessAlreadyEnabled;
+    }
+  }
+  CK(cudaSetDevice(src->device));
+  CK(cudaEventRecord(src->ev_xfer, src->s_lm));
+  CK(cudaSetDevice(dst->device));
+  CK(cudaStreamWaitEvent(dst->s_dt, src->ev_xfer, 0));
+  if (peer) {
+    // one link per token (mode 0 of link_tokens_kernel), staged through the pinned ring
+    const int e = static_cast<int>(dst->link_seq++ % 8);
+    CK(cudaEventSynchronize(dst->ev_links[e]));
+    int* hl = dst->h_links + static_cast<size_t>(e) * dst->cfg.max_rows * 4;
+    int* dl = dst->d_links + static_cast<size_t>(e) * dst->cfg.max_rows * 4;
+    int m = 0;
+    for (int i = 0; i < n; ++i) {
+      const int32_t* l = spans + 5 * i;
+      for (int k = 0; k < l[4]; ++k) {
+        if (m == dst->cfg.max_rows) return fail(dst, VOX_ERR_BATCH_TOO_LARGE, "more tokens than max_rows per copy");
+        int* o = hl + 4 * m++;
+        o[0] = l[0];
+        o[1] = l[1] + k;
+        o[2] = l[2];
+        o[3] = l[3] + k;
+      }
+    }
+    CK(cudaMemcpyAsync(dl, hl, static_cast<size_t>(m) * 16, cudaMemcpyHostToDevice, dst->s_dt));
+    launch_link_tokens(dl, m, src->token_store, src->cfg.max_ctx, dst->token_store, dst->cfg.max_ctx, 0, 0, 0,
+                       dst->s_dt);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(dst->ev_links[e], dst->s_dt));
+    dst->launches++;
+  } else {
+    for (int i = 0; i < n; ++i) {
+      const int32_t* l = spans + 5 * i;
+      CK(cudaMemcpyPeerAsync(dst->token_store + static_cast<int64_t>(l[0]) * dst->cfg.max_ctx + l[1], dst->device,
+                             src->token_store + static_cast<int64_t>(l[2]) * src->cfg.max_ctx + l[3], src->device,
+                             static_cast<size_t>(l[4]) * 4, dst->s_dt));
+    }
+  }
+  return VOX_OK;
+}
+
 int vox_slot_info(VoxCtx* c, int32_t slot, int32_t* prompt_len, int32_t* target_len) {
   if (!c || slot < 0 || slot >= c->cfg.max_slots || !c->slot_used[slot])
     return fail(c, VOX_ERR_CACHE_MISSING, "unknown slot");

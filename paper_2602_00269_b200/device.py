@@ -266,6 +266,12 @@ class VoxDevice:
         a = np.ascontiguousarray(links, dtype=np.int32)
         self._check(self.lib.vox_link_tokens(self.ctx, src.ctx, _ptr(a, C.c_int32), a.shape[0], offset, mode))
 
+    def copy_tokens(self, src: "VoxDevice", spans: np.ndarray) -> None:
+        """Token-store spans [n, 5] = (dst_slot, dst_pos, src_slot, src_pos, len) from the
+        LM context `src` into this (detokenizer) context -- disaggregated LM -> detok."""
+        arr = np.ascontiguousarray(spans, np.int32).reshape(-1, 5)
+        self._check(self.lib.vox_copy_tokens(self.ctx, src.ctx, arr.ctypes.data_as(_lib._i32p), arr.shape[0]))
+
     def trace_arm(self, capacity: int = 1 << 20) -> None:
         """Arm the in-graph kernel tracer (one record per CTA of every instrumented kernel)."""
         self._check(self.lib.vox_trace_arm(self.ctx, capacity))

@@ -44,6 +44,7 @@ class _Run:
     cache: model_api.DetokenizerCache
     slot: int
     pending_chunks: int = 0
+    dslot: int = -1  # slot on the detokenizer context (disaggregated mode)
 
 
 @dataclass
@@ -63,7 +64,12 @@ class EngineStats:
 
 class StreamingEngine:
     def __init__(self, dev: VoxDevice, profile, policy, seed: int, max_inflight: int = 2,
-                 delivery_overhead_us: int = 0, keep_pcm: bool = False):
+                 delivery_overhead_us: int = 0, keep_pcm: bool = False, detok_dev: Optional[VoxDevice] = None):
+        """detok_dev: disaggregated LM -> detok (reference engine.py:119-123,150-156,
+        PAPER.md:300): the LM runs on `dev`, detokenization on `detok_dev` (another GPU,
+        a ``config.detok_role`` context with the same detokenizer weights); each window's
+        tokens cross over vox_copy_tokens (NVLink peer copy) ordered after the forward
+        that produced them."""
         if profile.vocab_size != dev.cfg.vocab:
             raise ValueError("profile vocab must equal the model vocab")
         self.dev = dev
@@ -73,6 +79,8 @@ class StreamingEngine:
         self.max_inflight = max_inflight
         self.delivery_overhead_us = delivery_overhead_us
         self.sampling = Sampling.from_ref(profile.sampling_defaults)
+        self.ddev = detok_dev or dev
+        self.disaggregated = detok_dev is not None
         self.live: dict[int, _Run] = {}
         self.trace = core.Trace()
         self.stats = EngineStats()
@@ -81,6 +89,9 @@ class StreamingEngine:
         self._tickets: list[tuple[int, list[tuple[_Run, object, int, int]]]] = []
         self._fwd_seqs: list[int] = []
         self._t0 = 0.0
+        # on_chunk(request_id, chunk_index, available_us, playback_us, pcm or None, final):
+        # called from the engine loop when a chunk's PCM has landed (serve.py streams it)
+        self.on_chunk = None
 
     # ------------------------------------------------------------------ clock
     def now_us(self) -> int:
@@ -92,7 +103,10 @@ class StreamingEngine:
             prompt_tokens=spec.prompt_tokens, profile=self.profile, seed=self.seed, request_id=rid,
             arrival_us=spec.arrival_us, target_output_tokens=spec.target_output_tokens)
         slot = self.dev.admit(state.seed, spec.prompt_tokens, spec.target_output_tokens, self.sampling)
-        self.live[rid] = _Run(req=req, state=state, cache=cache, slot=slot)
+        dslot = -1
+        if self.disaggregated:
+            dslot = self.ddev.admit(state.seed, spec.prompt_tokens, spec.target_output_tokens, self.sampling)
+        self.live[rid] = _Run(req=req, state=state, cache=cache, slot=slot, dslot=dslot)
 
     def _snapshot(self) -> list:
         out = []
@@ -142,7 +156,7 @@ class StreamingEngine:
         st.decisions.append((len(decision.lm), len(decision.detok)))
 
     def _issue_detok(self, specs: Sequence) -> None:
-        cfg = self.dev.cfg
+        cfg = self.ddev.cfg
         batches, cur, frames = [], [], 0
         for w in specs:
             f = 4 * -(-w.new_tokens // cfg.frame_tokens)
@@ -157,9 +171,19 @@ class StreamingEngine:
             # a ticket is valid for VOX_TICKET_RING (32) calls: retire old ones first
             while len(self._tickets) >= 24:
                 self._poll(block=True)
-            arr = np.asarray([[self.live[w.request].slot, w.index, w.start, w.length, w.new_tokens, int(w.final)]
-                              for w in b], np.int32)
-            ns, ticket = self.dev.detok(arr, sync=False)
+            if self.disaggregated:
+                spans = []
+                for w in b:
+                    run = self.live[w.request]
+                    p0 = run.req.prompt_tokens + w.start
+                    spans.append([run.dslot, p0, run.slot, p0, w.length])
+                self.ddev.copy_tokens(self.dev, np.asarray(spans, np.int32))
+                arr = np.asarray([[self.live[w.request].dslot, w.index, w.start, w.length, w.new_tokens,
+                                   int(w.final)] for w in b], np.int32)
+            else:
+                arr = np.asarray([[self.live[w.request].slot, w.index, w.start, w.length, w.new_tokens,
+                                   int(w.final)] for w in b], np.int32)
+            ns, ticket = self.ddev.detok(arr, sync=False)
             items = []
             off = 0
             for w, n in zip(b, ns):
@@ -182,22 +206,24 @@ class StreamingEngine:
         done = 0
         while self._tickets:
             ticket, items = self._tickets[0]
-            ok, t_ms = self.dev.ticket_done(ticket)
+            ok, t_ms = self.ddev.ticket_done(ticket)
             if not ok:
                 if not block or done > 0:
                     break
-                self.dev.ticket_pcm(ticket)  # waits for the ticket's event
-                ok, t_ms = self.dev.ticket_done(ticket)
+                self.ddev.ticket_pcm(ticket)  # waits for the ticket's event
+                ok, t_ms = self.ddev.ticket_done(ticket)
             self._tickets.pop(0)
-            pcm = self.dev.ticket_pcm(ticket) if self.keep_pcm else None
+            pcm = self.ddev.ticket_pcm(ticket) if (self.keep_pcm or self.on_chunk is not None) else None
             avail = int(t_ms * 1000) + self.delivery_overhead_us
             for run, w, pb, (off, n) in items:
                 r = run.req
                 self.trace.chunks.append(core.ChunkEvent(request=r.id, index=w.index, available_us=avail,
                                                          playback_us=pb, new_tokens=w.new_tokens))
                 self.stats.pcm_samples += n
-                if pcm is not None:
+                if pcm is not None and self.keep_pcm:
                     self.pcm.setdefault(r.id, []).append(pcm[off:off + n].copy())
+                if self.on_chunk is not None:
+                    self.on_chunk(r.id, w.index, avail, pb, pcm[off:off + n].copy(), bool(w.final))
                 run.pending_chunks -= 1
                 if r.first_chunk_us is None:
                     r.first_chunk_us = avail
@@ -205,6 +231,8 @@ class StreamingEngine:
                 if r.done_generating and r.covered_tokens >= r.target_output_tokens and run.pending_chunks == 0:
                     r.phase = core.Phase.FINISHED
                     self.dev.release(run.slot)
+                    if self.disaggregated:
+                        self.ddev.release(run.dslot)
                     self.trace.requests.append(self.live.pop(r.id).req)
             done += 1
         return done
@@ -214,8 +242,11 @@ class StreamingEngine:
         while self._tickets:
             self._poll(block=True)
         self.dev.synchronize()
+        self.ddev.synchronize()
         for run in list(self.live.values()):
             self.dev.release(run.slot)
+            if self.disaggregated:
+                self.ddev.release(run.dslot)
         self.live.clear()
 
     # ------------------------------------------------------------------ full run
@@ -232,6 +263,8 @@ class StreamingEngine:
         gc.freeze()
         gc.disable()
         self.dev.clock_reset()
+        if self.disaggregated:
+            self.ddev.clock_reset()
         self._t0 = time.perf_counter()
         t_host = 0.0
         while idx < len(pending) or self.live:
@@ -266,6 +299,7 @@ class StreamingEngine:
         while self._tickets:
             self._poll(block=True)
         self.dev.synchronize()
+        self.ddev.synchronize()
         gc.unfreeze()
         if gc_on:
             gc.enable()
@@ -274,6 +308,58 @@ class StreamingEngine:
         self.trace.requests.sort(key=lambda r: r.id)
         self.trace.chunks.sort(key=lambda c: (c.available_us, c.request, c.index))
         return self.trace
+
+
+    # ------------------------------------------------------------------ online serving
+    def serve(self, inbox, stop, idle_s: float = 0.0005) -> None:
+        """Online twin of ``run``: arrivals come from ``inbox`` (a queue.Queue of
+        (request_id, prompt_tokens, output_tokens)) while the loop runs, each stamped with
+        the engine clock when it is admitted; chunks are delivered through ``on_chunk``.
+        Returns when ``stop`` is set and no request is live (graceful drain)."""
+        import queue as _queue
+
+        from ._ref import workload
+
+        gc_on = gc.isenabled()
+        gc.collect()
+        gc.freeze()
+        gc.disable()
+        self.dev.clock_reset()
+        if self.disaggregated:
+            self.ddev.clock_reset()
+        self._t0 = time.perf_counter()
+        waiting: list = []
+        try:
+            while True:
+                while True:
+                    try:
+                        waiting.append(inbox.get_nowait())
+                    except _queue.Empty:
+                        break
+                if stop.is_set() and not self.live and not waiting and not self._tickets:
+                    break
+                now = self.now_us()
+                cap = min(self.policy.max_live_requests, self.dev.cfg.max_slots)
+                while waiting and len(self.live) < cap:
+                    rid, P, T = waiting.pop(0)
+                    self.admit(rid, workload.ArrivalSpec(arrival_us=now, prompt_tokens=P, target_output_tokens=T))
+                self._poll()
+                if not self.live:
+                    time.sleep(idle_s)
+                    continue
+                decision = scheduler.schedule(self._snapshot(), now, self.policy)
+                if decision.empty:
+                    if self._tickets:
+                        self._poll(block=True)
+                    else:
+                        time.sleep(idle_s)
+                    continue
+                self.run_iteration(decision)
+            self.dev.synchronize()
+        finally:
+            gc.unfreeze()
+            if gc_on:
+                gc.enable()
 
 
 def orpheus_profile(max_batch: int = 256):
