@@ -166,6 +166,166 @@ inline size_t cd_attn_smem(int n, int hd) {
                           8 * kAttnQ * hd);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core variant (hd = 64): mma.sync m16n8k16 bf16 -> fp32, flash-style online
+// softmax over 64-key blocks.  One CTA (8 warps) per (segment, head): RoPE'd K staged as
+// bf16 [key][72] (B operand of S = Q K^T: 32-bit fragment loads, conflict-free), V staged
+// transposed as bf16 [dim][npad + 8] (B operand of O = P V); each warp takes 16 query rows
+// at a time, P goes from the S accumulators straight into A fragments (no smem).
+// Rounding: Q, K, V and P in bf16, scores / softmax / O in fp32 (the estimator's GEMM
+// operands are bf16 too).
+// ---------------------------------------------------------------------------
+VOX_DEV void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+VOX_DEV uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+constexpr int kTcHd = 64, kTcKs = 72;
+inline int cd_tc_npad(int n) { return (n + 63) / 64 * 64; }
+inline size_t cd_attn_tc_smem(int n) {
+  const int np = cd_tc_npad(n);
+  return 2 * (static_cast<size_t>(np) * kTcKs + static_cast<size_t>(kTcHd) * (np + 8) + 8 * 16 * kTcKs);
+}
+
+__global__ void __launch_bounds__(256) cd_attn_tc_kernel(const float* __restrict__ qkv, const SegDev* __restrict__ seg,
+                                                         int D, const float* __restrict__ inv_freq,
+                                                         bf16* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const SegDev q = seg[blockIdx.x];
+  const int hh = blockIdx.y;
+  const int n = q.nf, np = (n + 63) / 64 * 64, VS = np + 8;
+  constexpr int half = kTcHd / 2;
+  bf16* Ks = reinterpret_cast<bf16*>(smraw);          // [np][72]
+  bf16* Vt = Ks + np * kTcKs;                          // [64][np + 8]
+  bf16* Qs = Vt + kTcHd * VS;                          // [8 warps][16][72]
+  const float* base = qkv + static_cast<int64_t>(q.f_off) * 3 * D + hh * kTcHd;
+  for (int e = threadIdx.x; e < np * half; e += blockDim.x) {
+    const int j = e / half, i = e % half;
+    float k0 = 0.f, k1 = 0.f, sn = 0.f, cs = 1.f;
+    if (j < n) {
+      const float* kr = base + static_cast<int64_t>(j) * 3 * D + D;
+      k0 = kr[i];
+      k1 = kr[i + half];
+      sincosf(static_cast<float>(j) * inv_freq[i], &sn, &cs);
+    }
+    Ks[j * kTcKs + i] = f32_to_bf16(k0 * cs - k1 * sn);
+    Ks[j * kTcKs + i + half] = f32_to_bf16(k1 * cs + k0 * sn);
+  }
+  for (int e = threadIdx.x; e < np * kTcHd; e += blockDim.x) {
+    const int j = e / kTcHd, d = e % kTcHd;
+    Vt[d * VS + j] = f32_to_bf16(j < n ? base[static_cast<int64_t>(j) * 3 * D + 2 * D + d] : 0.f);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const float sl2 = rsqrtf(static_cast<float>(kTcHd)) * 1.4426950408889634f;  // scale * log2(e)
+  bf16* Q = Qs + warp * 16 * kTcKs;
+  for (int t0 = warp * 16; t0 < n; t0 += 8 * 16) {
+    for (int e = lane; e < 16 * half; e += 32) {
+      const int r = e / half, i = e % half, row = t0 + r;
+      float q0 = 0.f, q1 = 0.f, sn = 0.f, cs = 1.f;
+      if (row < n) {
+        const float* qr = base + static_cast<int64_t>(row) * 3 * D;
+        q0 = qr[i];
+        q1 = qr[i + half];
+        sincosf(static_cast<float>(row) * inv_freq[i], &sn, &cs);
+      }
+      Q[r * kTcKs + i] = f32_to_bf16(q0 * cs - q1 * sn);
+      Q[r * kTcKs + i + half] = f32_to_bf16(q1 * cs + q0 * sn);
+    }
+    __syncwarp();
+    uint32_t qa[4][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      qa[ks][0] = *reinterpret_cast<const uint32_t*>(&Q[g * kTcKs + ks * 16 + 2 * t]);
+      qa[ks][1] = *reinterpret_cast<const uint32_t*>(&Q[(g + 8) * kTcKs + ks * 16 + 2 * t]);
+      qa[ks][2] = *reinterpret_cast<const uint32_t*>(&Q[g * kTcKs + ks * 16 + 2 * t + 8]);
+      qa[ks][3] = *reinterpret_cast<const uint32_t*>(&Q[(g + 8) * kTcKs + ks * 16 + 2 * t + 8]);
+    }
+    float o[8][4] = {};
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+    for (int kb = 0; kb < np; kb += 64) {
+      float sc[8][4] = {};
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const bf16* kr = Ks + (kb + nt * 8 + g) * kTcKs + 2 * t;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma16816(sc[nt], qa[ks], *reinterpret_cast<const uint32_t*>(kr + ks * 16),
+                   *reinterpret_cast<const uint32_t*>(kr + ks * 16 + 8));
+      }
+      float x0 = -INFINITY, x1 = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int key = kb + nt * 8 + 2 * t + (e & 1);
+          const float v = key < n ? sc[nt][e] * sl2 : -INFINITY;
+          sc[nt][e] = v;
+          if (e < 2) x0 = fmaxf(x0, v); else x1 = fmaxf(x1, v);
+        }
+#pragma unroll
+      for (int off = 1; off < 4; off <<= 1) {
+        x0 = fmaxf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+        x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+      }
+      const float n0 = fmaxf(m0, x0), n1 = fmaxf(m1, x1);
+      const float al0 = exp2f(m0 - n0), al1 = exp2f(m1 - n1);
+      m0 = n0;
+      m1 = n1;
+      l0 *= al0;
+      l1 *= al1;
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        o[dt][0] *= al0; o[dt][1] *= al0; o[dt][2] *= al1; o[dt][3] *= al1;
+      }
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        sc[nt][0] = exp2f(sc[nt][0] - m0);
+        sc[nt][1] = exp2f(sc[nt][1] - m0);
+        sc[nt][2] = exp2f(sc[nt][2] - m1);
+        sc[nt][3] = exp2f(sc[nt][3] - m1);
+        l0 += sc[nt][0] + sc[nt][1];
+        l1 += sc[nt][2] + sc[nt][3];
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t pa[4] = {pack2(sc[2 * kk][0], sc[2 * kk][1]), pack2(sc[2 * kk][2], sc[2 * kk][3]),
+                                pack2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]),
+                                pack2(sc[2 * kk + 1][2], sc[2 * kk + 1][3])};
+#pragma unroll
+        for (int dt = 0; dt < 8; ++dt) {
+          const bf16* vr = Vt + (dt * 8 + g) * VS + kb + kk * 16 + 2 * t;
+          mma16816(o[dt], pa, *reinterpret_cast<const uint32_t*>(vr), *reinterpret_cast<const uint32_t*>(vr + 8));
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 1; off < 4; off <<= 1) {
+      l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, off);
+    }
+    const int r0 = t0 + g, r1 = t0 + g + 8;
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      const int d = hh * kTcHd + dt * 8 + 2 * t;
+      if (r0 < n)
+        *reinterpret_cast<__nv_bfloat162*>(out + (static_cast<int64_t>(q.f_off) + r0) * D + d) =
+            __floats2bfloat162_rn(o[dt][0] / l0, o[dt][1] / l0);
+      if (r1 < n)
+        *reinterpret_cast<__nv_bfloat162*>(out + (static_cast<int64_t>(q.f_off) + r1) * D + d) =
+            __floats2bfloat162_rn(o[dt][2] / l1, o[dt][3] / l1);
+    }
+    __syncwarp();
+  }
+}
+
 // x0: unit-variance uniform noise, bit-identical to oracle/weights.py:cosy_noise
 __global__ void cd_noise_kernel(const int32_t* __restrict__ row_seg, const SegDev* __restrict__ seg, int M,
                                 int64_t rows, float* __restrict__ x) {
@@ -355,6 +515,7 @@ struct VoxCosy {
   // workspaces
   int64_t max_erows = 0, max_vrows = 0;
   int max_seg = 0;  // token rows of the longest request in the current call
+  bool attn_fp32 = getenv("VOX_COSY_ATTN_FP32") != nullptr;  // A/B: CUDA-core fp32 attention
   float *h = nullptr, *qkv = nullptr, *tmp = nullptr, *mu_t = nullptr, *x = nullptr, *v = nullptr, *z = nullptr;
   float *mel = nullptr, *va = nullptr, *vb = nullptr, *vt = nullptr, *spec = nullptr, *wf = nullptr, *pcm = nullptr;
   bf16 *xbf = nullptr, *col = nullptr;
@@ -619,7 +780,10 @@ int xf_layers(VoxCosy* m, std::vector<CdXf>& layers, float* h, int64_t rows, int
   for (auto& w : layers) {
     CLK(launch_codec_ln(h, nullptr, nullptr, w.ln1w, w.ln1b, m->xbf, d, g.eps, rows, st));
     CRET(gemm(m, w.tm_qkv, 3 * d, m->xbf, d, rows, m->qkv, 3 * d, nullptr, nullptr, 0));
-    CLK(cd_attn_kernel<<<dim3(nseg, heads), 256, cd_attn_smem(max_rows, hd), st>>>(m->qkv, seg, d, hd, inv, m->xbf));
+    if (hd == kTcHd && !m->attn_fp32)
+      CLK(cd_attn_tc_kernel<<<dim3(nseg, heads), 256, cd_attn_tc_smem(max_rows), st>>>(m->qkv, seg, d, inv, m->xbf));
+    else
+      CLK(cd_attn_kernel<<<dim3(nseg, heads), 256, cd_attn_smem(max_rows, hd), st>>>(m->qkv, seg, d, hd, inv, m->xbf));
     CRET(gemm(m, w.tm_o, d, m->xbf, d, rows, h, d, nullptr, h, d));
     CLK(launch_codec_ln(h, nullptr, nullptr, w.ln2w, w.ln2b, m->xbf, d, g.eps, rows, st));
     CRET(gemm(m, w.tm_fc1, ffn, m->xbf, d, rows, m->tmp, ffn, nullptr, nullptr, 0));
@@ -784,6 +948,9 @@ int vox_cosy_create(int device, const VoxCosyCfg* cfg, uint64_t seed, VoxCosy** 
     rc = cfail(m, VOX_ERR_CUDA, "event create");
   if (rc == VOX_OK && cudaFuncSetAttribute(cd_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            static_cast<int>(cd_attn_smem(kCdMaxRows, 64))) != cudaSuccess)
+    rc = cfail(m, VOX_ERR_CUDA, "attention smem attribute");
+  if (rc == VOX_OK && cudaFuncSetAttribute(cd_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(cd_attn_tc_smem(kCdMaxRows))) != cudaSuccess)
     rc = cfail(m, VOX_ERR_CUDA, "attention smem attribute");
   if (rc == VOX_OK) rc = create(m, seed);
   if (rc == VOX_OK && cudaStreamSynchronize(m->st) != cudaSuccess) rc = cfail(m, VOX_ERR_CUDA, "init sync");

@@ -305,6 +305,13 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     int64_t ld_act = 0, int* planes_out = nullptr,
                     const GemmArgs* nrm = nullptr) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
+  {
+    // the effective split count: every split gets ceil(n_kb / splits) k-blocks, so a
+    // requested count that leaves trailing splits empty launches (and leaves) fewer planes
+    const int n_kb = K / 64;
+    const int per = (n_kb + splits - 1) / splits;
+    splits = (n_kb + per - 1) / per;
+  }
   if (plan.mc && wp == nullptr) plan = gemm_plan_1cta(M, rows, K);  // mc streams packed tiles only
   if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
     plan.pair = 0;
@@ -1950,6 +1957,7 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   CK(dalloc(&dw, static_cast<size_t>(M) * K));
   CK(dalloc(&dx, static_cast<size_t>(N) * K));
   CK(dalloc(&dout, static_cast<size_t>(splits) * N * M));
+  CK(cudaMemset(dout, 0, static_cast<size_t>(splits) * N * M * 4));
   CK(cudaMemcpy(dw, w, static_cast<size_t>(M) * K * 2, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dx, x, static_cast<size_t>(N) * K * 2, cudaMemcpyHostToDevice));
   if (bias) {
