@@ -211,14 +211,8 @@ VOX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 VOX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
-// CTA-pair (cta_group::2) helpers: two CTAs of a 2-CTA cluster on one TPC
-// issue one UMMA with M = 256 (each CTA holds 128 rows of A and half of the
-// N columns of B in its own shared memory; the accumulator rows are split
-// across the two SMs' TMEM).  The leader (rank 0) issues the MMAs; TMA loads
-// of both CTAs complete on the leader's mbarrier (peer bit cleared).
+// Thread-block cluster helpers
 // ---------------------------------------------------------------------------
-constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the rank-0 CTA
-
 VOX_DEV uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -227,43 +221,6 @@ VOX_DEV uint32_t cluster_ctarank() {
 VOX_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
-}
-VOX_DEV void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
-                              uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::"
-      "cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar) & kPeerBitMask),
-      "l"(policy)
-      : "memory");
-}
-VOX_DEV void tmem_alloc_pair(uint32_t* dst_smem, uint32_t ncols) {
-  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                   smem_u32(dst_smem)),
-               "r"(ncols));
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-}
-VOX_DEV void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols) {
-  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
-}
-VOX_DEV void umma_bf16_pair(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t idesc,
-                            uint32_t accumulate) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(desc_a), "l"(desc_b), "r"(idesc), "r"(accumulate));
-}
-// arrive (once) on the mbarrier at this smem offset in both CTAs of the pair
-// when all previously issued cta_group::2 MMAs of this thread have completed
-VOX_DEV void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(static_cast<uint16_t>(3))
-      : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -373,7 +330,7 @@ struct TraceScope {
 #define VOX_TRACE(tag) TraceScope vox_trace_scope_(g_vox_trace, (tag))
 enum TraceTag : uint32_t {
   kTrGemm = 1, kTrGemmMc = 2, kTrAttn = 3, kTrAttnCombine = 4, kTrQkvRope = 5, kTrResidNorm = 6,
-  kTrEmbedNorm = 7, kTrSilu = 8, kTrSampler = 9, kTrDetok = 10, kTrPair = 11
+  kTrEmbedNorm = 7, kTrSilu = 8, kTrSampler = 9, kTrDetok = 10
 };
 
 }  // namespace vox

@@ -672,179 +672,6 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
-// CTA-pair GEMM (tcgen05.mma.cta_group::2, M = 256 per pair).
-//
-// A 2-CTA cluster computes a 256 x BNP output tile: rank r streams weight rows
-// [m0 + 128 r, +128) and activation rows [n0 + r BNP/2, +BNP/2) into its own
-// shared memory; the leader issues UMMA M=256 x N=BNP over both CTAs' tiles,
-// so every activation byte loaded from L2 feeds 256 weight rows and every
-// weight byte all BNP rows.  At decode batch sizes (~224 rows) this halves the
-// L2 -> SM traffic of the single-CTA 128 x 128 tiling, which is what bounds
-// it (the chip's L2 read throughput, ~12 TB/s, not HBM).  Weights come from
-// the packed tile layout through a plain 2-D tensor map (rows of 128 B, no
-// TMA swizzle: the tiles are pre-swizzled in HBM).
-// ---------------------------------------------------------------------------
-// DEEP: one CTA per SM with a ~192 KB ring (grids of <= 148 CTAs: the loads in
-// flight per SM, not the CTA count, set the streaming rate); otherwise ~96 KB
-// so two CTAs share an SM.
-template <int BNP, bool DEEP>
-struct PairCfg {
-  static constexpr int kABytes = 128 * 64 * 2;        // this CTA's 128 weight rows
-  static constexpr int kBBytes = (BNP / 2) * 64 * 2;  // this CTA's half of the rows
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBudget = DEEP ? 200 * 1024 : 96 * 1024;
-  static constexpr int kStages = kBudget / kStageBytes > 12 ? 12 : kBudget / kStageBytes;
-  static constexpr int kTmemCols = BNP < 32 ? 32 : BNP;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
-};
-
-template <int BNP, bool DEEP>
-__global__ void __launch_bounds__(128, 1)
-    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                     GemmArgs p) {
-  VOX_TRACE(kTrPair);
-  using C = PairCfg<BNP, DEEP>;
-  extern __shared__ uint8_t smem_raw[];
-  // align to 1024 B by pointer arithmetic on the __shared__ array (an
-  // integer round-trip would turn every smem access into a generic LD/ST)
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
-  uint64_t* empty = full + C::kStages;
-  uint64_t* done = empty + C::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const int rank = static_cast<int>(cluster_ctarank());
-  const int m0 = blockIdx.y * 256;                            // pair's weight rows
-  const int n0 = (blockIdx.x >> 1) * BNP;                     // pair's activation rows
-  const int mw = m0 + rank * 128;                             // this CTA's weight rows
-  const int nx = n0 + rank * (BNP / 2);                       // this CTA's activation rows
-  const int split = blockIdx.z;
-  const int kb0 = split * p.kb_per_split;
-  const int kb1 = min(p.n_kb, kb0 + p.kb_per_split);
-  const int nkb = kb1 - kb0;  // host guarantees >= 1
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmW);
-    tma_prefetch_desc(&tmX);
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    mbar_init(done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 2) tmem_alloc_pair(tmem_slot, C::kTmemCols);
-  tc_fence_before();
-  cluster_sync();  // peer barriers initialised before any TMA / commit targets them
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  griddep_launch();
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer (both CTAs; bytes land on the leader's barrier) -------------
-    const uint64_t pol_w = policy_evict_first();
-    const uint64_t pol_x = policy_evict_last();
-    const int wrow0 = (mw / 128) * p.n_kb * 128;  // packed tile rows of this CTA's weight tile
-    const int pre = nkb < C::kStages ? nkb : C::kStages;
-    for (int i = 0; i < pre; ++i) {
-      if (rank == 0) mbar_arrive_expect_tx(&full[i], 2 * C::kStageBytes);
-      tma_load_2d_pair(smem + i * C::kStageBytes, &tmW, &full[i], 0, wrow0 + (kb0 + i) * 128, pol_w);
-    }
-    griddep_wait();
-    for (int i = 0; i < pre; ++i)
-      tma_load_2d_pair(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], (kb0 + i) * 64, nx,
-                       pol_x);
-    for (int i = pre; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
-      uint8_t* st = smem + s * C::kStageBytes;
-      if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * C::kStageBytes);
-      tma_load_2d_pair(st, &tmW, &full[s], 0, wrow0 + (kb0 + i) * 128, pol_w);
-      tma_load_2d_pair(st + C::kABytes, &tmX, &full[s], (kb0 + i) * 64, nx, pol_x);
-    }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
-    // ---------------- MMA issuer (leader only): UMMA 256 x BNP x 16 ----------------
-    constexpr uint32_t idesc = make_idesc_bf16(256, BNP);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      mbar_wait(&full[s], (i / C::kStages) & 1);
-      tc_fence_after();
-      const uint32_t a_addr = smem_u32(smem + s * C::kStageBytes);
-      const uint32_t b_addr = a_addr + C::kABytes;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        umma_bf16_pair(tmem, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + k * 32), idesc,
-                       (i > 0 || k > 0) ? 1u : 0u);
-      umma_commit_pair(&empty[s]);  // frees stage s in both CTAs
-    }
-    umma_commit_pair(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: this CTA's 128 accumulator rows ----------------
-  griddep_wait();
-  mbar_wait(done, 0);
-  tc_fence_after();
-  float* outp = p.out + static_cast<int64_t>(split) * p.split_stride;
-  // staged through the idle pipeline smem: [32 rows n][128 m] then 16-byte stores
-  float* stg = reinterpret_cast<float*>(smem);
-  constexpr int kSt = 128 + 4;
-  const bool full_m = mw + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
-                      (p.resid == nullptr || (p.ldr & 3) == 0) &&
-                      (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
-#pragma unroll 1
-  for (int c = 0; c < BNP; c += 32) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
-    tmem_ld_wait();
-    const int ml = warp * 32 + lane;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
-    __syncthreads();
-#pragma unroll 2
-    for (int e = threadIdx.x; e < 32 * 32; e += 128) {
-      const int j = e >> 5, q = (e & 31) * 4;
-      const int n = n0 + c + j;
-      if (n < p.N) {
-        float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
-        const int m = mw + q;
-        if (full_m) {
-          if (p.bias != nullptr) {
-            const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
-            v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
-          }
-          if (p.resid != nullptr) {
-            const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
-            v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
-          }
-          *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
-        } else {
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            if (m + t < p.m_valid) {
-              float o = vv[t];
-              if (p.bias != nullptr) o += p.bias[m + t];
-              if (p.resid != nullptr) o += p.resid[static_cast<int64_t>(n) * p.ldr + m + t];
-              outp[static_cast<int64_t>(n) * p.ldo + m + t] = o;
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  tc_fence_before();
-  cluster_sync();  // both CTAs done with TMEM before the pair deallocates
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_pair(tmem, C::kTmemCols);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -1010,70 +837,7 @@ cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int b
   }
 }
 
-template <int BNP, bool DEEP>
-static cudaError_t launch_pair(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a,
-                               int splits, cudaStream_t st) {
-  using C = PairCfg<BNP, DEEP>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_pair_kernel<BNP, DEEP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * ((a.N + BNP - 1) / BNP), (a.M + 255) / 256, splits);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = C::kSmemBytes;
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = 2;
-  at[1].val.clusterDim.y = 1;
-  at[1].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 2;
-  if (getenv("VOX_PAIR_NOPDL")) {  // debug: cluster launch without the PDL edge
-    at[0] = at[1];
-    cfg.numAttrs = 1;
-  }
-  return cudaLaunchKernelEx(&cfg, gemm_pair_kernel<BNP, DEEP>, tw, tx, a);
-}
 
-cudaError_t gemm_launch_pair(const CUtensorMap& tw_packed, const CUtensorMap& tx_half, GemmArgs a,
-                             int splits, int bnp, cudaStream_t st) {
-  a.n_kb = a.K / 64;
-  a.kb_per_split = (a.n_kb + splits - 1) / splits;
-  splits = (a.n_kb + a.kb_per_split - 1) / a.kb_per_split;
-  const int ctas = 2 * ((a.N + bnp - 1) / bnp) * ((a.M + 255) / 256) * splits;
-  const bool deep = ctas <= kNumSMs;
-  switch (bnp) {
-    case 64: return deep ? launch_pair<64, true>(tw_packed, tx_half, a, splits, st)
-                         : launch_pair<64, false>(tw_packed, tx_half, a, splits, st);
-    case 128: return deep ? launch_pair<128, true>(tw_packed, tx_half, a, splits, st)
-                          : launch_pair<128, false>(tw_packed, tx_half, a, splits, st);
-    default: return deep ? launch_pair<256, true>(tw_packed, tx_half, a, splits, st)
-                         : launch_pair<256, false>(tw_packed, tx_half, a, splits, st);
-  }
-}
-
-bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K) {
-  // packed tiles as a [rows = roundup(M, 256) / 128 * (K / 64) * 128][64] bf16 matrix of
-  // 128-byte rows; a 128-row box is one 16 KB tile, copied without swizzle
-  if (!load_encode()) return false;
-  const uint64_t rows = static_cast<uint64_t>((M + 255) / 256 * 2) * static_cast<uint64_t>(K / 64) * 128;
-  cuuint64_t dims[2] = {64, rows};
-  cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {64, 128};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
 
 int gemm_bn_for_rows(int rows) {
   if (rows <= 16) return 16;
@@ -1093,33 +857,19 @@ GemmPlan gemm_plan_1cta(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
   g.red = 0;
-  g.pair = 0;
   g.mc = 0;
   g.cs = 1;
   g.bn = gemm_bn_for_rows(rows);
   if (g.bn > 128) g.bn = 128;
   if (rows >= 128 && M <= 4096) g.bn = 64;
   g.mt = 1;
-  // CTA pairs (256 x 256 tile per 2 SMs): opt-in (VOX_GEMM_PAIR=1) until they
-  // beat the single-CTA tiling (profiles/gemm_sweep_r01.txt: parity at 224 rows)
-  if (rows > 128 && getenv("VOX_GEMM_PAIR") && atoi(getenv("VOX_GEMM_PAIR")) == 1) {
-    g.pair = 1;
-    g.bn = 256;
-  }
   if (const char* e = getenv("VOX_GEMM_BN_TEST")) {  // microbenchmarks only
     const int f = atoi(e);
     if (f == 16 || f == 32 || f == 64 || f == 128 || f == 256) g.bn = f;
   }
   if (const char* e = getenv("VOX_GEMM_MT_TEST")) g.mt = atoi(e) == 2 ? 2 : 1;
-  if (g.pair && g.bn < 64) g.bn = 64;
-  int tiles, slots;
-  if (g.pair) {
-    tiles = 2 * ((M + 255) / 256) * ((rows + g.bn - 1) / g.bn);  // CTAs per split
-    slots = kNumSMs;
-  } else {
-    tiles = ((M + 128 * g.mt - 1) / (128 * g.mt)) * ((rows + g.bn - 1) / g.bn);
-    slots = (g.mt == 2 ? 1 : 2) * kNumSMs;
-  }
+  const int tiles = ((M + 128 * g.mt - 1) / (128 * g.mt)) * ((rows + g.bn - 1) / g.bn);
+  const int slots = (g.mt == 2 ? 1 : 2) * kNumSMs;
   int best = 1;
   for (int s = 1; s <= kGemmMaxSplits; ++s) {
     const int per = (n_kb + s - 1) / s;
@@ -1136,7 +886,6 @@ GemmPlan gemm_plan_1cta(int M, int rows, int K) {
 GemmPlan gemm_plan(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
-  g.pair = 0;
   g.mc = 0;
   g.cs = 1;
   // Decode-sized row counts: the cluster-multicast kernel (one n-tile covering

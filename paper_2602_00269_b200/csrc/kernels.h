@@ -76,7 +76,6 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t inner, uint64_t
 int gemm_bn_for_rows(int rows);
 constexpr int kGemmMaxSplits = 16;
 struct GemmPlan {
-  int pair;    // 1: CTA-pair kernel (cta_group::2, 256 weight rows x bn rows per 2 CTAs)
   int bn;      // activation rows per tile (UMMA N)
   int mt;      // 128-row weight sub-tiles per CTA (1 or 2)
   int splits;  // split-K factor (fp32 partial planes)
@@ -87,13 +86,9 @@ struct GemmPlan {
 // fp32 output planes a GEMM with this plan leaves for its consumer
 inline int gemm_out_planes(const GemmPlan& g) { return g.red ? 1 : g.splits; }
 GemmPlan gemm_plan(int M, int rows, int K);
-GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA / pair kernels only
+GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA kernel only
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, int mt, cudaStream_t st);
-// pair kernel: tw_packed from make_tmap_packed, tx_half = activation map with box bnp / 2
-cudaError_t gemm_launch_pair(const CUtensorMap& tw_packed, const CUtensorMap& tx_half, GemmArgs a,
-                             int splits, int bnp, cudaStream_t st);
-bool make_tmap_packed(CUtensorMap* map, const void* base, int64_t M, int64_t K);
 // cluster-multicast kernel: txs = activation map with box rows bn / cs
 cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
                            cudaStream_t st);
@@ -106,7 +101,7 @@ void launch_init_bf16(bf16* w, int64_t n, uint64_t key, float scale, cudaStream_
 void launch_init_bf16_packed(bf16* w, int64_t M, int64_t K, int64_t row0, uint64_t key,
                              float scale, cudaStream_t st, int64_t interleave_half = 0);
 void launch_pack_bf16(const bf16* src, bf16* dst, int64_t M, int64_t K, cudaStream_t st);
-// rows padded to 256 so CTA pairs (256 weight rows) never read past the buffer
+// rows padded to 256 (two 128-row tiles) so a tile never reads past the buffer
 inline int64_t packed_elems(int64_t M, int64_t K) { return (M + 255) / 256 * 256 * K; }
 void launch_l2_flush(const void* buf, size_t bytes, uint32_t* sink, cudaStream_t st);
 // fp32 variant: w[i] = offset + unit_pm1(mix64(key+i)) * scale rounded through bf16.

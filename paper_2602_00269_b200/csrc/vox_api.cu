@@ -139,10 +139,7 @@ struct VoxCtx {
   float* inv_freq = nullptr;
   float2* rope_tab = nullptr;  // [max_ctx][hd/2] (cos, sin)
   bf16* w_head_audio = nullptr;  // packed copy of the tied head's audio rows
-  // 2-D tensor maps over the packed tiles (CTA-pair GEMM)
-  std::vector<CUtensorMap> tp_qkv, tp_o, tp_gu, tp_down;
-  CUtensorMap tp_head{};
-  CUtensorMap tm_head_full{};
+  CUtensorMap tm_head_full{};  // full-vocab (parity) head over the logical embedding
   int head_audio_rows = 0;
 
   // ---- activations [max_rows, ...]
@@ -296,12 +293,11 @@ static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* 
 
 // GEMM over `rows` activation rows of buffer map set `xm`.
 // `wp` non-null: W is in the packed tile layout (init.cu) and `tw` is unused;
-// `twp` is the 2-D tensor map over the packed tiles (CTA-pair kernel).
 static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>& xm, int M,
                     int rows, int K, float* out, int64_t ldo, int splits, const float* bias,
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm", const bf16* wp = nullptr,
-                    const CUtensorMap* twp = nullptr, bf16* act_out = nullptr,
+                    bf16* act_out = nullptr,
                     int64_t ld_act = 0, int* planes_out = nullptr,
                     const GemmArgs* nrm = nullptr) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
@@ -313,10 +309,6 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
     splits = (n_kb + per - 1) / per;
   }
   if (plan.mc && wp == nullptr) plan = gemm_plan_1cta(M, rows, K);  // mc streams packed tiles only
-  if (plan.pair && twp == nullptr) {      // pair kernel streams packed tiles only
-    plan.pair = 0;
-    plan.bn = (rows >= 128 && M <= 4096) ? 64 : 128;
-  }
   const int bn = plan.bn;
   GemmArgs a{};
   a.M = M;
@@ -355,13 +347,12 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   if (planes_out) *planes_out = a.red ? 1 : splits;
   a.act = act_out;
   a.ld_act = ld_act;
-  if (a.epi == 1 && (splits != 1 || plan.pair || plan.mt != 1))
+  if (a.epi == 1 && (splits != 1 || plan.mt != 1))
     return fail(c, VOX_ERR_INVALID, "fused SiLU epilogue needs one split, 1-CTA tiles");
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
   cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn / plan.cs), a, splits, bn, plan.cs, st)
-                  : plan.pair ? gemm_launch_pair(*twp, xm.at(bn / 2), a, splits, bn, st)
                               : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
@@ -453,20 +444,6 @@ static int create_backbone(VoxCtx* c) {
     CK(cudaMemcpy(c->rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
   }
 
-  c->tp_qkv.resize(L);
-  c->tp_o.resize(L);
-  c->tp_gu.resize(L);
-  c->tp_down.resize(L);
-  for (int l = 0; l < L; ++l) {
-    if (!make_tmap_packed(&c->tp_qkv[l], c->w_qkv + l * n_qkv, c->nqkv, d) ||
-        !make_tmap_packed(&c->tp_o[l], c->w_o + l * n_o, d, H * hd) ||
-        !make_tmap_packed(&c->tp_gu[l], c->w_gu + l * n_gu, 2 * dff, d) ||
-        !make_tmap_packed(&c->tp_down[l], c->w_down + l * n_dn, d, dff))
-      return fail(c, VOX_ERR_CUDA, "tensor map (packed weights)");
-  }
-  if (g.audio_base >= 0 &&
-      !make_tmap_packed(&c->tp_head, c->w_head_audio, g.frame_tokens * g.codebook_size, d))
-    return fail(c, VOX_ERR_CUDA, "tensor map (packed audio head)");
   if (!make_tmap_bf16(&c->tm_head_full, c->emb, d, V, d * 2ull, 128))
     return fail(c, VOX_ERR_CUDA, "tensor map (lm head)");
   if (g.audio_base >= 0) {
@@ -767,7 +744,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   const CUtensorMap& tw_unused = c->tm_head_full;  // packed weights: the W map is not read
   for (int l = 0; l < L; ++l) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
-                 nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv, &c->tp_qkv[l]));
+                 nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv));
     if (!fused_rope) {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * pl_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws,
@@ -785,10 +762,10 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
                          c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st, fused_rope ? &ri : nullptr);
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
-                 st, "gemm", c->w_o + l * n_o, &c->tp_o[l]));
+                 st, "gemm", c->w_o + l * n_o));
     // the O projection's residual + RMSNorm folds into the gate|up GEMM's
     // prologue when every gate|up CTA is co-resident (its grid barrier needs it)
-    const bool gu_fused = sp_gu == 1 && !gu_plan.pair && !c->silu_unfused;
+    const bool gu_fused = sp_gu == 1 && !c->silu_unfused;
     const bool norm_in_gu = gu_fused && gu_norm_fusable;
     if (!norm_in_gu) {
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_o + 10));
@@ -811,18 +788,18 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
         nrm.nrm_bar = c->nrm_bar;
       }
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, 1, nullptr, nullptr,
-                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l], c->act, dff, nullptr,
+                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, c->act, dff, nullptr,
                    norm_in_gu ? &nrm : nullptr));
     } else {
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
-                   nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, &c->tp_gu[l]));
+                   nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu));
       const int pl_gu = gemm_out_planes(gu_plan);
       TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * pl_gu + 2));
       launch_silu_mul(c->d_rows, nrows, c->ws, pl_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
-                 d, st, "gemm", c->w_down + l * n_dn, &c->tp_down[l]));
+                 d, st, "gemm", c->w_down + l * n_dn));
     {
       const bool last = (l == L - 1);
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_dn + 10));
@@ -839,7 +816,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
     if (one_slot)  // packed 128-row tiles: slot k starts at tile k * codebook_size / 128
       wh += static_cast<int64_t>(hslot) * (g.codebook_size / 128) * (d / 64) * 8192;
     RET(run_gemm(c, c->tm_head_full, c->tm_xf, M, nsamp, d, c->logits, M, 1, nullptr, nullptr, 0,
-                 M, st, "lm_head", wh, (audio && !one_slot) ? &c->tp_head : nullptr));
+                 M, st, "lm_head", wh));
     SampFusedArgs a{};
     a.rows = c->d_rows;
     a.sample_rows = c->d_sample_rows;
@@ -1185,7 +1162,7 @@ int vox_project_ext(VoxCtx* c, VoxCtx* src, int32_t n) {
   const int M = c->cfg.d_model, K = c->cfg.ext_dim;
   // one split: the result lands as a single fp32 plane straight in ext[n][d]
   return run_gemm(c, tw_unused, xm, M, n, K, c->ext, M, 1, nullptr, nullptr, 0, M, c->s_lm, "gemm",
-                  c->w_proj, nullptr);
+                  c->w_proj);
 }
 
 int vox_link_tokens(VoxCtx* dst, VoxCtx* src, const int32_t* links, int32_t n, int32_t offset,
@@ -1980,7 +1957,6 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   // VOX_GEMM_PACKED_TEST=1: stream W from the packed tile layout (the decode path)
   bf16* wpk = nullptr;
   bf16* xpk = nullptr;
-  CUtensorMap tpk{};
   if (getenv("VOX_GEMM_XPACKED_TEST") && atoi(getenv("VOX_GEMM_XPACKED_TEST")) == 1) {
     CK(dalloc(&xpk, static_cast<size_t>(packed_elems(N, K))));
     launch_pack_bf16(dx, xpk, N, K, c->s_lm);
@@ -1991,7 +1967,6 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     CK(dalloc(&wpk, static_cast<size_t>(packed_elems(M, K))));
     launch_pack_bf16(dw, wpk, M, K, c->s_lm);
     CK(cudaStreamSynchronize(c->s_lm));
-    if (!make_tmap_packed(&tpk, wpk, M, K)) return fail(c, VOX_ERR_CUDA, "tensor map (packed test)");
   }
   unsigned long long* dbg = nullptr;
   const size_t dbg_n = 8ull * 4096;
@@ -2010,7 +1985,7 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
     launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
     CK(cudaEventRecord(a, c->s_lm));
     rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm, "gemm", wpk, wpk ? &tpk : nullptr, nullptr, 0, &planes);
+                  c->s_lm, "gemm", wpk, nullptr, 0, &planes);
     CK(cudaEventRecord(b, c->s_lm));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;

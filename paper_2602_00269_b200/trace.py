@@ -13,9 +13,9 @@ import collections
 import numpy as np
 
 NAMES = {1: "gemm1cta", 2: "gemm_mc", 3: "attn", 4: "attn_comb", 5: "qkv_rope", 6: "resid_norm",
-         7: "embed_norm", 8: "silu", 9: "sampler", 10: "detok", 11: "gemm_pair"}
+         7: "embed_norm", 8: "silu", 9: "sampler", 10: "detok"}
 # kernel -> class of the eager per-class CUDA-event timing (vox_timing_read)
-CLASS = {"gemm1cta": "gemm", "gemm_mc": "gemm", "gemm_pair": "gemm", "attn": "attn", "attn_comb": "attn",
+CLASS = {"gemm1cta": "gemm", "gemm_mc": "gemm", "attn": "attn", "attn_comb": "attn",
          "qkv_rope": "qkv_rope", "resid_norm": "norm", "embed_norm": "norm", "silu": "silu",
          "sampler": "sampler", "detok": "detok"}
 
