@@ -330,7 +330,7 @@ struct TraceScope {
 #define VOX_TRACE(tag) TraceScope vox_trace_scope_(g_vox_trace, (tag))
 enum TraceTag : uint32_t {
   kTrGemm = 1, kTrGemmMc = 2, kTrAttn = 3, kTrAttnCombine = 4, kTrQkvRope = 5, kTrResidNorm = 6,
-  kTrEmbedNorm = 7, kTrSilu = 8, kTrSampler = 9, kTrDetok = 10
+  kTrEmbedNorm = 7, kTrSilu = 8, kTrSampler = 9, kTrDetok = 10, kTrChain = 11
 };
 
 }  // namespace vox

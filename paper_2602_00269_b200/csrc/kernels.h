@@ -160,6 +160,56 @@ void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
 void launch_silu_mul(const RowDev* rows, int n, const float* ws, int splits, int64_t split_stride,
                      const LmDims& dm, bf16* a_out, cudaStream_t st);
 
+// ---------------------------------------------------------------- layer chain (K6)
+// One persistent launch per decoder layer runs a list of jobs (layer_chain.cu).
+enum ChainKind { kChGemm = 0, kChNorm = 1, kChRope = 2 };
+constexpr int kChainMaxJobs = 8;
+constexpr int kChainCtrStride = 32;  // one counter per 128-byte line
+constexpr int kChainCtrInts = (2 * kChainMaxJobs + 1) * kChainCtrStride;  // claim[8], done[8], exit
+struct ChainJob {
+  int kind;
+  int dep;  // job whose outputs this job reads; -1 = the preceding kernel (griddep_wait)
+  // GEMM (packed weight tiles, activations via tensor map `xmap`: 0 x, 1 attn, 2 act)
+  const bf16* w;
+  int xmap, m_tiles, n_kb, splits, kb_per_split;
+  int epi;                 // 0: fp32 split planes, 1: act = bf16(SiLU(gate) * up)
+  float* out;
+  int64_t ldo, split_stride;
+  int m_valid;
+  bf16* act;
+  int64_t ld_act;
+  // NORM (split planes + residual -> h; bf16 RMSNorm rows -> x[out_index[r] or r])
+  // and ROPE (q|k|v planes (+ bias) -> RoPE -> q, K/V page append)
+  const float* ws;
+  int nsplits;
+  int64_t ss;
+  float* h;
+  const float* nw;
+  bf16* x;
+  const int* out_index;
+  const float* bias;
+  const int* page_table;
+  bf16* kc;
+  bf16* vc;
+  bf16* q;
+};
+struct ChainArgs {
+  ChainJob job[kChainMaxJobs];
+  int njobs;
+  const RowDev* rows;
+  int nrows;
+  LmDims dm;
+  const float2* rope;
+  int* ctr;  // kChainCtrInts zeroed ints (self-resetting)
+  int k_rotate;
+  int l2_ahead;  // k-blocks of the W unit pulled into L2 while stalled at a job boundary
+  int wst, xst;  // weight / activation ring depths (chain_stages)
+};
+void chain_stages(int bn, int* wst, int* xst);
+bool chain_supported_bn(int bn);
+cudaError_t launch_layer_chain(const CUtensorMap& mx, const CUtensorMap& mattn, const CUtensorMap& mact,
+                               const ChainArgs& a, int bn, cudaStream_t st);
+
 // ---------------------------------------------------------------- sampler (K1)
 struct SampRowDesc {
   int64_t logit_off;  // element offset of this row's column 0

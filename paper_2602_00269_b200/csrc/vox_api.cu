@@ -170,6 +170,14 @@ struct VoxCtx {
   RowDev* d_rows = nullptr;
   int* attn_sched = nullptr;  // persistent attention work counters (self-resetting)
   int* nrm_bar = nullptr;     // grid barrier of the GEMMs' fused norm prologue
+  int* chain_ctr = nullptr;   // layer-chain job counters: [n_layers + 1][kChainCtrInts]
+  // VOX_CHAIN=1: decode steps of <= 256 rows run each layer's projections + norms +
+  // RoPE as ONE persistent layer-chain launch (layer_chain.cu).  Opt-in: bit-identical
+  // to the per-kernel path but measured slower at the serving shape (224 rows: 136 vs
+  // ~78 us per layer; profiles/chain_timeline_r02.txt) -- the activation k-blocks
+  // (28 KB from L2, ~1.7 us under load) need the ring depth the per-kernel GEMM gives
+  // them, and the in-kernel norm / RoPE phases are latency chains as long as kernels
+  bool chain_on = getenv("VOX_CHAIN") && atoi(getenv("VOX_CHAIN")) == 1;
   // opt-in (VOX_FUSE_NORM=1): measured slower (750 -> 727 audio-s/s): 128 CTAs
   // normalising ~2 rows each serially + a grid barrier take longer than the
   // 224-CTA resid_norm launch whose boundary PDL already overlaps
@@ -540,6 +548,8 @@ static int create_buffers(VoxCtx* c) {
   }
   CK(dalloc(&c->nrm_bar, 2));
   CK(cudaMemset(c->nrm_bar, 0, 2 * sizeof(int)));
+  CK(dalloc(&c->chain_ctr, static_cast<size_t>(g.n_layers + 1) * kChainCtrInts));
+  CK(cudaMemset(c->chain_ctr, 0, static_cast<size_t>(g.n_layers + 1) * kChainCtrInts * sizeof(int)));
   CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
   CK(dalloc(&c->d_out_index, static_cast<size_t>(R)));
   CK(dalloc(&c->d_tokens, static_cast<size_t>(R)));
@@ -708,6 +718,128 @@ static int create_detok(VoxCtx* c) {
 }
 
 // ---------------------------------------------------------------------------
+// the decoder layers as persistent layer-chain launches (layer_chain.cu):
+//   chain(-1) = [QKV_0, RoPE_0]; per layer l: attention_l, then
+//   chain(l)  = [O_l, norm, gate|up_l (+SiLU), down_l, norm, QKV_l+1, RoPE_l+1]
+// (the last layer's second norm is the final norm into xf).  Split-K factors
+// and k-block rotation are the per-kernel path's, so the fp32 planes, h, x and
+// the KV pages are bit-identical to it.
+// ---------------------------------------------------------------------------
+static int chain_bn_for_rows(int rows) {
+  for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
+    if (rows <= b) return b;
+  return -1;
+}
+
+static int enqueue_layers_chain(VoxCtx* c, int nrows, int bn, cudaStream_t st) {
+  const VoxModelCfg& g = c->cfg;
+  const LmDims& dm = c->dm;
+  const int L = g.n_layers, d = g.d_model, dff = g.d_ff, Hhd = g.n_heads * g.head_dim;
+  const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
+  const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
+  const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
+  const int sp_qkv = gemm_plan(c->nqkv, nrows, d).splits, sp_o = gemm_plan(d, nrows, Hhd).splits;
+  const int sp_dn = gemm_plan(d, nrows, dff).splits;
+  auto gemm_job = [&](const bf16* w, int xmap, int M, int K, int splits, int dep, int epi) {
+    ChainJob j{};
+    j.kind = kChGemm;
+    j.dep = dep;
+    j.w = w;
+    j.xmap = xmap;
+    j.m_tiles = (M + 127) / 128;
+    j.n_kb = K / 64;
+    const int per = (j.n_kb + splits - 1) / splits;  // every split non-empty (as run_gemm)
+    j.splits = (j.n_kb + per - 1) / per;
+    j.kb_per_split = per;
+    j.epi = epi;
+    j.out = c->ws;
+    j.ldo = M;
+    j.split_stride = static_cast<int64_t>(nrows) * M;
+    j.m_valid = M;
+    j.act = c->act;
+    j.ld_act = dff;
+    return j;
+  };
+  auto planes = [](const ChainJob& j) { return j.splits; };
+  auto norm_job = [&](int dep, int nspl, const float* nw, bf16* x, const int* oi) {
+    ChainJob j{};
+    j.kind = kChNorm;
+    j.dep = dep;
+    j.ws = c->ws;
+    j.nsplits = nspl;
+    j.ss = static_cast<int64_t>(nrows) * d;
+    j.h = c->h;
+    j.nw = nw;
+    j.x = x;
+    j.out_index = oi;
+    return j;
+  };
+  auto rope_job = [&](int dep, int nspl, int l) {
+    ChainJob j{};
+    j.kind = kChRope;
+    j.dep = dep;
+    j.ws = c->ws;
+    j.nsplits = nspl;
+    j.ss = static_cast<int64_t>(nrows) * c->nqkv;
+    j.bias = c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr;
+    j.page_table = c->page_table;
+    j.kc = c->kc + l * kv_layer;
+    j.vc = c->vc + l * kv_layer;
+    j.q = c->q;
+    return j;
+  };
+  ChainArgs a{};
+  a.rows = c->d_rows;
+  a.nrows = nrows;
+  a.dm = dm;
+  a.rope = c->rope_tab;
+  a.k_rotate = c->gemm_k_rotate;
+  static const int l2a = getenv("VOX_CHAIN_L2") ? atoi(getenv("VOX_CHAIN_L2")) : 0;
+  a.l2_ahead = l2a;
+  chain_stages(bn, &a.wst, &a.xst);
+  const CUtensorMap &mx = c->tm_x.at(bn), &ma = c->tm_attn.at(bn), &mf = c->tm_act.at(bn);
+  const double act_b = static_cast<double>(nrows) * 2;
+  auto launch = [&](int slot, double bytes) -> int {
+    a.ctr = c->chain_ctr + static_cast<int64_t>(slot) * kChainCtrInts;
+    TimedLaunch tl(c, st, "chain", bytes);
+    cudaError_t e = launch_layer_chain(mx, ma, mf, a, bn, st);
+    if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("layer chain: ") + cudaGetErrorString(e));
+    return VOX_OK;
+  };
+  const double w_qkv = 2.0 * c->nqkv * d, w_o = 2.0 * d * Hhd, w_gu = 4.0 * dff * d, w_dn = 2.0 * d * dff;
+  // chain(-1): layer 0's q|k|v projection + RoPE/KV append
+  a.job[0] = gemm_job(c->w_qkv, 0, c->nqkv, d, sp_qkv, -1, 0);
+  a.job[1] = rope_job(0, planes(a.job[0]), 0);
+  a.njobs = 2;
+  RET(launch(L, w_qkv + act_b * d + act_b * 2 * c->nqkv));
+  for (int l = 0; l < L; ++l) {
+    {
+      const int asp = attn_pick_splits(nrows, g.n_kv_heads, g.max_ctx);
+      TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
+      launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
+                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st, nullptr);
+    }
+    const bool last = (l == L - 1);
+    a.job[0] = gemm_job(c->w_o + l * n_o, 1, d, Hhd, sp_o, -1, 0);
+    a.job[1] = norm_job(0, planes(a.job[0]), c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr);
+    a.job[2] = gemm_job(c->w_gu + l * n_gu, 0, 2 * dff, d, 1, 1, 1);
+    a.job[3] = gemm_job(c->w_down + l * n_dn, 2, d, dff, sp_dn, 2, 0);
+    a.job[4] = norm_job(3, planes(a.job[3]), last ? c->norm_final : c->norm_attn + static_cast<int64_t>(l + 1) * d,
+                        last ? c->xf : c->x, last ? c->d_out_index : nullptr);
+    a.njobs = 5;
+    double bytes = w_o + w_gu + w_dn + act_b * (Hhd + d + dff) + act_b * 2 * (d + dff + d);
+    if (!last) {
+      a.job[5] = gemm_job(c->w_qkv + (l + 1) * n_qkv, 0, c->nqkv, d, sp_qkv, 4, 0);
+      a.job[6] = rope_job(5, planes(a.job[5]), l + 1);
+      a.njobs = 7;
+      bytes += w_qkv + act_b * d + act_b * 2 * c->nqkv;
+    }
+    RET(launch(l, bytes));
+  }
+  return VOX_OK;
+}
+
+// ---------------------------------------------------------------------------
 // the decode step (eager or captured)
 // ---------------------------------------------------------------------------
 // hslot >= 0: every sampled row is at the same frame slot, so the LM head runs
@@ -742,7 +874,9 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
   const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
   const CUtensorMap& tw_unused = c->tm_head_full;  // packed weights: the W map is not read
-  for (int l = 0; l < L; ++l) {
+  const int cbn = c->chain_on ? chain_bn_for_rows(nrows) : -1;
+  if (cbn > 0) RET(enqueue_layers_chain(c, nrows, cbn, st));
+  for (int l = 0; l < L && cbn < 0; ++l) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
                  nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv));
     if (!fused_rope) {
@@ -961,7 +1095,7 @@ void vox_destroy(VoxCtx* c) {
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
-                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links, c->nrm_bar};
+                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links, c->nrm_bar, c->chain_ctr};
   if (c->ev_xfer) cudaEventDestroy(c->ev_xfer);
   for (auto& e : c->ev_links)
     if (e) cudaEventDestroy(e);
@@ -1864,6 +1998,7 @@ int vox_timing_read(VoxCtx* c, const char* name, double* total_ms, int64_t* laun
 }  // extern "C" (trace setters below are C++ symbols of the kernel TUs)
 namespace vox {
 void trace_set_attn(unsigned long long*);
+void trace_set_chain(unsigned long long*);
 void trace_set_detok_fused(unsigned long long*);
 void trace_set_detok(unsigned long long*);
 void trace_set_gemm(unsigned long long*);
@@ -1872,6 +2007,7 @@ void trace_set_sampler(unsigned long long*);
 }  // namespace vox
 static void trace_set_all(unsigned long long* b) {
   vox::trace_set_attn(b);
+  vox::trace_set_chain(b);
   vox::trace_set_detok_fused(b);
   vox::trace_set_detok(b);
   vox::trace_set_gemm(b);

@@ -13,9 +13,9 @@ import collections
 import numpy as np
 
 NAMES = {1: "gemm1cta", 2: "gemm_mc", 3: "attn", 4: "attn_comb", 5: "qkv_rope", 6: "resid_norm",
-         7: "embed_norm", 8: "silu", 9: "sampler", 10: "detok"}
+         7: "embed_norm", 8: "silu", 9: "sampler", 10: "detok", 11: "chain"}
 # kernel -> class of the eager per-class CUDA-event timing (vox_timing_read)
-CLASS = {"gemm1cta": "gemm", "gemm_mc": "gemm", "attn": "attn", "attn_comb": "attn",
+CLASS = {"chain": "chain", "gemm1cta": "gemm", "gemm_mc": "gemm", "attn": "attn", "attn_comb": "attn",
          "qkv_rope": "qkv_rope", "resid_norm": "norm", "embed_norm": "norm", "silu": "silu",
          "sampler": "sampler", "detok": "detok"}
 
@@ -23,7 +23,7 @@ CLASS = {"gemm1cta": "gemm", "gemm_mc": "gemm", "attn": "attn", "attn_comb": "at
 def launches(rec: np.ndarray) -> list[dict]:
     """Group per-CTA records into launches: a maximal run (by start time) of one tag,
     at most the launch's CTA count long."""
-    rec = np.sort(rec, order="t0")
+    rec = np.sort(rec[(rec["tag"] & 255) < 32], order="t0")  # >= 32: layer-chain event marks
     out: list[dict] = []
     open_: dict[int, dict] = {}
     for r in rec:
