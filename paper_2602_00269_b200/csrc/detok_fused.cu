@@ -34,14 +34,22 @@ struct ReqHdrF {
   int32_t n_req, n_lat;
 };
 
-VOX_DEV int find_req_f(const DetokReq* reqs, int n_req, int lat_row) {
-  int lo = 0, hi = n_req - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (reqs[mid].lat_off <= lat_row) lo = mid; else hi = mid - 1;
+// warp-cooperative lookup (lat_row uniform across the warp): the last request
+// whose lat_off <= lat_row, one coalesced round of loads per 32 requests
+// instead of log2(n_req) dependent loads
+VOX_DEV int find_req_w(const DetokReq* reqs, int n_req, int lat_row) {
+  const int lane = threadIdx.x & 31;
+  int best = 0;
+  for (int base = 0; base < n_req; base += 32) {
+    const int i = base + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, i < n_req && reqs[i].lat_off <= lat_row);
+    if (m == 0) break;
+    best = base + 31 - __clz(m);
+    if (m != 0xffffffffu) break;
   }
-  return lo;
+  return best;
 }
+
 
 VOX_DEV float snake_f(float x, float a) {
   const float s = snake_sin(__fmul_rn(a, x));
@@ -69,10 +77,10 @@ VOX_DEV uint32_t swz_off(int r, int k, int rows) {
 }  // namespace
 
 constexpr int kRuRows = 128;  // rows per tile (UMMA M)
-// threads: 4 warps per 32 columns of the tile (C = 128 runs 1 CTA per SM, so
-// it gets 16 warps to hide the Snake / dwconv latency chains)
+// threads: 8 threads per channel (C = 128 runs 1 CTA per SM, so it gets 32
+// warps to hide the Snake / dwconv latency chains)
 template <int C>
-__host__ __device__ constexpr int ru_threads() { return C == 64 ? 256 : 512; }
+__host__ __device__ constexpr int ru_threads() { return C == 64 ? 512 : 1024; }
 
 template <int C>
 struct RuSmem {
@@ -107,7 +115,8 @@ __global__ void __launch_bounds__(ru_threads<C>())
   uint8_t* sa = smem + L::kAOff;
   uint8_t* sb = smem + L::kBOff;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* xbar = bar + 1;  // bulk copy of the x tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int r0 = blockIdx.x * kRuRows;
@@ -120,57 +129,63 @@ __global__ void __launch_bounds__(ru_threads<C>())
   }
   if (tid == 0) {
     mbar_init(bar, 1);
+    mbar_init(xbar, 1);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc(tmem_slot, C);
+  __syncthreads();  // barriers initialised before thread 0 arms xbar
   griddep_wait();
   griddep_launch();
   const int n_rows = hdr->n_lat * up;
   const bool active = r0 < n_rows;
 
   // ---------------- 1. y1 = Snake(x) for the tile + causal halo ----------------
+  // The tile's x rows (and, for a request's first tile, the cached Snake'd
+  // left context) arrive by 1-D bulk copies into y1s -- one transfer instead of
+  // ~12 rounds of dependent per-thread loads -- then Snake runs in place.
   const int H = 6 * dil;
+  constexpr int kRowStep = kRuThreads / C;      // rows between a thread's elements
+  constexpr int kResRows = kRuRows / kRowStep;  // epilogue rows per thread
   int t0 = 0, n = 0;
   const float* hin = nullptr;
   float* hout = nullptr;
+  float xres[kResRows];  // residual x of the rows this thread stores in the epilogue
   if (active) {
-    const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+    const DetokReq q = reqs[find_req_w(reqs, hdr->n_req, r0 / up)];
     t0 = r0 - q.lat_off * up;  // local row of the tile's first row
     n = 4 * q.nf * up;         // rows of this request at this level
     hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
     hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
     const int nr = kRuRows + H;
-    // each thread owns one channel (kRuThreads % C == 0): per-channel constants
-    // once, rows strided by kRuThreads / C, 4 independent loads in flight
-    constexpr int kRowStep = kRuThreads / C;
+    const int i_first = t0 >= H ? 0 : H - t0;  // halo rows [0, i_first) come from the context
+    if (tid == 0) {
+      const uint32_t bx = static_cast<uint32_t>((nr - i_first) * C * 4);
+      const uint32_t bh = static_cast<uint32_t>(i_first * C * 4);
+      mbar_arrive_expect_tx(xbar, bx + bh);
+      const uint64_t pol = policy_evict_first();
+      bulk_load(y1s + i_first * C, x + static_cast<int64_t>(r0 - H + i_first) * C, bx, xbar, pol);
+      if (bh) bulk_load(y1s, hin + static_cast<int64_t>(t0) * C, bh, xbar, pol);
+    }
+    mbar_wait(xbar, 0);
     const int ch = tid % C;
+#pragma unroll
+    for (int k = 0; k < kResRows; ++k) xres[k] = y1s[(H + tid / C + k * kRowStep) * C + ch];
+    __syncthreads();  // every residual read before Snake overwrites in place
     const float a1 = alpha1[ch], inv1 = snake_inv(a1);
-    // 4 rows per round: all loads first (independent), then the Snakes
-    for (int i0 = tid / C; i0 < nr; i0 += 4 * kRowStep) {
-      float xv[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * kRowStep;
-        const int t = t0 - H + i;
-        xv[u] = 0.f;
-        if (i < nr) xv[u] = t >= 0 ? x[static_cast<int64_t>(r0 - H + i) * C + ch] : hin[(H + t) * C + ch];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int i = i0 + u * kRowStep;
-        const int t = t0 - H + i;
-        if (i < nr) {
-          const float v = t >= 0 ? snake_r(xv[u], a1, inv1) : xv[u];
-          if (t >= 0 && i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
-          y1s[i * C + ch] = v;
-        }
-      }
+#pragma unroll 4
+    for (int i = i_first + tid / C; i < nr; i += kRowStep) {
+      const float v = snake_r(y1s[i * C + ch], a1, inv1);
+      const int t = t0 - H + i;
+      if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;  // new left context
+      y1s[i * C + ch] = v;
     }
     // short requests (n < H): shift the old context
     for (int e = tid; e < kRuRows * C; e += kRuThreads) {
-      const int i = e / C, ch = e % C, t = t0 + i;
-      for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
+      const int i = e / C, c2 = e % C, t = t0 + i;
+      for (int hh = t; hh < H - n; hh += n) hout[hh * C + c2] = hin[(hh + n) * C + c2];
     }
+  } else {
+    __syncthreads();
   }
   __syncthreads();
 
@@ -226,7 +241,7 @@ __global__ void __launch_bounds__(ru_threads<C>())
     float* stg = y1s;  // y1 is dead now
     const int quarter = warp & 3, part = warp >> 2;  // 32 columns per part
     const int row = quarter * 32 + lane;
-    {
+    if (part * 32 < C) {  // warp-uniform: C / 32 parts x 4 lane quarters
       const int col = part * 32;
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + col, r);
@@ -239,13 +254,12 @@ __global__ void __launch_bounds__(ru_threads<C>())
   __syncthreads();
   if (active) {
     const float* stg = y1s;
-    constexpr int kRowStep = kRuThreads / C;
     const int ch = tid % C;
     const float pb = pw_b[ch];
-#pragma unroll 4
-    for (int i = tid / C; i < kRuRows; i += kRowStep) {
-      const int64_t gi = static_cast<int64_t>(r0 + i) * C + ch;
-      y[gi] = (stg[i * (C + 1) + ch] + pb) + x[gi];
+#pragma unroll
+    for (int k = 0; k < kResRows; ++k) {
+      const int i = tid / C + k * kRowStep;
+      y[static_cast<int64_t>(r0 + i) * C + ch] = (stg[i * (C + 1) + ch] + pb) + xres[k];
     }
   }
   if (warp == 0) {
@@ -293,40 +307,66 @@ void launch_ru_fused(const DetokReq* reqs, int rows, int up, const float* x, flo
 constexpr int kOutRows = 128;
 
 template <int C>
+struct OutSmem {
+  static constexpr int kS = (kOutRows + 6) * (C + 1);  // Snake'd rows, padded (conflict-free taps)
+  static constexpr int kW = C * 7;
+  static constexpr int kX = (kOutRows + 6) * C;        // raw x rows (bulk copy target)
+  static constexpr int kXOff = (kS + kW + 3) / 4 * 4;  // 16-byte aligned
+  static constexpr int kBytes = (kXOff + kX) * 4 + 16;
+};
+
+template <int C>
 __global__ void __launch_bounds__(kOutRows)
     detok_out_tiled_kernel(const ReqHdrF* hdr, const DetokReq* __restrict__ reqs, int up,
                            const float* __restrict__ x, const float* __restrict__ alpha,
                            const float* __restrict__ w, float b, float* __restrict__ state,
                            int64_t st_off, DetokDims dd, float* __restrict__ pcm) {
   VOX_TRACE(kTrDetok);
-  __shared__ float s[(kOutRows + 6) * (C + 1)];
-  __shared__ float ws[C * 7];
+  using L = OutSmem<C>;
+  extern __shared__ __align__(16) float osm[];
+  float* s = osm;
+  float* ws = osm + L::kS;
+  float* xs = osm + L::kXOff;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xs + L::kX);
   const int tid = threadIdx.x;
   for (int e = tid; e < C * 7; e += kOutRows) ws[e] = w[e];
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
   griddep_wait();
   griddep_launch();
   const int r0 = blockIdx.x * kOutRows;
   if (r0 >= hdr->n_lat * up) return;
-  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const DetokReq q = reqs[find_req_w(reqs, hdr->n_req, r0 / up)];
   const int t0 = r0 - q.lat_off * up;
   const int n = 4 * q.nf * up;
   constexpr int H = 6;
   const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
   float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
+  // the tile's x rows (+ halo rows inside the request) in one bulk copy; halo
+  // rows before the request start come from the cached (Snake'd) context
+  const int i_first = t0 >= H ? 0 : H - t0;
+  if (tid == 0) {
+    const uint32_t bx = static_cast<uint32_t>((kOutRows + H - i_first) * C * 4);
+    mbar_arrive_expect_tx(bar, bx);
+    bulk_load(xs + i_first * C, x + static_cast<int64_t>(r0 - H + i_first) * C, bx, bar, policy_evict_first());
+  }
   const int chx = tid % C;
   const float ax = alpha[chx], ix = snake_inv(ax);
+  for (int e = tid; e < i_first * C; e += kOutRows) {
+    const int i = e / C;
+    s[i * (C + 1) + chx] = hin[(t0 + i) * C + chx];
+  }
+  mbar_wait(bar, 0);
 #pragma unroll 4
-  for (int e = tid; e < (kOutRows + H) * C; e += kOutRows) {
-    const int i = e / C, ch = chx;  // kOutRows % C == 0: fixed channel per thread
+  for (int e = i_first * C + tid; e < (kOutRows + H) * C; e += kOutRows) {
+    const int i = e / C;  // kOutRows % C == 0: fixed channel per thread
     const int t = t0 - H + i;
-    float v;
-    if (t >= 0) {
-      v = snake_r(x[static_cast<int64_t>(r0 - H + i) * C + ch], ax, ix);
-      if (i >= H && t >= n - H) hout[(t - (n - H)) * C + ch] = v;
-    } else {
-      v = hin[(H + t) * C + ch];
-    }
-    s[i * (C + 1) + ch] = v;
+    const float v = snake_r(xs[e], ax, ix);
+    if (i >= H && t >= n - H) hout[(t - (n - H)) * C + chx] = v;
+    s[i * (C + 1) + chx] = v;
   }
   for (int e = tid; e < kOutRows * C; e += kOutRows) {
     const int i = e / C, ch = e % C, t = t0 + i;
@@ -351,9 +391,16 @@ void launch_detok_out_tiled(const DetokReq* reqs, int rows, int up, const float*
                             const float* alpha, const float* w, float b, float* state,
                             int64_t st_off, const DetokDims& dd, float* pcm, cudaStream_t st) {
   const ReqHdrF* hdr = reinterpret_cast<const ReqHdrF*>(reqs) - 1;
-  if (C == 64)
-    launch_k(detok_out_tiled_kernel<64>, dim3((rows + kOutRows - 1) / kOutRows), dim3(kOutRows), 0,
-             st, hdr, reqs, up, x, alpha, w, b, state, st_off, dd, pcm);
+  if (C == 64) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(detok_out_tiled_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           OutSmem<64>::kBytes);
+      attr = true;
+    }
+    launch_k(detok_out_tiled_kernel<64>, dim3((rows + kOutRows - 1) / kOutRows), dim3(kOutRows),
+             OutSmem<64>::kBytes, st, hdr, reqs, up, x, alpha, w, b, state, st_off, dd, pcm);
+  }
 }
 
 bool detok_out_tiled_supported(int C, int up) { return C == 64 && (4 * up) % kOutRows == 0; }
@@ -383,7 +430,7 @@ __global__ void __launch_bounds__(256)
   griddep_launch();
   const int r0 = blockIdx.x * R;
   if (r0 >= hdr->n_lat * up) return;
-  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const DetokReq q = reqs[find_req_w(reqs, hdr->n_req, r0 / up)];
   const int t0 = r0 - q.lat_off * up;
   const int n = 4 * q.nf * up;
   const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
@@ -395,19 +442,33 @@ __global__ void __launch_bounds__(256)
     if (ch < C)
       prev[k] = t0 > 0 ? snake_r(x[static_cast<int64_t>(r0 - 1) * C + ch], a[k], inv[k]) : hin[ch];
   }
-  for (int i = 0; i < R; ++i) {
-    const int r = r0 + i;
-    const float* xr = x + static_cast<int64_t>(r) * C;
-    bf16* o = out + static_cast<int64_t>(r) * 2 * C;
+  constexpr int kMaxR = 16;
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-      const int ch = tid + k * blockDim.x;
-      if (ch < C) {
-        const float cur = snake_r(xr[ch], a[k], inv[k]);
-        o[ch] = __float2bfloat16_rn(cur);
-        o[C + ch] = __float2bfloat16_rn(prev[k]);
-        if (t0 + i == n - 1) hout[ch] = cur;
-        prev[k] = cur;
+  for (int i0 = 0; i0 < kMaxR; i0 += 8) {
+    if (i0 >= R) break;
+    float xv[8][CPT];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int ch = tid + k * blockDim.x;
+        xv[i][k] = (i0 + i < R && ch < C) ? x[static_cast<int64_t>(r0 + i0 + i) * C + ch] : 0.f;
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i0 + i >= R) break;
+      const int r = r0 + i0 + i;
+      bf16* o = out + static_cast<int64_t>(r) * 2 * C;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int ch = tid + k * blockDim.x;
+        if (ch < C) {
+          const float cur = snake_r(xv[i][k], a[k], inv[k]);
+          o[ch] = __float2bfloat16_rn(cur);
+          o[C + ch] = __float2bfloat16_rn(prev[k]);
+          if (t0 + i0 + i == n - 1) hout[ch] = cur;
+          prev[k] = cur;
+        }
       }
     }
   }
@@ -447,23 +508,23 @@ __global__ void __launch_bounds__(256)
   griddep_launch();
   const int r0 = blockIdx.x * TR;
   if (r0 >= hdr->n_lat * up) return;
-  const DetokReq q = reqs[find_req_f(reqs, hdr->n_req, r0 / up)];
+  const DetokReq q = reqs[find_req_w(reqs, hdr->n_req, r0 / up)];
   const int t0 = r0 - q.lat_off * up;
   const int n = 4 * q.nf * up;
   const int H = 6 * dil;
   const float* hin = slot_state_f(state, dd, q.slot, q.parity) + st_off;
   float* hout = slot_state_f(state, dd, q.slot, q.parity ^ 1) + st_off;
   const int nr = TR + H;
-  for (int i0 = tid / kPrepCh; i0 < nr; i0 += 4 * rstep) {
-    float xv[4];
+  for (int i0 = tid / kPrepCh; i0 < nr; i0 += 8 * rstep) {
+    float xv[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * rstep, t = t0 - H + i;
       xv[u] = 0.f;
       if (i < nr) xv[u] = t >= 0 ? x[static_cast<int64_t>(r0 - H + i) * C + ch] : hin[(H + t) * C + ch];
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * rstep, t = t0 - H + i;
       if (i < nr) {
         const float v = t >= 0 ? snake_r(xv[u], a1, i1) : xv[u];
