@@ -208,7 +208,10 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  griddep_launch();  // let the next kernel start its own prologue
+  // Dependents launch only after this grid passed its own griddep_wait (the
+  // producer's, below): every kernel of the step follows wait-then-launch, so a
+  // kernel may read data written two or more launches upstream BEFORE its own
+  // griddep_wait (resid_norm prefetches h that way).
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
     const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(128, 1)
     };
     for (int i = pre; i < pre + p.l2_prefetch; ++i) pf(i);
     griddep_wait();
+    griddep_launch();
     for (int i = 0; i < pre; ++i)
       if (p.x_packed != nullptr)
         load_x_packed(smem + i * C::kStageBytes + C::kABytes, kbi(i), &full[i], pol_x);
@@ -301,6 +305,7 @@ __global__ void __launch_bounds__(128, 1)
 
   // ---------------- epilogue: TMEM -> registers -> global ----------------
   griddep_wait();  // outputs may alias buffers the preceding kernel was reading
+  griddep_launch();
   mbar_wait(done, 0);
   tc_fence_after();
   gemm_epilogue<BN, MT>(p, smem, tmem, warp, lane, m0, n0, split);
@@ -513,7 +518,6 @@ __global__ void __launch_bounds__(256, 1)
   const long long t_setup = clock64();
   long long t_first = 0, t_lastmma = 0;
 
-  griddep_launch();
   const uint64_t pol_w = policy_evict_first();
   const int pre = nkb < nst ? nkb : nst;
   if (warp == 0 && lane == 0) {
@@ -557,6 +561,7 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- producer: activation slices (and the remaining weights) ----------------
     const uint64_t pol_x = policy_evict_last();
     griddep_wait();
+    griddep_launch();  // wait-then-launch (see gemm_bf16_tc_kernel)
     const int xoff = C::kABytes + rank * kSlice * 128;
     for (int i = 0; i < pre; ++i) {
       if (CS > 1)
@@ -601,6 +606,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncwarp();
 
   griddep_wait();
+  griddep_launch();
   mbar_wait(done, 0);
   const long long t_done = clock64();
   tc_fence_after();

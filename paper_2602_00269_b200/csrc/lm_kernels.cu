@@ -138,24 +138,35 @@ __global__ void __launch_bounds__(256)
                            const float2* __restrict__ rope, const int* __restrict__ page_table,
                            bf16* __restrict__ kc, bf16* __restrict__ vc, bf16* __restrict__ q_out) {
   VOX_TRACE(kTrQkvRope);
-  griddep_wait();
-  griddep_launch();
+  // row descriptor, page-table entry and the RoPE table of this thread's first
+  // item do not depend on the QKV GEMM: load them before waiting for it
   const int r = blockIdx.x;
   const RowDev rw = rows[r];
-  if (rw.slot < 0) return;
   const int hd = dm.hd, half = hd / 2;
+  const int q4 = half / 4;
+  const int n_items = (dm.n_heads + dm.n_kv) * q4;
+  const int cta_stride = 256 * gridDim.y;
+  const int it0 = threadIdx.x + 256 * blockIdx.y;
+  int page = 0;
+  float2 cs0[4];
+  if (rw.slot >= 0) {
+    page = page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot + rw.pos / dm.page_size];
+    if (it0 < n_items) {
+      const float2* rp0 = rope + static_cast<int64_t>(rw.pos) * half + (it0 % q4) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) cs0[e] = rp0[e];
+    }
+  }
+  griddep_wait();
+  griddep_launch();
+  if (rw.slot < 0) return;
   const int nqkv = (dm.n_heads + 2 * dm.n_kv) * hd;
   const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * nqkv);
   const int64_t ss4 = split_stride / 4;
-  const int page = page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot +
-                              rw.pos / dm.page_size];
   const int off = rw.pos % dm.page_size;
   const float2* rp = rope + static_cast<int64_t>(rw.pos) * half;
   // rotated heads (q then k): thread handles 4 consecutive pair indices i..i+3;
   // gridDim.y CTAs share a row (interleaved items) for more loads in flight
-  const int q4 = half / 4;
-  const int n_items = (dm.n_heads + dm.n_kv) * q4;
-  const int cta_stride = 256 * gridDim.y;
   for (int it = threadIdx.x + 256 * blockIdx.y; it < n_items; it += cta_stride) {
     const int head = it / q4, i = (it % q4) * 4;
     const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
@@ -169,7 +180,7 @@ __global__ void __launch_bounds__(256)
     float o1[4], o2[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const float2 cs = rp[i + e];
+      const float2 cs = it == it0 ? cs0[e] : rp[i + e];
       o1[e] = __fsub_rn(__fmul_rn(x1[e], cs.x), __fmul_rn(x2[e], cs.y));
       o2[e] = __fadd_rn(__fmul_rn(x2[e], cs.x), __fmul_rn(x1[e], cs.y));
     }
@@ -212,18 +223,65 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const fl
 // ---------------------------------------------------------------------------
 // split-K reduce + residual add + RMSNorm (optionally compacting output rows)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(768)
     resid_norm_kernel(const RowDev* __restrict__ rows, const float* __restrict__ ws, int splits,
                       int64_t split_stride, int d, float eps, float* __restrict__ h,
                       const float* __restrict__ nw, bf16* __restrict__ x_out,
                       const int* __restrict__ out_index) {
   VOX_TRACE(kTrResidNorm);
-  griddep_wait();
-  griddep_launch();
   __shared__ float red[33];
   const int r = blockIdx.x;
-  if (rows[r].slot < 0) return;
-  resid_norm_row(r, ws, splits, split_stride, d, eps, h, nw, x_out, out_index ? out_index[r] : r, red);
+  const int d4 = d / 4, nt = blockDim.x;
+  if (d4 > 4 * nt) {  // wide rows: the generic path
+    griddep_wait();
+    griddep_launch();
+    if (rows[r].slot < 0) return;
+    resid_norm_row(r, ws, splits, split_stride, d, eps, h, nw, x_out, out_index ? out_index[r] : r, red);
+    return;
+  }
+  // h (written >= 2 launches upstream: every kernel of the step launches its
+  // dependents only after its own griddep_wait) and the norm weights do not
+  // depend on the preceding GEMM: load them before waiting for it
+  const bool live = rows[r].slot >= 0;
+  const int orow = out_index ? out_index[r] : r;
+  float4* h4 = reinterpret_cast<float4*>(h + static_cast<int64_t>(r) * d);
+  const float4* n4 = reinterpret_cast<const float4*>(nw);
+  float4 hv[4], nv[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * nt;
+    if (live && i < d4) {
+      hv[k] = h4[i];
+      nv[k] = n4[i];
+    }
+  }
+  griddep_wait();
+  griddep_launch();
+  if (!live) return;
+  const float4* w4 = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(r) * d);
+  const int64_t ss4 = split_stride / 4;
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * nt;
+    if (i < d4) {
+      hv[k] = add4(hv[k], sum_splits4(w4, splits, ss4, i));
+      h4[i] = hv[k];
+      ss = fmaf(hv[k].x, hv[k].x, ss);
+      ss = fmaf(hv[k].y, hv[k].y, ss);
+      ss = fmaf(hv[k].z, hv[k].z, ss);
+      ss = fmaf(hv[k].w, hv[k].w, ss);
+    }
+  }
+  ss = block_sum_any(ss, red);
+  if (orow < 0) return;
+  const float inv = 1.0f / sqrtf(ss / static_cast<float>(d) + eps);
+  bf16* xr = x_out + static_cast<int64_t>(orow) * d;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int i = threadIdx.x + k * nt;
+    if (i < d4) norm_store4(xr + 4 * i, hv[k], inv, nv[k]);
+  }
 }
 
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
@@ -235,10 +293,10 @@ void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
   static const int nt_env = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 0;
   int nt = 256;
   if (nt_env > 0) {
-    nt = nt_env;
+    nt = nt_env > 768 ? 768 : nt_env;
   } else if (n <= 32) {  // one float4 per thread (d = 3072: 768 threads)
     nt = (dm.d / 4 + 31) / 32 * 32;
-    nt = nt < 256 ? 256 : (nt > 1024 ? 1024 : nt);
+    nt = nt < 256 ? 256 : (nt > 768 ? 768 : nt);
   }
   launch_k(resid_norm_kernel, dim3(n), dim3(nt), 0, st, rows, ws, splits, split_stride, dm.d,
            dm.eps, h, norm_w, x_out, out_index);

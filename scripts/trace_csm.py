@@ -44,3 +44,18 @@ for a, b in iv:
 busy += ce - cs
 span = iv[-1][1] - iv[0][0]
 print(f"B={B}: wall {wall * 1e3:.2f} ms/frame; GPU span {span / 4e6:.2f} ms/frame, busy {busy / 4e6:.2f} ms/frame")
+from paper_2602_00269_b200 import trace  # noqa: E402
+
+ls = trace.launches(rec)
+per = {}
+for l in ls:
+    k = trace.name_of(l["tag"]) + f"[{l['tag'] >> 8}]"
+    n, t = per.get(k, (0, 0))
+    per[k] = (n + 1, t + l["t1max"] - l["t0"])
+print("per kernel (launch span), us/frame:")
+for k, (n, t) in sorted(per.items(), key=lambda kv: -kv[1][1])[:20]:
+    print(f"  {k:24s} {n / 4:7.1f} launches/frame {t / 4e3:9.1f} us/frame {t / n / 1e3:7.2f} us/launch")
+ex = trace.exposed(ls)
+print("exposed per kernel, us/frame:")
+for k, v in sorted(ex.items(), key=lambda kv: -kv[1])[:12]:
+    print(f"  {k:24s} {v / 4e3:9.1f}")
