@@ -46,8 +46,13 @@ struct GemmCfg {
 // ---------------------------------------------------------------------------
 template <int BN, int MT>
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, uint32_t tmem,
-                                              int warp, int lane, int m0, int n0, int split) {
+                                              int warp, int lane, int m0, int n0, int split,
+                                              uint64_t* done_bar) {
   if (MT == 1 && p.epi == 1) {
+    if (done_bar != nullptr) {
+      mbar_wait(done_bar, 0);
+      tc_fence_after();
+    }
     // fused SiLU(gate) * up: TMEM lanes 0-63 hold gate, 64-127 up of features
     // f = 64 * tile + (lane % 64).  32 accumulator columns (rows n) at a time are
     // staged transposed in the idle pipeline smem, then each thread turns 8
@@ -94,17 +99,42 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
   // Staged epilogue: 32 accumulator columns (= 32 output rows n) at a time go
   // TMEM -> registers -> shared memory (transposed to [n][m]) -> 16-byte
   // coalesced stores along m.  (Thread-per-m scalar stores issue 4x the store
-  // instructions and serialise on the per-SM store path.)
+  // instructions and serialise on the per-SM store path.)  The bias / residual
+  // operands of a chunk are loaded before its TMEM read and barrier (all 8 per
+  // thread in flight; chunk 0's before the accumulator is complete), so the
+  // residual read is not a dependent round trip per store.
   float* stg = reinterpret_cast<float*>(smem);  // [32][128 + 4], pipeline smem is idle now
   constexpr int kSt = 128 + 4;
+  float4 rr[8];
+  auto prefetch = [&](int mb, int c, bool full_m) {
+    if (!full_m || (p.resid == nullptr && p.bias == nullptr)) return;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = threadIdx.x + i * 128;
+      const int j = e >> 5, q = (e & 31) * 4;
+      const int n = n0 + c + j;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if ((c + j) < BN && n < p.N && p.resid != nullptr)
+        a = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + mb + q);
+      rr[i] = a;
+    }
+  };
+  auto is_full = [&](int mb) {
+    return mb + 128 <= p.m_valid && (p.ldo & 3) == 0 && (p.resid == nullptr || (p.ldr & 3) == 0) &&
+           (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
+  };
+  prefetch(m0, 0, is_full(m0));
+  if (done_bar != nullptr) {
+    mbar_wait(done_bar, 0);
+    tc_fence_after();
+  }
 #pragma unroll 1
   for (int mt = 0; mt < MT; ++mt) {
     const int mb = m0 + mt * 128;
-    const bool full_m = mb + 128 <= p.m_valid && (p.ldo & 3) == 0 &&
-                        (p.resid == nullptr || (p.ldr & 3) == 0) &&
-                        (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
+    const bool full_m = is_full(mb);
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
+      if (c > 0 || mt > 0) prefetch(mb, c, full_m);
       uint32_t r[32];
       tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + mt * BN + c, r);
       tmem_ld_wait();
@@ -113,8 +143,9 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
       for (int j = 0; j < 32; ++j) stg[j * kSt + ml] = __uint_as_float(r[j]);
       __syncthreads();
       // 32 rows n x 128 m: 1024 float4, 8 per thread
-#pragma unroll 2
-      for (int e = threadIdx.x; e < 32 * 32; e += 128) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int e = threadIdx.x + i * 128;
         const int j = e >> 5, q = (e & 31) * 4;
         const int n = n0 + c + j;
         if ((c + j) < BN && n < p.N) {
@@ -126,7 +157,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
               v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
             }
             if (p.resid != nullptr) {
-              const float4 r4 = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + m);
+              const float4 r4 = rr[i];
               v.x += r4.x; v.y += r4.y; v.z += r4.z; v.w += r4.w;
             }
             *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo + m) = v;
@@ -306,9 +337,7 @@ __global__ void __launch_bounds__(128, 1)
   // ---------------- epilogue: TMEM -> registers -> global ----------------
   griddep_wait();  // outputs may alias buffers the preceding kernel was reading
   griddep_launch();
-  mbar_wait(done, 0);
-  tc_fence_after();
-  gemm_epilogue<BN, MT>(p, smem, tmem, warp, lane, m0, n0, split);
+  gemm_epilogue<BN, MT>(p, smem, tmem, warp, lane, m0, n0, split, done);  // waits for `done`
 
   tc_fence_before();
   __syncthreads();
