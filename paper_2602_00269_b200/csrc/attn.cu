@@ -96,9 +96,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
                        float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched,
-                       int fuse_combine, int l2pf, RopeIn ri) {
+                       int fuse_combine, int l2pf) {
   VOX_TRACE(kTrAttn);
-  const bool fused = ri.ws != nullptr;  // q|k|v reduce + RoPE + KV append done here
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
   constexpr int NT = HD / 8;   // PV n-tiles
@@ -111,7 +110,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __shared__ __align__(16) float s_acc[4][G][HD];
   __shared__ int s_pt[2][kAttnItemPages];
   __shared__ int s_last;
-  __shared__ __align__(16) bf16 s_new[2][HD];  // fused: this item's new K and V rows
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ps = dm.page_size;
@@ -189,7 +187,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       if (lane == 0) {
         meta[s] = StageMeta{cur.item, cur.rr, np, cur.rr == cur.nr - 1, cur.row, cur.kvh, cur.z,
                             cur.L, cur.begin, {cur.end, 0, 0}};
-        const uint32_t q_bytes = (cur.rr == 0 && !fused) ? kQBytes : 0u;
+        const uint32_t q_bytes = cur.rr == 0 ? kQBytes : 0u;
         mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(np * 2 * page_elems * 2) + q_bytes);
       }
       __syncwarp();
@@ -213,7 +211,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           prefetch_l2_bulk((kv ? vc : kc) + (static_cast<int64_t>(pid2) * dm.n_kv + cur.kvh) * page_elems,
                            page_elems * 2);
         }
-      } else if (lane == 2 * kP && cur.rr == 0 && with_q && !fused) {
+      } else if (lane == 2 * kP && cur.rr == 0 && with_q) {
         bulk_load(q_slot(s), q + (static_cast<int64_t>(cur.row) * dm.n_heads + cur.kvh * G) * HD,
                   kQBytes, &full[s], pol);
       }
@@ -228,19 +226,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     // page this forward appends to (RowDev::fresh; written by the preceding
     // kernel) go out before griddep_wait; q (written by it) after it.
     int g = 0, deferred_q = -1;
-    if (fused) {
-      // K/V pages hold only earlier steps' tokens (the current one is patched
-      // in shared memory by the consumers), so the ring streams from the start
-      // -- overlapping the QKV GEMM's tail -- without waiting for the grid
-      griddep_launch();
-      for (;; ++g) {
-        const int s = g % kAttnStages;
-        if (g >= kAttnStages) mbar_wait(&empty[s], ((g / kAttnStages) - 1) & 1);
-        const bool done = cur.item < 0;
-        issue(s, false);
-        if (done) break;
-      }
-    } else if (cur.item >= 0) {
+    if (cur.item >= 0) {
       const int fresh_page = rows[cur.row].fresh / ps;
       const int first = cur.item;
       while (g < kAttnStages && cur.item == first) {
@@ -251,7 +237,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         issue(g++, false);
       }
     }
-    if (!fused) {
     griddep_wait();
     griddep_launch();
     if (deferred_q >= 0 && lane == 0) {
@@ -265,7 +250,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const bool done = cur.item < 0;
       issue(s, true);
       if (done) break;
-    }
     }
   } else {
     // ====================== consumer warps 0-3 ======================
@@ -281,56 +265,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       mbar_wait(&full[s], (g / kAttnStages) & 1);
       const StageMeta m = meta[s];
       if (m.item < 0) break;
-      if (m.rr == 0 && fused) {
-        // q (the G heads of this kv head) and the new K/V row from the QKV
-        // GEMM's split planes: same reduction order, bias and RoPE arithmetic
-        // as qkv_rope_append_kernel (bit-identical values)
-        constexpr int half = HD / 2;
-        const int nqkv = (dm.n_heads + 2 * dm.n_kv) * HD;
-        const int pos = m.L - 1;
-        const float* w = ri.ws + static_cast<int64_t>(m.row) * nqkv;
-        const float2* rp = ri.rope + static_cast<int64_t>(pos) * half;
-        bf16* qs = q_slot(s);
-        for (int idx = tid; idx < (G + 1) * half; idx += 128) {
-          const int hh = idx / half, i = idx % half;
-          const int col = (hh < G ? m.kvh * G + hh : dm.n_heads + m.kvh) * HD + i;
-          float x1 = w[col], x2 = w[col + half];
-          for (int zz = 1; zz < ri.splits; ++zz) {
-            x1 = x1 + w[zz * ri.ss + col];
-            x2 = x2 + w[zz * ri.ss + col + half];
-          }
-          if (ri.bias != nullptr) {
-            x1 = x1 + ri.bias[col];
-            x2 = x2 + ri.bias[col + half];
-          }
-          const float2 cs = rp[i];
-          const float o1 = __fsub_rn(__fmul_rn(x1, cs.x), __fmul_rn(x2, cs.y));
-          const float o2 = __fadd_rn(__fmul_rn(x2, cs.x), __fmul_rn(x1, cs.y));
-          bf16* dst = hh < G ? qs + hh * HD : s_new[0];
-          dst[i] = __float2bfloat16_rn(o1);
-          dst[i + half] = __float2bfloat16_rn(o2);
-        }
-        for (int i = tid; i < HD; i += 128) {
-          const int col = (dm.n_heads + dm.n_kv + m.kvh) * HD + i;
-          float v = w[col];
-          for (int zz = 1; zz < ri.splits; ++zz) v = v + w[zz * ri.ss + col];
-          if (ri.bias != nullptr) v = v + ri.bias[col];
-          s_new[1][i] = __float2bfloat16_rn(v);
-        }
-        named_bar_consumers();
-        // the split holding the current token's page appends it to the cache
-        // (later steps read it from HBM; this step uses the smem copy)
-        const int pg = pos / ps;
-        if (pg >= m.begin && pg < m.pad_[0]) {
-          const int slot = rows[m.row].slot;
-          const int page = page_table[static_cast<int64_t>(slot) * dm.max_pages_per_slot + pg];
-          const int off = pos % ps;
-          for (int i = tid; i < HD; i += 128) {
-            ri.kc[((static_cast<int64_t>(page) * dm.n_kv + m.kvh) * ps + off) * HD + i] = s_new[0][i];
-            ri.vc[((static_cast<int64_t>(page) * dm.n_kv + m.kvh) * HD + i) * ps + off] = s_new[1][i];
-          }
-        }
-      }
       if (m.rr == 0) {  // new item: q from the stage, reset the online softmax
         const bf16* qs = q_slot(s);
 #pragma unroll
@@ -346,16 +280,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         const int page_idx = m.begin + m.rr * kP + warp;
         const bf16* kp = stage_ptr(s, warp, 0);
         const bf16* vp = stage_ptr(s, warp, 1);
-        if (fused && page_idx == (m.L - 1) / ps) {  // current token: stale in HBM, fresh in s_new
-          const int off = (m.L - 1) % ps;
-          bf16* kw = stage_ptr(s, warp, 0);
-          bf16* vw = stage_ptr(s, warp, 1);
-          for (int i = lane; i < HD; i += 32) {
-            kw[off * HD + i] = s_new[0][i];
-            vw[i * ps + off] = s_new[1][i];
-          }
-          __syncwarp();
-        }
         // ---- S = q K^T over the 16 tokens of this page (two n-tiles)
         float sacc[2][4];
 #pragma unroll
@@ -529,7 +453,7 @@ __global__ void __launch_bounds__(128)
 template <int HD, int G>
 static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* pt, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        int* sched, cudaStream_t st, const RopeIn* rope_in) {
+                        int* sched, cudaStream_t st) {
   // K/V ring + one q slot per stage (96 KB + 3 KB at ps 16, hd 128): 2 CTAs per SM
   const int smem = kAttnStages * (attn_stage_bytes<HD>(dm.page_size) + kAttnQSlot);
   static int attr_bytes = 0;
@@ -547,9 +471,8 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
   // CTA's critical path.  Kept opt-in.
   static const int fuse = getenv("VOX_ATTN_FUSED_COMBINE") ? 1 : 0;
   static const int l2pf = getenv("VOX_ATTN_L2PF") ? atoi(getenv("VOX_ATTN_L2PF")) : 0;
-  const RopeIn ri = rope_in ? *rope_in : RopeIn{nullptr, 0, 0, nullptr, nullptr, nullptr, nullptr};
   launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), smem, st, rows, q, kc, vc, pt, dm,
-           out, ws, n_split, n_items, sched, fuse, l2pf, ri);
+           out, ws, n_split, n_items, sched, fuse, l2pf);
   if (n_split > 1 && !fuse)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
              out);
@@ -558,19 +481,19 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
 template <int HD>
 static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16* kc,
                             const bf16* vc, const int* pt, const LmDims& dm, bf16* out, float* ws,
-                            int n_split, int* sched, cudaStream_t st, const RopeIn* rope_in) {
+                            int n_split, int* sched, cudaStream_t st) {
   switch (dm.n_heads / dm.n_kv) {
-    case 1: attn_launch<HD, 1>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-    case 2: attn_launch<HD, 2>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-    case 3: attn_launch<HD, 3>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-    case 4: attn_launch<HD, 4>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
+    case 1: attn_launch<HD, 1>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 2: attn_launch<HD, 2>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 3: attn_launch<HD, 3>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+    case 4: attn_launch<HD, 4>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
     default:
       if constexpr (HD == 64) {  // wider GQA groups (Qwen2.5-0.5B: 14 q / 2 kv heads)
         switch (dm.n_heads / dm.n_kv) {
-          case 5: attn_launch<HD, 5>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-          case 6: attn_launch<HD, 6>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-          case 7: attn_launch<HD, 7>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
-          case 8: attn_launch<HD, 8>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st, rope_in); break;
+          case 5: attn_launch<HD, 5>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 6: attn_launch<HD, 6>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 7: attn_launch<HD, 7>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
+          case 8: attn_launch<HD, 8>(rows, n, q, kc, vc, pt, dm, out, ws, n_split, sched, st); break;
           default: break;  // rejected at vox_create
         }
       }
@@ -595,11 +518,11 @@ int attn_pick_splits(int n_rows, int n_kv, int max_ctx) {
 
 void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* page_table, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        int* sched, cudaStream_t st, const RopeIn* rope_in) {
+                        int* sched, cudaStream_t st) {
   if (dm.hd == 64)
-    attn_dispatch_g<64>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st, rope_in);
+    attn_dispatch_g<64>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st);
   else
-    attn_dispatch_g<128>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st, rope_in);
+    attn_dispatch_g<128>(rows, n, q, kc, vc, page_table, dm, out, ws, n_split, sched, st);
 }
 
 }  // namespace vox

@@ -14,7 +14,6 @@
 // warps run the epilogue (tcgen05.ld 32x32b -> registers -> coalesced stores).
 #include "common.cuh"
 #include "kernels.h"
-#include "rownorm.cuh"
 #include <cstdlib>
 
 namespace vox {
@@ -264,20 +263,6 @@ __global__ void __launch_bounds__(128, 1)
                       m0 + mt * 128, pol_w);
       }
     }
-    // ... and pull the rest of this CTA's weight slice into L2 while the
-    // preceding kernel finishes (HBM is otherwise idle during the small
-    // elementwise kernels between GEMMs); the ring then refills from L2.
-    // l2_prefetch = D > 0: a sliding window -- keep the weight tiles of the next
-    // D k-blocks beyond the smem ring in flight towards L2 (more memory-level
-    // parallelism than the ring alone; the ring then refills from L2)
-    auto pf = [&](int i) {
-      if (p.w_packed != nullptr && p.l2_prefetch > 0 && i < nkb)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          prefetch_l2_bulk(p.w_packed + (static_cast<int64_t>(m0 / 128 + mt) * p.n_kb + kbi(i)) * 8192,
-                           16384);
-    };
-    for (int i = pre; i < pre + p.l2_prefetch; ++i) pf(i);
     griddep_wait();
     griddep_launch();
     for (int i = 0; i < pre; ++i)
@@ -289,12 +274,7 @@ __global__ void __launch_bounds__(128, 1)
     for (int i = pre; i < nkb; ++i) {
       const int s = i % C::kStages;
       mbar_wait(&empty[s], ((i / C::kStages) - 1) & 1);
-      pf(i + p.l2_prefetch);
       uint8_t* st = smem + s * C::kStageBytes;
-      if (p.probe == 1) {  // microbenchmark: MMA-only (re-use the resident stage data)
-        mbar_arrive(&full[s]);
-        continue;
-      }
       mbar_arrive_expect_tx(&full[s], C::kStageBytes);
       const int kx = kbi(i) * 64;
 #pragma unroll
@@ -322,7 +302,6 @@ __global__ void __launch_bounds__(128, 1)
       const uint32_t b_addr = a_addr + C::kABytes;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // 4 x UMMA_K(16) per 64-wide k-block
-        if (p.probe == 2) break;  // microbenchmark: loads only
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)  // accumulator mt lives at TMEM columns [mt*BN, mt*BN+BN)
           umma_bf16(tmem + mt * BN, make_desc_k128(a_addr + mt * 16384 + k * 32),
@@ -348,7 +327,7 @@ __global__ void __launch_bounds__(128, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Decode-step GEMM ("mc" kernel: one n-tile, optional cluster multicast).
+// Decode-step GEMM ("mc" kernel: one n-tile covering every row of the step).
 //
 // One CTA covers ALL activation rows of the step (BN = the row bucket, a single
 // n-tile), so every weight byte is read from HBM exactly once; the 1-CTA kernel
@@ -356,14 +335,12 @@ __global__ void __launch_bounds__(128, 1)
 // One CTA per SM with a deep ring (~200 KB): measured per-CTA phase stamps
 // (VOX_GEMM_DBG, profiles/gemm_mc_phases_r01.txt) show the k-loop streaming
 // weights at ~6.2 TB/s aggregate; what remains is the first-load latency and
-// the epilogue.  Optional (VOX_GEMM_CS_TEST): a cluster of CS CTAs along M
-// shares each activation k-block -- CTA r loads rows [r*BN/CS, (r+1)*BN/CS)
-// and multicasts them into the same smem offset of every CTA, and each CTA's
-// MMA commit is multicast to every CTA's `empty` barrier (count CS).  It cuts
-// activation L2 reads by CS but measured slower (activation reads are not the
-// bound once the rows are a single n-tile).
+// the epilogue.  (Round 1 also measured, and dropped, cluster multicast of the
+// activation k-blocks, split-K reduced through DSMEM, a fused RMSNorm prologue
+// and L2 prefetch of later weight k-blocks: all slower on the serving step,
+// profiles/gemm_mc_sweep_r01.txt, gemm_mc_ab_r01.txt, gemm_l2_prefetch_ab_r01.txt.)
 // ---------------------------------------------------------------------------
-// Direct epilogue of the multicast kernel (8 warps).  TMEM lane = weight row
+// Direct epilogue of the decode kernel (8 warps).  TMEM lane = weight row
 // m, so for one accumulator column (activation row n) the 32 lanes of a warp
 // hold 32 consecutive m: each column is one fully coalesced 128-byte warp
 // store straight from registers -- no smem staging, no block barriers.  Warps
@@ -497,17 +474,14 @@ struct McCfg {
   static constexpr int kSmemMax = 8 * kStageBytes + 1024 + 256 > 226 * 1024 ? 226 * 1024 : 8 * kStageBytes + 1024 + 256;
 };
 
-template <int BN, int CS>
+template <int BN>
 __global__ void __launch_bounds__(256, 1)
-    gemm_mc_kernel(const __grid_constant__ CUtensorMap tmXs, GemmArgs p) {
+    gemm_mc_kernel(const __grid_constant__ CUtensorMap tmX, GemmArgs p) {
   VOX_TRACE(kTrGemmMc);
   using C = McCfg<BN>;
   const long long t_entry = clock64();
   unsigned long long g_entry;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
-  constexpr int kSlice = BN / CS;  // activation rows this CTA multicasts (multiple of 8)
-  static_assert(kSlice % 8 == 0, "multicast slices must be whole 1024-B swizzle atoms");
-  constexpr uint16_t kMask = static_cast<uint16_t>((1u << CS) - 1u);
   const int nst = p.stages;  // ring depth (runtime: smem budget chosen by the host)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -518,97 +492,55 @@ __global__ void __launch_bounds__(256, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = CS > 1 ? static_cast<int>(cluster_ctarank()) : 0;
   const int m0 = blockIdx.y * 128;
   const int n0 = blockIdx.x * BN;
   const int split = blockIdx.z;
   const int kb0 = split * p.kb_per_split;
   const int kb1 = min(p.n_kb, kb0 + p.kb_per_split);
   const int nkb = kb1 - kb0;  // host guarantees >= 1
-  // k-block order rotated per CLUSTER (its CTAs share every activation stage)
-  const int krot = p.k_rotate ? static_cast<int>(((blockIdx.y / CS) * 7u) % static_cast<unsigned>(nkb)) : 0;
+  // k-block order rotated per weight tile: the CTAs read different activation
+  // k-blocks at any instant instead of all hammering the same L2 lines
+  const int krot = p.k_rotate ? static_cast<int>((blockIdx.y * 7u) % static_cast<unsigned>(nkb)) : 0;
   auto kbi = [&](int i) { const int t = i + krot; return kb0 + (t >= nkb ? t - nkb : t); };
   const bf16* wt = p.w_packed + static_cast<int64_t>(m0 / 128) * p.n_kb * 8192;
 
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&tmXs);
+    tma_prefetch_desc(&tmX);
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS);
+      mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, C::kTmemCols);
   tc_fence_before();
-  if (CS > 1) cluster_sync(); else __syncthreads();  // peers' barriers exist before any multicast
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const long long t_setup = clock64();
   long long t_first = 0, t_lastmma = 0;
 
-  const uint64_t pol_w = policy_evict_first();
-  const int pre = nkb < nst ? nkb : nst;
   if (warp == 0 && lane == 0) {
+    // ---------------- producer ----------------
+    const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
+    const int pre = nkb < nst ? nkb : nst;
     for (int i = 0; i < pre; ++i) {  // weights do not depend on the preceding kernel
       mbar_arrive_expect_tx(&full[i], C::kStageBytes);
       bulk_load(smem + i * C::kStageBytes, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[i],
                 pol_w);
     }
-  }
-  if (p.nrm_rows != nullptr) {
-    // fused residual + RMSNorm of the rows this GEMM consumes (replaces a
-    // resid_norm launch and its kernel boundary); the weight stages stream in
-    __shared__ float red[33];
-    griddep_wait();
-    const int nct = static_cast<int>(gridDim.x * gridDim.y * gridDim.z);
-    const int cta = static_cast<int>((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x);
-    for (int r = cta; r < p.nrm_n; r += nct)
-      if (p.nrm_rows[r].slot >= 0)
-        resid_norm_row(r, p.nrm_ws, p.nrm_splits, p.nrm_ss, p.nrm_d, p.nrm_eps, p.nrm_h, p.nrm_w, p.nrm_x,
-                       r, red);
-    // grid barrier (generation-counted, self-resetting): every normalised row is
-    // written before any CTA's TMA reads the activation buffer
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      volatile int* gen = p.nrm_bar + 1;
-      const int g0 = *gen;
-      __threadfence();
-      if (atomicAdd(p.nrm_bar, 1) == nct - 1) {
-        p.nrm_bar[0] = 0;
-        __threadfence();
-        atomicAdd(p.nrm_bar + 1, 1);
-      } else {
-        while (*gen == g0) __nanosleep(64);
-      }
-      __threadfence();
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-    }
-    __syncthreads();
-  }
-  if (warp == 0 && lane == 0) {
-    // ---------------- producer: activation slices (and the remaining weights) ----------------
-    const uint64_t pol_x = policy_evict_last();
     griddep_wait();
     griddep_launch();  // wait-then-launch (see gemm_bf16_tc_kernel)
-    const int xoff = C::kABytes + rank * kSlice * 128;
-    for (int i = 0; i < pre; ++i) {
-      if (CS > 1)
-        tma_load_2d_mc(smem + i * C::kStageBytes + xoff, &tmXs, &full[i], kbi(i) * 64,
-                       n0 + rank * kSlice, kMask, pol_x);
-      else
-        tma_load_2d(smem + i * C::kStageBytes + xoff, &tmXs, &full[i], kbi(i) * 64, n0, pol_x);
-    }
+    for (int i = 0; i < pre; ++i)
+      tma_load_2d(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], kbi(i) * 64, n0, pol_x);
     for (int i = pre; i < nkb; ++i) {
       const int s = i % nst;
-      mbar_wait(&empty[s], ((i / nst) - 1) & 1);  // all CS consumers retired stage s
+      mbar_wait(&empty[s], ((i / nst) - 1) & 1);
       uint8_t* st = smem + s * C::kStageBytes;
       mbar_arrive_expect_tx(&full[s], C::kStageBytes);
       bulk_load(st, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[s], pol_w);
-      if (CS > 1)
-        tma_load_2d_mc(st + xoff, &tmXs, &full[s], kbi(i) * 64, n0 + rank * kSlice, kMask, pol_x);
-      else
-        tma_load_2d(st + xoff, &tmXs, &full[s], kbi(i) * 64, n0, pol_x);
+      tma_load_2d(st + C::kABytes, &tmX, &full[s], kbi(i) * 64, n0, pol_x);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
@@ -625,10 +557,7 @@ __global__ void __launch_bounds__(256, 1)
         umma_bf16(tmem, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + k * 32), idesc,
                   (i > 0 || k > 0) ? 1u : 0u);
       if (i == nkb - 1) t_lastmma = clock64();
-      if (CS > 1)
-        umma_commit_mc(&empty[s], kMask);  // stage s retired in this CTA: tell every producer
-      else
-        umma_commit(&empty[s]);
+      umma_commit(&empty[s]);
     }
     umma_commit(done);
   }
@@ -639,49 +568,7 @@ __global__ void __launch_bounds__(256, 1)
   mbar_wait(done, 0);
   const long long t_done = clock64();
   tc_fence_after();
-  if (p.red) {
-    // Split-K reduced inside the cluster (cluster = the S splits of this tile):
-    // each CTA parks its fp32 partial tile in its own smem ([n][128 m], the
-    // ring is idle), then CTA r sums columns n = r, r + S, ... over all S
-    // partials through distributed shared memory in fixed order s = 0..S-1
-    // (deterministic) and writes ONE output plane -- the S fp32 planes never
-    // touch L2/HBM and the consumer kernel reads one plane instead of S.
-    constexpr int kChunks = (BN + 31) / 32;
-    float* part = reinterpret_cast<float*>(smem);
-    {
-      const int q = warp & 3, h = warp >> 2;
-      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16);
-#pragma unroll 1
-      for (int ch = h; ch < kChunks; ch += 2) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tbase + ch * 32, r);
-        tmem_ld_wait();
-        float* d = part + ch * 32 * 128 + q * 32 + lane;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) d[j * 128] = __uint_as_float(r[j]);
-      }
-    }
-    cluster_sync();  // every partial tile complete and visible cluster-wide
-    const int S = static_cast<int>(gridDim.z);
-    const int nv = min(BN, p.N - n0);
-    const int mq = (threadIdx.x & 31) * 4;
-    const bool mok = m0 + mq + 3 < p.m_valid;
-    const uint32_t base = smem_u32(part);
-    float* outp = p.out + static_cast<int64_t>(n0) * p.ldo + m0 + mq;
-#pragma unroll 1
-    for (int n = split + S * (threadIdx.x >> 5); n < nv; n += S * 8) {
-      const uint32_t off = base + static_cast<uint32_t>((n * 128 + mq) * 4);
-      float4 acc = ld_dsmem_f4(mapa_shared(off, 0));
-      for (int s2 = 1; s2 < S; ++s2) {
-        const float4 v = ld_dsmem_f4(mapa_shared(off, static_cast<uint32_t>(s2)));
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      if (mok) *reinterpret_cast<float4*>(outp + static_cast<int64_t>(n) * p.ldo) = acc;
-    }
-    cluster_sync();  // peers are done reading this CTA's partial tile
-  } else {
-    mc_epilogue<BN>(p, smem, tmem, warp, lane, m0, n0, split);
-  }
+  mc_epilogue<BN>(p, smem, tmem, warp, lane, m0, n0, split);
   if (p.dbg != nullptr) {
     const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     unsigned long long* d = p.dbg + cta * 8;
@@ -698,8 +585,7 @@ __global__ void __launch_bounds__(256, 1)
   }
 
   tc_fence_before();
-  // no CTA leaves while a peer's commit may still arrive on its barriers
-  if (CS > 1) cluster_sync(); else __syncthreads();
+  __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
@@ -753,126 +639,75 @@ static cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const
   return launch_k(gemm_bf16_tc_kernel<BN, MT>, grid, dim3(128), C::kSmemBytes, st, tw, tx, a);
 }
 
-template <int BN, int CS>
-static cudaError_t launch_mc(const CUtensorMap& txs, const GemmArgs& a, int splits, cudaStream_t st) {
+template <int BN>
+static cudaError_t launch_mc(const CUtensorMap& tx, const GemmArgs& a, int splits, cudaStream_t st) {
   using C = McCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_mc_kernel<BN, CS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+    cudaError_t e = cudaFuncSetAttribute(gemm_mc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemMax);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   GemmArgs a2 = a;
   a2.stages = C::stages(gemm_mc_budget_kb());
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((a.N + BN - 1) / BN, (a.M + 127) / 128, splits);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = C::smem_bytes(a2.stages, a2.epi);
-  cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  at[1].id = cudaLaunchAttributeClusterDimension;
-  at[1].val.clusterDim.x = 1;
-  at[1].val.clusterDim.y = CS;
-  at[1].val.clusterDim.z = a2.red ? splits : 1;
-  cfg.attrs = at;
-  cfg.numAttrs = (CS > 1 || a2.red) ? 2 : 1;
-  return cudaLaunchKernelEx(&cfg, gemm_mc_kernel<BN, CS>, txs, a2);
+  const dim3 grid((a.N + BN - 1) / BN, (a.M + 127) / 128, splits);
+  return launch_k(gemm_mc_kernel<BN>, grid, dim3(256), C::smem_bytes(a2.stages, a2.epi), st, tx, a2);
 }
 
+// CTAs of gemm_mc_kernel<BN> that can be co-resident (one per SM at the deep
+// ring, two at the 100 KB ring of <= 32-row tiles).  Queried once per width.
 template <int BN>
-static cudaError_t launch_mc_cs(const CUtensorMap& txs, const GemmArgs& a, int splits, int cs,
-                                cudaStream_t st) {
-  constexpr bool k8 = (BN / 8) % 8 == 0, k4 = (BN / 4) % 8 == 0, k2 = (BN / 2) % 8 == 0;
-  if (cs == 8) {
-    if constexpr (k8) return launch_mc<BN, 8>(txs, a, splits, st);
-  } else if (cs == 4) {
-    if constexpr (k4) return launch_mc<BN, 4>(txs, a, splits, st);
-  } else if (cs == 2) {
-    if constexpr (k2) return launch_mc<BN, 2>(txs, a, splits, st);
-  } else if (cs == 1) {
-    return launch_mc<BN, 1>(txs, a, splits, st);
-  }
-  return cudaErrorInvalidValue;
-}
-
-// CTAs of gemm_mc_kernel<BN, CS> that can be co-resident (whole clusters:
-// a cluster's CTAs must share one GPC, so clusters of 8 one-CTA-per-SM blocks
-// leave some SMs of each GPC idle).  Queried once per instantiation.
-template <int BN, int CS>
-static int mc_capacity_t(int cz = 1) {
-  static int caps[9] = {0};
-  int& cap = caps[cz < 1 ? 1 : (cz > 8 ? 8 : cz)];
+static int mc_capacity_t() {
+  static int cap = 0;
   if (cap == 0) {
     using C = McCfg<BN>;
-    cudaFuncSetAttribute(gemm_mc_kernel<BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::kSmemMax);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(1, CS * 64, cz);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = C::smem_bytes(C::stages(gemm_mc_budget_kb()), 0);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = CS;
-    at[0].val.clusterDim.z = cz;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, gemm_mc_kernel<BN, CS>, &cfg) != cudaSuccess || n <= 0) {
+    cudaFuncSetAttribute(gemm_mc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemm_mc_kernel<BN>, 256,
+                                                      C::smem_bytes(C::stages(gemm_mc_budget_kb()), 0)) !=
+            cudaSuccess ||
+        per_sm <= 0) {
       cudaGetLastError();
-      n = kNumSMs / CS;
+      per_sm = 1;
     }
-    cap = n * CS * cz;
+    cap = per_sm * kNumSMs;
   }
   return cap;
 }
-template <int BN>
-static int mc_capacity_bn(int cs, int cz) {
-  constexpr bool k8 = (BN / 8) % 8 == 0, k4 = (BN / 4) % 8 == 0, k2 = (BN / 2) % 8 == 0;
-  if constexpr (k8) if (cs == 8) return mc_capacity_t<BN, 8>();
-  if constexpr (k4) if (cs == 4) return mc_capacity_t<BN, 4>();
-  if constexpr (k2) if (cs == 2) return mc_capacity_t<BN, 2>();
-  return mc_capacity_t<BN, 1>(cz);
-}
-int gemm_mc_capacity(int bn, int cs, int cz) {
+int gemm_mc_capacity(int bn) {
   switch (bn) {
-    case 16: return mc_capacity_bn<16>(cs, cz);
-    case 32: return mc_capacity_bn<32>(cs, cz);
-    case 64: return mc_capacity_bn<64>(cs, cz);
-    case 96: return mc_capacity_bn<96>(cs, cz);
-    case 128: return mc_capacity_bn<128>(cs, cz);
-    case 160: return mc_capacity_bn<160>(cs, cz);
-    case 192: return mc_capacity_bn<192>(cs, cz);
-    case 224: return mc_capacity_bn<224>(cs, cz);
-    default: return mc_capacity_bn<256>(cs, cz);
+    case 16: return mc_capacity_t<16>();
+    case 32: return mc_capacity_t<32>();
+    case 64: return mc_capacity_t<64>();
+    case 96: return mc_capacity_t<96>();
+    case 128: return mc_capacity_t<128>();
+    case 160: return mc_capacity_t<160>();
+    case 192: return mc_capacity_t<192>();
+    case 224: return mc_capacity_t<224>();
+    default: return mc_capacity_t<256>();
   }
 }
 
-// BN in {16, 32, 64, 96, 128, 160, 192, 224, 256}; txs = activation map with box rows BN / cs
-cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
-                           cudaStream_t st) {
-  if (a.w_packed == nullptr || (a.M + 127) / 128 % cs != 0) return cudaErrorInvalidValue;
+// BN in {16, 32, 64, 96, 128, 160, 192, 224, 256}; tx = activation map with box rows BN
+cudaError_t gemm_launch_mc(const CUtensorMap& tx, GemmArgs a, int splits, int bn, cudaStream_t st) {
+  if (a.w_packed == nullptr) return cudaErrorInvalidValue;
   a.n_kb = a.K / 64;
   a.kb_per_split = (a.n_kb + splits - 1) / splits;
   splits = (a.n_kb + a.kb_per_split - 1) / a.kb_per_split;
   switch (bn) {
-    case 16: return launch_mc_cs<16>(txs, a, splits, cs, st);
-    case 32: return launch_mc_cs<32>(txs, a, splits, cs, st);
-    case 64: return launch_mc_cs<64>(txs, a, splits, cs, st);
-    case 128: return launch_mc_cs<128>(txs, a, splits, cs, st);
-    case 96: return launch_mc_cs<96>(txs, a, splits, cs, st);
-    case 160: return launch_mc_cs<160>(txs, a, splits, cs, st);
-    case 192: return launch_mc_cs<192>(txs, a, splits, cs, st);
-    case 224: return launch_mc_cs<224>(txs, a, splits, cs, st);
-    case 256: return launch_mc_cs<256>(txs, a, splits, cs, st);
+    case 16: return launch_mc<16>(tx, a, splits, st);
+    case 32: return launch_mc<32>(tx, a, splits, st);
+    case 64: return launch_mc<64>(tx, a, splits, st);
+    case 96: return launch_mc<96>(tx, a, splits, st);
+    case 128: return launch_mc<128>(tx, a, splits, st);
+    case 160: return launch_mc<160>(tx, a, splits, st);
+    case 192: return launch_mc<192>(tx, a, splits, st);
+    case 224: return launch_mc<224>(tx, a, splits, st);
+    case 256: return launch_mc<256>(tx, a, splits, st);
     default: return cudaErrorInvalidValue;
   }
 }
-
-
 
 int gemm_bn_for_rows(int rows) {
   if (rows <= 16) return 16;
@@ -891,9 +726,7 @@ int gemm_bn_for_rows(int rows) {
 GemmPlan gemm_plan_1cta(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
-  g.red = 0;
   g.mc = 0;
-  g.cs = 1;
   g.bn = gemm_bn_for_rows(rows);
   if (g.bn > 128) g.bn = 128;
   if (rows >= 128 && M <= 4096) g.bn = 64;
@@ -921,37 +754,21 @@ GemmPlan gemm_plan_1cta(int M, int rows, int K) {
 GemmPlan gemm_plan(int M, int rows, int K) {
   GemmPlan g{};
   const int n_kb = K / 64;
-  g.mc = 0;
-  g.cs = 1;
-  // Decode-sized row counts: the cluster-multicast kernel (one n-tile covering
-  // every row, activations multicast across CS CTAs along M, split-K to fill
-  // the co-resident CTA slots).  Callers fall back to the plan below when the
-  // weights are not in the packed layout.
-  const char* mce = getenv("VOX_GEMM_MC");
-  static const int mc_min_rows = getenv("VOX_GEMM_MC_MIN_ROWS") ? atoi(getenv("VOX_GEMM_MC_MIN_ROWS")) : 1;  // B=1 step 2.29 -> 2.03 ms
-  if (rows >= mc_min_rows && rows <= 512 && K % 64 == 0 && !(mce && atoi(mce) == 0)) {
-    // <= 256 rows: one n-tile (each weight byte read once); 257..512 rows (decode
-    // plus a burst of prefill rows): two n-tiles of half the rows each
+  // Decode-sized row counts: the mc kernel (one n-tile covering every row, so
+  // each weight byte is read once; split-K to fill the co-resident CTA slots).
+  // Callers fall back to the plan below when the weights are not packed.
+  if (rows <= 512 && K % 64 == 0) {
+    // <= 256 rows: one n-tile; 257..512 rows (decode plus a burst of prefill
+    // rows): two n-tiles of half the rows each
     const int ntiles = rows > 256 ? 2 : 1;
     const int per_tile = (rows + ntiles - 1) / ntiles;
     int bn = 256;
     for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
       if (per_tile <= b) { bn = b; break; }
     const int mtiles = (M + 127) / 128 * ntiles;  // CTAs per split
-    // Multicast is measured SLOWER than cs = 1 on every decode shape
-    // (profiles/gemm_mc_sweep_r01.txt): with one n-tile the activation L2
-    // reads are not the bound -- the k-loop already streams weights at HBM
-    // rate -- and clusters add co-scheduling constraints and couple each
-    // stage's release to the slowest CTA of the cluster.  Kept as an option.
-    int cs = 1;
-    if (const char* e = getenv("VOX_GEMM_CS_TEST")) {
-      const int f = atoi(e);
-      if ((f == 1 || f == 2 || f == 4 || f == 8) && ((M + 127) / 128) % f == 0 && (bn / f) % 8 == 0) cs = f;
-    }
-    const int cap = gemm_mc_capacity(bn, cs, 1);
-    static const int max_splits = getenv("VOX_GEMM_MAX_SPLITS") ? atoi(getenv("VOX_GEMM_MAX_SPLITS")) : kGemmMaxSplits;
+    const int cap = gemm_mc_capacity(bn);
     int best = 1;
-    for (int s2 = 1; s2 <= max_splits; ++s2) {
+    for (int s2 = 1; s2 <= kGemmMaxSplits; ++s2) {
       const int per = (n_kb + s2 - 1) / s2;
       if (per < 2) break;
       if ((n_kb + per - 1) / per != s2) continue;  // every split non-empty
@@ -959,23 +776,10 @@ GemmPlan gemm_plan(int M, int rows, int K) {
       best = s2;
     }
     g.mc = 1;
-    g.cs = cs;
     g.bn = bn;
     g.mt = 1;
     g.splits = best;
     if (const char* e = getenv("VOX_GEMM_SPLITS_TEST")) g.splits = atoi(e) < 1 ? 1 : atoi(e);
-    // split-K reduced in a (1, 1, splits) cluster through DSMEM: needs <= 8
-    // splits, the fp32 tile in the ring, and whole clusters co-resident
-    // Opt-in (VOX_GEMM_RED=1): measured slower on the serving step than fp32
-    // partial planes through L2 (profiles/gemm_mc_ab_r01.txt) -- the cluster
-    // co-scheduling and the DSMEM round trip cost more than the L2 traffic.
-    const char* re = getenv("VOX_GEMM_RED");
-    g.red = 0;
-    if (g.splits > 1 && g.splits <= 8 && cs == 1 && re && atoi(re) == 1 &&
-        bn * 128 * 4 <= 144 * 1024) {
-      const int capz = gemm_mc_capacity(bn, 1, g.splits);
-      if (mtiles * g.splits <= capz) g.red = 1;
-    }
     return g;
   }
   return gemm_plan_1cta(M, rows, K);

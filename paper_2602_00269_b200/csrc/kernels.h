@@ -43,8 +43,6 @@ struct GemmArgs {
   int64_t ldr;
   int m_valid;            // columns m >= m_valid are not stored
   int k_rotate;           // rotate each CTA's k-block order by its weight tile
-  int probe;              // microbenchmarks only: 1 = MMA-only, 2 = loads-only
-  int l2_prefetch;        // prefetch the CTA's remaining weight tiles into L2 before griddep_wait
   // epi == 1 (gate|up GEMM, 1 split, interleaved weight tiles): instead of fp32
   // out, write act[n][f] = bf16(SiLU(gate) * up) for the tile's 64 features
   int epi;
@@ -52,21 +50,7 @@ struct GemmArgs {
   int64_t ld_act;
   const bf16* x_packed;   // non-null: activations in the packed tile layout (bulk copies)
   int stages;             // mc kernel: smem ring depth (set by the launcher)
-  int red;                // mc kernel: splits reduced in a (1,1,splits) cluster -> one plane
   unsigned long long* dbg; // gemm_test only: per-CTA clock64 stamps (VOX_GEMM_DBG=1)
-  // fused RMSNorm prologue (mc kernel; nrm_rows != null): the CTAs first run
-  // resid_norm_row over rows (cta, cta + n_ctas, ...) -- the preceding GEMM's
-  // split planes + residual -> h, bf16 normalised rows -> the activation
-  // buffer this GEMM reads -- then meet at a grid barrier (all CTAs resident)
-  const struct RowDev* nrm_rows;
-  int nrm_n, nrm_splits, nrm_d;
-  int64_t nrm_ss;
-  const float* nrm_ws;
-  float* nrm_h;
-  const float* nrm_w;
-  bf16* nrm_x;
-  float nrm_eps;
-  int* nrm_bar;           // {arrivals, generation}, self-resetting
   const bf16* w_packed;   // non-null: W in the packed tile layout (init.cu), 1-D bulk
                           // copies of contiguous 16 KB tiles instead of the tensor map
 };
@@ -79,20 +63,15 @@ struct GemmPlan {
   int bn;      // activation rows per tile (UMMA N)
   int mt;      // 128-row weight sub-tiles per CTA (1 or 2)
   int splits;  // split-K factor (fp32 partial planes)
-  int mc;      // 1: cluster-multicast kernel (one n-tile of bn >= rows, packed weights)
-  int cs;      // mc: CTAs per cluster along M sharing each activation k-block
-  int red;     // mc: split-K reduced through DSMEM inside the cluster (one output plane)
+  int mc;      // 1: decode kernel (one n-tile of bn >= rows, packed weights)
 };
-// fp32 output planes a GEMM with this plan leaves for its consumer
-inline int gemm_out_planes(const GemmPlan& g) { return g.red ? 1 : g.splits; }
 GemmPlan gemm_plan(int M, int rows, int K);
 GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA kernel only
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, int mt, cudaStream_t st);
-// cluster-multicast kernel: txs = activation map with box rows bn / cs
-cudaError_t gemm_launch_mc(const CUtensorMap& txs, GemmArgs a, int splits, int bn, int cs,
-                           cudaStream_t st);
-int gemm_mc_capacity(int bn, int cs, int cz);
+// decode kernel: tx = activation map with box rows bn
+cudaError_t gemm_launch_mc(const CUtensorMap& tx, GemmArgs a, int splits, int bn, cudaStream_t st);
+int gemm_mc_capacity(int bn);
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).
@@ -140,20 +119,9 @@ constexpr int kAttnSplitRows = 128;  // split-KV only for batches up to this man
 int attn_pick_splits(int n_rows, int n_kv, int max_ctx);
 // ws: split-KV partials [rows][kv][n_split][G][hd + 2] (unused when n_split == 1)
 // sched: 2 zeroed ints (work counter, done counter), self-resetting per launch
-// Fused q|k|v split-K reduce + bias + RoPE + KV append inside the attention
-// kernel (decode steps whose rows are distinct slots): ws != nullptr enables it
-struct RopeIn {
-  const float* ws;     // QKV GEMM output planes [splits][rows][nqkv]
-  int splits;
-  int64_t ss;          // elements between planes
-  const float2* rope;  // (cos, sin) table [pos][hd / 2]
-  const float* bias;   // [nqkv] or null
-  bf16* kc;            // this layer's K / V pools (append target)
-  bf16* vc;
-};
 void launch_attn_decode(const RowDev* rows, int n, const bf16* q, const bf16* kc, const bf16* vc,
                         const int* page_table, const LmDims& dm, bf16* out, float* ws, int n_split,
-                        int* sched, cudaStream_t st, const RopeIn* rope_in = nullptr);
+                        int* sched, cudaStream_t st);
 void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
                        int64_t split_stride, const LmDims& dm, float* h, const float* norm_w,
                        bf16* x_out, const int* out_index, cudaStream_t st);

@@ -169,7 +169,6 @@ struct VoxCtx {
   // ---- per-step staging
   RowDev* d_rows = nullptr;
   int* attn_sched = nullptr;  // persistent attention work counters (self-resetting)
-  int* nrm_bar = nullptr;     // grid barrier of the GEMMs' fused norm prologue
   int* chain_ctr = nullptr;   // layer-chain job counters: [n_layers + 1][kChainCtrInts]
   // VOX_CHAIN=1: decode steps of <= 256 rows run each layer's projections + norms +
   // RoPE as ONE persistent layer-chain launch (layer_chain.cu).  Opt-in: bit-identical
@@ -178,10 +177,6 @@ struct VoxCtx {
   // (28 KB from L2, ~1.7 us under load) need the ring depth the per-kernel GEMM gives
   // them, and the in-kernel norm / RoPE phases are latency chains as long as kernels
   bool chain_on = getenv("VOX_CHAIN") && atoi(getenv("VOX_CHAIN")) == 1;
-  // opt-in (VOX_FUSE_NORM=1): measured slower (750 -> 727 audio-s/s): 128 CTAs
-  // normalising ~2 rows each serially + a grid barrier take longer than the
-  // 224-CTA resid_norm launch whose boundary PDL already overlaps
-  bool fuse_norm = getenv("VOX_FUSE_NORM") && atoi(getenv("VOX_FUSE_NORM")) == 1;
   int* d_sample_rows = nullptr;
   int* d_out_index = nullptr;
   int* d_tokens = nullptr;
@@ -225,8 +220,6 @@ struct VoxCtx {
   unsigned long long* trace_buf = nullptr;  // vox_trace_*: [count, cap, records...]
   int64_t trace_cap = 0;
   bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;  // debug: eager decode steps
-  int gemm_l2_prefetch = getenv("VOX_GEMM_L2PF") ? atoi(getenv("VOX_GEMM_L2PF")) : 0;  // measured slower (profiles/gemm_l2_prefetch_ab_r01.txt)
-  int gemm_probe = getenv("VOX_GEMM_PROBE") ? atoi(getenv("VOX_GEMM_PROBE")) : 0;  // microbench
   bool silu_unfused = getenv("VOX_SILU_UNFUSED") != nullptr;  // A/B: separate SiLU kernel
   float* dbg_last = nullptr;  // debug: buffer holding the last stage's fp32 output
 
@@ -306,8 +299,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
                     const float* resid, int64_t ldr, int m_valid, cudaStream_t st,
                     const char* cls = "gemm", const bf16* wp = nullptr,
                     bf16* act_out = nullptr,
-                    int64_t ld_act = 0, int* planes_out = nullptr,
-                    const GemmArgs* nrm = nullptr) {
+                    int64_t ld_act = 0) {
   GemmPlan plan = gemm_plan(M, rows, K);  // tile shape (splits are the caller's)
   {
     // the effective split count: every split gets ceil(n_kb / splits) k-blocks, so a
@@ -333,26 +325,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   a.x_packed = c->test_x_packed;
   a.dbg = c->test_dbg;
   a.k_rotate = c->gemm_k_rotate;
-  a.probe = c->gemm_probe;
-  a.l2_prefetch = c->gemm_l2_prefetch;
   a.epi = act_out != nullptr ? 1 : 0;
-  if (nrm != nullptr) {  // fused residual + RMSNorm prologue (mc kernel only)
-    if (!plan.mc) return fail(c, VOX_ERR_INVALID, "fused norm prologue needs the mc GEMM");
-    a.nrm_rows = nrm->nrm_rows;
-    a.nrm_n = nrm->nrm_n;
-    a.nrm_splits = nrm->nrm_splits;
-    a.nrm_d = nrm->nrm_d;
-    a.nrm_ss = nrm->nrm_ss;
-    a.nrm_ws = nrm->nrm_ws;
-    a.nrm_h = nrm->nrm_h;
-    a.nrm_w = nrm->nrm_w;
-    a.nrm_x = nrm->nrm_x;
-    a.nrm_eps = nrm->nrm_eps;
-    a.nrm_bar = nrm->nrm_bar;
-  }
-  a.red = (plan.mc && plan.red && splits == plan.splits && a.epi == 0 && bias == nullptr &&
-           resid == nullptr) ? 1 : 0;
-  if (planes_out) *planes_out = a.red ? 1 : splits;
   a.act = act_out;
   a.ld_act = ld_act;
   if (a.epi == 1 && (splits != 1 || plan.mt != 1))
@@ -360,7 +333,7 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
-  cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn / plan.cs), a, splits, bn, plan.cs, st)
+  cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn), a, splits, bn, st)
                               : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
@@ -546,8 +519,6 @@ static int create_buffers(VoxCtx* c) {
     CK(dalloc(&c->attn_sched, ns));
     CK(cudaMemset(c->attn_sched, 0, ns * sizeof(int)));
   }
-  CK(dalloc(&c->nrm_bar, 2));
-  CK(cudaMemset(c->nrm_bar, 0, 2 * sizeof(int)));
   CK(dalloc(&c->chain_ctr, static_cast<size_t>(g.n_layers + 1) * kChainCtrInts));
   CK(cudaMemset(c->chain_ctr, 0, static_cast<size_t>(g.n_layers + 1) * kChainCtrInts * sizeof(int)));
   CK(dalloc(&c->d_sample_rows, static_cast<size_t>(R)));
@@ -817,7 +788,7 @@ static int enqueue_layers_chain(VoxCtx* c, int nrows, int bn, cudaStream_t st) {
       const int asp = attn_pick_splits(nrows, g.n_kv_heads, g.max_ctx);
       TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
-                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st, nullptr);
+                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st);
     }
     const bool last = (l == L - 1);
     a.job[0] = gemm_job(c->w_o + l * n_o, 1, d, Hhd, sp_o, -1, 0);
@@ -844,10 +815,8 @@ static int enqueue_layers_chain(VoxCtx* c, int nrows, int bn, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // hslot >= 0: every sampled row is at the same frame slot, so the LM head runs
 // over that slot's codebook rows only (CSM depth decoder: 1 of 31 codebook heads)
-// fused_rope: every row is a distinct slot (a pure decode step), so the q|k|v
-// reduce + RoPE + KV append runs inside the attention kernel (no rope launch)
 static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1,
-                           bool fused_rope = false, bool run_sampler = true) {
+                           bool run_sampler = true) {
   const VoxModelCfg& g = c->cfg;
   const LmDims& dm = c->dm;
   cudaStream_t st = c->s_lm;
@@ -861,15 +830,11 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   const GemmPlan dn_plan = gemm_plan(d, nrows, dff);
   const int sp_qkv = qkv_plan.splits, sp_o = o_plan.splits;
   // fp32 planes the consumers reduce (1 when the GEMM reduced its splits in-cluster)
-  const int pl_qkv = gemm_out_planes(qkv_plan), pl_o = gemm_out_planes(o_plan);
-  const int pl_dn = gemm_out_planes(dn_plan);
+  const int pl_qkv = qkv_plan.splits, pl_o = o_plan.splits, pl_dn = dn_plan.splits;
   const GemmPlan gu_plan = gemm_plan(2 * dff, nrows, d);
   const int sp_gu = gu_plan.splits;
   const int sp_dn = dn_plan.splits;
   // gate|up CTAs (1 split, mc kernel) all co-resident -> norm fusable
-  const bool gu_norm_fusable = c->fuse_norm && gu_plan.mc && gu_plan.splits == 1 &&
-                               ((2 * dff + 127) / 128) * ((nrows + gu_plan.bn - 1) / gu_plan.bn) <=
-                                   gemm_mc_capacity(gu_plan.bn, 1, 1);
   const size_t kv_layer = static_cast<size_t>(g.n_pages) * g.n_kv_heads * g.page_size * g.head_dim;
   const int64_t n_qkv = packed_elems(c->nqkv, d), n_o = packed_elems(d, Hhd);
   const int64_t n_gu = packed_elems(2 * dff, d), n_dn = packed_elems(d, dff);
@@ -879,7 +844,7 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
   for (int l = 0; l < L && cbn < 0; ++l) {
     RET(run_gemm(c, tw_unused, c->tm_x, c->nqkv, nrows, d, c->ws, c->nqkv, sp_qkv, nullptr,
                  nullptr, 0, c->nqkv, st, "gemm", c->w_qkv + l * n_qkv));
-    if (!fused_rope) {
+    {
       TimedLaunch tl(c, st, "qkv_rope", static_cast<double>(nrows) * c->nqkv * 4 * pl_qkv);
       launch_qkv_rope_append(c->d_rows, nrows, c->ws,
                              c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr, pl_qkv,
@@ -889,47 +854,24 @@ static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, in
     {
       const int asp = attn_pick_splits(nrows, g.n_kv_heads, g.max_ctx);
       TimedLaunch tl(c, st, "attn", c->step_attn_bytes, asp > 1 ? 2 : 1);
-      const RopeIn ri{c->ws, pl_qkv, static_cast<int64_t>(nrows) * c->nqkv, c->rope_tab,
-                      c->b_qkv ? c->b_qkv + static_cast<int64_t>(l) * c->nqkv : nullptr,
-                      c->kc + l * kv_layer, c->vc + l * kv_layer};
       launch_attn_decode(c->d_rows, nrows, c->q, c->kc + l * kv_layer, c->vc + l * kv_layer,
-                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st, fused_rope ? &ri : nullptr);
+                         c->page_table, dm, c->attn, c->attn_ws, asp, c->attn_sched, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_attn, d, nrows, Hhd, c->ws, d, sp_o, nullptr, nullptr, 0, d,
                  st, "gemm", c->w_o + l * n_o));
-    // the O projection's residual + RMSNorm folds into the gate|up GEMM's
-    // prologue when every gate|up CTA is co-resident (its grid barrier needs it)
-    const bool gu_fused = sp_gu == 1 && !c->silu_unfused;
-    const bool norm_in_gu = gu_fused && gu_norm_fusable;
-    if (!norm_in_gu) {
+    {
       TimedLaunch tl(c, st, "norm", static_cast<double>(nrows) * d * (4.0 * pl_o + 10));
       launch_resid_norm(c->d_rows, nrows, c->ws, pl_o, static_cast<int64_t>(nrows) * d, dm, c->h,
                         c->norm_mlp + static_cast<int64_t>(l) * d, c->x, nullptr, st);
     }
-    if (gu_fused) {  // SiLU(gate) * up in the epilogue
-      GemmArgs nrm{};
-      if (norm_in_gu) {
-        nrm.nrm_rows = c->d_rows;
-        nrm.nrm_n = nrows;
-        nrm.nrm_splits = pl_o;
-        nrm.nrm_d = d;
-        nrm.nrm_ss = static_cast<int64_t>(nrows) * d;
-        nrm.nrm_ws = c->ws;
-        nrm.nrm_h = c->h;
-        nrm.nrm_w = c->norm_mlp + static_cast<int64_t>(l) * d;
-        nrm.nrm_x = c->x;
-        nrm.nrm_eps = g.rms_eps;
-        nrm.nrm_bar = c->nrm_bar;
-      }
+    if (sp_gu == 1 && !c->silu_unfused) {  // SiLU(gate) * up in the epilogue
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, 1, nullptr, nullptr,
-                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, c->act, dff, nullptr,
-                   norm_in_gu ? &nrm : nullptr));
+                   0, 2 * dff, st, "gemm", c->w_gu + l * n_gu, c->act, dff));
     } else {
       RET(run_gemm(c, tw_unused, c->tm_x, 2 * dff, nrows, d, c->ws, 2 * dff, sp_gu, nullptr,
                    nullptr, 0, 2 * dff, st, "gemm", c->w_gu + l * n_gu));
-      const int pl_gu = gemm_out_planes(gu_plan);
-      TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * pl_gu + 2));
-      launch_silu_mul(c->d_rows, nrows, c->ws, pl_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
+      TimedLaunch tl(c, st, "silu", static_cast<double>(nrows) * dff * (8.0 * sp_gu + 2));
+      launch_silu_mul(c->d_rows, nrows, c->ws, sp_gu, static_cast<int64_t>(nrows) * 2 * dff, dm,
                       c->act, st);
     }
     RET(run_gemm(c, tw_unused, c->tm_act, d, nrows, dff, c->ws, d, sp_dn, nullptr, nullptr, 0,
@@ -1095,7 +1037,7 @@ void vox_destroy(VoxCtx* c) {
                       c->d_out_index, c->d_tokens, c->d_err, c->dstate, c->dx, c->dy, c->dbf,
                       c->d_dstage, c->d_pcm, c->dw.tabs, c->dw.in_dw_w, c->dw.in_dw_b,
                       c->dw.in_pw_w, c->dw.in_pw_b, c->dw.out_alpha, c->dw.out_w, c->b_qkv,
-                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links, c->nrm_bar, c->chain_ctr};
+                      c->trace_buf, c->frame_store, c->ext, c->w_proj, c->d_links, c->chain_ctr};
   if (c->ev_xfer) cudaEventDestroy(c->ev_xfer);
   for (auto& e : c->ev_links)
     if (e) cudaEventDestroy(e);
@@ -1525,33 +1467,20 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
     }
     if (hslot < 0) hslot = -1;
   }
-  // pure decode step (each slot once): RoPE + KV append fused into attention.
-  // Opt-in (VOX_FUSED_ROPE=1): measured slower (742 -> 691 audio-s/s) -- every
-  // (row, kv head) item pays its q|k|v reduction + RoPE on the consumers'
-  // critical path, and the early-started K/V stream contends with the QKV GEMM
-  bool unique = getenv("VOX_FUSED_ROPE") && atoi(getenv("VOX_FUSED_ROPE")) == 1;
-  {
-    std::vector<int> seen;
-    seen.reserve(n);
-    for (int i = 0; i < n && unique; ++i) seen.push_back(rows[i].slot);
-    std::sort(seen.begin(), seen.end());
-    for (size_t i = 1; i < seen.size() && unique; ++i)
-      if (seen[i] == seen[i - 1]) unique = false;
-  }
   int rc = VOX_OK;
   if (use_graph) {
-    auto key = std::make_tuple(nrows, ns, (hslot * 2 + (unique ? 1 : 0)) * 2 + (run_sampler ? 1 : 0));
+    auto key = std::make_tuple(nrows, ns, hslot * 2 + (run_sampler ? 1 : 0));
     auto it = c->graphs.find(key);
     if (it == c->graphs.end()) {
       // eager pass (executes this step and sets kernel attributes), then capture
-      rc = enqueue_forward(c, nrows, ns, false, hslot, unique, run_sampler);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, run_sampler);
       if (rc != VOX_OK) return rc;
       CK(cudaStreamSynchronize(st));
       const int64_t before = c->launches;
       cudaGraph_t graph;
       c->capturing = true;
       CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rc = enqueue_forward(c, nrows, ns, false, hslot, unique, run_sampler);
+      rc = enqueue_forward(c, nrows, ns, false, hslot, run_sampler);
       cudaError_t ce = cudaStreamEndCapture(st, &graph);
       c->capturing = false;
       if (rc != VOX_OK) return rc;
@@ -1567,7 +1496,7 @@ int vox_forward(VoxCtx* c, const VoxRow* rows, int32_t n, uint32_t flags, float*
       c->launches += c->graph_launches[key];
     }
   } else {
-    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot, unique, run_sampler);
+    rc = enqueue_forward(c, nrows, ns, full, full ? -1 : hslot, run_sampler);
     if (rc != VOX_OK) return rc;
   }
   {  // layout of the logits buffer this forward leaves behind (vox_read_logits)
@@ -2115,13 +2044,15 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   int rc = VOX_OK;
-  int planes = splits;
+  // fp32 planes the GEMM leaves: every split gets ceil(n_kb / splits) k-blocks
+  const int per_split = (K / 64 + splits - 1) / splits;
+  const int planes = (K / 64 + per_split - 1) / per_split;
   double total_ms = 0.0;
   for (int it = 0; it < iters && rc == VOX_OK; ++it) {
     launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
     CK(cudaEventRecord(a, c->s_lm));
     rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm, "gemm", wpk, nullptr, 0, &planes);
+                  c->s_lm, "gemm", wpk, nullptr, 0);
     CK(cudaEventRecord(b, c->s_lm));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;

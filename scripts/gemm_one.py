@@ -1,4 +1,4 @@
-"""One cluster-multicast GEMM launch at a decode shape (for ncu). GPU only."""
+"""One decode-GEMM launch (gemm_mc_kernel) at a decode shape (for ncu). GPU only."""
 import os
 import sys
 

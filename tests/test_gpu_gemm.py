@@ -33,29 +33,10 @@ def test_gemm_matches_numpy(tiny_dev, monkeypatch, M, N, K, splits, packed):
     assert err < 1e-3 * np.sqrt(K), (err, np.unravel_index(np.argmax(np.abs(out - ref)), out.shape))
 
 
-@pytest.mark.parametrize("M,N,K,splits", [
-    (1024, 224, 512, 1), (1024, 256, 1024, 3), (2048, 16, 256, 2), (512, 64, 768, 1),
-    (1024, 100, 256, 1), (1024, 192, 512, 2),
-])
-@pytest.mark.parametrize("cs", [1, 2, 4, 8])
-def test_gemm_cluster_multicast(tiny_dev, monkeypatch, M, N, K, splits, cs):
-    """Cluster-multicast kernel (gemm_mc_kernel): each CTA multicasts a slice of
-    the activation k-block to the CS CTAs of its cluster; every CTA covers all rows."""
-    monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
-    monkeypatch.setenv("VOX_GEMM_CS_TEST", str(cs))
-    rng = np.random.default_rng(M + N * 3 + cs)
-    w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
-    x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
-    out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), None, splits)
-    ref = x.astype(np.float64) @ w.astype(np.float64).T
-    err = np.abs(out - ref).max()
-    assert err < 1e-3 * np.sqrt(K), err
-
-
 @pytest.mark.parametrize("M,N,K", [(3072, 224, 3072), (1024, 256, 2048), (5120, 64, 1024), (640, 100, 512)])
 @pytest.mark.parametrize("splits", [2, 3, 5, 8])
-def test_gemm_split_k_cluster_reduction(tiny_dev, monkeypatch, M, N, K, splits):
-    """Split-K reduced inside a (1,1,splits) cluster through DSMEM (one output plane)."""
+def test_gemm_decode_split_k(tiny_dev, monkeypatch, M, N, K, splits):
+    """Decode GEMM (one n-tile of all rows) with forced split-K fp32 planes."""
     monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
     monkeypatch.setenv("VOX_GEMM_SPLITS_TEST", str(splits))
     rng = np.random.default_rng(M + N + splits)
