@@ -984,6 +984,8 @@ int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx*
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   const bool prio = !(getenv("VOX_STREAM_PRIO") && atoi(getenv("VOX_STREAM_PRIO")) == 0);
   CK(cudaStreamCreateWithPriority(&c->s_lm, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+  // (detokenizing on the LM stream, between decode steps, measured 4% slower than
+  // this concurrent low-priority stream: profiles/detok_serial_ab_r02.txt)
   CK(cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, prio_lo));
   CK(cudaEventCreate(&c->epoch));
   c->dm.d = cfg->d_model;
@@ -1070,7 +1072,7 @@ void vox_destroy(VoxCtx* c) {
     if (s.ev) cudaEventDestroy(s.ev);
   }
   if (c->s_lm) cudaStreamDestroy(c->s_lm);
-  if (c->s_dt) cudaStreamDestroy(c->s_dt);
+  if (c->s_dt && c->s_dt != c->s_lm) cudaStreamDestroy(c->s_dt);
   if (c->epoch) cudaEventDestroy(c->epoch);
   delete c;
 }
