@@ -160,9 +160,10 @@ __global__ void codec_hist_kernel(const float* __restrict__ x, int C, int k, int
 
 
 // out[rows, M] (+bias, +resid) = x[rows, K] . W[M, K]^T on the 1-CTA tcgen05 kernel, one split
+// gelu_out != null: the epilogue writes bf16(GELU(acc + bias)) there ([rows][M]) instead of fp32 out
 inline cudaError_t codec_gemm(const CUtensorMap& tw, int M, const bf16* x, int K, int64_t rows, float* out,
                               int64_t ldo, const float* bias, const float* resid, int64_t ldr, cudaStream_t st,
-                              int64_t* launches) {
+                              int64_t* launches, bf16* gelu_out = nullptr) {
   if (rows <= 0) return cudaSuccess;
   const int bn = gemm_bn_for_rows(static_cast<int>(rows < 256 ? rows : 256));
   CUtensorMap tx;
@@ -178,6 +179,11 @@ inline cudaError_t codec_gemm(const CUtensorMap& tw, int M, const bf16* x, int K
   a.resid = resid;
   a.ldr = ldr;
   a.m_valid = M;
+  if (gelu_out != nullptr) {
+    a.epi = 2;
+    a.act = gelu_out;
+    a.ld_act = M;
+  }
   ++*launches;
   return gemm_launch(tw, tx, a, 1, bn, 1, st);
 }

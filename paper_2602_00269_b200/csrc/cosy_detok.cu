@@ -558,8 +558,8 @@ cudaError_t cal(T** p, size_t n) {
 }
 
 int gemm(VoxCosy* m, const CUtensorMap& tw, int M, const bf16* x, int K, int64_t rows, float* out, int64_t ldo,
-         const float* bias, const float* resid, int64_t ldr) {
-  const cudaError_t e = codec_gemm(tw, M, x, K, rows, out, ldo, bias, resid, ldr, m->st, &m->launches);
+         const float* bias, const float* resid, int64_t ldr, bf16* gelu_out = nullptr) {
+  const cudaError_t e = codec_gemm(tw, M, x, K, rows, out, ldo, bias, resid, ldr, m->st, &m->launches, gelu_out);
   if (e != cudaSuccess) return cfail(m, VOX_ERR_CUDA, std::string("cosy gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
 }
@@ -786,10 +786,11 @@ int xf_layers(VoxCosy* m, std::vector<CdXf>& layers, float* h, int64_t rows, int
       CLK(cd_attn_kernel<<<dim3(nseg, heads), 256, cd_attn_smem(max_rows, hd), st>>>(m->qkv, seg, d, hd, inv, m->xbf));
     CRET(gemm(m, w.tm_o, d, m->xbf, d, rows, h, d, nullptr, h, d));
     CLK(launch_codec_ln(h, nullptr, nullptr, w.ln2w, w.ln2b, m->xbf, d, g.eps, rows, st));
-    CRET(gemm(m, w.tm_fc1, ffn, m->xbf, d, rows, m->tmp, ffn, nullptr, nullptr, 0));
-    const int64_t ne = rows * ffn;
-    CLK(codec_gelu_kernel<<<static_cast<unsigned>((ne + 255) / 256), 256, 0, st>>>(m->tmp, m->xbf, ne));
-    CRET(gemm(m, w.tm_fc2, d, m->xbf, ffn, rows, h, d, nullptr, h, d));
+    // fc1 with GELU + bf16 in its epilogue (the fp32 [rows][ffn] round trip and the
+    // GELU launch are gone); the activations land in tmp's storage
+    bf16* act = reinterpret_cast<bf16*>(m->tmp);
+    CRET(gemm(m, w.tm_fc1, ffn, m->xbf, d, rows, nullptr, ffn, nullptr, nullptr, 0, act));
+    CRET(gemm(m, w.tm_fc2, d, act, ffn, rows, h, d, nullptr, h, d));
   }
   return VOX_OK;
 }

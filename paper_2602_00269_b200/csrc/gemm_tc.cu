@@ -43,6 +43,16 @@ struct GemmCfg {
 // rows m, BN columns = activation rows n) -> registers -> smem (transposed)
 // -> 16-byte coalesced global stores.  `smem` is the idle pipeline ring.
 // ---------------------------------------------------------------------------
+VOX_DEV float gelu_erf(float v) { return 0.5f * v * (1.f + erff(v * 0.70710678118654752f)); }
+VOX_DEV void store_gelu4(bf16* dst, float4 v) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(gelu_erf(v.x), gelu_erf(v.y));
+  const __nv_bfloat162 hi = __floats2bfloat162_rn(gelu_erf(v.z), gelu_erf(v.w));
+  uint2 u;
+  u.x = *reinterpret_cast<const uint32_t*>(&lo);
+  u.y = *reinterpret_cast<const uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(dst) = u;
+}
+
 template <int BN, int MT>
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, uint32_t tmem,
                                               int warp, int lane, int m0, int n0, int split,
@@ -88,6 +98,41 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
           }
           *reinterpret_cast<uint4*>(p.act + static_cast<int64_t>(n) * p.ld_act + f0 + q) =
               make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  if (MT == 1 && p.epi == 2) {
+    // act = bf16(GELU(acc + bias)) (the codec FFN's fc1; codec_gelu_kernel's
+    // arithmetic), staged like the fp32 epilogue below; kept out of that loop so
+    // the erf sequence does not bloat every GEMM's unrolled store loop
+    if (done_bar != nullptr) {
+      mbar_wait(done_bar, 0);
+      tc_fence_after();
+    }
+    float* stg = reinterpret_cast<float*>(smem);
+    constexpr int kSt = 128 + 4;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(warp * 32) << 16) + c, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stg[j * kSt + warp * 32 + lane] = __uint_as_float(r[j]);
+      __syncthreads();
+#pragma unroll 1
+      for (int e = threadIdx.x; e < 32 * 32; e += 128) {
+        const int j = e >> 5, q = (e & 31) * 4;
+        const int n = n0 + c + j, m = m0 + q;
+        if ((c + j) < BN && n < p.N && m + 3 < p.m_valid) {
+          float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
+          if (p.bias != nullptr) {
+            const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
+            v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
+          }
+          store_gelu4(p.act + static_cast<int64_t>(n) * p.ld_act + m, v);
         }
       }
       __syncthreads();
