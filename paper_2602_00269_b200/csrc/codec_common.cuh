@@ -165,7 +165,11 @@ inline cudaError_t codec_gemm(const CUtensorMap& tw, int M, const bf16* x, int K
                               int64_t ldo, const float* bias, const float* resid, int64_t ldr, cudaStream_t st,
                               int64_t* launches, bf16* gelu_out = nullptr) {
   if (rows <= 0) return cudaSuccess;
-  const int bn = gemm_bn_for_rows(static_cast<int>(rows < 256 ? rows : 256));
+  // many-row GEMMs: 128-row activation tiles (3-stage, 96 KB ring, 128 TMEM
+  // columns) so two CTAs share an SM and one's epilogue overlaps the other's
+  // loads and MMAs (the 256-row tile ran one CTA per SM, load -> MMA -> epilogue
+  // serialised per wave)
+  const int bn = gemm_bn_for_rows(static_cast<int>(rows < 128 ? rows : 128));
   CUtensorMap tx;
   if (!make_tmap_bf16(&tx, x, K, rows, static_cast<uint64_t>(K) * 2, bn)) return cudaErrorInvalidValue;
   GemmArgs a{};

@@ -189,13 +189,26 @@ VOX_DEV uint32_t pack2(float lo, float hi) {
 
 constexpr int kTcHd = 64, kTcKs = 72;
 inline int cd_tc_npad(int n) { return (n + 63) / 64 * 64; }
+// one warp per 16 query rows of the longest segment (<= 16 warps)
+inline int cd_attn_tc_warps(int n) { const int w = (n + 15) / 16; return w < 1 ? 1 : (w > 16 ? 16 : w); }
 inline size_t cd_attn_tc_smem(int n) {
   const int np = cd_tc_npad(n);
-  return 2 * (static_cast<size_t>(np) * kTcKs + static_cast<size_t>(kTcHd) * (np + 8) + 8 * 16 * kTcKs);
+  return 2 * (static_cast<size_t>(np) * kTcKs + static_cast<size_t>(kTcHd) * (np + 8) +
+              static_cast<size_t>(cd_attn_tc_warps(n)) * 16 * kTcKs);
+}
+// RoPE (cos, sin) table [kCdMaxRows][hd / 2], filled once with the same sincosf
+// expression the attention kernels used per element (bit-identical values)
+__global__ void cd_rope_table_kernel(const float* __restrict__ inv_freq, int half, float2* __restrict__ tab) {
+  const int j = blockIdx.x, i = threadIdx.x;
+  if (i < half) {
+    float sn, cs;
+    sincosf(static_cast<float>(j) * inv_freq[i], &sn, &cs);
+    tab[j * half + i] = make_float2(cs, sn);
+  }
 }
 
-__global__ void __launch_bounds__(256) cd_attn_tc_kernel(const float* __restrict__ qkv, const SegDev* __restrict__ seg,
-                                                         int D, const float* __restrict__ inv_freq,
+__global__ void __launch_bounds__(512) cd_attn_tc_kernel(const float* __restrict__ qkv, const SegDev* __restrict__ seg,
+                                                         int D, const float2* __restrict__ rope,
                                                          bf16* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t smraw[];
   const SegDev q = seg[blockIdx.x];
@@ -206,38 +219,61 @@ __global__ void __launch_bounds__(256) cd_attn_tc_kernel(const float* __restrict
   bf16* Vt = Ks + np * kTcKs;                          // [64][np + 8]
   bf16* Qs = Vt + kTcHd * VS;                          // [8 warps][16][72]
   const float* base = qkv + static_cast<int64_t>(q.f_off) * 3 * D + hh * kTcHd;
-  for (int e = threadIdx.x; e < np * half; e += blockDim.x) {
-    const int j = e / half, i = e % half;
-    float k0 = 0.f, k1 = 0.f, sn = 0.f, cs = 1.f;
+  // staging: 4 consecutive dims per thread (float4 loads), loops unrolled so
+  // several rows' loads are in flight (the staging is latency-bound otherwise)
+#pragma unroll 4
+  for (int e = threadIdx.x; e < np * (half / 4); e += blockDim.x) {
+    const int j = e / (half / 4), i = (e % (half / 4)) * 4;
+    float4 k0 = make_float4(0.f, 0.f, 0.f, 0.f), k1 = k0;
+    float2 r[4] = {make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f)};
     if (j < n) {
       const float* kr = base + static_cast<int64_t>(j) * 3 * D + D;
-      k0 = kr[i];
-      k1 = kr[i + half];
-      sincosf(static_cast<float>(j) * inv_freq[i], &sn, &cs);
+      k0 = *reinterpret_cast<const float4*>(kr + i);
+      k1 = *reinterpret_cast<const float4*>(kr + i + half);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = rope[j * half + i + u];
     }
-    Ks[j * kTcKs + i] = f32_to_bf16(k0 * cs - k1 * sn);
-    Ks[j * kTcKs + i + half] = f32_to_bf16(k1 * cs + k0 * sn);
+    const float a0[4] = {k0.x, k0.y, k0.z, k0.w}, a1[4] = {k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      Ks[j * kTcKs + i + u] = f32_to_bf16(a0[u] * r[u].x - a1[u] * r[u].y);
+      Ks[j * kTcKs + i + u + half] = f32_to_bf16(a1[u] * r[u].x + a0[u] * r[u].y);
+    }
   }
-  for (int e = threadIdx.x; e < np * kTcHd; e += blockDim.x) {
-    const int j = e / kTcHd, d = e % kTcHd;
-    Vt[d * VS + j] = f32_to_bf16(j < n ? base[static_cast<int64_t>(j) * 3 * D + 2 * D + d] : 0.f);
+#pragma unroll 4
+  for (int e = threadIdx.x; e < np * (kTcHd / 4); e += blockDim.x) {
+    const int j = e / (kTcHd / 4), d = (e % (kTcHd / 4)) * 4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j < n) v = *reinterpret_cast<const float4*>(base + static_cast<int64_t>(j) * 3 * D + 2 * D + d);
+    Vt[d * VS + j] = f32_to_bf16(v.x);
+    Vt[(d + 1) * VS + j] = f32_to_bf16(v.y);
+    Vt[(d + 2) * VS + j] = f32_to_bf16(v.z);
+    Vt[(d + 3) * VS + j] = f32_to_bf16(v.w);
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int nw = blockDim.x >> 5;
   const float sl2 = rsqrtf(static_cast<float>(kTcHd)) * 1.4426950408889634f;  // scale * log2(e)
   bf16* Q = Qs + warp * 16 * kTcKs;
-  for (int t0 = warp * 16; t0 < n; t0 += 8 * 16) {
-    for (int e = lane; e < 16 * half; e += 32) {
-      const int r = e / half, i = e % half, row = t0 + r;
-      float q0 = 0.f, q1 = 0.f, sn = 0.f, cs = 1.f;
+  for (int t0 = warp * 16; t0 < n; t0 += nw * 16) {
+#pragma unroll
+    for (int e = lane; e < 16 * (half / 4); e += 32) {
+      const int rr = e / (half / 4), i = (e % (half / 4)) * 4, row = t0 + rr;
+      float4 q0 = make_float4(0.f, 0.f, 0.f, 0.f), q1 = q0;
+      float2 cs[4] = {make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f), make_float2(1.f, 0.f)};
       if (row < n) {
         const float* qr = base + static_cast<int64_t>(row) * 3 * D;
-        q0 = qr[i];
-        q1 = qr[i + half];
-        sincosf(static_cast<float>(row) * inv_freq[i], &sn, &cs);
+        q0 = *reinterpret_cast<const float4*>(qr + i);
+        q1 = *reinterpret_cast<const float4*>(qr + i + half);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cs[u] = rope[row * half + i + u];
       }
-      Q[r * kTcKs + i] = f32_to_bf16(q0 * cs - q1 * sn);
-      Q[r * kTcKs + i + half] = f32_to_bf16(q1 * cs + q0 * sn);
+      const float a0[4] = {q0.x, q0.y, q0.z, q0.w}, a1[4] = {q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        Q[rr * kTcKs + i + u] = f32_to_bf16(a0[u] * cs[u].x - a1[u] * cs[u].y);
+        Q[rr * kTcKs + i + u + half] = f32_to_bf16(a1[u] * cs[u].x + a0[u] * cs[u].y);
+      }
     }
     __syncwarp();
     uint32_t qa[4][4];
@@ -500,6 +536,7 @@ struct VoxCosy {
   float* step_bias = nullptr;  // [n_steps][d_est] = b_in + temb(t_i)
   std::vector<float> ts;
   float *inv_enc = nullptr, *inv_est = nullptr;
+  float2 *rope_enc = nullptr, *rope_est = nullptr;  // [kCdMaxRows][hd / 2] (cos, sin)
   bf16 *vpre = nullptr, *vpost = nullptr;
   float *vpreb = nullptr, *vpostb = nullptr;
   CUtensorMap tm_vpre, tm_vpost;
@@ -674,6 +711,11 @@ int create(VoxCosy* m, uint64_t seed) {
   };
   CRET(inv(&m->inv_enc, de, g.enc_heads));
   CRET(inv(&m->inv_est, ds, g.est_heads));
+  CCK(cal(&m->rope_enc, static_cast<size_t>(kCdMaxRows) * (de / g.enc_heads / 2)));
+  CCK(cal(&m->rope_est, static_cast<size_t>(kCdMaxRows) * (ds / g.est_heads / 2)));
+  cd_rope_table_kernel<<<kCdMaxRows, 64, 0, st>>>(m->inv_enc, de / g.enc_heads / 2, m->rope_enc);
+  cd_rope_table_kernel<<<kCdMaxRows, 64, 0, st>>>(m->inv_est, ds / g.est_heads / 2, m->rope_est);
+  CCK(cudaGetLastError());
   // vocoder
   const std::vector<int>& ch = m->ch;
   m->kp_pre = (g.voc_kernel * M + 63) / 64 * 64;
@@ -772,7 +814,7 @@ int create(VoxCosy* m, uint64_t seed) {
 }
 
 int xf_layers(VoxCosy* m, std::vector<CdXf>& layers, float* h, int64_t rows, int d, int heads, int ffn, int nseg,
-              const int32_t* row_seg, const SegDev* seg, const float* inv, int max_rows) {
+              const int32_t* row_seg, const SegDev* seg, const float* inv, const float2* rope, int max_rows) {
   (void)row_seg;
   const VoxCosyCfg& g = m->cfg;
   cudaStream_t st = m->st;
@@ -781,7 +823,8 @@ int xf_layers(VoxCosy* m, std::vector<CdXf>& layers, float* h, int64_t rows, int
     CLK(launch_codec_ln(h, nullptr, nullptr, w.ln1w, w.ln1b, m->xbf, d, g.eps, rows, st));
     CRET(gemm(m, w.tm_qkv, 3 * d, m->xbf, d, rows, m->qkv, 3 * d, nullptr, nullptr, 0));
     if (hd == kTcHd && !m->attn_fp32)
-      CLK(cd_attn_tc_kernel<<<dim3(nseg, heads), 256, cd_attn_tc_smem(max_rows), st>>>(m->qkv, seg, d, inv, m->xbf));
+      CLK(cd_attn_tc_kernel<<<dim3(nseg, heads), 32 * cd_attn_tc_warps(max_rows), cd_attn_tc_smem(max_rows), st>>>(
+          m->qkv, seg, d, rope, m->xbf));
     else
       CLK(cd_attn_kernel<<<dim3(nseg, heads), 256, cd_attn_smem(max_rows, hd), st>>>(m->qkv, seg, d, hd, inv, m->xbf));
     CRET(gemm(m, w.tm_o, d, m->xbf, d, rows, h, d, nullptr, h, d));
@@ -810,7 +853,8 @@ int enqueue(VoxCosy* m, int n, int64_t E, int64_t V) {
   StateView sv{m->state, 2 * m->half, m->half};
   // ---------------- flow: encoder over [ref | new] tokens
   CLK(cd_embed_kernel<<<static_cast<unsigned>(E), 128, 0, st>>>(row_seg, fseg, m->reftok, ref, toks, m->emb, de, m->h));
-  CRET(xf_layers(m, m->enc, m->h, E, de, g.enc_heads, g.enc_ffn, n, row_seg, fseg, m->inv_enc, m->max_seg));
+  CRET(xf_layers(m, m->enc, m->h, E, de, g.enc_heads, g.enc_ffn, n, row_seg, fseg, m->inv_enc, m->rope_enc,
+                 m->max_seg));
   CLK(launch_codec_ln(m->h, nullptr, nullptr, m->elnfw, m->elnfb, m->xbf, de, g.eps, E, st));
   CRET(gemm(m, m->tm_mu, M, m->xbf, de, E, m->mu_t, M, m->mub, nullptr, 0));
   // ---------------- flow matching ODE (CFG: rows [0, R) cond, [R, 2R) uncond)
@@ -824,7 +868,7 @@ int enqueue(VoxCosy* m, int n, int64_t E, int64_t V) {
                                                                                  m->refmel, ref, M, R, m->xbf));
     CRET(gemm(m, m->tm_in, ds, m->xbf, 4 * M, 2 * R, m->z, ds, m->step_bias + static_cast<int64_t>(i) * ds, nullptr, 0));
     CRET(xf_layers(m, m->est, m->z, 2 * R, ds, g.est_heads, g.est_ffn, 2 * n, mrow_seg, gseg, m->inv_est,
-                   2 * m->max_seg));
+                   m->rope_est, 2 * m->max_seg));
     CLK(launch_codec_ln(m->z, nullptr, nullptr, m->olnw, m->olnb, m->xbf, ds, g.eps, 2 * R, st));
     CRET(gemm(m, m->tm_out, M, m->xbf, ds, 2 * R, m->v, M, m->outb, nullptr, 0));
     CLK(cd_euler_kernel<<<static_cast<unsigned>((nx + 255) / 256), 256, 0, st>>>(m->x, m->v, nx, m->ts[i + 1] - m->ts[i], lam));
@@ -898,7 +942,8 @@ void vox_cosy_destroy(VoxCosy* m) {
                   static_cast<void*>(m->mub), static_cast<void*>(m->olnw), static_cast<void*>(m->olnb),
                   static_cast<void*>(m->outb), static_cast<void*>(m->mu), static_cast<void*>(m->w_in),
                   static_cast<void*>(m->w_out), static_cast<void*>(m->step_bias), static_cast<void*>(m->inv_enc),
-                  static_cast<void*>(m->inv_est), static_cast<void*>(m->vpre), static_cast<void*>(m->vpost),
+                  static_cast<void*>(m->inv_est), static_cast<void*>(m->rope_enc), static_cast<void*>(m->rope_est),
+                  static_cast<void*>(m->vpre), static_cast<void*>(m->vpost),
                   static_cast<void*>(m->vpreb), static_cast<void*>(m->vpostb), static_cast<void*>(m->reftok),
                   static_cast<void*>(m->spk), static_cast<void*>(m->refmel), static_cast<void*>(m->state),
                   static_cast<void*>(m->h), static_cast<void*>(m->qkv), static_cast<void*>(m->tmp),
