@@ -158,13 +158,17 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
       const int j = e >> 5, q = (e & 31) * 4;
       const int n = n0 + c + j;
       float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if ((c + j) < BN && n < p.N && p.resid != nullptr)
+      if ((c + j) < BN && n < p.N && p.resid != nullptr && mb + q < p.m_valid)
         a = *reinterpret_cast<const float4*>(p.resid + static_cast<int64_t>(n) * p.ldr + mb + q);
       rr[i] = a;
     }
   };
+  // float4 path whenever every 4-column group is wholly valid or wholly past
+  // m_valid (M % 4 == 0: e.g. the 32/64-channel codec convs that fill only part
+  // of the 128-row weight tile) and the rows are 16-byte aligned
   auto is_full = [&](int mb) {
-    return mb + 128 <= p.m_valid && (p.ldo & 3) == 0 && (p.resid == nullptr || (p.ldr & 3) == 0) &&
+    (void)mb;
+    return (p.m_valid & 3) == 0 && (p.ldo & 3) == 0 && (p.resid == nullptr || (p.ldr & 3) == 0) &&
            (reinterpret_cast<uintptr_t>(outp) & 15) == 0;
   };
   prefetch(m0, 0, is_full(m0));
@@ -196,6 +200,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& p, uint8_t* smem, 
           float4 v = *reinterpret_cast<const float4*>(&stg[j * kSt + q]);
           const int m = mb + q;
           if (full_m) {
+            if (m >= p.m_valid) continue;
             if (p.bias != nullptr) {
               const float4 b4 = *reinterpret_cast<const float4*>(p.bias + m);
               v.x += b4.x; v.y += b4.y; v.z += b4.z; v.w += b4.w;
