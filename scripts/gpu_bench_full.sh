@@ -1,4 +1,7 @@
+# full evidence run: GPU tests, smoke, default bench (SLO + CPU + configs 3/4), reference arm
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -4 > gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1
 timeout 2400 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-head -c 600 gpurun_out/bench_full.json; echo; head -c 300 gpurun_out/bench_ref.json
+cat gpurun_out/pytest_gpu.log; tail -1 gpurun_out/smoke.log; head -c 400 gpurun_out/bench_full.json; echo
