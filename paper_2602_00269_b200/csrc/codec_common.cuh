@@ -3,6 +3,7 @@
 // GELU, causal-conv im2col with cached history, history update, and the tcgen05 GEMM
 // call (gemm_tc.cu) on plain row-major bf16 weights.
 #pragma once
+#include <cstdlib>
 #include <cuda.h>
 
 #include <string>
@@ -189,6 +190,12 @@ inline cudaError_t codec_gemm(const CUtensorMap& tw, int M, const bf16* x, int K
     a.ld_act = M;
   }
   ++*launches;
+  // many tiles: the persistent kernel (epilogue of tile t overlaps tile t+1)
+  // (M >= 256: 256-row weight tiles, so each activation stage feeds two MMAs)
+  static const int persist = getenv("VOX_CODEC_PERSIST") ? atoi(getenv("VOX_CODEC_PERSIST")) : 2;
+  const int64_t tiles = (rows + bn - 1) / bn * ((M + 127) / 128);
+  if (persist > 0 && bn == 128 && tiles >= 2 * kNumSMs)
+    return gemm_launch_persist(tw, tx, a, bn, (persist == 2 && M >= 256) ? 2 : 1, st);
   return gemm_launch(tw, tx, a, 1, bn, 1, st);
 }
 

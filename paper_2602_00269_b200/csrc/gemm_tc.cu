@@ -643,6 +643,171 @@ __global__ void __launch_bounds__(256, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent GEMM for many-tile activation streams (the codec detokenizers'
+// transformer / conv GEMMs: tens of thousands of rows, K = 256..2048).
+//
+// One CTA per SM loops over 128 x BN output tiles (n-tiles fastest, so the CTAs
+// of a wave share each weight tile in L2).  Warp 0 / lane 0 streams W and X
+// k-blocks by TMA through one ring that runs on across tiles, warp 1 / lane 0
+// issues tcgen05.mma into one of two TMEM accumulators, and warps 4..11 drain
+// the other accumulator straight to global (TMEM lane = output channel m, so a
+// warp's 32 lanes write 32 consecutive channels of one row: 128-byte stores, no
+// smem staging) -- tile t's epilogue overlaps tile t+1's loads and MMAs,
+// instead of one load -> MMA -> epilogue per CTA lifetime.
+// Epilogues: fp32 out (+ bias[m]) (+ resid[n][m]); epi == 2: bf16(GELU(acc + b)).
+// ---------------------------------------------------------------------------
+constexpr int kPersistThreads = 384;
+template <int BN, int MT>
+struct PersistCfg {
+  static constexpr int kABytes = MT * 128 * 64 * 2;  // MT weight sub-tiles share one X stage
+  static constexpr int kStageBytes = kABytes + BN * 64 * 2;
+  static constexpr int kStages = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kCols = MT * (BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256);  // per buffer
+  static constexpr int kSmem = 1024 + kStages * kStageBytes + 256;
+};
+
+template <int BN, int MT>
+__global__ void __launch_bounds__(kPersistThreads, 1)
+    gemm_persist_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                        GemmArgs p) {
+  VOX_TRACE(kTrGemm);
+  using C = PersistCfg<BN, MT>;
+  constexpr int ST = C::kStages;
+  constexpr int kSub = C::kCols / MT;  // TMEM columns of one weight sub-tile
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ST * C::kStageBytes);
+  uint64_t* empty = full + ST;
+  uint64_t* tfull = empty + ST;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_nt = (p.N + BN - 1) / BN, n_mt = (p.M + 128 * MT - 1) / (128 * MT);
+  const int ntiles = n_nt * n_mt;
+  const int nkb = p.n_kb;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmW);
+    tma_prefetch_desc(&tmX);
+    for (int s = 0; s < ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 2 * C::kCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint64_t pol_w = policy_evict_last(), pol_x = policy_evict_first();
+      griddep_wait();  // X is the preceding kernel's output
+      griddep_launch();
+      int g = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = (t / n_nt) * 128 * MT, n0 = (t % n_nt) * BN;
+        for (int i = 0; i < nkb; ++i, ++g) {
+          const int s = g % ST;
+          if (g >= ST) mbar_wait(&empty[s], ((g / ST) - 1) & 1);
+          uint8_t* st = smem + s * C::kStageBytes;
+          mbar_arrive_expect_tx(&full[s], C::kStageBytes);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) tma_load_2d(st + mt * 16384, &tmW, &full[s], i * 64, m0 + mt * 128, pol_w);
+          tma_load_2d(st + C::kABytes, &tmX, &full[s], i * 64, n0, pol_x);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+      int g = 0, u = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++u) {
+        const int b = u & 1;
+        if (u >= 2) mbar_wait(&tempty[b], ((u >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + b * C::kCols;
+        for (int i = 0; i < nkb; ++i, ++g) {
+          const int s = g % ST;
+          mbar_wait(&full[s], (g / ST) & 1);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + s * C::kStageBytes);
+          const uint32_t b_addr = a_addr + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+              umma_bf16(d + mt * kSub, make_desc_k128(a_addr + mt * 16384 + k * 32), make_desc_k128(b_addr + k * 32),
+                        idesc, (i > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[b]);
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // MT == 1: warps w and w + 4 split the tile's 32-column chunks; MT == 2: warps
+    // 4..7 drain weight sub-tile 0, warps 8..11 sub-tile 1
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    const int sub = MT == 2 ? h : 0, c0 = MT == 2 ? 0 : h, cstep = MT == 2 ? 1 : 2;
+    griddep_wait();  // outputs may alias buffers the preceding kernel was reading
+    griddep_launch();
+    constexpr int kChunks = (BN + 31) / 32;
+    int u = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++u) {
+      const int m0 = (t / n_nt) * 128 * MT + sub * 128, n0 = (t % n_nt) * BN;
+      const int b = u & 1;
+      const int m = m0 + q * 32 + lane;
+      const bool mok = m < p.m_valid;
+      const float bias = (p.bias != nullptr && mok) ? p.bias[m] : 0.f;
+      const int nv = min(BN, p.N - n0);
+      mbar_wait(&tfull[b], (u >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + b * C::kCols + sub * kSub;
+#pragma unroll 1
+      for (int ch = c0; ch < kChunks; ch += cstep) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tbase + ch * 32, r);
+        tmem_ld_wait();
+        if (!mok) continue;
+        const int lim = nv - ch * 32;
+        const int64_t n = n0 + ch * 32;
+        if (p.epi == 2) {
+          bf16* o = p.act + n * p.ld_act + m;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) o[j * p.ld_act] = __float2bfloat16_rn(gelu_erf(__uint_as_float(r[j]) + bias));
+        } else if (p.resid != nullptr) {
+          const float* rs = p.resid + n * p.ldr + m;
+          float rv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rv[j] = j < lim ? rs[j * p.ldr] : 0.f;
+          float* o = p.out + n * p.ldo + m;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) o[j * p.ldo] = (__uint_as_float(r[j]) + bias) + rv[j];
+        } else {
+          float* o = p.out + n * p.ldo + m;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) o[j * p.ldo] = __uint_as_float(r[j]) + bias;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 2 * C::kCols);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -856,6 +1021,32 @@ cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a
     case 128: return launch_bn<128, 1>(tw, tx, a, splits, st);
     default: return launch_bn<256, 1>(tw, tx, a, splits, st);
   }
+}
+
+template <int BN, int MT>
+static cudaError_t launch_persist(const CUtensorMap& tw, const CUtensorMap& tx, const GemmArgs& a, cudaStream_t st) {
+  using C = PersistCfg<BN, MT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_persist_kernel<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((a.N + BN - 1) / BN) * ((a.M + 128 * MT - 1) / (128 * MT));
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  return launch_k(gemm_persist_kernel<BN, MT>, dim3(grid), dim3(kPersistThreads), C::kSmem, st, tw, tx, a);
+}
+
+// one split; tx = activation map with box rows bn (128); mt = 2: 256-row weight
+// tiles sharing each activation stage (activations read from L2 half as often)
+cudaError_t gemm_launch_persist(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int bn, int mt,
+                                cudaStream_t st) {
+  a.n_kb = a.K / 64;
+  a.kb_per_split = a.n_kb;
+  if (a.epi == 2 && a.resid != nullptr) return cudaErrorInvalidValue;
+  if (bn != 128) return cudaErrorInvalidValue;
+  return mt == 2 ? launch_persist<128, 2>(tw, tx, a, st) : launch_persist<128, 1>(tw, tx, a, st);
 }
 
 }  // namespace vox

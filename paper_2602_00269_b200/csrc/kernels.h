@@ -69,6 +69,9 @@ GemmPlan gemm_plan(int M, int rows, int K);
 GemmPlan gemm_plan_1cta(int M, int rows, int K);  // the 1-CTA kernel only
 cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int splits,
                         int bn, int mt, cudaStream_t st);
+// persistent many-tile GEMM (codec detokenizers): one split, bn 128, mt 1 or 2
+cudaError_t gemm_launch_persist(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int bn, int mt,
+                                cudaStream_t st);
 // decode kernel: tx = activation map with box rows bn
 cudaError_t gemm_launch_mc(const CUtensorMap& tx, GemmArgs a, int splits, int bn, cudaStream_t st);
 int gemm_mc_capacity(int bn);
