@@ -1,5 +1,5 @@
 """DRAM traffic per launch (dram__bytes_read.sum + dram__bytes_write.sum) from ncu
---set full captures -> profiles/traffic_r01.json ({kernel class: bytes per launch}),
+--set full captures -> profiles/traffic_rNN.json (NN from $VOX_ROUND, default 02) ({kernel class: bytes per launch}),
 plus a one-line-per-launch summary of the key counters.
 
 usage: python scripts/ncu_traffic.py gemm=gpurun_out/prof_gemm.ncu-rep attn=gpurun_out/prof_attn.ncu-rep
@@ -48,7 +48,9 @@ def main():
                          f"tensor% {l.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 0):5.1f}  "
                          f"lts% {l.get('lts__throughput.avg.pct_of_peak_sustained_elapsed', 0):5.1f}  "
                          f"regs {int(l.get('launch__registers_per_thread', 0))}")
-    (ROOT / "profiles" / "traffic_r01.json").write_text(json.dumps(res, indent=1) + "\n")
+    import os
+    rnd = os.environ.get("VOX_ROUND", "02")
+    (ROOT / "profiles" / f"traffic_r{rnd}.json").write_text(json.dumps(res, indent=1) + "\n")
     print("\n".join(lines))
     print(json.dumps(res))
 
