@@ -851,6 +851,45 @@ def reference_host_path(n_rows: int = 60):
                     "of config 1 (4 x 64 tokens, orpheus_like at V=156,940, async) -- hash-stub LM, no audio"}
 
 
+def reference_protocol(device: int):
+    """The drop-in boundary measured: BASELINE config 1's workload (4 requests x 64 tokens
+    at t=0, orpheus_like at V = 156,940, async pipeline) through the UNMODIFIED reference
+    SimEngine (engine.py:146 run) with ``engine.executor = B200Executor(...)`` on the
+    config-1 model (2-layer Llama, SNAC-style decoder; the host's reference sample()
+    still picks every token from the returned logits), next to the same engine with the
+    reference's own SyntheticExecutor (hash-stub LM, no audio)."""
+    from dataclasses import replace
+
+    from paper_2602_00269_b200._ref import core, profiles, ref_engine, scheduler, workload
+    from paper_2602_00269_b200.config import tiny
+    from paper_2602_00269_b200.executor import B200Executor
+
+    V = 156940
+    prof = replace(profiles.builtin_profile("orpheus_like"), vocab_size=V)
+    arr = list(enumerate(workload.build_workload(workload.WorkloadSpec(
+        rate=0.0, offline_count=4, prompt_dist=workload.fixed(50), output_dist=workload.fixed(64), seed=0))))
+    out = {}
+    for name in ("reference_synthetic", "b200_executor"):
+        eng = ref_engine.SimEngine(prof, scheduler.PolicyConfig(), ref_engine.PipelineMode.ASYNCHRONOUS, seed=0)
+        ex = None
+        if name == "b200_executor":
+            ex = B200Executor(prof, tiny(max_slots=8, max_ctx=1024, max_rows=256, max_detok_frames=256), 0, device)
+            eng.executor = ex
+        t0 = time.perf_counter()
+        tr = eng.run(arr)
+        wall = time.perf_counter() - t0
+        rep = core.build_report(tr)
+        toks = sum(r.tokens_generated for r in tr.requests)
+        out[name] = {"wall_s": round(wall, 3), "tokens": toks, "tok_per_s": round(toks / wall, 1),
+                     "requests_completed": rep.requests_completed}
+        if ex is not None:
+            ex.dev.close()
+    out["what"] = ("config 1 (4 x 64 tokens) through the unmodified reference SimEngine: its own SyntheticExecutor "
+                   "vs engine.executor = B200Executor (real 2-layer LM + SNAC-style audio on the B200; the "
+                   "reference's host sample() at V = 156,940 still picks every token)")
+    return out
+
+
 def cpu_port_sample(seconds_budget: float = 20.0):
     """Oracle port of the same step on host cores (bounded sample); returns audio-s/s."""
     from oracle.cpu_step import time_cpu_step
@@ -1014,6 +1053,13 @@ def main():
         except Exception as e:  # report, never mask the headline
             csm = {"error": repr(e)[:200]}
 
+    proto = None
+    if not args.no_cpu and rank == 0:
+        try:
+            proto = reference_protocol(local)
+        except Exception as e:  # report, never mask the headline
+            proto = {"error": repr(e)[:200]}
+
     cpu = None
     if not args.no_cpu and rank == 0:
         from oracle.cpu_step import time_cpu_step
@@ -1038,6 +1084,7 @@ def main():
             "cpu_baseline": cpu,
             "slo": slo,
             "config3_csm_frames": csm,
+            "reference_protocol": proto,
             "config4_cosyvoice2_lm": cosy,
             "detail": {"tokens_decoded": decoded, "chunks": chunks, "pcm_samples": pcm,
                        "mean_decode_ctx": round(res["mean_ctx"], 1), "prefill_rows": res["prefill_rows"],
