@@ -110,6 +110,7 @@ struct LmDims {
 // embedding; ext (nullable): fp32 [rows][d] inputs of token == -2 rows
 void launch_link_tokens(const int* links, int n, const int* src_ts, int src_max_ctx, int* dst,
                         int dst_max_ctx, int nfc, int offset, int mode, cudaStream_t st);
+void launch_advance_rows(RowDev* rows, int n, cudaStream_t st);
 void launch_embed_norm(const RowDev* rows, int n, int* token_store, const int* frame, int nfc,
                        const float* ext, int max_ctx, const bf16* emb,
                        const float* norm_w, const LmDims& dm, float* h, bf16* x, cudaStream_t st);

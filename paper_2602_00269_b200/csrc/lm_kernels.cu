@@ -103,6 +103,24 @@ void launch_embed_norm(const RowDev* rows, int n, int* token_store, const int* f
            emb, norm_w, dm.d, dm.eps, h, x);
 }
 
+// multi-step decode (vox_forward_steps): every live row moves to its next position and
+// takes its input from the token store (the previous step's sample); one row per
+// slot, so the row's position is also the lowest position it appends (fresh)
+__global__ void advance_rows_kernel(RowDev* rows, int n) {
+  griddep_wait();
+  griddep_launch();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && rows[i].slot >= 0) {
+    rows[i].pos += 1;
+    rows[i].token = -1;
+    rows[i].fresh = rows[i].pos;
+  }
+}
+
+void launch_advance_rows(RowDev* rows, int n, cudaStream_t st) {
+  launch_k(advance_rows_kernel, dim3((n + 127) / 128), dim3(128), 0, st, rows, n);
+}
+
 // token hand-over between two contexts (CSM backbone <-> depth decoder)
 __global__ void link_tokens_kernel(const int* __restrict__ links, int n, const int* __restrict__ src_ts,
                                    int src_max_ctx, int* __restrict__ dst, int dst_max_ctx, int nfc,

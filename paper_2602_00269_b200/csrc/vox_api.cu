@@ -192,6 +192,10 @@ struct VoxCtx {
   // ---- graphs keyed by (row bucket, sample bucket)
   // key = (row bucket, sample bucket, head frame slot or -1)
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
+  // vox_forward_steps: steps 1.. of a multi-step decode as ONE graph, keyed by
+  // (row bucket, sample bucket, first head frame slot, steps, sampler on)
+  std::map<std::tuple<int, int, int, int, int>, cudaGraphExec_t> step_graphs;
+  std::map<std::tuple<int, int, int, int, int>, int64_t> step_graph_launches;
   std::map<std::tuple<int, int, int>, int64_t> graph_launches;
   int64_t fwd_seq = 0;
   std::vector<cudaEvent_t> fwd_events;  // ring
@@ -1021,6 +1025,7 @@ void vox_destroy(VoxCtx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : c->step_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : c->detok_graphs) cudaGraphExecDestroy(kv.second);
   for (auto& t : c->tickets) {
     if (t.ev) cudaEventDestroy(t.ev);
@@ -1353,16 +1358,104 @@ int vox_forward_steps(VoxCtx* c, const VoxRow* rows, int32_t n, int32_t steps, u
   if (!c || !rows || n <= 0 || steps < 1 || !(flags & VOX_FWD_SAMPLE) ||
       (flags & (VOX_FWD_FULL_LOGITS | VOX_FWD_SYNC)))
     return fail(c, VOX_ERR_INVALID, "bad multi-step forward");
-  std::vector<VoxRow> r(rows, rows + n);
-  for (int k = 0; k < steps; ++k) {
-    if (k > 0)
-      for (auto& x : r) {
-        ++x.pos;
-        x.token = -1;  // the previous step's sample, from the token store
-      }
-    const int rc = vox_forward(c, r.data(), n, flags, nullptr, nullptr);
-    if (rc != VOX_OK) return rc;
+  const VoxModelCfg& g = c->cfg;
+  // every row: one distinct slot, sampled, the same step of the same prompt length
+  // (the CSM depth decoder) -> steps 1.. run as one graph of [advance rows, step]
+  bool uniform = steps > 1 && !(flags & VOX_FWD_NO_GRAPH) && !c->timing && !c->no_graphs;
+  for (int i = 0; i < n && uniform; ++i) {
+    const VoxRow& r = rows[i];
+    if (!r.sample || r.slot < 0 || r.slot >= g.max_slots || !c->slot_used[r.slot]) uniform = false;
+    else if (r.pos - c->h_prompt[r.slot] != rows[0].pos - c->h_prompt[rows[0].slot]) uniform = false;
+    else {
+      const int cap = static_cast<int>(c->slot_pages[r.slot].size()) * g.page_size;
+      if (r.pos + steps - 1 >= cap || r.pos + steps >= g.max_ctx) uniform = false;
+    }
   }
+  if (uniform) {
+    std::vector<int> sl(n);
+    for (int i = 0; i < n; ++i) sl[i] = rows[i].slot;
+    std::sort(sl.begin(), sl.end());
+    for (int i = 1; i < n && uniform; ++i)
+      if (sl[i] == sl[i - 1]) uniform = false;
+  }
+  if (!uniform) {
+    std::vector<VoxRow> r(rows, rows + n);
+    for (int k = 0; k < steps; ++k) {
+      if (k > 0)
+        for (auto& x : r) {
+          ++x.pos;
+          x.token = -1;  // the previous step's sample, from the token store
+        }
+      const int rc = vox_forward(c, r.data(), n, flags, nullptr, nullptr);
+      if (rc != VOX_OK) return rc;
+    }
+    return VOX_OK;
+  }
+  // step 0 uploads the rows; steps 1.. advance them on the device
+  int rc = vox_forward(c, rows, n, flags, nullptr, nullptr);
+  if (rc != VOX_OK) return rc;
+  int nrows = bucket_of(n);
+  if (nrows < 0 || nrows > g.max_rows) nrows = n;
+  int ns = bucket_of(n);
+  if (ns < 0 || ns > nrows) ns = n;
+  const bool run_sampler = true;
+  auto hslot_of = [&](int k) {  // vox_forward's frame-slot rule at step k
+    if (g.audio_base < 0 || g.frame_tokens <= 1 || g.codebook_size % 128) return -1;
+    const int step = rows[0].pos + k + 1 - c->h_prompt[rows[0].slot];
+    return ((step % g.frame_tokens) + g.frame_tokens) % g.frame_tokens;
+  };
+  cudaStream_t st = c->s_lm;
+  auto key = std::make_tuple(nrows, ns, hslot_of(1), steps, run_sampler ? 1 : 0);
+  auto it = c->step_graphs.find(key);
+  if (it == c->step_graphs.end()) {
+    const int64_t before = c->launches;
+    cudaGraph_t graph;
+    c->capturing = true;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    for (int k = 1; k < steps && rc == VOX_OK; ++k) {
+      launch_advance_rows(c->d_rows, nrows, st);
+      rc = enqueue_forward(c, nrows, ns, false, hslot_of(k), run_sampler);
+    }
+    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    c->capturing = false;
+    if (rc != VOX_OK) return rc;
+    CK(ce);
+    cudaGraphExec_t ex;
+    CK(cudaGraphInstantiate(&ex, graph, 0));
+    cudaGraphDestroy(graph);
+    c->step_graph_launches[key] = c->launches - before;
+    c->step_graphs[key] = ex;
+    it = c->step_graphs.find(key);
+    c->launches = before;
+  }
+  CK(cudaGraphLaunch(it->second, st));
+  c->launches += c->step_graph_launches[key];
+  {  // the logits buffer now holds the last step's head rows
+    const int hs = hslot_of(steps - 1);
+    c->last_logit_rows = n;
+    c->last_logit_ld = hs >= 0 ? g.codebook_size : (g.audio_base >= 0 ? c->head_audio_rows : g.vocab);
+    c->last_logit_base = g.audio_base >= 0 ? g.audio_base + (hs >= 0 ? hs * g.codebook_size : 0) : 0;
+  }
+  // error flag / ordering bookkeeping of one forward for the whole sequence
+  FwdStage& sg = c->stages[static_cast<size_t>(c->stage_seq++ % static_cast<int64_t>(c->stages.size()))];
+  if (sg.in_flight) {
+    CK(cudaEventSynchronize(sg.ev));
+    sg.in_flight = false;
+    if (*sg.err) {
+      const int e = *sg.err;
+      *sg.err = 0;
+      return check_err_value(c, e);
+    }
+  }
+  CK(cudaMemcpyAsync(sg.err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemsetAsync(c->d_err, 0, sizeof(int), st));
+  CK(cudaEventRecord(sg.ev, st));
+  sg.in_flight = true;
+  const int64_t seq = ++c->fwd_seq;
+  const int ei = static_cast<int>(seq % static_cast<int64_t>(c->fwd_events.size()));
+  CK(cudaEventRecord(c->fwd_events[ei], st));
+  c->fwd_event_seq[ei] = seq;
+  for (int i = 0; i < n; ++i) c->slot_last_fwd[rows[i].slot] = seq;
   return VOX_OK;
 }
 
