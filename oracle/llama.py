@@ -8,8 +8,10 @@ Qwen2 variant (q/k/v projections with bias: [3P] models/qwen2/modeling_qwen2.py
 Qwen2Attention) -- and mirrors the GPU rounding points exactly: bf16 weights,
 fp32 residual stream, bf16 GEMM inputs (normalised x, attention output,
 SiLU*up), fp32 accumulation, fp32 logits.
-Parity status: UNPINNED by the reference (no LM arithmetic there); checked
-against the device path by tests/test_gpu_lm.py and tests/test_gpu_cosy.py.
+Parity status: no LM arithmetic in the reference; pinned to transformers'
+LlamaForCausalLM / Qwen2ForCausalLM on shared weights (tests/test_llama_oracle.py:
+1.1e-6 max-relative with the rounding points off) and checked against the device
+path by tests/test_gpu_lm.py, test_gpu_config2_parity.py and test_gpu_cosy.py.
 """
 
 from __future__ import annotations
