@@ -2146,8 +2146,26 @@ int vox_gemm_test(VoxCtx* c, const uint16_t* w, const uint16_t* x, const float* 
   for (int it = 0; it < iters && rc == VOX_OK; ++it) {
     launch_l2_flush(flush, flush_bytes, sink, c->s_lm);  // clean L2 lines, not dirty ones
     CK(cudaEventRecord(a, c->s_lm));
-    rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
-                  c->s_lm, "gemm", wpk, nullptr, 0);
+    // VOX_GEMM_PERSIST_TEST=1|2: the codec detokenizers' persistent kernel (MT 1|2), one split
+    const int pt = getenv("VOX_GEMM_PERSIST_TEST") ? atoi(getenv("VOX_GEMM_PERSIST_TEST")) : 0;
+    if (pt == 1 || pt == 2) {
+      CUtensorMap tx;
+      if (splits != 1 || !make_tmap_bf16(&tx, dx, K, N, K * 2ull, 128))
+        return fail(c, VOX_ERR_INVALID, "persistent GEMM test: one split, tensor map");
+      GemmArgs ga{};
+      ga.M = M;
+      ga.N = N;
+      ga.K = K;
+      ga.out = dout;
+      ga.ldo = M;
+      ga.bias = db;
+      ga.m_valid = M;
+      const cudaError_t e = gemm_launch_persist(tw, tx, ga, 128, pt, c->s_lm);
+      if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("persistent gemm: ") + cudaGetErrorString(e));
+    } else {
+      rc = run_gemm(c, tw, xm, M, N, K, dout, M, splits, splits == 1 ? db : nullptr, nullptr, 0, M,
+                    c->s_lm, "gemm", wpk, nullptr, 0);
+    }
     CK(cudaEventRecord(b, c->s_lm));
     CK(cudaEventSynchronize(b));
     float ms = 0.f;

@@ -58,3 +58,19 @@ def test_gemm_two_row_tiles(tiny_dev, monkeypatch, M, N, K):
     out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), None, 1)
     ref = x.astype(np.float64) @ w.astype(np.float64).T
     assert np.abs(out - ref).max() < 1e-3 * np.sqrt(K)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 4096, 256), (768, 5000, 256), (1024, 3000, 1024), (80, 2500, 512),
+                                   (384, 4100, 768)])
+@pytest.mark.parametrize("mt", [1, 2])
+def test_gemm_persistent(tiny_dev, monkeypatch, M, N, K, mt):
+    """The codec detokenizers' persistent many-tile GEMM (gemm_persist_kernel): TMA ring
+    across tiles, double-buffered TMEM, direct epilogue with bias; ragged M and N tails."""
+    monkeypatch.setenv("VOX_GEMM_PERSIST_TEST", str(mt))
+    rng = np.random.default_rng(M + N + K + mt)
+    w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
+    x = bf16_round(rng.uniform(-1, 1, size=(N, K)).astype(np.float32))
+    bias = rng.uniform(-1, 1, size=M).astype(np.float32)
+    out, _ = tiny_dev.gemm_test(_bits(w), _bits(x), bias, 1)
+    ref = x.astype(np.float64) @ w.astype(np.float64).T + bias
+    assert np.abs(out - ref).max() < 1e-3 * np.sqrt(K)
