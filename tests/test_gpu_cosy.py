@@ -111,3 +111,56 @@ def test_greedy_speech_tokens(cosy):
     for r, sl in enumerate(slots):
         dev.release(sl)
         orc.release(("g", r))
+
+
+def test_greedy_speech_tokens_bit_exact_planted():
+    """CosyVoice2-style LM (q|k|v bias, GQA 14:2), planted-margin init as config 1's
+    (config.tiny_planted's embedding scale): 2 greedy requests x 32 speech tokens, rp
+    1.1, free-running on the serving path.  Precondition asserted at EVERY decision:
+    the oracle's penalised top-2 margin exceeds 10x that step's measured device /
+    oracle logit error; then every device token equals the oracle's greedy choice on
+    the same history, so the device stream IS the oracle's free-running stream."""
+    from dataclasses import replace
+
+    from paper_2602_00269_b200.config import PLANTED_EMBED_MULT, PLANTED_WEIGHT_SEED, tiny_cosy
+    from paper_2602_00269_b200.device import VoxDevice
+
+    base = tiny_cosy(max_slots=4)
+    cfg = replace(base, embed_scale=PLANTED_EMBED_MULT * base.embed_half_width)
+    dev = VoxDevice(cfg, weight_seed=PLANTED_WEIGHT_SEED)
+    orc = LlamaOracle(cfg, PLANTED_WEIGHT_SEED)
+    P, T, R, pen = 30, 32, 2, 1.1
+    greedy = Sampling(temperature=0.0, repetition_penalty=pen)
+    slots = [dev.admit(request_seed(19, r), P, T, greedy) for r in range(R)]
+    dev.forward(np.concatenate([np.array([[s, p, -1, 0] for p in range(P - 1)], np.int32) for s in slots]),
+                sample=False)
+    prompts = [np.array(prompt_ids(request_seed(19, r), P, cfg.text_vocab)) for r in range(R)]
+    for r in range(R):
+        orc.forward(("p", r), prompts[r][:-1], np.arange(P - 1), want_logits=False)
+    wins = [osamp.RingWindow(64, cfg.vocab) for _ in range(R)]
+    lo, hi = audio_range(cfg, 0)
+    got = np.zeros((R, T), np.int64)
+    ratio = np.zeros((R, T))
+    for s in range(T):
+        toks, _ = dev.forward(np.array([[sl, P - 1 + s, -1, 1] for sl in slots], np.int32), want_tokens=True)
+        got[:, s] = toks
+        dlog, col0 = dev.read_logits()
+        for r in range(R):
+            tok_in = int(prompts[r][-1]) if s == 0 else int(got[r, s - 1])
+            ol, _ = orc.forward(("p", r), np.array([tok_in]), np.array([P - 1 + s]))
+            d_full = np.full(cfg.vocab, -np.inf)
+            d_full[col0:col0 + dlog.shape[1]] = dlog[r]
+            dpen = osamp.apply_repetition_penalty(masked(d_full, lo, hi), pen, wins[r])
+            opn = osamp.apply_repetition_penalty(masked(ol[0], lo, hi), pen, wins[r])
+            assert int(np.argmax(dpen)) == got[r, s], (r, s)  # K1 in situ
+            err = np.abs(dpen[lo:hi] - opn[lo:hi]).max()
+            srt = np.sort(opn[lo:hi])[::-1]
+            ratio[r, s] = (srt[0] - srt[1]) / max(err, 1e-30)
+            assert ratio[r, s] >= 10.0, (r, s, srt[0] - srt[1], err)  # precondition
+            assert int(np.argmax(opn)) == got[r, s], (r, s)
+            wins[r].append(int(got[r, s]))
+    print(f"cosy planted greedy: min margin/err {ratio.min():.1f}")
+    for r, sl in enumerate(slots):
+        dev.release(sl)
+        orc.release(("p", r))
+    dev.close()
