@@ -679,19 +679,26 @@ __global__ void __launch_bounds__(kST)
 
 __global__ void __launch_bounds__(kST) sample_fused_kernel(SampFusedArgs a) {
   VOX_TRACE(kTrSampler);
-  griddep_wait();
-  griddep_launch();
+  // everything but the logits was written by the host or >= 2 launches upstream
+  // (every kernel launches its dependents only after its own griddep_wait), so the
+  // row, slot parameters and penalty window load before waiting for the LM head
   extern __shared__ uint32_t dyn_bm[];
   __shared__ SampSmem S;
   __shared__ int wbuf[kMaxWin];
   const int i = blockIdx.x;
   const int ri = a.sample_rows[i];
   if (ri < 0) {  // padding of the sample bucket
+    griddep_wait();
+    griddep_launch();
     if (threadIdx.x == 0) a.tokens_out[i] = -1;
     return;
   }
   const RowDev rw = a.rows[ri];
-  if (rw.slot < 0) return;
+  if (rw.slot < 0) {
+    griddep_wait();
+    griddep_launch();
+    return;
+  }
   const int slot = rw.slot;
   const int P = a.slot_prompt_len[slot];
   const VoxSampling prm = a.slot_params[slot];
@@ -708,6 +715,8 @@ __global__ void __launch_bounds__(kST) sample_fused_kernel(SampFusedArgs a) {
   const int wlen = ngen < W ? ngen : W;
   const int* ts = a.token_store + static_cast<int64_t>(slot) * a.max_ctx;
   for (int j = threadIdx.x; j < wlen; j += kST) wbuf[j] = ts[P + ngen - wlen + j];
+  griddep_wait();  // the LM head's logits
+  griddep_launch();
   __syncthreads();
   const int tok = sample_row(S, dyn_bm, a.logits + static_cast<int64_t>(i) * a.ld, a.col_base, lo,
                              hi, wbuf, wlen, a.slot_seed[slot], static_cast<uint64_t>(step), prm,
