@@ -21,6 +21,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <cmath>
 #include <mutex>
 #include <string>
@@ -40,6 +42,7 @@ enum : uint64_t {
   T_CD_R1W = 454, T_CD_R1B = 455, T_CD_R2W = 456, T_CD_R2B = 457, T_CD_VPOST = 458, T_CD_VPOSTB = 459,
 };
 
+constexpr int kCdMaxGraphs = 64;  // call shapes kept as CUDA graphs
 constexpr int kCdMaxRows = 256;  // rows of one attention group (2 * (ref + max_chunk))
 
 VOX_DEV uint64_t seg_key(const SegDev& q) {
@@ -527,6 +530,11 @@ struct VoxCosy {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double last_ms = 0.0;
   int64_t launches = 0;
+  // one CUDA graph per call shape (requests, token rows, vocoder rows, longest
+  // segment): a call is ~700 launches, host-bound at small batches without it
+  std::map<std::tuple<int, int64_t, int64_t, int>, cudaGraphExec_t> graphs;
+  std::map<std::tuple<int, int64_t, int64_t, int>, int64_t> graph_launches;
+  bool no_graphs = getenv("VOX_NO_GRAPH") != nullptr;
   // weights
   float* emb = nullptr;
   std::vector<CdXf> enc, est;
@@ -928,6 +936,7 @@ void vox_cosy_destroy(VoxCosy* m) {
   if (!m) return;
   cudaSetDevice(m->device);
   if (m->st) cudaStreamSynchronize(m->st);
+  for (auto& kv : m->graphs) cudaGraphExecDestroy(kv.second);
   for (auto* v : {&m->enc, &m->est})
     for (auto& w : *v)
       for (void* p : {static_cast<void*>(w.ln1w), static_cast<void*>(w.ln1b), static_cast<void*>(w.ln2w),
@@ -1097,7 +1106,33 @@ int vox_cosy_decode(VoxCosy* m, const VoxCosyReq* reqs, int32_t n, const int32_t
   }
   CCK(cudaMemcpyAsync(m->d_stage, hs, L.total * 4, cudaMemcpyHostToDevice, m->st));
   CCK(cudaEventRecord(m->ev0, m->st));
-  CRET(enqueue(m, n, E, V));
+  {
+    const auto key = std::make_tuple(n, E, V, m->max_seg);
+    auto it = m->graphs.find(key);
+    if (m->no_graphs || (it == m->graphs.end() && m->graphs.size() >= kCdMaxGraphs)) {
+      CRET(enqueue(m, n, E, V));
+    } else if (it == m->graphs.end()) {
+      // first call of this shape: run it eagerly (sets kernel attributes), then capture
+      const int64_t before = m->launches;
+      CRET(enqueue(m, n, E, V));
+      const int64_t per_call = m->launches - before;
+      cudaGraph_t graph;
+      CCK(cudaStreamBeginCapture(m->st, cudaStreamCaptureModeThreadLocal));
+      const int rc = enqueue(m, n, E, V);
+      const cudaError_t ce = cudaStreamEndCapture(m->st, &graph);
+      if (rc != VOX_OK) return rc;
+      CCK(ce);
+      cudaGraphExec_t ex;
+      CCK(cudaGraphInstantiate(&ex, graph, 0));
+      cudaGraphDestroy(graph);
+      m->graphs[key] = ex;
+      m->graph_launches[key] = per_call;
+      m->launches = before + per_call;
+    } else {
+      CCK(cudaGraphLaunch(it->second, m->st));
+      m->launches += m->graph_launches[key];
+    }
+  }
   CCK(cudaEventRecord(m->ev1, m->st));
   int64_t spm = g.hop;
   for (int b = 0; b < g.n_ratios; ++b) spm *= g.ratios[b];
