@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256)
   VOX_TRACE(kTrDetok);
   griddep_wait();
   griddep_launch();
+  // grid: (latent rows, channel blocks of 256): each thread owns one channel of one row
   const int row = blockIdx.x;
   if (row >= hdr->n_lat) return;
   const int ri = find_req(reqs, hdr->n_req, row);
@@ -79,21 +80,24 @@ __global__ void __launch_bounds__(256)
   const int t = row - q.lat_off;
   const int n = 4 * q.nf;
   const int C = dd.latent, H = 6;
+  const int ch = blockIdx.y * 256 + threadIdx.x;
+  if (ch >= C) return;
   const int* ts = token_store + static_cast<int64_t>(q.slot) * dd.max_ctx;
   const float* hin = slot_state(state, dd, q.slot, q.parity) + dd.off_in;
   float* hout = slot_state(state, dd, q.slot, q.parity ^ 1) + dd.off_in;
-  for (int ch = threadIdx.x; ch < C; ch += 256) {
-    float acc = dw_b[ch];
+  // the 7 taps' latents first (independent gathers in flight), then the conv
+  float z[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
-      const int tt = t - 6 + k;
-      const float z = tt >= 0 ? vq_latent(ts, q, dd, tabs, tt, ch) : hin[(H + tt) * C + ch];
-      acc = fmaf(dw_w[ch * 7 + k], z, acc);
-    }
-    out[static_cast<int64_t>(row) * C + ch] = __float2bfloat16_rn(acc);
-    if (t >= n - H) hout[(t - (n - H)) * C + ch] = vq_latent(ts, q, dd, tabs, t, ch);
-    for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
+  for (int k = 0; k < 7; ++k) {
+    const int tt = t - 6 + k;
+    z[k] = tt >= 0 ? vq_latent(ts, q, dd, tabs, tt, ch) : hin[(H + tt) * C + ch];
   }
+  float acc = dw_b[ch];
+#pragma unroll
+  for (int k = 0; k < 7; ++k) acc = fmaf(dw_w[ch * 7 + k], z[k], acc);
+  out[static_cast<int64_t>(row) * C + ch] = __float2bfloat16_rn(acc);
+  if (t >= n - H) hout[(t - (n - H)) * C + ch] = z[6];  // vq_latent at t (tap 6)
+  for (int hh = t; hh < H - n; hh += n) hout[hh * C + ch] = hin[(hh + n) * C + ch];
 }
 
 void launch_vq_dwconv(const DetokReq* reqs, int n_req, int n_lat, const int* token_store,
@@ -101,8 +105,8 @@ void launch_vq_dwconv(const DetokReq* reqs, int n_req, int n_lat, const int* tok
                       const DetokDims& dd, bf16* out_bf16, cudaStream_t st) {
   const ReqHdr* hdr = reinterpret_cast<const ReqHdr*>(reqs) - 1;
   (void)n_req;
-  launch_k(vq_dwconv_kernel, dim3(n_lat), dim3(256), 0, st, hdr, reqs, token_store, tabs, dw_w, dw_b, state, dd,
-                                          out_bf16);
+  launch_k(vq_dwconv_kernel, dim3(n_lat, (dd.latent + 255) / 256), dim3(256), 0, st, hdr, reqs, token_store, tabs,
+           dw_w, dw_b, state, dd, out_bf16);
 }
 
 // Snake + build the transposed-conv GEMM operand [s(x_t) | s(x_{t-1})] (bf16),
