@@ -210,59 +210,6 @@ VOX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 VOX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// ---------------------------------------------------------------------------
-// Thread-block cluster helpers
-// ---------------------------------------------------------------------------
-VOX_DEV uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-VOX_DEV void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// Cluster multicast (1-CTA MMAs, activations shared across a cluster): one
-// CTA's TMA load lands at the same smem offset in every CTA of `mask` and
-// completes tx bytes on each destination CTA's mbarrier at `bar`'s offset.
-// ---------------------------------------------------------------------------
-VOX_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
-                            uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::"
-      "cluster.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5, %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(mask),
-      "l"(policy)
-      : "memory");
-}
-// arrive (once) on the mbarrier at this smem offset in every CTA of `mask`
-// when all previously issued cta_group::1 MMAs of this thread have completed
-VOX_DEV void umma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-      "[%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
-// Distributed shared memory: address of the same smem offset in CTA `rank`
-// of this cluster, and a 16-byte load from it.
-VOX_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-VOX_DEV float4 ld_dsmem_f4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(addr)
-               : "memory");
-  return v;
-}
-
 // Programmatic dependent launch: wait for the preceding grid's completion
 // (and memory flush) / allow the next grid to start its prologue.
 VOX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

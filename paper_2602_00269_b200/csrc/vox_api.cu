@@ -287,8 +287,8 @@ struct TimedLaunch {  // RAII event pair around a launch (eager + timing only)
 
 static bool make_act_maps(VoxCtx* c, std::map<int, CUtensorMap>& m, const bf16* base, int K,
                           int rows) {
-  // box rows: the 1-CTA tiles (16..256) and the multicast slices (bn / cs)
-  for (int bn : {8, 16, 20, 24, 28, 32, 40, 48, 56, 64, 80, 96, 112, 128, 160, 192, 224, 256}) {
+  // box rows: the decode GEMM's row buckets and the 1-CTA kernel's tile widths
+  for (int bn : {16, 32, 64, 96, 128, 160, 192, 224, 256}) {
     CUtensorMap t;
     if (!make_tmap_bf16(&t, base, K, rows, static_cast<uint64_t>(K) * 2, bn)) return false;
     m[bn] = t;
