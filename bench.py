@@ -566,7 +566,7 @@ def slo_run(dev, rate: float, seconds: float, seed: int, prompt: int, ws: int, r
 
 def run_slo(dev, start: float, seconds: float, probe_seconds: float, seed: int, prompt: int, ws: int = 1,
             rank: int = 0, max_batch: int = 256, startup_limit: int = 16, coarse: float = 8.0,
-            fine: float = 2.0):
+            fine: float = 2.0, max_full: int = 5):
     """Paper protocol (Poisson arrivals, 60 s runs, p90 TTFA, pooled
     viability): the highest offered rate, on a `fine`-req/s grid, whose full-length run
     keeps viability >= 0.99 and p90 TTFA <= 0.5 s.  Short probes (probe_seconds, `coarse`
@@ -581,29 +581,46 @@ def run_slo(dev, start: float, seconds: float, probe_seconds: float, seed: int, 
         last_ok, r = r, r + coarse
     if last_ok is None:  # even the start rate fails: walk down
         r = start - fine
-        while r > 0:
+        n = 0
+        while r > 0 and n < max_full:
             ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
             sweep.append(row)
+            n += 1
             if ok:
                 return r, sweep
-            r -= fine
+            r -= coarse / 2
         return 0.0, sweep
-    best, r = None, last_ok
-    while r < last_ok + coarse:  # full-length runs upward from the last passing probe
+    # full-length runs, at most max_full of them (bounds the bench's wall time):
+    # upward on the fine grid from the last passing probe; if that rate fails at
+    # full length, walk down in coarse/2 steps, then refine upward on the fine grid
+    best, r, n = None, last_ok, 0
+    while r < last_ok + coarse and n < max_full:
         ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
         sweep.append(row)
+        n += 1
         if not ok:
             break
         best, r = r, r + fine
-    if best is None:  # the probe rate fails at full length: walk down
-        r = last_ok - fine
-        while r > 0:
+    if best is None:
+        step = coarse / 2
+        r = last_ok - step
+        while r > 0 and n < max_full:
             ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
             sweep.append(row)
+            n += 1
             if ok:
                 best = r
                 break
-            r -= fine
+            r -= step
+        if best is not None:
+            r = best + fine
+            while r < best + step and n < max_full:
+                ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
+                sweep.append(row)
+                n += 1
+                if not ok:
+                    break
+                best, r = r, r + fine
     return (best or 0.0), sweep
 
 
@@ -1024,6 +1041,14 @@ def main():
     value = audio_s / (dev_ms / 1000.0)
     e2e = audio_s / wall_s
 
+    t_phase = [time.time()]
+
+    def phase(name):  # wall time per bench phase, to stderr (the JSON line stays alone on stdout)
+        now = time.time()
+        print(f"[bench] {name}: {now - t_phase[0]:.1f} s", file=sys.stderr, flush=True)
+        t_phase[0] = now
+
+    phase("headline steps")
     roof = None
     if not args.no_roofline and rank == 0:
         classes, step_ms, ctx, sweep, in_graph, nrows = kernel_roofline(dev, args.batch, args.prompt,
@@ -1037,6 +1062,7 @@ def main():
         except Exception as e:  # report, never mask the headline
             roof["detok"] = {"error": repr(e)[:200]}
 
+    phase("roofline")
     slo = None
     if not args.no_slo:
         best, sweep = run_slo(dev, args.slo_start * ws, args.slo_seconds, args.slo_probe_seconds, args.seed,
@@ -1046,9 +1072,11 @@ def main():
                "startup_concurrency_limit": args.slo_startup_limit, "criterion": "viability>=0.99 and p90 TTFA<=0.5s",
                "duration_s": args.slo_seconds, "grid_req_s": 2.0 * ws,
                "protocol": f"{args.slo_probe_seconds:.0f} s probes in {8 * ws} req/s steps bracket the rate; "
-                           f"the result is the highest {2 * ws} req/s-grid rate passing a {args.slo_seconds:.0f} s run",
+                           f"the result is the highest {2 * ws} req/s-grid rate passing a {args.slo_seconds:.0f} s run "
+                           f"(at most 5 full-length runs; a failing probe rate walks down in {4 * ws} req/s steps)",
                "routing": "reference route_dp (seeded uniform), replicas", "sweep": sweep}
 
+    phase("slo")
     cosy = None
     if not args.no_cosy and rank == 0:
         try:
@@ -1056,6 +1084,7 @@ def main():
         except Exception as e:  # report, never mask the headline
             cosy = {"error": repr(e)[:200]}
 
+    phase("config-4 cosy")
     csm = None
     if not args.no_csm and rank == 0:
         try:
@@ -1067,6 +1096,7 @@ def main():
         except Exception as e:  # report, never mask the headline
             csm = {"error": repr(e)[:200]}
 
+    phase("config-3 csm")
     proto = None
     if not args.no_cpu and rank == 0:
         try:
@@ -1074,6 +1104,7 @@ def main():
         except Exception as e:  # report, never mask the headline
             proto = {"error": repr(e)[:200]}
 
+    phase("reference protocol")
     cpu = None
     if not args.no_cpu and rank == 0:
         from oracle.cpu_step import time_cpu_step
@@ -1082,6 +1113,7 @@ def main():
         cpu = {"value": round(r["audio_s_per_s"], 5), "unit": UNIT, "cores": r["cores"], "kind": "port",
                "sample": r["sample"]}
 
+    phase("cpu baseline")
     if rank == 0:
         steps = args.steps
         h2d = (res["rows"] / steps) * 40 + 64  # RowDev (32 B) + out_index + sample_rows per row

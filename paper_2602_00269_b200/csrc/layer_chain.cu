@@ -122,17 +122,11 @@ VOX_DEV int job_units(const ChainArgs& a, int j) {
 
 // ---- elementwise jobs (epilogue group, 256 threads, rows read through L2) ----
 VOX_DEV float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
-VOX_DEV float4 sum_planes4(const float* w, int splits, int64_t ss, int64_t i4) {
-  float4 a = ldcg4(w + 4 * i4);
-  for (int s = 1; s < splits; ++s) a = add4(a, ldcg4(w + s * ss + 4 * i4));
-  return a;
-}
-
 // resid_norm_row at 256 threads (same accumulation and reduction order) for up
 // to kPar rows at once: every row's loads are in flight together and the rows
 // share one set of block barriers; each thread keeps its h values in registers
 constexpr int kPar = 2;
-constexpr int kMaxD4PerThread = 4;  // d <= 4096
+constexpr int kMaxD4PerThread = 3;  // d <= 3072 (host: chain_bn_for_rows)
 VOX_DEV void chain_norm_rows(const ChainJob& j, const RowDev* rows, int r0, int nr, int d, float eps,
                              int eg, float* red) {
   const int d4 = d / 4;
@@ -144,6 +138,10 @@ VOX_DEV void chain_norm_rows(const ChainJob& j, const RowDev* rows, int r0, int 
     live[p] = p < nr && rows[r0 + p].slot >= 0;
     ss[p] = 0.f;
   }
+  // split-major: every (row, k) load of one plane is in flight at once, so the
+  // L2 round trips are one per plane (h rides with plane 0), not one per
+  // (row, k, plane); the per-element sum order is still h + (p0 + p1 + ...)
+  float4 hv[kPar][kMaxD4PerThread];
 #pragma unroll
   for (int k = 0; k < kMaxD4PerThread; ++k) {
     const int i = eg + k * kEpiThreads;
@@ -151,9 +149,34 @@ VOX_DEV void chain_norm_rows(const ChainJob& j, const RowDev* rows, int r0, int 
     for (int p = 0; p < kPar; ++p) {
       if (live[p] && i < d4) {
         const int64_t ro = static_cast<int64_t>(r0 + p) * d;
-        v[p][k] = add4(ldcg4(j.h + ro + 4 * i), sum_planes4(j.ws + ro, j.nsplits, j.ss, i));
+        hv[p][k] = ldcg4(j.h + ro + 4 * i);
+        v[p][k] = ldcg4(j.ws + ro + 4 * i);
       }
     }
+  }
+  for (int s = 1; s < j.nsplits; ++s) {
+    float4 t[kPar][kMaxD4PerThread];
+#pragma unroll
+    for (int k = 0; k < kMaxD4PerThread; ++k) {
+      const int i = eg + k * kEpiThreads;
+#pragma unroll
+      for (int p = 0; p < kPar; ++p)
+        if (live[p] && i < d4) t[p][k] = ldcg4(j.ws + s * j.ss + static_cast<int64_t>(r0 + p) * d + 4 * i);
+    }
+#pragma unroll
+    for (int k = 0; k < kMaxD4PerThread; ++k) {
+      const int i = eg + k * kEpiThreads;
+#pragma unroll
+      for (int p = 0; p < kPar; ++p)
+        if (live[p] && i < d4) v[p][k] = add4(v[p][k], t[p][k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxD4PerThread; ++k) {
+    const int i = eg + k * kEpiThreads;
+#pragma unroll
+    for (int p = 0; p < kPar; ++p)
+      if (live[p] && i < d4) v[p][k] = add4(hv[p][k], v[p][k]);
   }
 #pragma unroll
   for (int k = 0; k < kMaxD4PerThread; ++k) {
@@ -212,56 +235,116 @@ VOX_DEV void chain_rope_rows(const ChainJob& j, const RowDev* rows, int r0, int 
   const int nqkv = (dm.n_heads + 2 * dm.n_kv) * hd;
   const int q4 = half / 4;
   const int n_items = (dm.n_heads + dm.n_kv) * q4;
-  for (int t = eg; t < nr * n_items; t += kEpiThreads) {
-    const int r = r0 + t / n_items, it = t % n_items;
-    const RowDev rw = rows[r];
-    if (rw.slot < 0) continue;
-    const float* w = j.ws + static_cast<int64_t>(r) * nqkv;
-    const int head = it / q4, i = (it % q4) * 4;
-    const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
-    float4 a = sum_planes4(w, j.nsplits, j.ss, c1);
-    float4 b = sum_planes4(w, j.nsplits, j.ss, c2);
-    if (j.bias != nullptr) {
-      a = add4(a, reinterpret_cast<const float4*>(j.bias)[c1]);
-      b = add4(b, reinterpret_cast<const float4*>(j.bias)[c2]);
-    }
-    const float2* rp = rope + static_cast<int64_t>(rw.pos) * half;
-    const float x1[4] = {a.x, a.y, a.z, a.w}, x2[4] = {b.x, b.y, b.z, b.w};
-    float o1[4], o2[4];
+  // kRB items per thread per pass, their plane loads issued split-major (one L2
+  // round trip per plane for all of them) together with the rope / page-table
+  // loads; the per-element arithmetic is the per-kernel path's
+  constexpr int kRB = 2;
+  for (int t0 = eg; t0 < nr * n_items; t0 += kRB * kEpiThreads) {
+    bool ok[kRB];
+    float4 xa[kRB], xb[kRB];
+    const float* pa[kRB];  // plane-0 address of the item's first half (second: + half)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const float2 cs = rp[i + e];
-      o1[e] = __fsub_rn(__fmul_rn(x1[e], cs.x), __fmul_rn(x2[e], cs.y));
-      o2[e] = __fadd_rn(__fmul_rn(x2[e], cs.x), __fmul_rn(x1[e], cs.y));
+    for (int m = 0; m < kRB; ++m) {
+      const int t = t0 + m * kEpiThreads;
+      ok[m] = t < nr * n_items;
+      const int r = r0 + (ok[m] ? t / n_items : 0), it = ok[m] ? t % n_items : 0;
+      ok[m] = ok[m] && rows[r].slot >= 0;
+      pa[m] = j.ws + static_cast<int64_t>(r) * nqkv + (it / q4) * hd + (it % q4) * 4;
+      if (ok[m]) {
+        xa[m] = ldcg4(pa[m]);
+        xb[m] = ldcg4(pa[m] + half);
+      }
     }
-    bf16* dst;
-    if (head < dm.n_heads) {
-      dst = j.q + (static_cast<int64_t>(r) * dm.n_heads + head) * hd;
-    } else {
-      const int page = j.page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot + rw.pos / dm.page_size];
-      const int kvh = head - dm.n_heads;
-      dst = j.kc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + rw.pos % dm.page_size) * hd;
+    for (int s = 1; s < j.nsplits; ++s) {
+      float4 ta[kRB], tb[kRB];
+#pragma unroll
+      for (int m = 0; m < kRB; ++m)
+        if (ok[m]) {
+          ta[m] = ldcg4(pa[m] + s * j.ss);
+          tb[m] = ldcg4(pa[m] + s * j.ss + half);
+        }
+#pragma unroll
+      for (int m = 0; m < kRB; ++m)
+        if (ok[m]) {
+          xa[m] = add4(xa[m], ta[m]);
+          xb[m] = add4(xb[m], tb[m]);
+        }
     }
-    store_bf16x4(dst + i, o1[0], o1[1], o1[2], o1[3]);
-    store_bf16x4(dst + i + half, o2[0], o2[1], o2[2], o2[3]);
+#pragma unroll
+    for (int m = 0; m < kRB; ++m) {
+      if (!ok[m]) continue;
+      const int t = t0 + m * kEpiThreads;
+      const int r = r0 + t / n_items, it = t % n_items;
+      const RowDev rw = rows[r];
+      const int head = it / q4, i = (it % q4) * 4;
+      const int c1 = (head * hd + i) / 4, c2 = (head * hd + i + half) / 4;
+      float4 av = xa[m], bv = xb[m];
+      if (j.bias != nullptr) {
+        av = add4(av, reinterpret_cast<const float4*>(j.bias)[c1]);
+        bv = add4(bv, reinterpret_cast<const float4*>(j.bias)[c2]);
+      }
+      const float2* rp = rope + static_cast<int64_t>(rw.pos) * half;
+      const float x1[4] = {av.x, av.y, av.z, av.w}, x2[4] = {bv.x, bv.y, bv.z, bv.w};
+      float o1[4], o2[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 cs = rp[i + e];
+        o1[e] = __fsub_rn(__fmul_rn(x1[e], cs.x), __fmul_rn(x2[e], cs.y));
+        o2[e] = __fadd_rn(__fmul_rn(x2[e], cs.x), __fmul_rn(x1[e], cs.y));
+      }
+      bf16* dst;
+      if (head < dm.n_heads) {
+        dst = j.q + (static_cast<int64_t>(r) * dm.n_heads + head) * hd;
+      } else {
+        const int page = j.page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot + rw.pos / dm.page_size];
+        const int kvh = head - dm.n_heads;
+        dst = j.kc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * dm.page_size + rw.pos % dm.page_size) * hd;
+      }
+      store_bf16x4(dst + i, o1[0], o1[1], o1[2], o1[3]);
+      store_bf16x4(dst + i + half, o2[0], o2[1], o2[2], o2[3]);
+    }
   }
   const int vbase4 = (dm.n_heads + dm.n_kv) * hd / 4;
   const int hd4 = hd / 4;
   const int nv = dm.n_kv * hd4;
-  for (int t = eg; t < nr * nv; t += kEpiThreads) {
-    const int r = r0 + t / nv, e = t % nv;
-    const RowDev rw = rows[r];
-    if (rw.slot < 0) continue;
-    const float* w = j.ws + static_cast<int64_t>(r) * nqkv;
-    float4 v = sum_planes4(w, j.nsplits, j.ss, vbase4 + e);
-    if (j.bias != nullptr) v = add4(v, reinterpret_cast<const float4*>(j.bias)[vbase4 + e]);
-    const int page = j.page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot + rw.pos / dm.page_size];
-    const int kvh = e / hd4, dd = (e % hd4) * 4;
-    bf16* vt = j.vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * hd + dd) * dm.page_size + rw.pos % dm.page_size;
-    vt[0] = __float2bfloat16_rn(v.x);
-    vt[dm.page_size] = __float2bfloat16_rn(v.y);
-    vt[2 * dm.page_size] = __float2bfloat16_rn(v.z);
-    vt[3 * dm.page_size] = __float2bfloat16_rn(v.w);
+  for (int t0 = eg; t0 < nr * nv; t0 += kRB * kEpiThreads) {
+    bool ok[kRB];
+    float4 xv[kRB];
+    const float* wp[kRB];
+#pragma unroll
+    for (int m = 0; m < kRB; ++m) {
+      const int t = t0 + m * kEpiThreads;
+      ok[m] = t < nr * nv;
+      const int r = r0 + (ok[m] ? t / nv : 0), e = ok[m] ? t % nv : 0;
+      ok[m] = ok[m] && rows[r].slot >= 0;
+      wp[m] = j.ws + static_cast<int64_t>(r) * nqkv + 4 * (vbase4 + e);
+      if (ok[m]) xv[m] = ldcg4(wp[m]);
+    }
+    for (int s = 1; s < j.nsplits; ++s) {
+      float4 tv[kRB];
+#pragma unroll
+      for (int m = 0; m < kRB; ++m)
+        if (ok[m]) tv[m] = ldcg4(wp[m] + s * j.ss);
+#pragma unroll
+      for (int m = 0; m < kRB; ++m)
+        if (ok[m]) xv[m] = add4(xv[m], tv[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < kRB; ++m) {
+      if (!ok[m]) continue;
+      const int t = t0 + m * kEpiThreads;
+      const int e = t % nv;
+      const RowDev rw = rows[r0 + t / nv];
+      float4 v = xv[m];
+      if (j.bias != nullptr) v = add4(v, reinterpret_cast<const float4*>(j.bias)[vbase4 + e]);
+      const int page = j.page_table[static_cast<int64_t>(rw.slot) * dm.max_pages_per_slot + rw.pos / dm.page_size];
+      const int kvh = e / hd4, dd = (e % hd4) * 4;
+      bf16* vt = j.vc + ((static_cast<int64_t>(page) * dm.n_kv + kvh) * hd + dd) * dm.page_size + rw.pos % dm.page_size;
+      vt[0] = __float2bfloat16_rn(v.x);
+      vt[dm.page_size] = __float2bfloat16_rn(v.y);
+      vt[2 * dm.page_size] = __float2bfloat16_rn(v.z);
+      vt[3 * dm.page_size] = __float2bfloat16_rn(v.w);
+    }
   }
 }
 
@@ -324,117 +407,78 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ======================= producer =======================
+      // ======================= W producer =======================
+      // claims GEMM units in job order, publishes them to the queue, streams
+      // their weight k-blocks (weights never wait for a job's inputs)
+      const uint64_t pol_w = policy_evict_first();
+      int wj = 0, wk = 0, wg = 0;
+      for (;;) {
+        int u = -1;
+        while (wj < a.njobs) {
+          if (a.job[wj].kind == kChGemm) {
+            u = atomicAdd(claim_ctr(wj), 1);
+            if (u < job_units(a, wj)) break;
+          }
+          ++wj;
+        }
+        const int qs = wk % kQN;
+        if (wk >= kQN) mbar_wait(&qempty[qs], ((wk / kQN) - 1) & 1);
+        qbuf[qs] = wj < a.njobs ? ((wj << 24) | u) : -1;
+        mbar_arrive(&qfull[qs]);
+        ++wk;
+        if (wj >= a.njobs) break;
+        const Unit wu = decode_unit(a.job[wj], wj, u, a.k_rotate);
+        const bf16* wsrc = a.job[wj].w + static_cast<int64_t>(wu.tile) * a.job[wj].n_kb * 8192;
+        for (int i = 0; i < wu.nkb; ++i, ++wg) {
+          const int s = wg % WST;
+          if (wg >= WST) mbar_wait(&wempty[s], ((wg / WST) - 1) & 1);
+          mbar_arrive_expect_tx(&wfull[s], C::kWBytes);
+          bulk_load(wring + s * C::kWBytes, wsrc + static_cast<int64_t>(unit_kb(wu, i)) * 8192, C::kWBytes,
+                    &wfull[s], pol_w);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ======================= X producer =======================
+      // follows the queue; a unit's activation k-blocks go out once its job's
+      // inputs are complete (the preceding kernel, or an earlier job's counter)
       tma_prefetch_desc(&mx0);
       tma_prefetch_desc(&mx1);
       tma_prefetch_desc(&mx2);
-      const uint64_t pol_w = policy_evict_first(), pol_x = policy_evict_last();
-      // W cursor (claims units, pushes them to the queue, streams their weights)
-      int wj = 0, wk = 0, wg = 0, wi = 0, pf = 0;
-      bool w_have = false, w_end = false;
-      Unit wu{};
-      const bf16* wsrc = nullptr;
-      // X cursor (follows the queue; activations once the job's inputs exist)
-      int xk = 0, xg = 0, xi = 0, dep_job = -2;
-      bool x_have = false, x_end = false, x_dep = false, gdw = false;
-      Unit xu{};
-      const CUtensorMap* xmap = nullptr;
-      for (;;) {
-        bool prog = false;
-        if (!w_have && !w_end) {
-          const int qs = wk % kQN;
-          if (wk < kQN || mbar_test(&qempty[qs], ((wk / kQN) - 1) & 1)) {
-            int u = -1;
-            while (wj < a.njobs) {
-              if (a.job[wj].kind == kChGemm) {
-                u = atomicAdd(claim_ctr(wj), 1);
-                if (u < job_units(a, wj)) break;
-              }
-              ++wj;
-            }
-            if (wj < a.njobs) {
-              qbuf[qs] = (wj << 24) | u;
-              wu = decode_unit(a.job[wj], wj, u, a.k_rotate);
-              wsrc = a.job[wj].w + static_cast<int64_t>(wu.tile) * a.job[wj].n_kb * 8192;
-              wi = 0;
-              pf = 0;
-              w_have = true;
-            } else {
-              qbuf[qs] = -1;
-              w_end = true;
-            }
-            mbar_arrive(&qfull[qs]);
-            ++wk;
-            prog = true;
-          }
-        }
-        if (!x_have && !x_end && xk < wk) {
-          const int e = qbuf[xk % kQN];
-          mbar_arrive(&qempty[xk % kQN]);
-          ++xk;
-          if (e < 0) {
-            x_end = true;
-          } else {
-            const int jj = e >> 24;
-            xu = decode_unit(a.job[jj], jj, e & 0xFFFFFF, a.k_rotate);
-            const int m = a.job[jj].xmap;
-            xmap = m == 0 ? &mx0 : (m == 1 ? &mx1 : &mx2);
-            if (jj != dep_job) { dep_job = jj; x_dep = false; }
-            xi = 0;
-            x_have = true;
-          }
-          prog = true;
-        }
-        if (x_have && !x_dep) {
-          const int dj = a.job[xu.job].dep;
+      const uint64_t pol_x = policy_evict_last();
+      int xg = 0, dep_ok_job = -1;
+      bool gdw = false;
+      for (int k = 0;; ++k) {
+        const int qs = k % kQN;
+        mbar_wait(&qfull[qs], (k / kQN) & 1);
+        const int e = qbuf[qs];
+        mbar_arrive(&qempty[qs]);
+        if (e < 0) break;
+        const int jj = e >> 24;
+        const Unit xu = decode_unit(a.job[jj], jj, e & 0xFFFFFF, a.k_rotate);
+        if (jj != dep_ok_job) {
+          const int dj = a.job[jj].dep;
           if (dj < 0) {
-            // the preceding kernel: wait for it only once the W ring cannot advance
-            if (gdw || !w_have || wg >= WST) {
-              if (!gdw) griddep_wait();
-              gdw = true;
-              x_dep = true;
-              chain_mark(kEvDep + xu.job, t_entry, vox_now());
-            }
-          } else if (ld_acquire(done_ctr(dj)) >= job_units(a, dj)) {
+            if (!gdw) griddep_wait();
+            gdw = true;
+          } else {
+            const int need = job_units(a, dj);
+            while (ld_acquire(done_ctr(dj)) < need) __nanosleep(64);
             fence_proxy_async_global();  // generic-proxy writes -> TMA reads
-            x_dep = true;
-            chain_mark(kEvDep + xu.job, t_entry, vox_now());
           }
+          chain_mark(kEvDep + jj, t_entry, vox_now());
+          dep_ok_job = jj;
         }
-        if (x_have && x_dep) {
+        const int m = a.job[jj].xmap;
+        const CUtensorMap* xmap = m == 0 ? &mx0 : (m == 1 ? &mx1 : &mx2);
+        for (int i = 0; i < xu.nkb; ++i, ++xg) {
           const int s = xg % XST;
-          if (xg < XST || mbar_test(&xempty[s], ((xg / XST) - 1) & 1)) {
-            mbar_arrive_expect_tx(&xfull[s], C::kXBytes);
-            tma_load_2d(xring + s * C::kXBytes, xmap, &xfull[s], unit_kb(xu, xi) * 64, 0, pol_x);
-            ++xg;
-            if (++xi == xu.nkb) x_have = false;
-            prog = true;
-          }
+          if (xg >= XST) mbar_wait(&xempty[s], ((xg / XST) - 1) & 1);
+          mbar_arrive_expect_tx(&xfull[s], C::kXBytes);
+          tma_load_2d(xring + s * C::kXBytes, xmap, &xfull[s], unit_kb(xu, i) * 64, 0, pol_x);
         }
-        if (w_have) {
-          const int s = wg % WST;
-          if (wg < WST || mbar_test(&wempty[s], ((wg / WST) - 1) & 1)) {
-            mbar_arrive_expect_tx(&wfull[s], C::kWBytes);
-            bulk_load(wring + s * C::kWBytes, wsrc + static_cast<int64_t>(unit_kb(wu, wi)) * 8192,
-                      C::kWBytes, &wfull[s], pol_w);
-            ++wg;
-            if (++wi == wu.nkb) w_have = false;
-            prog = true;
-          }
-        }
-        // stalled at a job boundary (inputs not ready, W ring full): pull the W
-        // unit's next k-blocks into L2 so HBM keeps streaming through the
-        // elementwise phases; the ring then refills from L2
-        if (!prog && w_have && x_have && !x_dep && a.l2_ahead > 0) {
-          if (pf < wi) pf = wi;
-          if (pf < wu.nkb && pf < wi + a.l2_ahead) {
-            prefetch_l2_bulk(wsrc + static_cast<int64_t>(unit_kb(wu, pf)) * 8192, C::kWBytes);
-            ++pf;
-            prog = true;
-          }
-        }
-        if (x_end && !w_have) break;
-        if (!prog) __nanosleep(x_have && !x_dep ? 128 : 32);
       }
     }
     __syncwarp();

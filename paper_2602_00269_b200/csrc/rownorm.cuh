@@ -37,11 +37,23 @@ VOX_DEV float block_sum_any(float v, float* red) {
 
 VOX_DEV float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
 
-// sum of the split-K partial planes at float4 index i (fixed split order)
+// sum of the split-K partial planes at float4 index i (fixed split order).  The
+// plane loads are issued G at a time before the first add so their L2 latencies
+// overlap (a plain running sum serialises one L2 round trip per plane); the
+// additions still run plane 0, 1, 2, ... so the result is bit-identical.
+template <int G = 4>
 VOX_DEV float4 sum_splits4(const float4* __restrict__ w, int splits, int64_t split_stride4,
                            int64_t i) {
   float4 a = w[i];
-  for (int s = 1; s < splits; ++s) a = add4(a, w[s * split_stride4 + i]);
+  for (int s0 = 1; s0 < splits; s0 += G) {
+    float4 t[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+      if (s0 + u < splits) t[u] = w[(s0 + u) * split_stride4 + i];
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+      if (s0 + u < splits) a = add4(a, t[u]);
+  }
   return a;
 }
 
