@@ -388,7 +388,9 @@ def batch_sweep(dev, slots, ctx: int, hbm: float, tflops: float):
     cfg = dev.cfg
     d, hd = cfg.d_model, cfg.head_dim
     proj = 2 * cfg.n_layers * ((cfg.n_heads + 2 * cfg.n_kv_heads) * hd * d + d * cfg.n_heads * hd + 3 * d * cfg.d_ff)
-    head = 2 * cfg.frame_tokens * cfg.codebook_size * d
+    # every row sits at the same frame position, so the LM head reads one frame slot's
+    # codebook (vox_forward's one-slot rule), not all frame_tokens x codebook_size rows
+    head = 2 * cfg.codebook_size * d
     flops_tok = proj + head  # 2 FLOP per bf16 weight (2 bytes) per row
     lm_s, _ = dev.streams()
     st = torch.cuda.ExternalStream(lm_s)
@@ -414,14 +416,16 @@ def batch_sweep(dev, slots, ctx: int, hbm: float, tflops: float):
     return out
 
 
-def step_work(cfg, rows: int, ctx_sum: float):
+def step_work(cfg, rows: int, ctx_sum: float, head_slots: int | None = None):
     """Algorithmic work of one decode step per kernel class: what the
     math must move / compute, independent of how the kernels split it (no split-K
-    partial planes, no re-reads).  Returns {class: (flops, bytes)} for the whole step."""
+    partial planes, no re-reads).  head_slots = distinct frame slots among the sampled
+    rows (the LM head reads head_slots x codebook_size weight rows; default: all
+    frame_tokens).  Returns {class: (flops, bytes)} for the whole step."""
     d, H, KV, hd, dff, L = cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.d_ff, cfg.n_layers
     nqkv, Hhd, R = (H + 2 * KV) * hd, H * hd, rows
     w_layer = nqkv * d + d * Hhd + 2 * dff * d + d * dff
-    A = cfg.frame_tokens * cfg.codebook_size
+    A = (cfg.frame_tokens if head_slots is None else head_slots) * cfg.codebook_size
     return {
         # 4 projections per layer: bf16 weights + bf16 inputs + outputs (fp32 q|k|v, O and
         # down results; bf16 SiLU(gate)*up from the fused epilogue)
@@ -449,7 +453,7 @@ def roofline_summary(cfg, classes, rows: int, ctx: int, hbm: float, tfl: float, 
     and HBM roofs (arithmetic intensity vs the ridge peak_tflops / peak_hbm).  The
     dominant class (largest time) is the headline.  traffic = ncu dram bytes per launch
     of that class (profiles/traffic_r02.json), or null."""
-    work = step_work(cfg, rows, float(rows) * ctx)
+    work = step_work(cfg, rows, float(rows) * ctx, head_slots=1)  # the eager rows share one position
     out = {}
     for name, c in classes.items():
         if c["launches"] <= 0 or c["ms"] <= 0 or name not in work:

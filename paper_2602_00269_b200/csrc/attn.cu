@@ -463,7 +463,8 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
     attr_bytes = smem;
   }
   const int n_items = n * dm.n_kv * n_split;
-  const int grid = n_items < 2 * kNumSMs ? n_items : 2 * kNumSMs;
+  const int sms = vox_sm_budget();
+  const int grid = n_items < 2 * sms ? n_items : 2 * sms;
   // VOX_ATTN_FUSED_COMBINE=1: the last split CTA of each (row, kv head) merges the
   // partials (no combine launch).  Measured slower than the separate combine kernel
   // (B=1 decode 2.06 -> 2.29 ms, CSM frame 8.58 -> 9.30 ms): every split item pays a
@@ -510,7 +511,7 @@ int attn_pick_splits(int n_rows, int n_kv, int max_ctx) {
   if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) return atoi(e) < 1 ? 1 : atoi(e);  // debug
   if (max_ctx < 1024) return 1;
   const int ctas = n_rows * n_kv;
-  int s = (2 * kNumSMs) / ctas;
+  int s = (2 * vox_sm_budget()) / ctas;
   if (s > kAttnMaxSplits) s = kAttnMaxSplits;
   if (n_rows > kAttnSplitRows) s = 1;
   return s < 1 ? 1 : s;

@@ -502,7 +502,10 @@ struct McCfg {
   static constexpr int kABytes = 128 * 64 * 2;
   static constexpr int kBBytes = BN * 64 * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : BN <= 256 ? 256 : 512;
+  // BN > 256 (decode rows plus a prefill burst): two MMAs per k-step over one
+  // weight stage, N = 256 on activation rows [0, 256) and N = BN - 256 on the rest
+  static constexpr int kN2 = BN > 256 ? BN - 256 : 0;
   // ring depth from a smem budget (KB): ~200 = one CTA per SM, deep; ~100 lets
   // the next kernel's CTA co-reside (PDL prologue overlap)
   static int stages(int budget_kb) {
@@ -526,7 +529,8 @@ struct McCfg {
 
 template <int BN>
 __global__ void __launch_bounds__(256, 1)
-    gemm_mc_kernel(const __grid_constant__ CUtensorMap tmX, GemmArgs p) {
+    gemm_mc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmX2,
+                   GemmArgs p) {
   VOX_TRACE(kTrGemmMc);
   using C = McCfg<BN>;
   const long long t_entry = clock64();
@@ -556,6 +560,7 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmX);
+    if (C::kN2 > 0) tma_prefetch_desc(&tmX2);
     for (int s = 0; s < nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -580,21 +585,26 @@ __global__ void __launch_bounds__(256, 1)
       bulk_load(smem + i * C::kStageBytes, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[i],
                 pol_w);
     }
+    // activation k-block: one box of BN rows, or 256 + (BN - 256) rows (TMA box <= 256)
+    auto load_x = [&](uint8_t* dst, int kb, uint64_t* bar) {
+      tma_load_2d(dst, &tmX, bar, kb * 64, n0, pol_x);
+      if (C::kN2 > 0) tma_load_2d(dst + 256 * 128, &tmX2, bar, kb * 64, n0 + 256, pol_x);
+    };
     griddep_wait();
     griddep_launch();  // wait-then-launch (see gemm_bf16_tc_kernel)
-    for (int i = 0; i < pre; ++i)
-      tma_load_2d(smem + i * C::kStageBytes + C::kABytes, &tmX, &full[i], kbi(i) * 64, n0, pol_x);
+    for (int i = 0; i < pre; ++i) load_x(smem + i * C::kStageBytes + C::kABytes, kbi(i), &full[i]);
     for (int i = pre; i < nkb; ++i) {
       const int s = i % nst;
       mbar_wait(&empty[s], ((i / nst) - 1) & 1);
       uint8_t* st = smem + s * C::kStageBytes;
       mbar_arrive_expect_tx(&full[s], C::kStageBytes);
       bulk_load(st, wt + static_cast<int64_t>(kbi(i)) * 8192, 16384, &full[s], pol_w);
-      tma_load_2d(st + C::kABytes, &tmX, &full[s], kbi(i) * 64, n0, pol_x);
+      load_x(st + C::kABytes, kbi(i), &full[s]);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = make_idesc_bf16(128, BN);
+    constexpr uint32_t idesc = make_idesc_bf16(128, BN > 256 ? 256 : BN);
+    constexpr uint32_t idesc2 = make_idesc_bf16(128, C::kN2 > 0 ? C::kN2 : 16);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % nst;
       mbar_wait(&full[s], (i / nst) & 1);
@@ -603,9 +613,13 @@ __global__ void __launch_bounds__(256, 1)
       const uint32_t a_addr = smem_u32(smem + s * C::kStageBytes);
       const uint32_t b_addr = a_addr + C::kABytes;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < 4; ++k) {
         umma_bf16(tmem, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + k * 32), idesc,
                   (i > 0 || k > 0) ? 1u : 0u);
+        if (C::kN2 > 0)
+          umma_bf16(tmem + 256, make_desc_k128(a_addr + k * 32), make_desc_k128(b_addr + 256 * 128 + k * 32),
+                    idesc2, (i > 0 || k > 0) ? 1u : 0u);
+      }
       if (i == nkb - 1) t_lastmma = clock64();
       umma_commit(&empty[s]);
     }
@@ -855,7 +869,8 @@ static cudaError_t launch_bn(const CUtensorMap& tw, const CUtensorMap& tx, const
 }
 
 template <int BN>
-static cudaError_t launch_mc(const CUtensorMap& tx, const GemmArgs& a, int splits, cudaStream_t st) {
+static cudaError_t launch_mc(const CUtensorMap& tx, const CUtensorMap& tx2, const GemmArgs& a, int splits,
+                            cudaStream_t st) {
   using C = McCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -867,15 +882,19 @@ static cudaError_t launch_mc(const CUtensorMap& tx, const GemmArgs& a, int split
   GemmArgs a2 = a;
   a2.stages = C::stages(gemm_mc_budget_kb());
   const dim3 grid((a.N + BN - 1) / BN, (a.M + 127) / 128, splits);
-  return launch_k(gemm_mc_kernel<BN>, grid, dim3(256), C::smem_bytes(a2.stages, a2.epi), st, tx, a2);
+  return launch_k(gemm_mc_kernel<BN>, grid, dim3(256), C::smem_bytes(a2.stages, a2.epi), st, tx, tx2, a2);
 }
 
 // CTAs of gemm_mc_kernel<BN> that can be co-resident (one per SM at the deep
 // ring, two at the 100 KB ring of <= 32-row tiles).  Queried once per width.
+static int g_sm_budget = kNumSMs;
+void vox_set_sm_budget(int sms) { g_sm_budget = (sms > 0 && sms <= kNumSMs) ? sms : kNumSMs; }
+int vox_sm_budget() { return g_sm_budget; }
+
 template <int BN>
 static int mc_capacity_t() {
-  static int cap = 0;
-  if (cap == 0) {
+  static int per_sm_c = 0;
+  if (per_sm_c == 0) {
     using C = McCfg<BN>;
     cudaFuncSetAttribute(gemm_mc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemMax);
     int per_sm = 0;
@@ -886,9 +905,9 @@ static int mc_capacity_t() {
       cudaGetLastError();
       per_sm = 1;
     }
-    cap = per_sm * kNumSMs;
+    per_sm_c = per_sm;
   }
-  return cap;
+  return per_sm_c * g_sm_budget;
 }
 int gemm_mc_capacity(int bn) {
   switch (bn) {
@@ -900,26 +919,34 @@ int gemm_mc_capacity(int bn) {
     case 160: return mc_capacity_t<160>();
     case 192: return mc_capacity_t<192>();
     case 224: return mc_capacity_t<224>();
+    case 288: return mc_capacity_t<288>();
+    case 320: return mc_capacity_t<320>();
+    case 384: return mc_capacity_t<384>();
     default: return mc_capacity_t<256>();
   }
 }
 
-// BN in {16, 32, 64, 96, 128, 160, 192, 224, 256}; tx = activation map with box rows BN
-cudaError_t gemm_launch_mc(const CUtensorMap& tx, GemmArgs a, int splits, int bn, cudaStream_t st) {
+// BN in {16, 32, 64, 96, 128, 160, 192, 224, 256, 288, 320, 384}; tx = activation map
+// with box rows min(BN, 256), tx2 = box rows BN - 256 (BN > 256 only)
+cudaError_t gemm_launch_mc(const CUtensorMap& tx, const CUtensorMap& tx2, GemmArgs a, int splits, int bn,
+                           cudaStream_t st) {
   if (a.w_packed == nullptr) return cudaErrorInvalidValue;
   a.n_kb = a.K / 64;
   a.kb_per_split = (a.n_kb + splits - 1) / splits;
   splits = (a.n_kb + a.kb_per_split - 1) / a.kb_per_split;
   switch (bn) {
-    case 16: return launch_mc<16>(tx, a, splits, st);
-    case 32: return launch_mc<32>(tx, a, splits, st);
-    case 64: return launch_mc<64>(tx, a, splits, st);
-    case 96: return launch_mc<96>(tx, a, splits, st);
-    case 128: return launch_mc<128>(tx, a, splits, st);
-    case 160: return launch_mc<160>(tx, a, splits, st);
-    case 192: return launch_mc<192>(tx, a, splits, st);
-    case 224: return launch_mc<224>(tx, a, splits, st);
-    case 256: return launch_mc<256>(tx, a, splits, st);
+    case 16: return launch_mc<16>(tx, tx2, a, splits, st);
+    case 32: return launch_mc<32>(tx, tx2, a, splits, st);
+    case 64: return launch_mc<64>(tx, tx2, a, splits, st);
+    case 96: return launch_mc<96>(tx, tx2, a, splits, st);
+    case 128: return launch_mc<128>(tx, tx2, a, splits, st);
+    case 160: return launch_mc<160>(tx, tx2, a, splits, st);
+    case 192: return launch_mc<192>(tx, tx2, a, splits, st);
+    case 224: return launch_mc<224>(tx, tx2, a, splits, st);
+    case 256: return launch_mc<256>(tx, tx2, a, splits, st);
+    case 288: return launch_mc<288>(tx, tx2, a, splits, st);
+    case 320: return launch_mc<320>(tx, tx2, a, splits, st);
+    case 384: return launch_mc<384>(tx, tx2, a, splits, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -952,7 +979,7 @@ GemmPlan gemm_plan_1cta(int M, int rows, int K) {
   }
   if (const char* e = getenv("VOX_GEMM_MT_TEST")) g.mt = atoi(e) == 2 ? 2 : 1;
   const int tiles = ((M + 128 * g.mt - 1) / (128 * g.mt)) * ((rows + g.bn - 1) / g.bn);
-  const int slots = (g.mt == 2 ? 1 : 2) * kNumSMs;
+  const int slots = (g.mt == 2 ? 1 : 2) * g_sm_budget;
   int best = 1;
   for (int s = 1; s <= kGemmMaxSplits; ++s) {
     const int per = (n_kb + s - 1) / s;
@@ -973,12 +1000,13 @@ GemmPlan gemm_plan(int M, int rows, int K) {
   // each weight byte is read once; split-K to fill the co-resident CTA slots).
   // Callers fall back to the plan below when the weights are not packed.
   if (rows <= 512 && K % 64 == 0) {
-    // <= 256 rows: one n-tile; 257..512 rows (decode plus a burst of prefill
-    // rows): two n-tiles of half the rows each
-    const int ntiles = rows > 256 ? 2 : 1;
+    // <= 384 rows (decode plus a burst of prefill rows): one n-tile, so every
+    // weight byte is read once (BN > 256 runs two MMAs per k-step); 385..512
+    // rows: two n-tiles of half the rows each
+    const int ntiles = rows > 384 ? 2 : 1;
     const int per_tile = (rows + ntiles - 1) / ntiles;
     int bn = 256;
-    for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256})
+    for (int b : {16, 32, 64, 96, 128, 160, 192, 224, 256, 288, 320, 384})
       if (per_tile <= b) { bn = b; break; }
     const int mtiles = (M + 127) / 128 * ntiles;  // CTAs per split
     const int cap = gemm_mc_capacity(bn);
@@ -1034,7 +1062,7 @@ static cudaError_t launch_persist(const CUtensorMap& tw, const CUtensorMap& tx, 
     attr_set = true;
   }
   const int tiles = ((a.N + BN - 1) / BN) * ((a.M + 128 * MT - 1) / (128 * MT));
-  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  const int grid = tiles < g_sm_budget ? tiles : g_sm_budget;
   return launch_k(gemm_persist_kernel<BN, MT>, dim3(grid), dim3(kPersistThreads), C::kSmem, st, tw, tx, a);
 }
 

@@ -73,8 +73,13 @@ cudaError_t gemm_launch(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a
 cudaError_t gemm_launch_persist(const CUtensorMap& tw, const CUtensorMap& tx, GemmArgs a, int bn, int mt,
                                 cudaStream_t st);
 // decode kernel: tx = activation map with box rows bn
-cudaError_t gemm_launch_mc(const CUtensorMap& tx, GemmArgs a, int splits, int bn, cudaStream_t st);
+cudaError_t gemm_launch_mc(const CUtensorMap& tx, const CUtensorMap& tx2, GemmArgs a, int splits, int bn,
+                           cudaStream_t st);
 int gemm_mc_capacity(int bn);
+// SMs the LM stream's kernels may use (kNumSMs unless the context split the GPU
+// into LM / detok partitions): grids and split-K plans are sized to it
+void vox_set_sm_budget(int sms);
+int vox_sm_budget();
 
 // ---------------------------------------------------------------- init
 // w[i] = bf16(unit_pm1(mix64(key + i)) * scale); key per tensor (host-derived).

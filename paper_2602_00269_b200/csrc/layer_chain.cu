@@ -125,7 +125,7 @@ VOX_DEV float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const floa
 // resid_norm_row at 256 threads (same accumulation and reduction order) for up
 // to kPar rows at once: every row's loads are in flight together and the rows
 // share one set of block barriers; each thread keeps its h values in registers
-constexpr int kPar = 2;
+constexpr int kPar = 1;
 constexpr int kMaxD4PerThread = 3;  // d <= 3072 (host: chain_bn_for_rows)
 VOX_DEV void chain_norm_rows(const ChainJob& j, const RowDev* rows, int r0, int nr, int d, float eps,
                              int eg, float* red) {
@@ -154,21 +154,29 @@ VOX_DEV void chain_norm_rows(const ChainJob& j, const RowDev* rows, int r0, int 
       }
     }
   }
-  for (int s = 1; s < j.nsplits; ++s) {
-    float4 t[kPar][kMaxD4PerThread];
+  for (int s = 1; s < j.nsplits; s += 2) {  // two planes per round trip
+    const bool two = s + 1 < j.nsplits;
+    float4 t[kPar][kMaxD4PerThread], u[kPar][kMaxD4PerThread];
 #pragma unroll
     for (int k = 0; k < kMaxD4PerThread; ++k) {
       const int i = eg + k * kEpiThreads;
 #pragma unroll
       for (int p = 0; p < kPar; ++p)
-        if (live[p] && i < d4) t[p][k] = ldcg4(j.ws + s * j.ss + static_cast<int64_t>(r0 + p) * d + 4 * i);
+        if (live[p] && i < d4) {
+          const float* src = j.ws + s * j.ss + static_cast<int64_t>(r0 + p) * d + 4 * i;
+          t[p][k] = ldcg4(src);
+          if (two) u[p][k] = ldcg4(src + j.ss);
+        }
     }
 #pragma unroll
     for (int k = 0; k < kMaxD4PerThread; ++k) {
       const int i = eg + k * kEpiThreads;
 #pragma unroll
       for (int p = 0; p < kPar; ++p)
-        if (live[p] && i < d4) v[p][k] = add4(v[p][k], t[p][k]);
+        if (live[p] && i < d4) {
+          v[p][k] = add4(v[p][k], t[p][k]);
+          if (two) v[p][k] = add4(v[p][k], u[p][k]);
+        }
     }
   }
 #pragma unroll
@@ -679,7 +687,7 @@ static cudaError_t launch_chain_bn(const CUtensorMap& m0, const CUtensorMap& m1,
   }
   const int smem = C::smem(a.wst, a.xst);
   if (smem > 227 * 1024 || a.wst < 2 || a.xst < 2 || a.wst > 16 || a.xst > 8) return cudaErrorInvalidValue;
-  return launch_k(layer_chain_kernel<BN>, dim3(kNumSMs), dim3(kThreads), smem, st, m0, m1, m2, a);
+  return launch_k(layer_chain_kernel<BN>, dim3(vox_sm_budget()), dim3(kThreads), smem, st, m0, m1, m2, a);
 }
 
 // ring depths for a tile width: X (activation, L2-resident) stages first, then as

@@ -54,9 +54,10 @@ enum TensorId : uint64_t {
 };
 
 // decode-step row buckets (one CUDA graph each): steps of 32 rows between 64
-// and 256 so a step pays at most 31 padding rows of tensor work -- at ~224 rows
-// the projections are at the tensor/HBM ridge
-constexpr int kBuckets[] = {16, 32, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512, 1024, 2048};
+// and 320 so a step pays at most 31 padding rows of tensor work -- at ~224 rows
+// the projections are at the tensor/HBM ridge; 257..384 rows
+// (decode rows plus a prefill burst) still run as one GEMM n-tile
+constexpr int kBuckets[] = {16, 32, 64, 96, 128, 160, 192, 224, 256, 288, 320, 384, 448, 512, 1024, 2048};
 constexpr int kTicketRing = 32;  // in-flight detok calls (VOX_TICKET_RING in voxb200.h)
 
 struct TimingRec {
@@ -117,6 +118,9 @@ struct VoxCtx {
   uint64_t seed = 0;
   std::string err;
   cudaStream_t s_lm = nullptr, s_dt = nullptr;
+  // optional spatial split (VOX_DETOK_SMS): green contexts owning the LM / detok SMs
+  CUgreenCtx green_lm = nullptr, green_dt = nullptr;
+  int lm_sms = kNumSMs, dt_sms = 0;
   cudaEvent_t epoch = nullptr;
   LmDims dm{};
   int nqkv = 0, max_pages_per_slot = 0;
@@ -337,7 +341,8 @@ static int run_gemm(VoxCtx* c, const CUtensorMap& tw, std::map<int, CUtensorMap>
   const double bytes = static_cast<double>(m_valid) * K * 2 + static_cast<double>(rows) * K * 2 +
                        static_cast<double>(rows) * m_valid * 4 * splits;
   TimedLaunch tl(c, st, cls, bytes);
-  cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn), a, splits, bn, st)
+  cudaError_t e = plan.mc     ? gemm_launch_mc(xm.at(bn > 256 ? 256 : bn), xm.at(bn > 256 ? bn - 256 : bn), a,
+                                               splits, bn, st)
                               : gemm_launch(tw, xm.at(bn), a, splits, bn, plan.mt, st);
   if (e != cudaSuccess) return fail(c, VOX_ERR_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
   return VOX_OK;
@@ -965,6 +970,8 @@ static int validate_cfg(const VoxModelCfg* g) {
   return 1;
 }
 
+static bool make_partition_streams(VoxCtx* c, int dt_want, int prio_lm, int prio_dt);
+
 int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx** out) {
   VoxCtx* c = nullptr;
   if (!cfg || !out) return fail(nullptr, VOX_ERR_INVALID, "null argument");
@@ -987,10 +994,16 @@ int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx*
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   const bool prio = !(getenv("VOX_STREAM_PRIO") && atoi(getenv("VOX_STREAM_PRIO")) == 0);
-  CK(cudaStreamCreateWithPriority(&c->s_lm, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
-  // (detokenizing on the LM stream, between decode steps, measured 4% slower than
-  // this concurrent low-priority stream: profiles/detok_serial_ab_r02.txt)
-  CK(cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, prio_lo));
+  const int dt_sms = getenv("VOX_DETOK_SMS") ? atoi(getenv("VOX_DETOK_SMS")) : 0;
+  if (dt_sms > 0 && make_partition_streams(c, dt_sms, prio ? prio_hi : prio_lo, prio_lo)) {
+    vox_set_sm_budget(c->lm_sms);
+  } else {
+    if (dt_sms > 0) return fail(c, VOX_ERR_CUDA, "VOX_DETOK_SMS: green-context SM partition failed");
+    CK(cudaStreamCreateWithPriority(&c->s_lm, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
+    // (detokenizing on the LM stream, between decode steps, measured 4% slower than
+    // this concurrent low-priority stream: profiles/detok_serial_ab_r02.txt)
+    CK(cudaStreamCreateWithPriority(&c->s_dt, cudaStreamNonBlocking, prio_lo));
+  }
   CK(cudaEventCreate(&c->epoch));
   c->dm.d = cfg->d_model;
   c->dm.n_heads = cfg->n_heads;
@@ -1018,6 +1031,50 @@ int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx*
   CK(cudaEventRecord(c->epoch, c->s_lm));
   *out = c;
   return VOX_OK;
+}
+
+// Spatial split of the GPU between the LM step and detokenization: the detok
+// stream gets a green context of `dt_want` SMs (rounded up to the partition
+// granularity, 8 SMs on sm_90+), the LM stream one of the remaining SMs, so detok
+// CTAs never hold SMs an LM kernel is waiting for.  CUDA graphs keep the partition
+// of the stream they were captured on.  Returns false (and leaves the streams
+// unset) when the driver lacks the API or the split fails.
+static bool make_partition_streams(VoxCtx* c, int dt_want, int prio_lm, int prio_dt) {
+  auto sym = [](const char* n) -> void* {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(n, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return fn;
+  };
+  auto getdev = reinterpret_cast<decltype(&cuDeviceGet)>(sym("cuDeviceGet"));
+  auto getres = reinterpret_cast<decltype(&cuDeviceGetDevResource)>(sym("cuDeviceGetDevResource"));
+  auto split = reinterpret_cast<decltype(&cuDevSmResourceSplitByCount)>(sym("cuDevSmResourceSplitByCount"));
+  auto gendesc = reinterpret_cast<decltype(&cuDevResourceGenerateDesc)>(sym("cuDevResourceGenerateDesc"));
+  auto mkctx = reinterpret_cast<decltype(&cuGreenCtxCreate)>(sym("cuGreenCtxCreate"));
+  auto mkstream = reinterpret_cast<decltype(&cuGreenCtxStreamCreate)>(sym("cuGreenCtxStreamCreate"));
+  if (!getdev || !getres || !split || !gendesc || !mkctx || !mkstream) return false;
+  CUdevice dev;
+  CUdevResource all{}, grp{}, rest{};
+  unsigned nb = 1;
+  if (getdev(&dev, c->device) != CUDA_SUCCESS || getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(&grp, &nb, &all, &rest, 0, static_cast<unsigned>(dt_want)) != CUDA_SUCCESS || nb != 1 ||
+      rest.sm.smCount < 64)
+    return false;
+  CUdevResourceDesc d_dt, d_lm;
+  if (gendesc(&d_dt, &grp, 1) != CUDA_SUCCESS || gendesc(&d_lm, &rest, 1) != CUDA_SUCCESS) return false;
+  if (mkctx(&c->green_dt, d_dt, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      mkctx(&c->green_lm, d_lm, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return false;
+  CUstream a = nullptr, b = nullptr;
+  if (mkstream(&a, c->green_lm, CU_STREAM_NON_BLOCKING, prio_lm) != CUDA_SUCCESS ||
+      mkstream(&b, c->green_dt, CU_STREAM_NON_BLOCKING, prio_dt) != CUDA_SUCCESS)
+    return false;
+  c->s_lm = reinterpret_cast<cudaStream_t>(a);
+  c->s_dt = reinterpret_cast<cudaStream_t>(b);
+  c->lm_sms = static_cast<int>(rest.sm.smCount);
+  c->dt_sms = static_cast<int>(grp.sm.smCount);
+  return true;
 }
 
 void vox_destroy(VoxCtx* c) {
@@ -1079,6 +1136,16 @@ void vox_destroy(VoxCtx* c) {
   if (c->s_lm) cudaStreamDestroy(c->s_lm);
   if (c->s_dt && c->s_dt != c->s_lm) cudaStreamDestroy(c->s_dt);
   if (c->epoch) cudaEventDestroy(c->epoch);
+  if (c->green_lm || c->green_dt) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuGreenCtxDestroy", &fn, cudaEnableDefault, &q) == cudaSuccess && fn) {
+      auto destroy = reinterpret_cast<decltype(&cuGreenCtxDestroy)>(fn);
+      if (c->green_dt) destroy(c->green_dt);
+      if (c->green_lm) destroy(c->green_lm);
+    }
+    vox_set_sm_budget(kNumSMs);
+  }
   delete c;
 }
 
@@ -1728,7 +1795,17 @@ int vox_sample_logits(VoxCtx* c, const float* logits, int32_t n, int32_t vocab,
 // ---------------------------------------------------------------------------
 // detokenizer
 // ---------------------------------------------------------------------------
+// plans made while enqueueing detok work size their grids to the detok partition
+struct SmBudgetScope {
+  int prev;
+  explicit SmBudgetScope(int sms) : prev(vox_sm_budget()) {
+    if (sms > 0) vox_set_sm_budget(sms);
+  }
+  ~SmBudgetScope() { vox_set_sm_budget(prev); }
+};
+
 static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
+  SmBudgetScope sms(c->dt_sms);
   const DetokDims& dd = c->dd;
   DetokW& w = c->dw;
   cudaStream_t st = c->s_dt;

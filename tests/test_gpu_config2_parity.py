@@ -2,7 +2,8 @@
 
 Orpheus-3B-style geometry (d 3072, 24 q / 8 kv heads x 128, FFN 8192, vocab
 156,940, tied head) with 2 of the 28 layers, one mixed batch of 200 or 256
-decode rows -- the 224- and 256-row graph buckets the serving bench runs --
+decode rows -- the 224- and 256-row graph buckets the serving bench runs, and
+273 / 300 rows (decode plus a prefill burst: one GEMM n-tile of 288 / 320 rows) --
 through the DEFAULT serving path: CUDA-graph-captured step with PDL, the mc
 tcgen05 GEMM with its split-K fp32 planes for QKV / O / down and the fused
 SiLU(gate)*up epilogue on gate|up, paged attention, the packed audio-row LM
@@ -39,7 +40,7 @@ PEN = 1.3
 
 @pytest.fixture(scope="module")
 def c2():
-    cfg = orpheus3b(n_layers=2, max_slots=264, max_ctx=64, max_rows=1024, detok_enabled=False)
+    cfg = orpheus3b(n_layers=2, max_slots=320, max_ctx=64, max_rows=1024, detok_enabled=False)
     dev = VoxDevice(cfg, weight_seed=WS)
     orc = LlamaOracle(cfg, WS, lazy_emb=True)
     yield cfg, dev, orc
@@ -58,7 +59,7 @@ def _plan(cfg, n, salt):
     return reqs
 
 
-@pytest.mark.parametrize("n", [200, 256])
+@pytest.mark.parametrize("n", [200, 256, 273, 300])
 def test_config2_dims_decode_step(c2, n):
     cfg, dev, orc = c2
     reqs = _plan(cfg, n, 0)

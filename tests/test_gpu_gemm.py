@@ -48,9 +48,11 @@ def test_gemm_decode_split_k(tiny_dev, monkeypatch, M, N, K, splits):
     assert err < 1e-3 * np.sqrt(K), err
 
 
-@pytest.mark.parametrize("M,N,K", [(1024, 300, 512), (2048, 512, 1024), (640, 448, 768)])
+@pytest.mark.parametrize("M,N,K", [(1024, 300, 512), (2048, 512, 1024), (640, 448, 768), (3072, 273, 3072),
+                                   (1024, 384, 1024), (16384, 288, 3072), (640, 257, 512)])
 def test_gemm_two_row_tiles(tiny_dev, monkeypatch, M, N, K):
-    """257..512 rows: the decode GEMM splits the rows over two n-tiles."""
+    """257..384 rows: one n-tile, two MMAs per k-step (N = 256 + rest);
+    385..512 rows: the decode GEMM splits the rows over two n-tiles."""
     monkeypatch.setenv("VOX_GEMM_PACKED_TEST", "1")
     rng = np.random.default_rng(M + N)
     w = bf16_round(rng.uniform(-1, 1, size=(M, K)).astype(np.float32))
