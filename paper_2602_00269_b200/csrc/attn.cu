@@ -33,13 +33,23 @@ namespace vox {
 VOX_TRACE_TU(trace_set_attn)
 
 
-constexpr int kAttnStages = 3;
-constexpr int kAttnPagesPerStage = 4;  // one page per warp
+// K/V ring depth: 3 stages of 32 KB (hd 128 x 4 pages, hd 64 x 8 pages)
+template <int HD>
+__host__ __device__ constexpr int attn_stages() {
+  return 3;
+}
+// consumer warps = K/V head-pages per stage (one page per warp): 4 at hd 128;
+// 8 at hd 64, whose per-page math is a short latency chain, so a lone item (as
+// many items as CTA slots, e.g. 128 rows x 2 kv heads) needs more pages in flight
+template <int HD>
+__host__ __device__ constexpr int attn_warps() {
+  return HD == 64 ? 8 : 4;
+}
 constexpr int kAttnQSlot = 1024;       // per-stage q slot (G * hd * 2 <= 1 KB)
 
 template <int HD>
 __host__ __device__ constexpr int attn_stage_bytes(int ps) {
-  return kAttnPagesPerStage * 2 * ps * HD * 2;
+  return attn_warps<HD>() * 2 * ps * HD * 2;
 }
 
 VOX_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
@@ -56,8 +66,8 @@ VOX_DEV uint32_t pack_bf16x2(float lo, float hi) {
 }
 
 // Work item = (row, kv head, kv split), item = ((row * n_kv) + kvh) * n_split + z.
-// Persistent CTAs (2 per SM), warp-specialised: warps 0-3 consume one K/V
-// head-page each per stage; warp 4 is the producer.  The producer pulls items
+// Persistent CTAs (2 per SM), warp-specialised: warps 0..NW-1 consume one K/V
+// head-page each per stage; warp NW is the producer.  The producer pulls items
 // from a device counter ONE ITEM AHEAD (counter, row descriptor and the item's
 // page ids, loaded lane-parallel into shared memory, are ready before they are
 // needed) and walks a flat sequence of stages across items, so the ring keeps
@@ -85,13 +95,17 @@ VOX_DEV void attn_item_decode(int item, int n_kv, int n_split, int& r, int& kvh,
   r = t / n_kv;
 }
 
-VOX_DEV void named_bar_consumers() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int NW>
+VOX_DEV void named_bar_consumers() { asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory"); }
 
-constexpr int kAttnThreads = 160;
+template <int HD>
+__host__ __device__ constexpr int attn_threads() {
+  return 32 * (attn_warps<HD>() + 1);
+}
 constexpr int kAttnItemPages = 64;  // page ids staged per item (1024 tokens at ps 16)
 
 template <int HD, int G>
-__global__ void __launch_bounds__(kAttnThreads, 2)
+__global__ void __launch_bounds__(attn_threads<HD>(), 2)
     attn_decode_kernel(const RowDev* __restrict__ rows, const bf16* __restrict__ q,
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
@@ -101,13 +115,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
   constexpr int NT = HD / 8;   // PV n-tiles
-  constexpr int kP = kAttnPagesPerStage;
+  constexpr int kP = attn_warps<HD>();
+  constexpr int NW = kP;  // consumer warps
   constexpr int kQBytes = G * HD * 2;
+  constexpr int kAttnStages = attn_stages<HD>();
   extern __shared__ __align__(128) uint8_t stage_raw[];
   __shared__ uint64_t full[kAttnStages], empty[kAttnStages];
   __shared__ __align__(16) StageMeta meta[kAttnStages];
-  __shared__ float s_m[4][G], s_l[4][G];
-  __shared__ __align__(16) float s_acc[4][G][HD];
+  __shared__ float s_m[NW][G], s_l[NW][G];
+  __shared__ __align__(16) float s_acc[NW][G][HD];
   __shared__ int s_pt[2][kAttnItemPages];
   __shared__ int s_last;
 
@@ -119,7 +135,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   if (tid == 0) {
     for (int s = 0; s < kAttnStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 4);
+      mbar_init(&empty[s], NW);
     }
     fence_mbar_init();
   }
@@ -133,7 +149,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                                    static_cast<size_t>(s) * kAttnQSlot);
   };
 
-  if (warp == 4) {
+  if (warp == NW) {
     // ====================== producer warp ======================
     // The counter is zeroed by the last CTA of the previous launch; every kernel
     // between two attention launches does griddep_wait before griddep_launch,
@@ -252,7 +268,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       if (done) break;
     }
   } else {
-    // ====================== consumer warps 0-3 ======================
+    // ====================== consumer warps 0..NW-1 ======================
     griddep_wait();
     griddep_launch();
     const int gn = lane >> 2, j = lane & 3;  // mma row/col group, k-slot group
@@ -354,15 +370,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             s_acc[warp][gn][8 * t + 2 * j + 1] = acc[t][1];
           }
         }
-        named_bar_consumers();
-        for (int idx = tid; idx < G * HD; idx += 128) {
+        named_bar_consumers<NW>();
+        for (int idx = tid; idx < G * HD; idx += 32 * NW) {
           const int gg = idx / HD, dd = idx % HD;
           float M = -INFINITY;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) M = fmaxf(M, s_m[w][gg]);
+          for (int w = 0; w < NW; ++w) M = fmaxf(M, s_m[w][gg]);
           float Ls = 0.f, A = 0.f;
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
+          for (int w = 0; w < NW; ++w) {
             const float f = (s_m[w][gg] == -INFINITY) ? 0.f : exp2f(s_m[w][gg] - M);
             Ls += s_l[w][gg] * f;
             A += s_acc[w][gg][dd] * f;
@@ -384,14 +400,14 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           // the last split of (row, kv head) to finish merges all n_split partials in
           // fixed z order (deterministic whichever CTA is last): no combine launch
           __threadfence();
-          named_bar_consumers();
+          named_bar_consumers<NW>();
           int* cnt = sched + 2 + m.row * dm.n_kv + m.kvh;
           if (tid == 0) s_last = (atomicAdd(cnt, 1) == n_split - 1);
-          named_bar_consumers();
+          named_bar_consumers<NW>();
           if (s_last) {
             __threadfence();
             const float* base = ws + (static_cast<int64_t>(m.row) * dm.n_kv + m.kvh) * n_split * G * (HD + 2);
-            for (int idx = tid; idx < G * HD; idx += 128) {
+            for (int idx = tid; idx < G * HD; idx += 32 * NW) {
               const int g = idx / HD, dd = idx % HD;
               float M = -INFINITY;
               for (int zz = 0; zz < n_split; ++zz)
@@ -409,7 +425,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             if (tid == 0) *cnt = 0;
           }
         }
-        named_bar_consumers();  // s_acc / s_m / s_l are reused by the next item
+        named_bar_consumers<NW>();  // s_acc / s_m / s_l are reused by the next item
       }
     }
   }
@@ -455,7 +471,7 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
                         const int* pt, const LmDims& dm, bf16* out, float* ws, int n_split,
                         int* sched, cudaStream_t st) {
   // K/V ring + one q slot per stage (96 KB + 3 KB at ps 16, hd 128): 2 CTAs per SM
-  const int smem = kAttnStages * (attn_stage_bytes<HD>(dm.page_size) + kAttnQSlot);
+  const int smem = attn_stages<HD>() * (attn_stage_bytes<HD>(dm.page_size) + kAttnQSlot);
   static int attr_bytes = 0;
   if (smem > attr_bytes) {
     cudaFuncSetAttribute(attn_decode_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -472,7 +488,7 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
   // CTA's critical path.  Kept opt-in.
   static const int fuse = getenv("VOX_ATTN_FUSED_COMBINE") ? 1 : 0;
   static const int l2pf = getenv("VOX_ATTN_L2PF") ? atoi(getenv("VOX_ATTN_L2PF")) : 0;
-  launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(kAttnThreads), smem, st, rows, q, kc, vc, pt, dm,
+  launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(attn_threads<HD>()), smem, st, rows, q, kc, vc, pt, dm,
            out, ws, n_split, n_items, sched, fuse, l2pf);
   if (n_split > 1 && !fuse)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,

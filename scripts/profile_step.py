@@ -21,7 +21,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
 
-from paper_2602_00269_b200.config import orpheus3b  # noqa: E402
+from paper_2602_00269_b200.config import CONFIGS  # noqa: E402
 from paper_2602_00269_b200.device import Sampling, VoxDevice  # noqa: E402
 
 
@@ -32,11 +32,13 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--detok", type=int, default=32)
     ap.add_argument("--graph", action="store_true", help="graph-captured decode steps")
+    ap.add_argument("--config", default="orpheus3b", help="orpheus3b | cosyvoice2 (no SNAC detok: --detok 0)")
     a = ap.parse_args()
     import torch
 
-    dev = VoxDevice(orpheus3b(max_slots=max(a.batch, 8)), 0)
-    prm = Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3)
+    dev = VoxDevice(CONFIGS[a.config](max_slots=max(a.batch, 8)), 0)
+    prm = (Sampling(temperature=0.8, top_p=0.95, top_k=50, repetition_penalty=1.1) if "cosy" in a.config
+           else Sampling(temperature=0.6, top_p=0.8, repetition_penalty=1.3))
     P = 50
     slots = [dev.admit(1000 + i, P, 688, prm) for i in range(a.batch)]
     per = max(1, 1000 // (a.ctx - 1))
