@@ -33,10 +33,12 @@ namespace vox {
 VOX_TRACE_TU(trace_set_attn)
 
 
-// K/V ring depth: 3 stages of 32 KB (hd 128 x 4 pages, hd 64 x 8 pages)
+// K/V ring depth: 3 stages of 32 KB at hd 128 (4 pages); 2 at hd 64 (8 pages), whose
+// 8-warp merge buffers (14 KB static) would otherwise leave room for only one CTA
+// per SM (measured: 108 of 256 CTAs in a second wave at 128 rows x 2 kv heads)
 template <int HD>
 __host__ __device__ constexpr int attn_stages() {
-  return 3;
+  return HD == 64 ? 2 : 3;
 }
 // consumer warps = K/V head-pages per stage (one page per warp): 4 at hd 128;
 // 8 at hd 64, whose per-page math is a short latency chain, so a lone item (as
@@ -68,9 +70,10 @@ VOX_DEV uint32_t pack_bf16x2(float lo, float hi) {
 // Work item = (row, kv head, kv split), item = ((row * n_kv) + kvh) * n_split + z.
 // Persistent CTAs (2 per SM), warp-specialised: warps 0..NW-1 consume one K/V
 // head-page each per stage; warp NW is the producer.  The producer pulls items
-// from a device counter ONE ITEM AHEAD (counter, row descriptor and the item's
-// page ids, loaded lane-parallel into shared memory, are ready before they are
-// needed) and walks a flat sequence of stages across items, so the ring keeps
+// from a device counter, claiming the next one as the current item's last stage
+// goes out (counter, row descriptor and the item's page ids, loaded lane-parallel
+// into shared memory, come back while the ring still holds the current item's
+// stages) and walks a flat sequence of stages across items, so the ring keeps
 // streaming through item boundaries.  Everything the consumers need about an
 // item travels in the stage descriptor (no global loads on their side).
 struct StageMeta {
@@ -187,8 +190,7 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
     };
     AttnItem cur, nxt;
     int buf = 0;
-    fetch(cur, 0);
-    fetch(nxt, 1);
+    fetch(cur, 0);  // the next item is claimed when cur's last stage goes out (below)
     // issue the next stage of `cur` into slot s (q optionally deferred)
     auto issue = [&](int s, bool with_q) {
       if (cur.item < 0) {
@@ -232,10 +234,14 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
                   kQBytes, &full[s], pol);
       }
       __syncwarp();
-      if (++cur.rr == cur.nr) {  // next item (prefetched); refill the look-ahead
+      // Claim the next item only as cur's last stage goes out: claiming it a whole
+      // item ahead let early CTAs hoard two items each while late ones found none
+      // (128 rows x 2 kv heads: half the CTAs did two items, half none); the ring
+      // still holds cur's stages while the claim and its page ids come back.
+      if (cur.rr == cur.nr - 1) fetch(nxt, buf ^ 1);
+      if (++cur.rr == cur.nr) {
         cur = nxt;
         buf ^= 1;
-        fetch(nxt, buf ^ 1);
       }
     };
     // ---- prologue: stages of the first item whose pages all precede the first
