@@ -70,11 +70,10 @@ VOX_DEV uint32_t pack_bf16x2(float lo, float hi) {
 // Work item = (row, kv head, kv split), item = ((row * n_kv) + kvh) * n_split + z.
 // Persistent CTAs (2 per SM), warp-specialised: warps 0..NW-1 consume one K/V
 // head-page each per stage; warp NW is the producer.  The producer pulls items
-// from a device counter, claiming the next one as the current item's last stage
-// goes out (counter, row descriptor and the item's page ids, loaded lane-parallel
-// into shared memory, come back while the ring still holds the current item's
-// stages) and walks a flat sequence of stages across items, so the ring keeps
-// streaming through item boundaries.  Everything the consumers need about an
+// from a device counter ONE ITEM AHEAD when there are more items than CTAs
+// (counter, row descriptor and the item's page ids, loaded lane-parallel into
+// shared memory, are ready before they are needed) and walks a flat sequence of
+// stages across items, so the ring keeps streaming through item boundaries.  Everything the consumers need about an
 // item travels in the stage descriptor (no global loads on their side).
 struct StageMeta {
   int item;  // -1: no more work
@@ -190,7 +189,19 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
     };
     AttnItem cur, nxt;
     int buf = 0;
-    fetch(cur, 0);  // the next item is claimed when cur's last stage goes out (below)
+    // Look one item ahead (the ring streams through item boundaries) when there are
+    // more items than CTAs; with at most one item per CTA a look-ahead claim lets
+    // early CTAs hoard a second item while late ones get none (128 rows x 2 kv
+    // heads: half the CTAs did two items, half none), so each CTA then claims its
+    // next item only as cur's last stage goes out (finding none).  A mixed policy
+    // (look-ahead until fewer items than CTAs remain) measured slower at 64-224 rows.
+    const bool ahead = n_items > static_cast<int>(gridDim.x);
+    bool have_nxt = false;
+    fetch(cur, 0);
+    if (ahead) {
+      fetch(nxt, 1);
+      have_nxt = true;
+    }
     // issue the next stage of `cur` into slot s (q optionally deferred)
     auto issue = [&](int s, bool with_q) {
       if (cur.item < 0) {
@@ -234,14 +245,18 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
                   kQBytes, &full[s], pol);
       }
       __syncwarp();
-      // Claim the next item only as cur's last stage goes out: claiming it a whole
-      // item ahead let early CTAs hoard two items each while late ones found none
-      // (128 rows x 2 kv heads: half the CTAs did two items, half none); the ring
-      // still holds cur's stages while the claim and its page ids come back.
-      if (cur.rr == cur.nr - 1) fetch(nxt, buf ^ 1);
+      if (!have_nxt && cur.rr == cur.nr - 1) {
+        fetch(nxt, buf ^ 1);
+        have_nxt = true;
+      }
       if (++cur.rr == cur.nr) {
         cur = nxt;
         buf ^= 1;
+        have_nxt = false;
+        if (ahead) {
+          fetch(nxt, buf ^ 1);
+          have_nxt = true;
+        }
       }
     };
     // ---- prologue: stages of the first item whose pages all precede the first
