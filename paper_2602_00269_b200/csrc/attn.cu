@@ -111,8 +111,7 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
     attn_decode_kernel(const RowDev* __restrict__ rows, const bf16* __restrict__ q,
                        const bf16* __restrict__ kc, const bf16* __restrict__ vc,
                        const int* __restrict__ page_table, LmDims dm, bf16* __restrict__ out,
-                       float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched,
-                       int fuse_combine, int l2pf) {
+                       float* __restrict__ ws, int n_split, int n_items, int* __restrict__ sched) {
   VOX_TRACE(kTrAttn);
   static_assert(G <= 8, "GQA group must fit the mma row tile");
   constexpr int NB = HD / 32;  // 32-dim blocks (2 k-blocks each)
@@ -127,7 +126,6 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
   __shared__ float s_m[NW][G], s_l[NW][G];
   __shared__ __align__(16) float s_acc[NW][G][HD];
   __shared__ int s_pt[2][kAttnItemPages];
-  __shared__ int s_last;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ps = dm.page_size;
@@ -229,17 +227,6 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
                             : page_table[static_cast<int64_t>(cur.slot) * dm.max_pages_per_slot + pa + jp];
         const int64_t base = (static_cast<int64_t>(pid) * dm.n_kv + cur.kvh) * page_elems;
         bulk_load(stage_ptr(s, jp, kv), (kv ? vc : kc) + base, page_elems * 2, &full[s], pol);
-        // l2pf > 0: also pull this item's pages l2pf stages ahead into L2 -- the
-        // smem ring (96 KB per CTA) caps the bytes in flight per SM; L2
-        // prefetches add memory-level parallelism without smem
-        const int off2 = off + l2pf * kP;
-        if (l2pf > 0 && cur.begin + off2 < cur.end) {
-          const int pid2 = off2 < kAttnItemPages
-                               ? s_pt[buf][off2]
-                               : page_table[static_cast<int64_t>(cur.slot) * dm.max_pages_per_slot + cur.begin + off2];
-          prefetch_l2_bulk((kv ? vc : kc) + (static_cast<int64_t>(pid2) * dm.n_kv + cur.kvh) * page_elems,
-                           page_elems * 2);
-        }
       } else if (lane == 2 * kP && cur.rr == 0 && with_q) {
         bulk_load(q_slot(s), q + (static_cast<int64_t>(cur.row) * dm.n_heads + cur.kvh * G) * HD,
                   kQBytes, &full[s], pol);
@@ -417,35 +404,6 @@ __global__ void __launch_bounds__(attn_threads<HD>(), 2)
             }
           }
         }
-        if (n_split > 1 && fuse_combine) {
-          // the last split of (row, kv head) to finish merges all n_split partials in
-          // fixed z order (deterministic whichever CTA is last): no combine launch
-          __threadfence();
-          named_bar_consumers<NW>();
-          int* cnt = sched + 2 + m.row * dm.n_kv + m.kvh;
-          if (tid == 0) s_last = (atomicAdd(cnt, 1) == n_split - 1);
-          named_bar_consumers<NW>();
-          if (s_last) {
-            __threadfence();
-            const float* base = ws + (static_cast<int64_t>(m.row) * dm.n_kv + m.kvh) * n_split * G * (HD + 2);
-            for (int idx = tid; idx < G * HD; idx += 32 * NW) {
-              const int g = idx / HD, dd = idx % HD;
-              float M = -INFINITY;
-              for (int zz = 0; zz < n_split; ++zz)
-                M = fmaxf(M, __ldcg(base + zz * G * (HD + 2) + g * (HD + 2) + HD));
-              float Ls = 0.f, A = 0.f;
-              for (int zz = 0; zz < n_split; ++zz) {
-                const float* pz = base + zz * G * (HD + 2) + g * (HD + 2);
-                const float mz = __ldcg(pz + HD);
-                const float f = (mz == -INFINITY) ? 0.f : exp2f(mz - M);
-                Ls += __ldcg(pz + HD + 1) * f;
-                A += __ldcg(pz + dd) * f;
-              }
-              out[(static_cast<int64_t>(m.row) * dm.n_heads + m.kvh * G + g) * HD + dd] = __float2bfloat16_rn(A / Ls);
-            }
-            if (tid == 0) *cnt = 0;
-          }
-        }
         named_bar_consumers<NW>();  // s_acc / s_m / s_l are reused by the next item
       }
     }
@@ -502,16 +460,12 @@ static void attn_launch(const RowDev* rows, int n, const bf16* q, const bf16* kc
   const int n_items = n * dm.n_kv * n_split;
   const int sms = vox_sm_budget();
   const int grid = n_items < 2 * sms ? n_items : 2 * sms;
-  // VOX_ATTN_FUSED_COMBINE=1: the last split CTA of each (row, kv head) merges the
-  // partials (no combine launch).  Measured slower than the separate combine kernel
-  // (B=1 decode 2.06 -> 2.29 ms, CSM frame 8.58 -> 9.30 ms): every split item pays a
-  // fence + two consumer barriers + an atomic, and the merge lengthens the last
-  // CTA's critical path.  Kept opt-in.
-  static const int fuse = getenv("VOX_ATTN_FUSED_COMBINE") ? 1 : 0;
-  static const int l2pf = getenv("VOX_ATTN_L2PF") ? atoi(getenv("VOX_ATTN_L2PF")) : 0;
+  // (merging the splits in the last split's CTA instead of a combine launch, and L2
+  // prefetch of pages beyond the smem ring, both measured slower and were removed:
+  // DESIGN.md section 9)
   launch_k(attn_decode_kernel<HD, G>, dim3(grid), dim3(attn_threads<HD>()), smem, st, rows, q, kc, vc, pt, dm,
-           out, ws, n_split, n_items, sched, fuse, l2pf);
-  if (n_split > 1 && !fuse)
+           out, ws, n_split, n_items, sched);
+  if (n_split > 1)
     launch_k(attn_combine_kernel<HD, G>, dim3(n, dm.n_kv), dim3(128), 0, st, rows, ws, dm, n_split,
              out);
 }

@@ -179,7 +179,6 @@ struct ChainArgs {
   const float2* rope;
   int* ctr;  // kChainCtrInts zeroed ints (self-resetting)
   int k_rotate;
-  int l2_ahead;  // k-blocks of the W unit pulled into L2 while stalled at a job boundary
   int wst, xst;  // weight / activation ring depths (chain_stages)
 };
 void chain_stages(int bn, int* wst, int* xst);

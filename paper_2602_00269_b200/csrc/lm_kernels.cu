@@ -233,8 +233,7 @@ void launch_qkv_rope_append(const RowDev* rows, int n, const float* ws, const fl
                             const int* page_table, bf16* kc, bf16* vc, bf16* q_out,
                             cudaStream_t st) {
   // CTAs per row (8 for <= 32 rows measured no different from 2)
-  static const int gy = getenv("VOX_ROPE_Y") ? atoi(getenv("VOX_ROPE_Y")) : 2;
-  launch_k(qkv_rope_append_kernel, dim3(n, gy), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
+  launch_k(qkv_rope_append_kernel, dim3(n, 2), dim3(256), 0, st, rows, ws, bias, splits, split_stride, dm,
            rope, page_table, kc, vc, q_out);
 }
 
@@ -308,11 +307,8 @@ void launch_resid_norm(const RowDev* rows, int n, const float* ws, int splits,
   // few rows: more threads per row shorten each row's dependent-load chain; many
   // rows: 256-thread CTAs co-reside with the PDL-launched GEMM CTAs (768 threads
   // measured slower at 224 rows, profiles/gemm_mc_ab_r01.txt)
-  static const int nt_env = getenv("VOX_NORM_THREADS") ? atoi(getenv("VOX_NORM_THREADS")) : 0;
   int nt = 256;
-  if (nt_env > 0) {
-    nt = nt_env > 768 ? 768 : nt_env;
-  } else if (n <= 32) {  // one float4 per thread (d = 3072: 768 threads)
+  if (n <= 32) {  // one float4 per thread (d = 3072: 768 threads)
     nt = (dm.d / 4 + 31) / 32 * 32;
     nt = nt < 256 ? 256 : (nt > 768 ? 768 : nt);
   }

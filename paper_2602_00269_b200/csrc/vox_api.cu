@@ -774,8 +774,6 @@ static int enqueue_layers_chain(VoxCtx* c, int nrows, int bn, cudaStream_t st) {
   a.dm = dm;
   a.rope = c->rope_tab;
   a.k_rotate = c->gemm_k_rotate;
-  static const int l2a = getenv("VOX_CHAIN_L2") ? atoi(getenv("VOX_CHAIN_L2")) : 0;
-  a.l2_ahead = l2a;
   chain_stages(bn, &a.wst, &a.xst);
   const CUtensorMap &mx = c->tm_x.at(bn), &ma = c->tm_attn.at(bn), &mf = c->tm_act.at(bn);
   const double act_b = static_cast<double>(nrows) * 2;
