@@ -499,7 +499,10 @@ static void attn_dispatch_g(const RowDev* rows, int n, const bf16* q, const bf16
 // unsplit; CosyVoice2 LM at 128 rows 1.38 -> 1.19 ms), so split only when
 // contexts can exceed 1024 tokens and the items leave half the CTA slots idle.
 int attn_pick_splits(int n_rows, int n_kv, int max_ctx) {
-  if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) return atoi(e) < 1 ? 1 : atoi(e);  // debug
+  if (const char* e = getenv("VOX_ATTN_SPLITS_TEST")) {  // debug; the partials workspace holds
+    const int f = atoi(e) < 1 ? 1 : (atoi(e) > kAttnMaxSplits ? kAttnMaxSplits : atoi(e));  // kAttnSplitRows
+    return n_rows > kAttnSplitRows ? 1 : f;
+  }
   if (max_ctx < 1024) return 1;
   const int ctas = n_rows * n_kv;
   int s = (2 * vox_sm_budget()) / ctas;
