@@ -1,14 +1,17 @@
 // attn.cu — K2: paged GQA decode attention (HBM-bound) + split-KV combine.
 //
-// One CTA (4 warps) per (row, kv head, kv split).  The G = H/KV query heads
-// that share a kv head are processed together, so every K/V byte is read from
-// HBM exactly once per step.
+// Work item = (row, kv head, kv split).  The G = H/KV query heads that share a
+// kv head are processed together, so every K/V byte is read from HBM exactly
+// once per step.  Persistent CTAs (two per SM) pull items from a device counter
+// (see the producer below for the look-ahead rule).
 //
-// Data movement: thread 0 streams whole head-pages (K page [ps][hd] and the
-// TRANSPOSED V page [hd][ps], 4 KB each at ps=16, hd=128) into a 3-stage
-// shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier
-// transaction counts), 4 pages (64 tokens, 32 KB) per stage, so ~96 KB per CTA
-// is in flight independent of registers.
+// Data movement: one producer warp streams whole head-pages (K page [ps][hd] and
+// the TRANSPOSED V page [hd][ps], 4 KB each at ps=16, hd=128) into a 3-stage
+// shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier transaction
+// counts), one page per consumer warp per stage: 4 pages (64 tokens, 32 KB) at
+// hd 128, 8 pages at hd 64, so the loads in flight do not depend on registers.
+// Pages that precede the position appended by this step are issued before
+// griddepcontrol.wait (PDL).
 //
 // Math on tensor cores (mma.sync m16n8k16 bf16 -> fp32), one page per warp per
 // stage, fragments loaded with single vector loads thanks to consistent
@@ -21,10 +24,11 @@
 //   PV:   A = P straight from the QK accumulators (tokens 4j..4j+3 are lane j's
 //         k-slots 2j,2j+1,2j+8,2j+9), B = V: with V^T stored per page, lane j
 //         reads V^T[dim][4j..4j+3] as one 8-byte load per 8-dim n-tile.
-// Online softmax in exp2 (scores scaled by log2(e)/sqrt(hd) in fp32); P is
-// rounded to bf16 for the PV product.  Small batches split the context across
-// blockIdx.z (fixed split count per launch -> graph-capturable) and a combine
-// pass merges the partial (m, l, acc) triples.
+// Online softmax in exp2 (scores scaled by log2(e)/sqrt(hd) in fp32); P enters
+// the PV product as a bf16 hi + lo pair (near-fp32 probabilities).  The warps'
+// partial (m, l, acc) are merged per item in shared memory.  Small batches with
+// long contexts split each item's pages (fixed split count per launch ->
+// graph-capturable) and a combine launch merges the partials.
 #include "common.cuh"
 #include "kernels.h"
 #include <cstdlib>
