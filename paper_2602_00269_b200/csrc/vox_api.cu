@@ -822,8 +822,20 @@ static int enqueue_layers_chain(VoxCtx* c, int nrows, int bn, cudaStream_t st) {
 // ---------------------------------------------------------------------------
 // hslot >= 0: every sampled row is at the same frame slot, so the LM head runs
 // over that slot's codebook rows only (CSM depth decoder: 1 of 31 codebook heads)
+// Grids and split-K plans follow the partition of the stream being enqueued to:
+// the LM stream's SMs for forwards, the detok partition for detok calls (the
+// budget is process-wide state, so every enqueue sets its own).
+struct SmBudgetScope {
+  int prev;
+  explicit SmBudgetScope(int sms) : prev(vox_sm_budget()) {
+    if (sms > 0) vox_set_sm_budget(sms);
+  }
+  ~SmBudgetScope() { vox_set_sm_budget(prev); }
+};
+
 static int enqueue_forward(VoxCtx* c, int nrows, int nsamp, bool full_logits, int hslot = -1,
                            bool run_sampler = true) {
+  SmBudgetScope sms(c->lm_sms);
   const VoxModelCfg& g = c->cfg;
   const LmDims& dm = c->dm;
   cudaStream_t st = c->s_lm;
@@ -992,11 +1004,18 @@ int vox_create(int device, const VoxModelCfg* cfg, uint64_t weight_seed, VoxCtx*
   int prio_lo = 0, prio_hi = 0;
   CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   const bool prio = !(getenv("VOX_STREAM_PRIO") && atoi(getenv("VOX_STREAM_PRIO")) == 0);
-  const int dt_sms = getenv("VOX_DETOK_SMS") ? atoi(getenv("VOX_DETOK_SMS")) : 0;
+  // Contexts that detokenize split the GPU by default: 16 SMs (two partition
+  // granules) for the detok stream, the rest for the LM -- the serving step measured
+  // 1.0-1.5% faster than sharing every SM (detok CTAs no longer hold SMs an LM
+  // GEMM is waiting for; the LM step itself is as fast on 132 SMs).  VOX_DETOK_SMS=N
+  // sets the size, 0 shares the whole GPU.  If the driver cannot make the partition
+  // the default falls back to shared streams; an explicit request fails loudly.
+  const char* dt_env = getenv("VOX_DETOK_SMS");
+  const int dt_sms = dt_env ? atoi(dt_env) : (cfg->detok_enabled ? 16 : 0);
   if (dt_sms > 0 && make_partition_streams(c, dt_sms, prio ? prio_hi : prio_lo, prio_lo)) {
-    vox_set_sm_budget(c->lm_sms);
+    // grids follow c->lm_sms / c->dt_sms per enqueue (SmBudgetScope)
   } else {
-    if (dt_sms > 0) return fail(c, VOX_ERR_CUDA, "VOX_DETOK_SMS: green-context SM partition failed");
+    if (dt_sms > 0 && dt_env) return fail(c, VOX_ERR_CUDA, "VOX_DETOK_SMS: green-context SM partition failed");
     CK(cudaStreamCreateWithPriority(&c->s_lm, cudaStreamNonBlocking, prio ? prio_hi : prio_lo));
     // (detokenizing on the LM stream, between decode steps, measured 4% slower than
     // this concurrent low-priority stream: profiles/detok_serial_ab_r02.txt)
@@ -1142,7 +1161,6 @@ void vox_destroy(VoxCtx* c) {
       if (c->green_dt) destroy(c->green_dt);
       if (c->green_lm) destroy(c->green_lm);
     }
-    vox_set_sm_budget(kNumSMs);
   }
   delete c;
 }
@@ -1793,17 +1811,8 @@ int vox_sample_logits(VoxCtx* c, const float* logits, int32_t n, int32_t vocab,
 // ---------------------------------------------------------------------------
 // detokenizer
 // ---------------------------------------------------------------------------
-// plans made while enqueueing detok work size their grids to the detok partition
-struct SmBudgetScope {
-  int prev;
-  explicit SmBudgetScope(int sms) : prev(vox_sm_budget()) {
-    if (sms > 0) vox_set_sm_budget(sms);
-  }
-  ~SmBudgetScope() { vox_set_sm_budget(prev); }
-};
-
 static int enqueue_detok(VoxCtx* c, int n_req, int n_lat) {
-  SmBudgetScope sms(c->dt_sms);
+  SmBudgetScope sms(c->dt_sms > 0 ? c->dt_sms : c->lm_sms);
   const DetokDims& dd = c->dd;
   DetokW& w = c->dw;
   cudaStream_t st = c->s_dt;
