@@ -198,6 +198,9 @@ int vox_timing_enable(VoxCtx* ctx, int32_t on);
 int vox_timing_read(VoxCtx* ctx, const char* name, double* total_ms, int64_t* launches,
                     double* bytes);
 int vox_launch_count(VoxCtx* ctx, int64_t* launches); /* our kernels launched so far */
+/* SMs of the LM stream's and the detok stream's partitions (detok 0: no split,
+   both streams share every SM); VOX_DETOK_SMS at vox_create sets the split */
+int vox_sm_partition(VoxCtx* ctx, int32_t* lm_sms, int32_t* detok_sms);
 
 /* in-graph kernel tracer (diagnostics): vox_trace_arm allocates room for
  * `capacity` records and arms every instrumented kernel; vox_trace_read

@@ -145,6 +145,7 @@ _SIGS = {
     "vox_timing_read": (C.c_int, [_P, C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                   C.POINTER(C.c_double)]),
     "vox_launch_count": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "vox_sm_partition": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "vox_trace_arm": (C.c_int, [_P, C.c_int64]),
     "vox_trace_read": (C.c_int, [_P, _P, C.c_int64, C.POINTER(C.c_int64)]),
     "vox_debug_detok": (C.c_int, [_P, C.c_int32, _f32p, C.c_size_t, C.POINTER(C.c_uint16), C.c_size_t]),

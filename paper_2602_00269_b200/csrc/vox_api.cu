@@ -2157,6 +2157,13 @@ int vox_launch_count(VoxCtx* c, int64_t* launches) {
   return VOX_OK;
 }
 
+int vox_sm_partition(VoxCtx* c, int32_t* lm_sms, int32_t* detok_sms) {
+  if (!c || !lm_sms || !detok_sms) return fail(c, VOX_ERR_INVALID, "null argument");
+  *lm_sms = c->lm_sms;
+  *detok_sms = c->dt_sms;
+  return VOX_OK;
+}
+
 int vox_debug_detok(VoxCtx* c, int32_t stop_after, float* out, size_t n_floats, uint16_t* bf_out,
                     size_t n_bf) {
   if (!c) return fail(c, VOX_ERR_INVALID, "null ctx");

@@ -289,6 +289,12 @@ class VoxDevice:
         self._check(self.lib.vox_launch_count(self.ctx, C.byref(n)))
         return n.value
 
+    def sm_partition(self) -> tuple[int, int]:
+        """(LM-stream SMs, detok-stream SMs); detok 0 = both streams share every SM."""
+        lm, dt = C.c_int32(), C.c_int32()
+        self._check(self.lib.vox_sm_partition(self.ctx, C.byref(lm), C.byref(dt)))
+        return lm.value, dt.value
+
     def gemm_test(self, w_bits: np.ndarray, x_bits: np.ndarray, bias=None, splits: int = 1, iters: int = 1):
         """K3 alone: w_bits [M,K], x_bits [N,K] uint16 bf16 bits -> (out [N,M] fp32, mean ms)."""
         w = np.ascontiguousarray(w_bits, dtype=np.uint16)
