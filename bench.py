@@ -548,6 +548,9 @@ def detok_roofline(dev, tfl: float, hbm: float, n_win: int = 32, calls: int = 12
             "audio_s_per_s": round(n_win * 2048 / 24000 / (ms / 1e3), 1)}
 
 
+DRAIN_S = 20.0  # seconds after the last arrival for a load-test run to finish every request
+
+
 def slo_run(dev, rate: float, seconds: float, seed: int, prompt: int, ws: int, rank: int, max_batch: int,
             startup_limit: int):
     """One Poisson load test (config 5) at the WHOLE-JOB offered rate: reference workload
@@ -564,11 +567,20 @@ def slo_run(dev, rate: float, seconds: float, seed: int, prompt: int, ws: int, r
     mine = dp.route(arr, ws, seed)[rank]
     policy = scheduler.PolicyConfig(max_lm_batch=max_batch, max_detok_batch=max_batch,
                                     startup_concurrency_limit=startup_limit)
+    t_run = time.perf_counter()
     eng = StreamingEngine(dev, prof, policy, seed)
-    tr = eng.run(mine)
+    # A run whose backlog has not drained DRAIN_S after the last arrival is over
+    # capacity: it stops there and fails (an overloaded 60 s run otherwise spends
+    # minutes draining its queue -- the bench's wall time, not its result).
+    tr = eng.run(mine, max_wall_s=seconds + DRAIN_S)
+    eng.shutdown()  # releases the slots of requests cut off by the wall limit
+    t_served = time.perf_counter()
     rep = dp.gather_pool(dp.local_summary(tr), ws)
-    ok = rep["viability"] >= 0.99 and rep["ttfa_p90"] <= 0.5
-    return ok, dict(rate=rate, seconds=seconds, requests=len(arr), ttfa_p50=rep["ttfa_p50"],
+    drained = rep["completed"] >= len(arr)
+    ok = drained and rep["viability"] >= 0.99 and rep["ttfa_p90"] <= 0.5
+    t_end = time.perf_counter()
+    return ok, dict(rate=rate, seconds=seconds, requests=len(arr), drained=drained,
+                    wall_s=round(t_end - t_run, 1), report_s=round(t_end - t_served, 1), ttfa_p50=rep["ttfa_p50"],
                     ttfa_p90=rep["ttfa_p90"], ttfa_p99=rep["ttfa_p99"], viability=rep["viability"],
                     inverse_rtf=rep["inverse_rtf"], audio_s=rep["audio_s"], completed=rep["completed"], ok=ok)
 
@@ -581,6 +593,15 @@ def run_slo(dev, start: float, seconds: float, probe_seconds: float, seed: int, 
     keeps viability >= 0.99 and p90 TTFA <= 0.5 s.  Short probes (probe_seconds, `coarse`
     steps) bracket it first; only full-length runs decide the result."""
     sweep = []
+    tested = {}  # full-length results by rate (a rate is run at most once)
+
+    def full(rate):
+        if rate not in tested:
+            ok_, row_ = slo_run(dev, rate, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
+            sweep.append(row_)
+            tested[rate] = ok_
+        return tested[rate]
+
     r, last_ok = start, None
     while True:  # coarse bracket (short probes)
         ok, row = slo_run(dev, r, probe_seconds, seed, prompt, ws, rank, max_batch, startup_limit)
@@ -588,48 +609,53 @@ def run_slo(dev, start: float, seconds: float, probe_seconds: float, seed: int, 
         if not ok:
             break
         last_ok, r = r, r + coarse
-    if last_ok is None:  # even the start rate fails: walk down
-        r = start - fine
-        n = 0
-        while r > 0 and n < max_full:
-            ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
-            sweep.append(row)
-            n += 1
-            if ok:
-                return r, sweep
-            r -= coarse / 2
-        return 0.0, sweep
-    # full-length runs, at most max_full of them (bounds the bench's wall time):
-    # upward on the fine grid from the last passing probe; if that rate fails at
-    # full length, walk down in coarse/2 steps, then refine upward on the fine grid
-    best, r, n = None, last_ok, 0
-    while r < last_ok + coarse and n < max_full:
-        ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
-        sweep.append(row)
+    n = 0
+
+    def try_full(rate):  # None once the full-length budget is spent
+        nonlocal n
+        if rate in tested:
+            return tested[rate]
+        if n >= max_full:
+            return None
         n += 1
-        if not ok:
+        return full(rate)
+
+    # Full-length runs decide, each rate at most once and at most max_full of them
+    # (bounds the bench's wall time): find a passing and a failing full-length rate
+    # (up on the fine grid from the last passing probe, or down from it in coarse
+    # steps), then bisect between them on the fine grid.
+    lo_pass, hi_fail = None, None
+    r = last_ok if last_ok is not None else start - coarse
+    while r > 0:
+        ok = try_full(r)
+        if ok is None:
             break
-        best, r = r, r + fine
-    if best is None:
-        step = coarse / 2
-        r = last_ok - step
-        while r > 0 and n < max_full:
-            ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
-            sweep.append(row)
-            n += 1
-            if ok:
-                best = r
+        if ok:
+            lo_pass = r
+            break
+        hi_fail = r
+        r -= coarse
+    if lo_pass is not None and hi_fail is None:  # the probe rate passed: go up
+        top = (last_ok if last_ok is not None else start) + coarse  # the failing probe
+        r = lo_pass + fine
+        while r < top:
+            ok = try_full(r)
+            if ok is None:
                 break
-            r -= step
-        if best is not None:
-            r = best + fine
-            while r < best + step and n < max_full:
-                ok, row = slo_run(dev, r, seconds, seed, prompt, ws, rank, max_batch, startup_limit)
-                sweep.append(row)
-                n += 1
-                if not ok:
-                    break
-                best, r = r, r + fine
+            if not ok:
+                hi_fail = r
+                break
+            lo_pass, r = r, r + fine
+    while lo_pass is not None and hi_fail is not None and hi_fail - lo_pass > fine:
+        mid = lo_pass + fine * max(1, round((hi_fail - lo_pass) / (2 * fine)))
+        ok = try_full(mid)
+        if ok is None:
+            break
+        if ok:
+            lo_pass = mid
+        else:
+            hi_fail = mid
+    best = lo_pass
     return (best or 0.0), sweep
 
 
@@ -970,7 +996,7 @@ def main():
     ap.add_argument("--prompt", type=int, default=50)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--slo-seconds", type=float, default=60.0, help="full-length run (PAPER.md:257)")
-    ap.add_argument("--slo-probe-seconds", type=float, default=15.0, help="bracketing probes")
+    ap.add_argument("--slo-probe-seconds", type=float, default=30.0, help="bracketing probes")
     ap.add_argument("--slo-start", type=float, default=72.0, help="first offered rate per GPU (req/s)")
     ap.add_argument("--no-slo", action="store_true")
     ap.add_argument("--slo-max-batch", type=int, default=256, help="LM batch cap of the load test")
@@ -1082,7 +1108,8 @@ def main():
                "duration_s": args.slo_seconds, "grid_req_s": 2.0 * ws,
                "protocol": f"{args.slo_probe_seconds:.0f} s probes in {8 * ws} req/s steps bracket the rate; "
                            f"the result is the highest {2 * ws} req/s-grid rate passing a {args.slo_seconds:.0f} s run "
-                           f"(at most 5 full-length runs; a failing probe rate walks down in {4 * ws} req/s steps)",
+                           f"(at most 5 full-length runs: a passing and a failing rate, then bisection; "
+                           f"a run whose backlog is not drained {DRAIN_S:.0f} s after its last arrival fails)",
                "routing": "reference route_dp (seeded uniform), replicas", "sweep": sweep}
 
     phase("slo")
